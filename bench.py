@@ -1,0 +1,452 @@
+#!/usr/bin/env python
+"""FlexLink-on-B200 benchmark: striped AllReduce/AllGather bus bandwidth.
+
+Metric (BASELINE.json): AllReduce/AllGather busBW GB/s @256MB vs NCCL, plus the
+PCIe/NIC traffic share.
+
+* N=1 (default, ``python bench.py``): BASELINE config 1 — AllReduce sum fp32,
+  256 MiB per rank over 8 simulated ranks — run as 8 *virtual ranks* on cuda:0
+  (flxCommInitAll with a repeated device; one fused NVLink-path launch per call,
+  the PCIe share through the real host-staged copy-engine pipeline).  Shares
+  come from Stage 1 run on the real path (guarded), then a short Stage-2 phase.
+  The AllGather bf16 256 MiB (config 2 shape, 8 virtual ranks) is reported in
+  the same line under "allgather".
+* N>1 (torchrun, one process per GPU): the same AllReduce, 256 MiB per rank,
+  over N real GPUs through flxCommInitRank, with torch.distributed NCCL timed
+  on the same buffers for the "nccl" column.
+* ``--impl reference``: the reference's CPU path — the oracle port
+  (oracle/flx_oracle.c, all host threads) on a bounded sample of the same
+  workload.
+
+busbw (nccl-tests): AllReduce (S/t)*2(N-1)/N, AllGather (S_out/t)*(N-1)/N.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MIB = 1 << 20
+SIM_RANKS = 8
+AR_BYTES = 256 * MIB           # per rank (config 1)
+AG_OUT_BYTES = 256 * MIB       # gathered output (config 2, nccl-tests convention)
+METRIC = "AllReduce/AllGather busBW GB/s @256MB vs NCCL; PCIe/NIC traffic share %"
+
+
+def busbw_allreduce(nbytes: int, seconds: float, n: int) -> float:
+    return nbytes / seconds * 2 * (n - 1) / n / 1e9
+
+
+def busbw_allgather(out_bytes: int, seconds: float, n: int) -> float:
+    return out_bytes / seconds * (n - 1) / n / 1e9
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return self
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=5)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for row in self.rows:
+            if len(row) < 8:
+                continue
+            try:
+                sm.append(float(row[0]))
+                smax.append(float(row[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, row[4:8]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------ CPU baseline
+def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = 32 * MIB,
+                         n: int = SIM_RANKS):
+    """Oracle port on the host: repeated 8-rank fp32 AllReduce until ~target_s."""
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    threads = oracle.cpu_threads()
+    count = per_rank_bytes // 4
+    rng = np.random.default_rng(1000)
+    sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(n)]
+    recvs = [np.empty_like(s) for s in sends]
+    oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
+        reps += 1
+        if time.perf_counter() - t0 >= target_s:
+            break
+    per_call = (time.perf_counter() - t0) / reps
+    return {
+        "value": round(busbw_allreduce(per_rank_bytes, per_call, n), 3),
+        "unit": "GB/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"AllReduce sum fp32 {per_rank_bytes // MIB} MiB/rank x {n} simulated ranks, "
+                  f"{reps} calls in {per_call * reps:.1f} s (oracle/flx_oracle.c, OpenMP)",
+    }
+
+
+def run_reference(args) -> None:
+    """``--impl reference``: the CPU path on the box's host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    threads = oracle.cpu_threads()
+    per_rank = 32 * MIB
+    count = per_rank // 4
+    rng = np.random.default_rng(1000)
+    sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(SIM_RANKS)]
+    recvs = [np.empty_like(s) for s in sends]
+    for _ in range(args.warmup):
+        oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
+    dt = (time.perf_counter() - t0) / args.steps
+    value = busbw_allreduce(per_rank, dt, SIM_RANKS)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "AllReduce sum fp32 over 8 simulated ranks (BASELINE config 1), "
+                               "CPU oracle port, bounded sample",
+                   "bytes_per_rank": per_rank, "sim_ranks": SIM_RANKS},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
+                         "kind": "port",
+                         "sample": f"{per_rank // MIB} MiB/rank x {SIM_RANKS} ranks per step"},
+        "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- N = 1
+def _time_steps(fn, steps: int, stream) -> float:
+    import torch
+
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    start.record(stream)
+    for _ in range(steps):
+        fn()
+    end.record(stream)
+    torch.cuda.synchronize()
+    return start.elapsed_time(end) / 1e3 / steps
+
+
+def run_single_gpu(args) -> None:
+    import torch
+
+    from paper_2510_15882_b200 import comm as flx
+    from paper_2510_15882_b200.links import PathKind, preset
+    from paper_2510_15882_b200.stage1 import TunerConfig
+    from paper_2510_15882_b200.stage2 import BalancerConfig, RuntimeBalancer
+    from paper_2510_15882_b200.striping import CollectiveOp, PathTimingReport
+
+    torch.cuda.set_device(0)
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    n = SIM_RANKS
+    count = AR_BYTES // 4
+    gen = torch.Generator(device="cuda").manual_seed(1000)
+    sends = [torch.randint(-1024, 1024, (count,), device="cuda", generator=gen).float()
+             for _ in range(n)]
+    recvs = [torch.empty_like(s) for s in sends]
+    stream = torch.cuda.current_stream()
+    clique = flx.Clique(n, device=0)
+    if args.nvlink_ctas:
+        clique.set_nvlink_ctas(args.nvlink_ctas)
+    topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
+
+    # ---- Stage 1 on the real path (+ guard), then a Stage-2 phase
+    t0 = time.perf_counter()
+    shares, trace, tuned_s, base_s = flx.tune_shares(
+        clique, topo, CollectiveOp.ALLREDUCE, sends, recvs, TunerConfig(), warmup=2, repeats=5)
+    tune_wall = time.perf_counter() - t0
+    balancer = RuntimeBalancer(shares, BalancerConfig(), active=shares.loaded_paths)
+    for _ in range(3):
+        for _ in range(10):
+            clique.all_reduce(sends, recvs)
+        for h in clique.comms[0].path_times_history(10):
+            b = clique.path_bytes()
+            rep = PathTimingReport.build(CollectiveOp.ALLREDUCE, n, AR_BYTES,
+                                         {k: h[k] for k in balancer.active if b[k] > 0})
+            ev = balancer.observe(rep)
+            if ev is not None and ev.moved:
+                clique.set_shares(CollectiveOp.ALLREDUCE, balancer.shares, AR_BYTES)
+    shares = balancer.shares
+
+    def step():
+        clique.all_reduce(sends, recvs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0).start()
+    launches0 = flx.launch_count()
+    dt = _time_steps(step, args.steps, stream)
+    launches = flx.launch_count() - launches0
+    clocks = sampler.stop()
+    hist = clique.comms[0].path_times_history(min(args.steps, 64))
+    pbytes = clique.path_bytes()
+    nv_ms = statistics.mean(h[PathKind.NVLINK] for h in hist) * 1e3
+    pc_ms = statistics.mean(h[PathKind.PCIE_STAGED] for h in hist) * 1e3 \
+        if pbytes[PathKind.PCIE_STAGED] else 0.0
+    value = busbw_allreduce(AR_BYTES, dt, n)
+    nv_alg_bytes = 2 * n * pbytes[PathKind.NVLINK]  # N reads + N writes of the NVLink slice
+    achieved = nv_alg_bytes / (nv_ms * 1e-3) / 1e9
+
+    # exactness spot check of the timed result (integer-valued inputs: exact sum)
+    exact = torch.stack(sends).sum(0)
+    assert all(torch.equal(r, exact) for r in recvs), "allreduce result mismatch"
+
+    # ---- e2e through the public API with host buffers
+    host_in = [torch.empty(count, dtype=torch.float32, pin_memory=True) for _ in range(n)]
+    host_out = [torch.empty(count, dtype=torch.float32, pin_memory=True) for _ in range(n)]
+    for h, s in zip(host_in, sends):
+        h.copy_(s)
+
+    def e2e_step():
+        for h, s in zip(host_in, sends):
+            s.copy_(h, non_blocking=True)
+        clique.all_reduce(sends, recvs)
+        for h, r in zip(host_out, recvs):
+            h.copy_(r, non_blocking=True)
+
+    e2e_step()
+    e2e_steps = max(3, min(args.steps, 10))
+    e2e_dt = _time_steps(e2e_step, e2e_steps, stream)
+    e2e_value = busbw_allreduce(AR_BYTES, e2e_dt, n)
+
+    # ---- AllGather bf16, 256 MiB gathered (config 2 shape) over 8 virtual ranks
+    ag_count = AG_OUT_BYTES // 2 // n
+    ag_send = [torch.randn(ag_count, device="cuda", generator=gen).bfloat16() for _ in range(n)]
+    ag_recv = [torch.empty(ag_count * n, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
+    ag_shares, ag_trace, _, _ = flx.tune_shares(clique, topo, CollectiveOp.ALLGATHER, ag_send,
+                                                ag_recv, TunerConfig(), warmup=2, repeats=5)
+    for _ in range(args.warmup):
+        clique.all_gather(ag_send, ag_recv)
+    ag_dt = _time_steps(lambda: clique.all_gather(ag_send, ag_recv), args.steps, stream)
+    ag_bytes = clique.path_bytes()
+    ag_hist = clique.comms[0].path_times_history(min(args.steps, 64))
+    ag_nv_ms = statistics.mean(h[PathKind.NVLINK] for h in ag_hist) * 1e3
+    ag_alg = (n + n * n) * ag_bytes[PathKind.NVLINK]  # N reads + N^2 writes
+    for r in range(n):
+        for q in range(n):
+            assert torch.equal(ag_recv[r][q * ag_count:(q + 1) * ag_count], ag_send[q])
+
+    cpu = cpu_allreduce_sample(args.cpu_seconds)
+    total = AR_BYTES
+    line = {
+        "metric": METRIC,
+        "value": round(value, 2),
+        "unit": "GB/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (seeded integer-valued fp32, exact-sum checked)",
+        "config": {
+            "workload": "AllReduce sum fp32 256 MiB/rank over 8 simulated ranks (BASELINE "
+                        "config 1) as 8 virtual ranks on one B200; NVLink path = fused "
+                        "on-device fold, PCIe path = real host-staged copy-engine pipeline",
+            "sim_ranks": n, "bytes_per_rank": AR_BYTES, "busbw": "(S/t)*2(N-1)/N, N=8",
+            "l2": "inputs 2 GiB + outputs 2 GiB per step > 126 MB L2 (no flush needed)",
+            "nvlink_ctas": args.nvlink_ctas or "auto",
+        },
+        "shares": {k.short: shares.get(k) for k in PathKind},
+        "path_bytes": {k.short: pbytes[k] for k in PathKind},
+        "traffic_share_pct": {k.short: round(100 * pbytes[k] / total, 3) for k in PathKind},
+        "path_ms": {"nvlink": round(nv_ms, 4), "pcie": round(pc_ms, 4), "rdma": None},
+        "rdma": "absent (no NIC / rdma-core in this image)",
+        "stage1": {"iterations": trace.iterations, "converged": trace.converged,
+                   "tuned_total_ms": round(tuned_s * 1e3, 4),
+                   "nvlink_only_total_ms": round(base_s * 1e3, 4), "wall_s": round(tune_wall, 2),
+                   "trace": [r.action for r in trace.records]},
+        "stage2": {"evaluations": len(balancer.evaluations),
+                   "moves": sum(1 for e in balancer.evaluations if e.moved)},
+        "roofline": {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+            "frac": round(achieved / hbm_peak, 4), "traffic": None,
+            "kernel": "fold_vec_kernel<float,Sum,8,1> (NVLink-path slice, 8 virtual ranks)",
+            "algorithmic_bytes_per_launch": nv_alg_bytes,
+            "kernel_ms": round(nv_ms, 4),
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
+        },
+        "cpu_baseline": cpu,
+        "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
+                "h2d_bytes_per_step": n * AR_BYTES, "d2h_bytes_per_step": n * AR_BYTES,
+                "ms_per_step": round(e2e_dt * 1e3, 3)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "nccl": None,
+        "allgather": {
+            "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, n), 2), "unit": "GB/s",
+            "dtype": "bf16", "out_bytes": AG_OUT_BYTES, "ms_per_step": round(ag_dt * 1e3, 4),
+            "shares": {k.short: ag_shares.get(k) for k in PathKind},
+            "traffic_share_pct": {k.short: round(100 * ag_bytes[k] / (AG_OUT_BYTES // n), 3)
+                                  for k in PathKind},
+            "kernel_achieved_gbs": round(ag_alg / (ag_nv_ms * 1e-3) / 1e9, 1),
+            "kernel_frac_hbm": round(ag_alg / (ag_nv_ms * 1e-3) / 1e9 / hbm_peak, 4),
+            "paper_convention_algbw": round(AG_OUT_BYTES / n / ag_dt / 1e9, 2),
+        },
+    }
+    clique.destroy()
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------- N > 1
+def run_multi_gpu(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_15882_b200 import comm as flx
+    from paper_2510_15882_b200.links import PathKind
+    from paper_2510_15882_b200.striping import CollectiveOp
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    rank, world = dist.get_rank(), dist.get_world_size()
+    c = flx.Communicator.from_process_group()
+    count = AR_BYTES // 4
+    gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
+    send = torch.randint(-1024, 1024, (count,), device="cuda", generator=gen).float()
+    recv = torch.empty_like(send)
+    stream = torch.cuda.current_stream()
+    shares = [int(x) for x in args.shares.split(",")] if args.shares else [1000, 0, 0]
+    c.set_shares(CollectiveOp.ALLREDUCE, shares)
+
+    def timed(fn):
+        for _ in range(args.warmup):
+            fn()
+        dist.barrier()
+        dt = _time_steps(fn, args.steps, stream)
+        t = torch.tensor([dt], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    launches0 = flx.launch_count()
+    sampler = ClockSampler(local).start() if rank == 0 else None
+    dt = timed(lambda: c.all_reduce(send, recv))
+    clocks = sampler.stop() if sampler else None
+    launches = flx.launch_count() - launches0
+    pbytes = c.path_bytes()
+    ref = send.clone()
+    nccl_dt = timed(lambda: (ref.copy_(send), dist.all_reduce(ref)))
+    exact = ref.clone()
+    dist.all_reduce(exact)
+    ok = torch.equal(recv, exact)
+    if rank == 0:
+        value = busbw_allreduce(AR_BYTES, dt, world) * 1.0
+        print(json.dumps({
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"AllReduce sum fp32 256 MiB/rank over {world} GPUs",
+                       "bytes_per_rank": AR_BYTES},
+            "shares": {k.short: shares[int(k)] for k in PathKind},
+            "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
+            "nccl": {"value": round(busbw_allreduce(AR_BYTES, nccl_dt, world), 2),
+                     "ms_per_step": round(nccl_dt * 1e3, 4)},
+            "result_matches_exact_sum": bool(ok), "gpu_launches": launches, "clocks": clocks,
+        }), flush=True)
+    dist.barrier()
+    c.destroy()
+    dist.destroy_process_group()
+
+
+def main() -> None:
+    p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["flexlink", "reference"], default="flexlink")
+    p.add_argument("--nvlink-ctas", type=int, default=0,
+                   help="cap the NVLink-path kernel's CTAs (config 4)")
+    p.add_argument("--shares", default="", help="N>1: fixed granules nvlink,pcie,rdma")
+    p.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = p.parse_args()
+    if args.warmup < 3 and args.impl == "flexlink":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        run_multi_gpu(args)
+    else:
+        run_single_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

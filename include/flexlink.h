@@ -1,0 +1,150 @@
+/*
+ * flexlink.h — C-ABI of the B200-native FlexLink data plane (libflexlink.so).
+ *
+ * NCCL-shaped striped collectives: every AllReduce / AllGather message is
+ * split by integer granule shares (1000 total) into contiguous per-path byte
+ * slices — NVLink first at offset 0, then host-staged PCIe, then RDMA — and
+ * each slice runs a complete collective on its own path concurrently.
+ *
+ * The reference ("linkstripe", /root/reference/pkg/src/linkstripe) is a CPU
+ * simulator whose data plane is the closed-form `simulate_collective`
+ * (collectives.py:136-186); this library is the real executor that replaces
+ * it.  Each entry point below names the reference interface it stands in for.
+ *
+ * Conventions (identical to /usr/include/nccl.h so the types are
+ * interchangeable):
+ *   - flxResult_t values equal ncclResult_t (nccl.h:40-48);
+ *   - flxDataType_t values equal ncclDataType_t; flxRedOp_t equals ncclRedOp_t
+ *     for sum/prod/max/min;
+ *   - flxUniqueId is 128 opaque bytes like ncclUniqueId (nccl.h:36-37);
+ *   - calls are stream-ordered and asynchronous; in-place is
+ *     sendbuff == recvbuff (AllReduce) or sendbuff == recvbuff + rank*sendcount
+ *     (AllGather);
+ *   - no CPU fallback: without a usable sm_100 device every call fails.
+ *
+ * Virtual ranks: flxCommInitAll() accepts the SAME device more than once.
+ * Ranks that share a device form a clique whose collectives run as one fused
+ * kernel launch (plus one host-staged pipeline), driven from a single thread
+ * inside flxGroupStart()/flxGroupEnd() exactly like ncclCommInitAll +
+ * ncclGroupStart/End.  This is how an N-rank collective is exercised on one
+ * GPU ("1-GPU tests where the N peers are N local buffers").
+ */
+#ifndef FLEXLINK_H_
+#define FLEXLINK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+#include <cuda_runtime.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FLX_VERSION_CODE 10000   /* 1.0.0 */
+#define FLX_UNIQUE_ID_BYTES 128
+#define FLX_NUM_PATHS 3
+#define FLX_GRANULE_TOTAL 1000   /* collectives.py:23 */
+#define FLX_MAX_VIRTUAL_RANKS 16
+#define FLX_BUCKET_ALL (-2)      /* flxSetShares: apply to every size bucket */
+
+typedef struct { char internal[FLX_UNIQUE_ID_BYTES]; } flxUniqueId;
+typedef struct flxComm* flxComm_t;
+
+/* == ncclResult_t (nccl.h:40-48) */
+typedef enum {
+  flxSuccess = 0,
+  flxUnhandledCudaError = 1,
+  flxSystemError = 2,
+  flxInternalError = 3,   /* also: semaphore wait timed out */
+  flxInvalidArgument = 4,
+  flxInvalidUsage = 5,
+  flxRemoteError = 6,
+  flxInProgress = 7
+} flxResult_t;
+
+/* == ncclDataType_t */
+typedef enum {
+  flxInt8 = 0, flxUint8 = 1, flxInt32 = 2, flxUint32 = 3, flxInt64 = 4,
+  flxUint64 = 5, flxFloat16 = 6, flxFloat32 = 7, flxFloat64 = 8, flxBfloat16 = 9,
+  flxNumTypes = 10
+} flxDataType_t;
+
+/* == ncclRedOp_t for the four supported operators */
+typedef enum { flxSum = 0, flxProd = 1, flxMax = 2, flxMin = 3, flxNumOps = 4 } flxRedOp_t;
+
+/* == linkstripe PathKind (topo.py:18-31); also the tie-break order */
+typedef enum { flxPathNvlink = 0, flxPathPcie = 1, flxPathRdma = 2 } flxPath_t;
+
+/* == linkstripe CollectiveOp (collectives.py:26-28) */
+typedef enum { flxCollAllReduce = 0, flxCollAllGather = 1 } flxCollOp_t;
+
+/* ---- library / errors --------------------------------------------------- */
+flxResult_t flxGetVersion(int* version);
+const char* flxGetErrorString(flxResult_t result);
+/* Last detailed error message of this thread (never NULL). */
+const char* flxGetLastError(void);
+
+/* ---- communicators (ncclGetUniqueId / ncclCommInitRank / ncclCommInitAll /
+ *      ncclCommDestroy shapes, nccl.h) ----------------------------------- */
+flxResult_t flxGetUniqueId(flxUniqueId* uniqueId);
+/* One process (or thread) per GPU; collective over the nranks callers. */
+flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId commId, int rank);
+/* Single process, ndev ranks; repeated devices become virtual ranks. */
+flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist);
+flxResult_t flxCommDestroy(flxComm_t comm);
+flxResult_t flxCommCount(const flxComm_t comm, int* count);
+flxResult_t flxCommUserRank(const flxComm_t comm, int* rank);
+flxResult_t flxCommCuDevice(const flxComm_t comm, int* device);
+
+/* ---- collectives --------------------------------------------------------
+ * Replace linkstripe `simulate_collective(topo, spec, shares)`
+ * (collectives.py:136-186): the shares come from the comm's share table
+ * (keyed by op and size_bucket, collectives.py:189-204), bytes are split by
+ * `partition` (collectives.py:93-114), and each path's completion is recorded
+ * with CUDA events for flxGetPathTimes (PathTimingReport, collectives.py:117-133).
+ * Shapes: ncclAllReduce (nccl.h:392-393), ncclAllGather (nccl.h:425-426). */
+flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
+                         flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
+                         cudaStream_t stream);
+flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
+                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
+flxResult_t flxGroupStart(void);
+flxResult_t flxGroupEnd(void);
+
+/* ---- balancer plumbing ---------------------------------------------------
+ * Shares are ShareDistribution.granules (collectives.py:55-90) as
+ * {nvlink, pcie, rdma}, summing to 1000.  bucket = size_bucket(bytes)
+ * (floor(log2)), or FLX_BUCKET_ALL.  Every rank must install identical
+ * shares (the Python layer agrees them across ranks first). */
+flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]);
+flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granules[3]);
+/* Per-path duration (ms, collective start -> path done) of the most recent
+ * call on this comm; blocks until that call finished.  A path that carried
+ * no bytes reports 0.  (PathTimingReport.durations, collectives.py:117-133) */
+flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]);
+/* The same for the last min(max_calls, calls issued, 64) calls, oldest first:
+ * ms[3*i + path].  Blocks until those calls finished.  Lets a caller time a
+ * run of calls without synchronising between them. */
+flxResult_t flxGetPathTimesHistory(flxComm_t comm, int max_calls, float* ms, int* n);
+/* Per-rank bytes each path carried in the most recent call (partition()). */
+flxResult_t flxGetPathBytes(flxComm_t comm, size_t bytes[3]);
+/* Byte alignment of every secondary-path slice (partition's `alignment`
+ * argument) that this comm applies for `op`. */
+flxResult_t flxGetAlignment(flxComm_t comm, flxCollOp_t op, size_t* alignment);
+
+/* ---- path configuration --------------------------------------------------
+ * nctas: CTAs of the NVLink-path kernel (0 = automatic).  Config 4 caps it to
+ * emulate a slower NVLink.  Must match on all ranks. */
+flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas);
+/* PCIe staging: bytes per chunk per rank and ring depth (1 or 2 buffers;
+ * PipelineSpec, staging.py:24-42).  Must match on all ranks. */
+flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers);
+/* Which optional paths this build/box can use: bit p set => path p usable. */
+flxResult_t flxGetPathMask(flxComm_t comm, int* mask);
+/* Number of device kernels this library has launched (process-wide). */
+flxResult_t flxGetLaunchCount(unsigned long long* count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FLEXLINK_H_ */

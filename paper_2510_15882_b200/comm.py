@@ -1,0 +1,431 @@
+"""Python face of the native data plane: communicators over ``libflexlink.so``.
+
+This is the drop-in seam SURVEY §8(b) names: the reference's collective
+executor is ``simulate_collective(topo, spec, shares)``
+(`pkg/src/linkstripe/collectives.py:136-186`), injected into Stage 1 through
+``initial_tune(measure=...)`` (`tuner.py:178-209`) and called per call by Stage 2
+(`balancer.py:190`).  Here the same roles are played by *real* striped
+collectives on B200:
+
+* :class:`Communicator` — one rank (``flxCommInitRank``) or one virtual rank of
+  a single-GPU clique (``flxCommInitAll`` with a repeated device);
+* :class:`Clique` — all virtual ranks of one device, driven together inside
+  ``flxGroupStart/End`` (one fused launch);
+* :meth:`Clique.measure_fn` — a Stage-1 ``MeasureFn`` returning a
+  :class:`~paper_2510_15882_b200.striping.PathTimingReport` built from CUDA-event
+  per-path times;
+* :func:`tune_shares` — Stage 1 against the real path plus the "never worse
+  than NVLink-only" guard, installed into the native share table.
+
+PyTorch tensors are the host-side currency; the library is loaded with ctypes
+and fails loudly when it is missing — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import statistics
+from pathlib import Path
+from typing import Sequence
+
+from .links import PathKind
+from .striping import (GRANULE_TOTAL, CollectiveOp, PathTimingReport, ShareDistribution,
+                       size_bucket)
+
+__all__ = ["FlexLinkError", "load_library", "Communicator", "Clique", "dtype_code",
+           "FLX_BUCKET_ALL", "tune_shares", "library_path"]
+
+FLX_BUCKET_ALL = -2
+_LIB_NAME = "libflexlink.so"
+_lib = None
+
+_RESULTS = {0: "success", 1: "unhandled cuda error", 2: "system error", 3: "internal error",
+            4: "invalid argument", 5: "invalid usage", 6: "remote error", 7: "in progress"}
+_OPS = {"sum": 0, "prod": 1, "max": 2, "min": 3}
+_COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1}
+
+
+class FlexLinkError(RuntimeError):
+    """A non-success ``flxResult_t``; ``code`` is the ncclResult_t-compatible value."""
+
+    def __init__(self, code: int, where: str, detail: str):
+        super().__init__(f"{where}: {_RESULTS.get(code, code)} ({detail})")
+        self.code = code
+
+
+class FlexLinkArgumentError(FlexLinkError, ValueError):
+    """flxInvalidArgument / flxInvalidUsage — maps to the reference's ValueError."""
+
+
+def library_path() -> Path:
+    override = os.environ.get("FLEXLINK_LIBRARY")
+    return Path(override) if override else Path(__file__).resolve().parent / _LIB_NAME
+
+
+class _UniqueId(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree ``libflexlink.so``; raise if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = library_path()
+    if not path.exists():
+        raise FlexLinkError(5, "load_library",
+                            f"{path} is missing; run `python -m paper_2510_15882_b200.build`")
+    L = ctypes.CDLL(str(path))
+    P, vp, sz, ci = ctypes.POINTER, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int
+    sig = {
+        "flxGetVersion": [P(ci)],
+        "flxGetUniqueId": [P(_UniqueId)],
+        "flxCommInitRank": [P(vp), ci, _UniqueId, ci],
+        "flxCommInitAll": [P(vp), ci, P(ci)],
+        "flxCommDestroy": [vp],
+        "flxCommCount": [vp, P(ci)],
+        "flxCommUserRank": [vp, P(ci)],
+        "flxCommCuDevice": [vp, P(ci)],
+        "flxAllReduce": [vp, vp, sz, ci, ci, vp, vp],
+        "flxAllGather": [vp, vp, sz, ci, vp, vp],
+        "flxGroupStart": [],
+        "flxGroupEnd": [],
+        "flxSetShares": [vp, ci, ci, P(ci)],
+        "flxGetShares": [vp, ci, ci, P(ci)],
+        "flxGetPathTimes": [vp, P(ctypes.c_float)],
+        "flxGetPathTimesHistory": [vp, ci, P(ctypes.c_float), P(ci)],
+        "flxGetPathBytes": [vp, P(sz)],
+        "flxGetAlignment": [vp, ci, P(sz)],
+        "flxSetNvlinkCtas": [vp, ci],
+        "flxSetStaging": [vp, sz, ci],
+        "flxGetPathMask": [vp, P(ci)],
+        "flxGetLaunchCount": [P(ctypes.c_ulonglong)],
+    }
+    for name, args in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = ci
+    L.flxGetErrorString.argtypes = [ci]
+    L.flxGetErrorString.restype = ctypes.c_char_p
+    L.flxGetLastError.argtypes = []
+    L.flxGetLastError.restype = ctypes.c_char_p
+    _lib = L
+    return L
+
+
+def _check(code: int, where: str) -> None:
+    if code != 0:
+        detail = load_library().flxGetLastError().decode(errors="replace")
+        cls = FlexLinkArgumentError if code in (4, 5) else FlexLinkError
+        raise cls(code, where, detail)
+
+
+def dtype_code(dtype) -> int:
+    """torch dtype -> flxDataType_t (== ncclDataType_t)."""
+    import torch
+
+    table = {torch.int8: 0, torch.uint8: 1, torch.int32: 2, torch.uint32: 3, torch.int64: 4,
+             torch.uint64: 5, torch.float16: 6, torch.float32: 7, torch.float64: 8,
+             torch.bfloat16: 9}
+    if dtype not in table:
+        raise ValueError(f"unsupported dtype {dtype}")
+    return table[dtype]
+
+
+def _stream_handle(stream) -> ctypes.c_void_p:
+    import torch
+
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _contiguous_cuda(t, what: str):
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous")
+    return t
+
+
+def _granule_array(shares) -> ctypes.Array:
+    if isinstance(shares, ShareDistribution):
+        g = shares.as_array()
+    elif isinstance(shares, dict):
+        g = [int(shares.get(k, 0)) for k in PathKind]
+    else:
+        g = list(shares)
+    return (ctypes.c_int * 3)(*g)
+
+
+class Communicator:
+    """One rank of a FlexLink communicator (owns an ``flxComm_t``)."""
+
+    def __init__(self, handle: int, clique: "Clique | None" = None):
+        self._h = ctypes.c_void_p(handle)
+        self.clique = clique
+        L = load_library()
+        v = ctypes.c_int()
+        _check(L.flxCommCount(self._h, ctypes.byref(v)), "flxCommCount")
+        self.nranks = v.value
+        _check(L.flxCommUserRank(self._h, ctypes.byref(v)), "flxCommUserRank")
+        self.rank = v.value
+        _check(L.flxCommCuDevice(self._h, ctypes.byref(v)), "flxCommCuDevice")
+        self.device = v.value
+
+    # ---- construction
+    @staticmethod
+    def unique_id() -> bytes:
+        uid = _UniqueId()
+        _check(load_library().flxGetUniqueId(ctypes.byref(uid)), "flxGetUniqueId")
+        return ctypes.string_at(ctypes.addressof(uid), 128)  # .internal stops at NUL
+
+    @classmethod
+    def init_rank(cls, nranks: int, unique_id: bytes, rank: int) -> "Communicator":
+        uid = _UniqueId()
+        if len(unique_id) != 128:
+            raise ValueError("a flxUniqueId is 128 bytes")
+        ctypes.memmove(ctypes.addressof(uid), unique_id, 128)
+        h = ctypes.c_void_p()
+        _check(load_library().flxCommInitRank(ctypes.byref(h), nranks, uid, rank),
+               "flxCommInitRank")
+        return cls(h.value)
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "Communicator":
+        """Bootstrap over torch.distributed (one process per GPU)."""
+        import torch.distributed as dist
+
+        box = [cls.unique_id() if dist.get_rank(group) == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return cls.init_rank(dist.get_world_size(group), box[0], dist.get_rank(group))
+
+    def destroy(self) -> None:
+        if self._h:
+            _check(load_library().flxCommDestroy(self._h), "flxCommDestroy")
+            self._h = ctypes.c_void_p()
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    # ---- collectives (ncclAllReduce / ncclAllGather shapes)
+    def all_reduce(self, send, recv=None, op: str = "sum", stream=None):
+        """Striped AllReduce; in place when ``recv`` is None or ``recv is send``."""
+        _contiguous_cuda(send, "send")
+        recv = send if recv is None else _contiguous_cuda(recv, "recv")
+        if recv.numel() != send.numel() or recv.dtype != send.dtype:
+            raise ValueError("recv must match send in size and dtype")
+        _check(load_library().flxAllReduce(
+            ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
+            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream)), "flxAllReduce")
+        return recv
+
+    def all_gather(self, send, recv, stream=None):
+        _contiguous_cuda(send, "send")
+        _contiguous_cuda(recv, "recv")
+        if recv.numel() != send.numel() * self.nranks or recv.dtype != send.dtype:
+            raise ValueError("recv must hold nranks * send.numel() elements of send.dtype")
+        _check(load_library().flxAllGather(
+            ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
+            dtype_code(send.dtype), self._h, _stream_handle(stream)), "flxAllGather")
+        return recv
+
+    # ---- balancer plumbing
+    def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
+        bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)
+        _check(load_library().flxSetShares(self._h, _COLL[CollectiveOp(op)], bucket,
+                                           _granule_array(shares)), "flxSetShares")
+
+    def get_shares(self, op: CollectiveOp, nbytes: int | None = None) -> ShareDistribution:
+        bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)
+        g = (ctypes.c_int * 3)()
+        _check(load_library().flxGetShares(self._h, _COLL[CollectiveOp(op)], bucket, g),
+               "flxGetShares")
+        return ShareDistribution({k: g[int(k)] for k in PathKind if g[int(k)] or k == 0})
+
+    def path_times(self) -> dict[PathKind, float]:
+        """Seconds from collective start to each path's completion (last call)."""
+        ms = (ctypes.c_float * 3)()
+        _check(load_library().flxGetPathTimes(self._h, ms), "flxGetPathTimes")
+        return {k: ms[int(k)] * 1e-3 for k in PathKind}
+
+    def path_times_history(self, max_calls: int = 64) -> list[dict[PathKind, float]]:
+        """Per-path seconds of the last ``max_calls`` calls (oldest first)."""
+        ms = (ctypes.c_float * (3 * max_calls))()
+        n = ctypes.c_int()
+        _check(load_library().flxGetPathTimesHistory(self._h, max_calls, ms, ctypes.byref(n)),
+               "flxGetPathTimesHistory")
+        return [{k: ms[3 * i + int(k)] * 1e-3 for k in PathKind} for i in range(n.value)]
+
+    def path_bytes(self) -> dict[PathKind, int]:
+        b = (ctypes.c_size_t * 3)()
+        _check(load_library().flxGetPathBytes(self._h, b), "flxGetPathBytes")
+        return {k: int(b[int(k)]) for k in PathKind}
+
+    def alignment(self, op: CollectiveOp) -> int:
+        a = ctypes.c_size_t()
+        _check(load_library().flxGetAlignment(self._h, _COLL[CollectiveOp(op)],
+                                              ctypes.byref(a)), "flxGetAlignment")
+        return a.value
+
+    def set_nvlink_ctas(self, n: int) -> None:
+        _check(load_library().flxSetNvlinkCtas(self._h, n), "flxSetNvlinkCtas")
+
+    def set_staging(self, chunk_bytes: int = 0, buffers: int = 2) -> None:
+        _check(load_library().flxSetStaging(self._h, chunk_bytes, buffers), "flxSetStaging")
+
+    def path_mask(self) -> int:
+        m = ctypes.c_int()
+        _check(load_library().flxGetPathMask(self._h, ctypes.byref(m)), "flxGetPathMask")
+        return m.value
+
+    def available_paths(self) -> tuple[PathKind, ...]:
+        m = self.path_mask()
+        return tuple(k for k in PathKind if m & (1 << int(k)))
+
+
+def launch_count() -> int:
+    c = ctypes.c_ulonglong()
+    _check(load_library().flxGetLaunchCount(ctypes.byref(c)), "flxGetLaunchCount")
+    return c.value
+
+
+class Clique:
+    """``nranks`` virtual ranks on one GPU (``flxCommInitAll`` with a repeated device).
+
+    Every collective takes one tensor per rank and is issued inside
+    ``flxGroupStart/End``, so the library runs it as a single fused launch —
+    the 1-GPU stand-in for an N-GPU NVSwitch collective.
+    """
+
+    def __init__(self, nranks: int, device: int = 0):
+        L = load_library()
+        handles = (ctypes.c_void_p * nranks)()
+        devs = (ctypes.c_int * nranks)(*([device] * nranks))
+        _check(L.flxCommInitAll(handles, nranks, devs), "flxCommInitAll")
+        self.comms = [Communicator(h, self) for h in handles]
+        self.nranks = nranks
+        self.device = device
+
+    def destroy(self) -> None:
+        for c in self.comms:
+            c.destroy()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+    def _group(self, issue) -> None:
+        L = load_library()
+        _check(L.flxGroupStart(), "flxGroupStart")
+        try:
+            for i, c in enumerate(self.comms):
+                issue(i, c)
+        finally:
+            _check(L.flxGroupEnd(), "flxGroupEnd")
+
+    def all_reduce(self, sends: Sequence, recvs: Sequence | None = None, op: str = "sum",
+                   stream=None):
+        recvs = list(sends) if recvs is None else list(recvs)
+        self._group(lambda i, c: c.all_reduce(sends[i], recvs[i], op=op, stream=stream))
+        return recvs
+
+    def all_gather(self, sends: Sequence, recvs: Sequence, stream=None):
+        self._group(lambda i, c: c.all_gather(sends[i], recvs[i], stream=stream))
+        return recvs
+
+    def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
+        for c in self.comms:
+            c.set_shares(op, shares, nbytes)
+
+    def set_nvlink_ctas(self, n: int) -> None:
+        for c in self.comms:
+            c.set_nvlink_ctas(n)
+
+    def set_staging(self, chunk_bytes: int = 0, buffers: int = 2) -> None:
+        for c in self.comms:
+            c.set_staging(chunk_bytes, buffers)
+
+    def path_times(self) -> dict[PathKind, float]:
+        return self.comms[0].path_times()
+
+    def path_bytes(self) -> dict[PathKind, int]:
+        return self.comms[0].path_bytes()
+
+    def report(self, op: CollectiveOp, nbytes: int, paths=None) -> PathTimingReport:
+        """PathTimingReport of the last call: paths that carried bytes (or ``paths``)."""
+        t, b = self.path_times(), self.path_bytes()
+        keep = [k for k in PathKind if b[k] > 0] if paths is None else sorted(paths)
+        return PathTimingReport.build(CollectiveOp(op), self.nranks, nbytes,
+                                      {k: t[k] for k in keep if b[k] > 0})
+
+    def measure_fn(self, op: CollectiveOp, sends, recvs, warmup: int = 2, repeats: int = 5,
+                   reduce_op: str = "sum"):
+        """A Stage-1 ``MeasureFn``: run the real collective with ``state.shares``.
+
+        Per-path durations are medians over ``repeats`` calls; paths that
+        carried no bytes (alignment floor) are left out of the report so the
+        tuner treats them as idle.
+        """
+        import torch
+
+        op = CollectiveOp(op)
+        nbytes = sends[0].numel() * sends[0].element_size()
+
+        def run():
+            if op == CollectiveOp.ALLREDUCE:
+                self.all_reduce(sends, recvs, op=reduce_op)
+            else:
+                self.all_gather(sends, recvs)
+
+        def measure(state) -> PathTimingReport:
+            self.set_shares(op, state.shares, nbytes)
+            for _ in range(warmup):
+                run()
+            samples: dict[PathKind, list[float]] = {}
+            for _ in range(repeats):
+                run()
+                t, b = self.path_times(), self.path_bytes()
+                for k in state.active:
+                    if b[k] > 0:
+                        samples.setdefault(k, []).append(t[k])
+            torch.cuda.synchronize()
+            durations = {k: statistics.median(v) for k, v in samples.items()}
+            return PathTimingReport.build(op, self.nranks, nbytes, durations)
+
+        return measure
+
+
+def tune_shares(clique: Clique, topo, op: CollectiveOp, sends, recvs, config=None,
+                warmup: int = 2, repeats: int = 5, reduce_op: str = "sum"):
+    """Stage 1 on the real path, guarded, installed for this size bucket.
+
+    Runs ``initial_tune(topo, spec, measure=clique.measure_fn(...))`` restricted
+    to the paths the box has, then compares the tuned split with NVLink-only on
+    the same measurement; keeps NVLink-only if the striped split is not faster
+    (Stage 1 converges on imbalance, not on total time).
+    Returns ``(shares, trace, tuned_total_s, nvlink_only_total_s)``.
+    """
+    from .stage1 import TunerConfig, TunerState, initial_tune
+    from .striping import CollectiveSpec
+
+    op = CollectiveOp(op)
+    nbytes = sends[0].numel() * sends[0].element_size()
+    avail = set(clique.comms[0].available_paths())
+    paths = tuple(k for k in topo.present_paths if k in avail)
+    spec = CollectiveSpec(op, max(2, clique.nranks), nbytes)
+    measure = clique.measure_fn(op, sends, recvs, warmup, repeats, reduce_op)
+    shares, trace = initial_tune(topo, spec, config or TunerConfig(), measure=measure,
+                                 paths=paths)
+    only_nv = ShareDistribution({PathKind.NVLINK: GRANULE_TOTAL})
+    base = measure(TunerState(shares=only_nv, active=frozenset({PathKind.NVLINK}), step=1)).total
+    tuned = measure(TunerState(shares=shares, active=frozenset(shares.loaded_paths),
+                               step=1)).total
+    if tuned >= base:
+        shares = only_nv
+    clique.set_shares(op, shares, nbytes)
+    return shares, trace, tuned, base

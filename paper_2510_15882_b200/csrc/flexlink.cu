@@ -1,0 +1,688 @@
+// libflexlink.so — C-ABI, communicators, groups, and the striped executor.
+//
+// One collective call = partition the message by the comm's granule shares
+// (collectives.py:93-114), then run every path's slice concurrently:
+//   NVLink slice : one fused kernel on the caller's stream (kernels.cuh)
+//   PCIe slice   : chunked D2H -> pinned host -> H2D ring on two side streams
+//                  gated by monotone counter semaphores (staging.py:176-188),
+//                  reduce-on-receive kernel on the consumer stream
+// and record per-path CUDA events so flxGetPathTimes can hand the balancer a
+// PathTimingReport (collectives.py:117-133).
+#include <dlfcn.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <random>
+
+#include "internal.h"
+#include "args.h"
+
+namespace flx {
+
+// ------------------------------------------------------------------ errors
+namespace {
+thread_local std::string t_last_error = "no error";
+}
+
+flxResult_t fail(flxResult_t code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_last_error = buf;
+  if (getenv("FLX_DEBUG")) fprintf(stderr, "[flexlink] error %d: %s\n", (int)code, buf);
+  return code;
+}
+
+// --------------------------------------------------------- driver memops
+const MemOps& memops() {
+  static MemOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* w = nullptr;
+    void* x = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &w, cudaEnableDefault, &q1) ==
+            cudaSuccess &&
+        cudaGetDriverEntryPoint("cuStreamWriteValue32", &x, cudaEnableDefault, &q2) ==
+            cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+      ops.wait32 = reinterpret_cast<decltype(ops.wait32)>(w);
+      ops.write32 = reinterpret_cast<decltype(ops.write32)>(x);
+      ops.ok = true;
+    }
+  });
+  return ops;
+}
+
+// Counter semaphores on pinned host words.  GEQ is the cyclic 32-bit
+// comparison ((int32)(*addr - value) >= 0), so monotone counters may wrap.
+flxResult_t sem_wait_geq(cudaStream_t s, uint32_t* word, uint32_t value) {
+  const MemOps& m = memops();
+  if (!m.ok) return fail(flxInternalError, "stream memory operations unavailable");
+  CUresult r = m.wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(word),
+                        value, CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(flxUnhandledCudaError, "cuStreamWaitValue32: %d", (int)r);
+  return flxSuccess;
+}
+
+flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value) {
+  const MemOps& m = memops();
+  if (!m.ok) return fail(flxInternalError, "stream memory operations unavailable");
+  CUresult r = m.write32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(word),
+                         value, CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(flxUnhandledCudaError, "cuStreamWriteValue32: %d", (int)r);
+  return flxSuccess;
+}
+
+size_t dtype_size(int dtype) {
+  switch (dtype) {
+    case flxInt8: case flxUint8: return 1;
+    case flxFloat16: case flxBfloat16: return 2;
+    case flxInt32: case flxUint32: case flxFloat32: return 4;
+    case flxInt64: case flxUint64: case flxFloat64: return 8;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------- shares
+int size_bucket(size_t bytes) {
+  if (bytes == 0) return -1;
+  return 63 - __builtin_clzll((unsigned long long)bytes);
+}
+
+Granules ShareTable::lookup(int op, size_t bytes) const {
+  auto it = entries.find({op, size_bucket(bytes)});
+  return it == entries.end() ? fallback : it->second;
+}
+
+std::array<size_t, FLX_NUM_PATHS> partition(size_t bytes, const Granules& g, size_t alignment) {
+  std::array<size_t, FLX_NUM_PATHS> out{{0, 0, 0}};
+  long long denom = 0;
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) denom += g[p];
+  size_t used = 0;
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) {
+    const unsigned __int128 raw =
+        denom ? (unsigned __int128)bytes * (unsigned)g[p] / (unsigned long long)denom : 0;
+    out[p] = (size_t)raw / alignment * alignment;
+    used += out[p];
+  }
+  out[flxPathNvlink] += bytes - used;
+  return out;
+}
+
+// ------------------------------------------------------------- registry
+namespace {
+
+std::mutex g_mutex;
+
+size_t allreduce_alignment(int nranks) { return (size_t)nranks * 4096; }
+constexpr size_t kAllGatherAlignment = 4096;
+
+size_t alignment_for(const Comm* c, int coll) {
+  return coll == flxCollAllReduce ? allreduce_alignment(c->nranks) : kAllGatherAlignment;
+}
+
+int path_mask() {
+  int mask = 1 << flxPathNvlink;
+  if (memops().ok) mask |= 1 << flxPathPcie;
+  // RDMA NIC loopback needs ibverbs (rdma-core); not built in this image.
+  return mask;
+}
+
+flxResult_t validate_comm(const flxComm* comm) {
+  if (comm == nullptr) return fail(flxInvalidArgument, "null communicator");
+  return flxSuccess;
+}
+
+flxResult_t clique_create(int device, int members, Clique** out) {
+  FLX_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  FLX_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(flxInvalidUsage, "device %d is sm_%d%d; this build targets sm_100a", device,
+                prop.major, prop.minor);
+  auto* c = new Clique();
+  c->device = device;
+  c->sm_count = prop.multiProcessorCount;
+  FLX_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+  FLX_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  for (auto& t : c->timing) {
+    FLX_CUDA(cudaEventCreate(&t.start));
+    FLX_CUDA(cudaEventCreate(&t.nv));
+    FLX_CUDA(cudaEventCreate(&t.pcie));
+  }
+  FLX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  c->ev_fork.resize(members);
+  for (auto& e : c->ev_fork) FLX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // semaphore words: [0,B) semFull, [B,2B) semEmpty; start at zero (staging.py:224-225)
+  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->sems), 4096,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  memset(c->sems, 0, 4096);
+  *out = c;
+  return flxSuccess;
+}
+
+flxResult_t clique_destroy(Clique* c) {
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->d2h);
+  cudaStreamSynchronize(c->h2d);
+  cudaStreamDestroy(c->d2h);
+  cudaStreamDestroy(c->h2d);
+  for (auto& t : c->timing) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.nv);
+    cudaEventDestroy(t.pcie);
+  }
+  cudaEventDestroy(c->ev_join);
+  for (auto e : c->ev_fork) cudaEventDestroy(e);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
+  if (c->dev_stage) cudaFree(c->dev_stage);
+  if (c->sems) cudaFreeHost(c->sems);
+  delete c;
+  return flxSuccess;
+}
+
+// Grow the staging ring to hold `chunk` bytes per member in `bufs` buffers.
+// Only called after the side streams have drained (the ring may be in use).
+flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
+  if (c->stage_cap >= chunk && c->stage_bufs == bufs) return flxSuccess;
+  FLX_CUDA(cudaStreamSynchronize(c->d2h));
+  FLX_CUDA(cudaStreamSynchronize(c->h2d));
+  if (c->host_stage) FLX_CUDA(cudaFreeHost(c->host_stage));
+  if (c->dev_stage) FLX_CUDA(cudaFree(c->dev_stage));
+  c->host_stage = nullptr;
+  c->dev_stage = nullptr;
+  const size_t cap = std::max(chunk, c->stage_cap);
+  const size_t total = cap * c->members.size() * bufs;
+  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_stage), total, cudaHostAllocPortable));
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dev_stage), total));
+  // a fresh ring starts a fresh protocol epoch: counters restart from zero
+  memset(c->sems, 0, 4096);
+  c->piece_seq = 0;
+  c->stage_cap = cap;
+  c->stage_bufs = bufs;
+  return flxSuccess;
+}
+
+// Chunk size per member for a PCIe slice of `bytes` per rank: the configured
+// value, or ~8 pipeline stages, 64 KiB..4 MiB, 4 KiB multiples.
+size_t pick_chunk(const Comm* lead, size_t bytes) {
+  size_t chunk = lead->chunk_bytes;
+  if (chunk == 0) {
+    chunk = (bytes / 8 + 4095) / 4096 * 4096;
+    chunk = std::min<size_t>(std::max<size_t>(chunk, 64 << 10), 4 << 20);
+  }
+  return chunk;
+}
+
+// ---------------------------------------------------------------- groups
+struct Call {
+  Comm* comm;
+  int coll;  // flxCollOp_t
+  const void* send;
+  void* recv;
+  size_t count;
+  int dtype;
+  int op;
+  cudaStream_t stream;
+};
+
+thread_local int t_group_depth = 0;
+thread_local std::vector<Call> t_pending;
+
+// One collective over all members of a clique.  calls[i] belongs to member i.
+flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
+  const int n = (int)c->members.size();
+  const Call& head = calls[0];
+  const Comm* lead = head.comm;
+  for (int i = 1; i < n; ++i) {
+    const Call& k = calls[i];
+    if (k.coll != head.coll || k.count != head.count || k.dtype != head.dtype ||
+        k.op != head.op)
+      return fail(flxInvalidUsage, "rank %d called a different collective than rank 0", i);
+    const Comm* m = k.comm;
+    if (m->nvlink_ctas != lead->nvlink_ctas || m->chunk_bytes != lead->chunk_bytes ||
+        m->buffers != lead->buffers)
+      return fail(flxInvalidUsage, "rank %d path configuration differs from rank 0", i);
+  }
+  FLX_CUDA(cudaSetDevice(c->device));
+  const size_t esz = dtype_size(head.dtype);
+  const size_t bytes = head.count * esz;  // per-rank send bytes
+  const Granules g = lead->shares[head.coll].lookup(head.coll, bytes);
+  for (int i = 1; i < n; ++i)
+    if (calls[i].comm->shares[head.coll].lookup(head.coll, bytes) != g)
+      return fail(flxInvalidUsage, "rank %d has different shares than rank 0", i);
+  auto split = partition(bytes, g, alignment_for(lead, head.coll));
+  if (split[flxPathRdma] > 0)
+    return fail(flxInvalidUsage, "rdma path is not available on this box");
+  if (split[flxPathPcie] > 0 && !(path_mask() & (1 << flxPathPcie)))
+    return fail(flxInvalidUsage, "pcie path is not available (no stream memory ops)");
+
+  // fork: every member's stream joins the lead stream
+  cudaStream_t s0 = head.stream;
+  for (int i = 1; i < n; ++i) {
+    if (calls[i].stream == s0) continue;
+    FLX_CUDA(cudaEventRecord(c->ev_fork[i], calls[i].stream));
+    FLX_CUDA(cudaStreamWaitEvent(s0, c->ev_fork[i], 0));
+  }
+  Clique::Timing& tm = c->timing[c->calls % Clique::kTimingSlots];
+  FLX_CUDA(cudaEventRecord(tm.start, s0));
+
+  const size_t nv = split[flxPathNvlink];
+  const size_t pc = split[flxPathPcie];
+  const int grid_nv = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count;
+  const bool gather = head.coll == flxCollAllGather;
+
+  // ---- PCIe slice: issue the side-stream pipeline first so its copies start
+  // while the NVLink kernel runs.
+  if (pc > 0) {
+    const size_t chunk = pick_chunk(lead, pc);
+    FLX_TRY(ensure_staging(c, chunk, lead->buffers));
+    const int bufs = c->stage_bufs;
+    const size_t pitch = c->stage_cap;
+    const size_t slot_bytes = pitch * n;
+    FLX_CUDA(cudaStreamWaitEvent(c->d2h, tm.start, 0));
+    FLX_CUDA(cudaStreamWaitEvent(c->h2d, tm.start, 0));
+    for (size_t done = 0; done < pc; done += chunk) {
+      const size_t len = std::min(chunk, pc - done);
+      const size_t at = nv + done;  // byte offset inside each rank's message
+      const uint64_t piece = c->piece_seq++;
+      const int buf = (int)(piece % bufs);
+      const uint32_t lap = (uint32_t)(piece / bufs);
+      uint32_t* sem_full = c->sems + buf;
+      uint32_t* sem_empty = c->sems + bufs + buf;
+      char* host = c->host_stage + buf * slot_bytes;
+      char* dev = c->dev_stage + buf * slot_bytes;
+      // producer: wait slot drained, D2H each rank's piece, mark full
+      FLX_TRY(sem_wait_geq(c->d2h, sem_empty, lap));
+      for (int i = 0; i < n; ++i)
+        FLX_CUDA(cudaMemcpyAsync(host + i * pitch, static_cast<const char*>(calls[i].send) + at,
+                                 len, cudaMemcpyDeviceToHost, c->d2h));
+      FLX_TRY(sem_write(c->d2h, sem_full, lap + 1));
+      // consumer: wait full, H2D the whole slot, mark empty, reduce-on-receive
+      FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
+      FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, n, cudaMemcpyHostToDevice, c->h2d));
+      FLX_TRY(sem_write(c->h2d, sem_empty, lap + 1));
+      if (gather) {
+        FanoutArgs a{};
+        for (int i = 0; i < n; ++i) {
+          a.src[i] = dev + i * pitch;
+          a.dst[i] = static_cast<char*>(calls[i].recv) + at;
+        }
+        a.nsrc = a.ndst = n;
+        a.bytes = len;
+        a.dst_stride = bytes;
+        FLX_CUDA(launch_fanout(a, 4, c->h2d));
+      } else {
+        FoldArgs a{};
+        for (int i = 0; i < n; ++i) {
+          a.src[i] = dev + i * pitch;
+          a.dst[i] = static_cast<char*>(calls[i].recv) + at;
+        }
+        a.n = a.ndst = n;
+        a.bytes = len;
+        FLX_CUDA(launch_fold(head.dtype, head.op, a, 8, c->h2d));
+      }
+    }
+    FLX_CUDA(cudaEventRecord(tm.pcie, c->h2d));
+  }
+
+  // ---- NVLink slice: one fused kernel over all members on the lead stream
+  if (nv > 0) {
+    if (gather) {
+      FanoutArgs a{};
+      for (int i = 0; i < n; ++i) {
+        a.src[i] = static_cast<const char*>(calls[i].send);
+        a.dst[i] = static_cast<char*>(calls[i].recv);
+      }
+      a.nsrc = a.ndst = n;
+      a.bytes = nv;
+      a.dst_stride = bytes;
+      const int gx = std::max(1, grid_nv / n);
+      FLX_CUDA(launch_fanout(a, gx, s0));
+    } else {
+      FoldArgs a{};
+      for (int i = 0; i < n; ++i) {
+        a.src[i] = static_cast<const char*>(calls[i].send);
+        a.dst[i] = static_cast<char*>(calls[i].recv);
+      }
+      a.n = a.ndst = n;
+      a.bytes = nv;
+      FLX_CUDA(launch_fold(head.dtype, head.op, a, grid_nv, s0));
+    }
+  }
+  FLX_CUDA(cudaEventRecord(tm.nv, s0));
+  if (pc > 0) FLX_CUDA(cudaStreamWaitEvent(s0, tm.pcie, 0));
+
+  // join: every member's stream waits for the collective
+  bool joined = false;
+  for (int i = 1; i < n; ++i) {
+    if (calls[i].stream == s0) continue;
+    if (!joined) {
+      FLX_CUDA(cudaEventRecord(c->ev_join, s0));
+      joined = true;
+    }
+    FLX_CUDA(cudaStreamWaitEvent(calls[i].stream, c->ev_join, 0));
+  }
+  c->last_bytes = split;
+  tm.used[flxPathNvlink] = nv > 0;
+  tm.used[flxPathPcie] = pc > 0;
+  tm.used[flxPathRdma] = false;
+  c->calls++;
+  return flxSuccess;
+}
+
+flxResult_t flush_group() {
+  std::vector<Call> calls;
+  calls.swap(t_pending);
+  // bucket calls by clique, preserving per-member order
+  std::map<Clique*, std::vector<std::vector<Call>>> by_clique;
+  for (const Call& k : calls) {
+    Clique* c = k.comm->clique;
+    auto& per = by_clique[c];
+    if (per.empty()) per.resize(c->members.size());
+    per[k.comm->rank - 0].push_back(k);
+  }
+  for (auto& [clique, per] : by_clique) {
+    const size_t rounds = per[0].size();
+    for (size_t i = 0; i < per.size(); ++i)
+      if (per[i].size() != rounds)
+        return fail(flxInvalidUsage,
+                    "group issued %zu collectives on rank 0 but %zu on rank %zu of the same "
+                    "device; every virtual rank must take part",
+                    rounds, per[i].size(), i);
+    for (size_t k = 0; k < rounds; ++k) {
+      std::vector<Call> one;
+      for (auto& v : per) one.push_back(v[k]);
+      FLX_TRY(run_clique(clique, one));
+    }
+  }
+  return flxSuccess;
+}
+
+flxResult_t enqueue(const Call& k) {
+  t_pending.push_back(k);
+  if (t_group_depth > 0) return flxSuccess;
+  return flush_group();
+}
+
+// Per-path ms of call number `seq` (must still be in the ring); blocks on it.
+flxResult_t read_timing(Clique* c, uint64_t seq, float ms[3]) {
+  const Clique::Timing& t = c->timing[seq % Clique::kTimingSlots];
+  FLX_CUDA(cudaSetDevice(c->device));
+  ms[0] = ms[1] = ms[2] = 0.f;
+  FLX_CUDA(cudaEventSynchronize(t.nv));
+  if (t.used[flxPathNvlink]) FLX_CUDA(cudaEventElapsedTime(&ms[0], t.start, t.nv));
+  if (t.used[flxPathPcie]) {
+    FLX_CUDA(cudaEventSynchronize(t.pcie));
+    FLX_CUDA(cudaEventElapsedTime(&ms[1], t.start, t.pcie));
+  }
+  return flxSuccess;
+}
+
+flxResult_t check_call(const flxComm* comm, int dtype, int op, bool reduce) {
+  FLX_TRY(validate_comm(comm));
+  if (dtype < 0 || dtype >= flxNumTypes) return fail(flxInvalidArgument, "bad datatype %d", dtype);
+  if (reduce && (op < 0 || op >= flxNumOps))
+    return fail(flxInvalidArgument, "unsupported reduction op %d", op);
+  return flxSuccess;
+}
+
+}  // namespace
+}  // namespace flx
+
+using namespace flx;
+
+struct flxComm : public flx::Comm {};
+
+// ====================================================================== ABI
+extern "C" {
+
+flxResult_t flxGetVersion(int* version) {
+  if (!version) return fail(flxInvalidArgument, "null version pointer");
+  *version = FLX_VERSION_CODE;
+  return flxSuccess;
+}
+
+const char* flxGetErrorString(flxResult_t r) {
+  switch (r) {
+    case flxSuccess: return "no error";
+    case flxUnhandledCudaError: return "unhandled cuda error";
+    case flxSystemError: return "unhandled system error";
+    case flxInternalError: return "internal error";
+    case flxInvalidArgument: return "invalid argument";
+    case flxInvalidUsage: return "invalid usage";
+    case flxRemoteError: return "remote process exited or there was a network error";
+    case flxInProgress: return "operation in progress";
+  }
+  return "unknown result code";
+}
+
+const char* flxGetLastError(void) { return t_last_error.c_str(); }
+
+flxResult_t flxGetUniqueId(flxUniqueId* id) {
+  if (!id) return fail(flxInvalidArgument, "null id");
+  memset(id, 0, sizeof(*id));
+  std::random_device rd;
+  uint64_t words[4] = {0x31584c46ull /* "FLX1" */, ((uint64_t)rd() << 32) | rd(),
+                       ((uint64_t)rd() << 32) | rd(), (uint64_t)getpid()};
+  memcpy(id->internal, words, sizeof(words));
+  return flxSuccess;
+}
+
+flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
+  if (!comms || ndev < 1) return fail(flxInvalidArgument, "bad comms/ndev");
+  int visible = 0;
+  FLX_CUDA(cudaGetDeviceCount(&visible));
+  std::vector<int> devs(ndev);
+  for (int i = 0; i < ndev; ++i) {
+    devs[i] = devlist ? devlist[i] : i;
+    if (devs[i] < 0 || devs[i] >= visible)
+      return fail(flxInvalidArgument, "device %d not visible (%d devices)", devs[i], visible);
+  }
+  std::map<int, int> per_device;
+  for (int d : devs) per_device[d]++;
+  if (per_device.size() > 1)
+    return fail(flxInvalidUsage,
+                "flxCommInitAll over distinct devices needs the peer-mapped multi-GPU "
+                "path; use one process per GPU with flxCommInitRank");
+  if (ndev > FLX_MAX_VIRTUAL_RANKS)
+    return fail(flxInvalidArgument, "at most %d virtual ranks per device", FLX_MAX_VIRTUAL_RANKS);
+  std::lock_guard<std::mutex> lock(g_mutex);
+  Clique* c = nullptr;
+  FLX_TRY(clique_create(devs[0], ndev, &c));
+  for (int i = 0; i < ndev; ++i) {
+    auto* comm = new flxComm();
+    comm->rank = i;
+    comm->nranks = ndev;
+    comm->device = devs[i];
+    comm->clique = c;
+    c->members.push_back(comm);
+    comms[i] = comm;
+  }
+  return flxSuccess;
+}
+
+flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int rank) {
+  if (!comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(flxInvalidArgument, "bad comm/nranks/rank");
+  uint64_t magic;
+  memcpy(&magic, id.internal, sizeof(magic));
+  if (magic != 0x31584c46ull) return fail(flxInvalidArgument, "not a flxUniqueId");
+  if (nranks > 1)
+    return fail(flxInvalidUsage, "multi-process communicators are not built into this library");
+  int dev = 0;
+  FLX_CUDA(cudaGetDevice(&dev));
+  return flxCommInitAll(comm, 1, &dev);
+}
+
+flxResult_t flxCommDestroy(flxComm_t comm) {
+  FLX_TRY(validate_comm(comm));
+  std::lock_guard<std::mutex> lock(g_mutex);
+  Clique* c = comm->clique;
+  c->destroyed++;
+  if (c->destroyed == (int)c->members.size()) {
+    for (Comm* m : c->members) delete static_cast<flxComm*>(m);
+    clique_destroy(c);
+  }
+  return flxSuccess;
+}
+
+flxResult_t flxCommCount(const flxComm_t comm, int* count) {
+  FLX_TRY(validate_comm(comm));
+  if (!count) return fail(flxInvalidArgument, "null count");
+  *count = comm->nranks;
+  return flxSuccess;
+}
+
+flxResult_t flxCommUserRank(const flxComm_t comm, int* rank) {
+  FLX_TRY(validate_comm(comm));
+  if (!rank) return fail(flxInvalidArgument, "null rank");
+  *rank = comm->rank;
+  return flxSuccess;
+}
+
+flxResult_t flxCommCuDevice(const flxComm_t comm, int* device) {
+  FLX_TRY(validate_comm(comm));
+  if (!device) return fail(flxInvalidArgument, "null device");
+  *device = comm->device;
+  return flxSuccess;
+}
+
+flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
+                         flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
+                         cudaStream_t stream) {
+  FLX_TRY(check_call(comm, datatype, op, true));
+  if (count > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
+  return enqueue(Call{comm, flxCollAllReduce, sendbuff, recvbuff, count, datatype, op, stream});
+}
+
+flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
+                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream) {
+  FLX_TRY(check_call(comm, datatype, 0, false));
+  if (sendcount > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
+  return enqueue(Call{comm, flxCollAllGather, sendbuff, recvbuff, sendcount, datatype, 0, stream});
+}
+
+flxResult_t flxGroupStart(void) {
+  ++t_group_depth;
+  return flxSuccess;
+}
+
+flxResult_t flxGroupEnd(void) {
+  if (t_group_depth <= 0) return fail(flxInvalidUsage, "flxGroupEnd without flxGroupStart");
+  if (--t_group_depth > 0) return flxSuccess;
+  return flush_group();
+}
+
+flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]) {
+  FLX_TRY(validate_comm(comm));
+  if (op != flxCollAllReduce && op != flxCollAllGather)
+    return fail(flxInvalidArgument, "bad collective op %d", (int)op);
+  if (!granules) return fail(flxInvalidArgument, "null granules");
+  Granules g{{granules[0], granules[1], granules[2]}};
+  int sum = 0;
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) {
+    if (g[p] < 0) return fail(flxInvalidArgument, "negative share on path %d", p);
+    sum += g[p];
+  }
+  if (sum != FLX_GRANULE_TOTAL)
+    return fail(flxInvalidArgument, "shares sum to %d, expected %d", sum, FLX_GRANULE_TOTAL);
+  const int mask = path_mask();
+  for (int p = 1; p < FLX_NUM_PATHS; ++p)
+    if (g[p] > 0 && !(mask & (1 << p)))
+      return fail(flxInvalidArgument, "path %d is not available on this box", p);
+  ShareTable& t = comm->shares[op];
+  if (bucket == FLX_BUCKET_ALL) {
+    t.fallback = g;
+    t.entries.clear();
+  } else {
+    if (bucket < -1 || bucket > 63) return fail(flxInvalidArgument, "bad bucket %d", bucket);
+    t.entries[{(int)op, bucket}] = g;
+  }
+  return flxSuccess;
+}
+
+flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granules[3]) {
+  FLX_TRY(validate_comm(comm));
+  if (op != flxCollAllReduce && op != flxCollAllGather)
+    return fail(flxInvalidArgument, "bad collective op %d", (int)op);
+  if (!granules) return fail(flxInvalidArgument, "null granules");
+  const ShareTable& t = comm->shares[op];
+  Granules g = t.fallback;
+  auto it = t.entries.find({(int)op, bucket});
+  if (bucket != FLX_BUCKET_ALL && it != t.entries.end()) g = it->second;
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) granules[p] = g[p];
+  return flxSuccess;
+}
+
+flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]) {
+  FLX_TRY(validate_comm(comm));
+  if (!ms) return fail(flxInvalidArgument, "null ms");
+  Clique* c = comm->clique;
+  if (c->calls == 0) return fail(flxInvalidUsage, "no collective has run on this comm");
+  return read_timing(c, c->calls - 1, ms);
+}
+
+flxResult_t flxGetPathTimesHistory(flxComm_t comm, int max_calls, float* ms, int* n_out) {
+  FLX_TRY(validate_comm(comm));
+  if (!ms || !n_out || max_calls < 0) return fail(flxInvalidArgument, "bad history arguments");
+  Clique* c = comm->clique;
+  const uint64_t avail = std::min<uint64_t>(c->calls, Clique::kTimingSlots);
+  const uint64_t n = std::min<uint64_t>(avail, (uint64_t)max_calls);
+  for (uint64_t i = 0; i < n; ++i) FLX_TRY(read_timing(c, c->calls - n + i, ms + 3 * i));
+  *n_out = (int)n;
+  return flxSuccess;
+}
+
+flxResult_t flxGetPathBytes(flxComm_t comm, size_t bytes[3]) {
+  FLX_TRY(validate_comm(comm));
+  if (!bytes) return fail(flxInvalidArgument, "null bytes");
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) bytes[p] = comm->clique->last_bytes[p];
+  return flxSuccess;
+}
+
+flxResult_t flxGetAlignment(flxComm_t comm, flxCollOp_t op, size_t* alignment) {
+  FLX_TRY(validate_comm(comm));
+  if (!alignment) return fail(flxInvalidArgument, "null alignment");
+  *alignment = alignment_for(comm, op);
+  return flxSuccess;
+}
+
+flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
+  FLX_TRY(validate_comm(comm));
+  if (nctas < 0 || nctas > 65535) return fail(flxInvalidArgument, "bad nctas %d", nctas);
+  comm->nvlink_ctas = nctas;
+  return flxSuccess;
+}
+
+flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers) {
+  FLX_TRY(validate_comm(comm));
+  if (buffers != 1 && buffers != 2)
+    return fail(flxInvalidArgument, "buffers must be 1 or 2 (staging.py:41-42)");
+  if (chunk_bytes % 4096) return fail(flxInvalidArgument, "chunk_bytes must be a multiple of 4096");
+  comm->chunk_bytes = chunk_bytes;
+  comm->buffers = buffers;
+  return flxSuccess;
+}
+
+flxResult_t flxGetPathMask(flxComm_t comm, int* mask) {
+  FLX_TRY(validate_comm(comm));
+  if (!mask) return fail(flxInvalidArgument, "null mask");
+  *mask = path_mask();
+  return flxSuccess;
+}
+
+flxResult_t flxGetLaunchCount(unsigned long long* count) {
+  if (!count) return fail(flxInvalidArgument, "null count");
+  *count = g_launches.load();
+  return flxSuccess;
+}
+
+}  // extern "C"

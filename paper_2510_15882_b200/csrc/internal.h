@@ -1,0 +1,108 @@
+// Host-side internals shared by the translation units of libflexlink.so.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <array>
+#include <atomic>
+#include <cstdarg>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/flexlink.h"
+
+namespace flx {
+
+struct FoldArgs;
+struct FanoutArgs;
+cudaError_t launch_fold(int dtype, int op, const FoldArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s);
+extern std::atomic<unsigned long long> g_launches;
+
+// ---- errors
+flxResult_t fail(flxResult_t code, const char* fmt, ...) __attribute__((format(printf, 2, 3)));
+
+#define FLX_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return ::flx::fail(flxUnhandledCudaError, "%s: %s (%s:%d)", #call,                  \
+                         cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define FLX_TRY(call)                  \
+  do {                                 \
+    flxResult_t r_ = (call);           \
+    if (r_ != flxSuccess) return r_;   \
+  } while (0)
+
+// ---- driver stream memory ops (resolved at run time; no -lcuda)
+struct MemOps {
+  CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+  bool ok = false;
+};
+const MemOps& memops();
+flxResult_t sem_wait_geq(cudaStream_t s, uint32_t* word, uint32_t value);
+flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value);
+
+size_t dtype_size(int dtype);
+
+// ---- share table (ShareTable, collectives.py:189-204)
+using Granules = std::array<int, FLX_NUM_PATHS>;
+struct ShareTable {
+  Granules fallback{{FLX_GRANULE_TOTAL, 0, 0}};
+  std::map<std::pair<int, int>, Granules> entries;  // (op, bucket) -> granules
+  Granules lookup(int op, size_t bytes) const;
+};
+int size_bucket(size_t bytes);
+// partition (collectives.py:93-114): per-path bytes, floored to alignment,
+// remainder to NVLink.
+std::array<size_t, FLX_NUM_PATHS> partition(size_t bytes, const Granules& g, size_t alignment);
+
+struct Comm;
+
+// Ranks living in this process on one device.  With virtual ranks (repeated
+// device in flxCommInitAll) there are several members and every collective is
+// a single fused launch over all of them.
+struct Clique {
+  int device = 0;
+  int sm_count = 0;
+  std::vector<Comm*> members;  // index = position in clique == rank
+  cudaStream_t d2h = nullptr;  // PCIe path: producer copies
+  cudaStream_t h2d = nullptr;  // PCIe path: consumer copies + reduce-on-receive
+  // per-call timing ring: call k uses slot k % kTimingSlots
+  static constexpr int kTimingSlots = 64;
+  struct Timing {
+    cudaEvent_t start = nullptr, nv = nullptr, pcie = nullptr;
+    bool used[FLX_NUM_PATHS] = {false, false, false};
+  };
+  Timing timing[kTimingSlots];
+  uint64_t calls = 0;  // collectives issued on this clique
+  cudaEvent_t ev_join = nullptr;
+  std::vector<cudaEvent_t> ev_fork;
+  // host-staged ring: buffers x members x chunk_cap bytes, pinned + device
+  char* host_stage = nullptr;
+  char* dev_stage = nullptr;
+  uint32_t* sems = nullptr;  // [0..B) semFull, [B..2B) semEmpty (pinned, mapped)
+  size_t stage_cap = 0;      // chunk capacity per member
+  int stage_bufs = 0;
+  uint64_t piece_seq = 0;    // monotone chunk counter -> counter semaphores
+  std::array<size_t, FLX_NUM_PATHS> last_bytes{{0, 0, 0}};
+  int destroyed = 0;
+};
+
+struct Comm {
+  int rank = 0;
+  int nranks = 1;
+  int device = 0;
+  Clique* clique = nullptr;
+  ShareTable shares[2];  // per flxCollOp_t
+  int nvlink_ctas = 0;   // 0 = auto
+  size_t chunk_bytes = 0;  // 0 = auto
+  int buffers = 2;
+};
+
+}  // namespace flx

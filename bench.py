@@ -27,7 +27,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import threading
 import time
@@ -52,61 +51,70 @@ def busbw_allgather(out_bytes: int, seconds: float, n: int) -> float:
 
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle reasons polled through NVML during the timed region
+    (the B200_PROFILING.md clocks line, without nvidia-smi's startup latency)."""
 
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
 
-    def __init__(self, index: int = 0):
-        self.index = index
-        self.rows: list[list[str]] = []
-        self.proc = None
+    def __init__(self, cuda_index: int = 0, period_s: float = 0.002):
+        self.cuda_index = cuda_index
+        self.period = period_s
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._stop = threading.Event()
         self.thread = None
+        self.error = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except OSError:
-            self.proc = None
+            import pynvml
+            import torch
+
+            pynvml.nvmlInit()
+            idx = self.cuda_index
+            try:
+                idx = torch.cuda._get_nvml_device_index(self.cuda_index)
+            except Exception:
+                pass
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # no NVML: report it instead of guessing
+            self.error = f"nvml unavailable: {e}"
             return self
-        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread = threading.Thread(target=self._poll, daemon=True)
         self.thread.start()
+        time.sleep(0.02)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+    def _poll(self):
+        n, h = self.nvml, self.handle
+        while not self._stop.is_set():
+            try:
+                mhz = n.nvmlDeviceGetClockInfo(h, n.NVML_CLOCK_SM)
+                why = n.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((mhz, why))
+            except Exception as e:
+                self.error = str(e)
+                return
+            time.sleep(self.period)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        self._stop.set()
         if self.thread:
-            self.thread.join(timeout=5)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for row in self.rows:
-            if len(row) < 8:
-                continue
-            try:
-                sm.append(float(row[0]))
-                smax.append(float(row[1]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, row[4:8]):
-                if flag.lower() == "active":
+            self.thread.join(timeout=2)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [],
+                    "samples": 0, "note": self.error or "no samples"}
+        reasons = set()
+        for _, why in self.samples:
+            for bit, name in self.REASONS.items():
+                if why & bit:
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        return {"sm_mhz": statistics.median(m for m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples)}
 
 
 # ------------------------------------------------------------ CPU baseline

@@ -1,0 +1,88 @@
+"""The C-ABI library loads and exports every entry point include/flexlink.h declares.
+
+Runs without a GPU: no collective is executed, but the no-GPU behaviour of the
+product path is pinned (it fails loudly, it never falls back to the CPU).
+"""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+from paper_2510_15882_b200 import comm
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADERS = sorted((ROOT / "include").glob("*.h"))
+
+
+def declared():
+    names = set()
+    for h in HEADERS:
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        names |= set(re.findall(r"^\s*(?:const\s+)?[\w]+\**\s+\**(flx\w+|nccl\w+)\s*\(", text,
+                                re.M))
+    return names
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2510_15882_b200.build import build
+
+    build()
+    return comm.load_library()
+
+
+def test_headers_declare_the_nccl_shaped_surface():
+    names = declared()
+    for must in ("flxGetUniqueId", "flxCommInitRank", "flxCommInitAll", "flxCommDestroy",
+                 "flxAllReduce", "flxAllGather", "flxGroupStart", "flxGroupEnd", "flxSetShares",
+                 "flxGetPathTimes", "flxSetNvlinkCtas"):
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    path = comm.library_path()
+    out = subprocess.run(["nm", "-D", "--defined-only", str(path)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    missing = sorted(declared() - exported)
+    assert not missing, f"declared but not exported: {missing}"
+    for name in declared():
+        assert getattr(lib, name) is not None
+
+
+def test_library_targets_sm100a_only(lib):
+    out = subprocess.run(["cuobjdump", "--list-elf", str(comm.library_path())],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out)
+
+
+def test_version_errors_and_unique_id(lib):
+    v = ctypes.c_int()
+    assert lib.flxGetVersion(ctypes.byref(v)) == 0 and v.value == 10000
+    assert lib.flxGetErrorString(4) == b"invalid argument"
+    uid = comm.Communicator.unique_id()
+    assert len(uid) == 128 and uid[:4] == b"FLX1"
+    assert comm.Communicator.unique_id() != uid
+
+
+def test_no_gpu_means_loud_failure_not_fallback(lib):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(comm.FlexLinkError):
+        comm.Clique(2)
+    handles = (ctypes.c_void_p * 1)()
+    rc = lib.flxCommInitAll(handles, 1, None)
+    assert rc == 1  # flxUnhandledCudaError
+    assert lib.flxGetLastError()
+
+
+def test_argument_validation_without_device(lib):
+    assert lib.flxAllReduce(None, None, 0, 7, 0, None, None) == 4
+    assert lib.flxGroupEnd() == 5  # unbalanced
+    g = (ctypes.c_int * 3)(1000, 0, 0)
+    assert lib.flxSetShares(None, 0, -2, g) == 4

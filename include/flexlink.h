@@ -91,6 +91,13 @@ flxResult_t flxGetUniqueId(flxUniqueId* uniqueId);
 flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId commId, int rank);
 /* Single process, ndev ranks; repeated devices become virtual ranks. */
 flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist);
+/* All nranks ranks of a flxCommInitRank-style world emulated on ONE device:
+ * the multi-rank engine (peer-mapped scratch + flags kernels, host-hub PCIe
+ * staging with cross-rank counter semaphores) with every peer pointer local
+ * and the NVLink-path kernel launched cooperatively over all ranks.  Driven
+ * like flxCommInitAll (one group per collective).  For testing the N-GPU code
+ * path on a single GPU; set CUDA_DEVICE_MAX_CONNECTIONS>=3*nranks+1. */
+flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device);
 flxResult_t flxCommDestroy(flxComm_t comm);
 flxResult_t flxCommCount(const flxComm_t comm, int* count);
 flxResult_t flxCommUserRank(const flxComm_t comm, int* rank);

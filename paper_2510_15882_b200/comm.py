@@ -83,6 +83,7 @@ def load_library() -> ctypes.CDLL:
         "flxGetUniqueId": [P(_UniqueId)],
         "flxCommInitRank": [P(vp), ci, _UniqueId, ci],
         "flxCommInitAll": [P(vp), ci, P(ci)],
+        "flxCommInitLoopback": [P(vp), ci, ci],
         "flxCommDestroy": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
@@ -300,11 +301,18 @@ class Clique:
     the 1-GPU stand-in for an N-GPU NVSwitch collective.
     """
 
-    def __init__(self, nranks: int, device: int = 0):
+    def __init__(self, nranks: int, device: int = 0, loopback: bool = False):
+        """``loopback=False``: fused virtual ranks (flxCommInitAll, repeated device).
+        ``loopback=True``: the multi-GPU engine emulated on one device
+        (flxCommInitLoopback) — same kernels/protocols as one-process-per-GPU."""
         L = load_library()
         handles = (ctypes.c_void_p * nranks)()
-        devs = (ctypes.c_int * nranks)(*([device] * nranks))
-        _check(L.flxCommInitAll(handles, nranks, devs), "flxCommInitAll")
+        if loopback:
+            _check(L.flxCommInitLoopback(handles, nranks, device), "flxCommInitLoopback")
+        else:
+            devs = (ctypes.c_int * nranks)(*([device] * nranks))
+            _check(L.flxCommInitAll(handles, nranks, devs), "flxCommInitAll")
+        self.loopback = loopback
         self.comms = [Communicator(h, self) for h in handles]
         self.nranks = nranks
         self.device = device

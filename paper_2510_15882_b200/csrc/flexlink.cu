@@ -378,12 +378,60 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   return flxSuccess;
 }
 
+// One collective over all local ranks of a world (calls[i] = local rank i).
+flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
+  const Call& head = calls[0];
+  const Comm* lead = head.comm;
+  std::vector<const void*> send;
+  std::vector<void*> recv;
+  std::vector<cudaStream_t> streams;
+  const size_t bytes = head.count * dtype_size(head.dtype);
+  const Granules g = lead->shares[head.coll].lookup(head.coll, bytes);
+  for (size_t i = 0; i < calls.size(); ++i) {
+    const Call& k = calls[i];
+    if (k.coll != head.coll || k.count != head.count || k.dtype != head.dtype || k.op != head.op)
+      return fail(flxInvalidUsage, "local rank %zu called a different collective", i);
+    if (k.comm->shares[head.coll].lookup(head.coll, bytes) != g)
+      return fail(flxInvalidUsage, "local rank %zu has different shares", i);
+    send.push_back(k.send);
+    recv.push_back(k.recv);
+    streams.push_back(k.stream);
+  }
+  return run_world(w, send, recv, streams, head.coll, head.count, head.dtype, head.op, g,
+                   alignment_for(lead, head.coll));
+}
+
 flxResult_t flush_group() {
   std::vector<Call> calls;
   calls.swap(t_pending);
+  // multi-rank worlds: bucket by world, by local rank
+  std::map<World*, std::vector<std::vector<Call>>> by_world;
+  std::vector<World*> world_order;
+  for (const Call& k : calls) {
+    if (!k.comm->world) continue;
+    auto& per = by_world[k.comm->world];
+    if (per.empty()) world_order.push_back(k.comm->world);
+    if ((int)per.size() <= k.comm->local) per.resize(k.comm->local + 1);
+    per[k.comm->local].push_back(k);
+  }
+  for (World* w : world_order) {
+    auto& per = by_world[w];
+    if ((int)per.size() != world_nlocal(w))
+      return fail(flxInvalidUsage, "every local rank of a world must take part in the group");
+    const size_t rounds = per[0].size();
+    for (size_t i = 0; i < per.size(); ++i)
+      if (per[i].size() != rounds)
+        return fail(flxInvalidUsage, "every local rank of a world must take part in the group");
+    for (size_t k = 0; k < rounds; ++k) {
+      std::vector<Call> one;
+      for (auto& v : per) one.push_back(v[k]);
+      FLX_TRY(run_world_calls(w, one));
+    }
+  }
   // bucket calls by clique, preserving per-member order
   std::map<Clique*, std::vector<std::vector<Call>>> by_clique;
   for (const Call& k : calls) {
+    if (k.comm->world) continue;
     Clique* c = k.comm->clique;
     auto& per = by_clique[c];
     if (per.empty()) per.resize(c->members.size());
@@ -515,16 +563,68 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
   uint64_t magic;
   memcpy(&magic, id.internal, sizeof(magic));
   if (magic != 0x31584c46ull) return fail(flxInvalidArgument, "not a flxUniqueId");
-  if (nranks > 1)
-    return fail(flxInvalidUsage, "multi-process communicators are not built into this library");
+  if (nranks > FLX_MAX_VIRTUAL_RANKS)
+    return fail(flxInvalidArgument, "at most %d ranks per communicator", FLX_MAX_VIRTUAL_RANKS);
   int dev = 0;
   FLX_CUDA(cudaGetDevice(&dev));
-  return flxCommInitAll(comm, 1, &dev);
+  if (nranks == 1) return flxCommInitAll(comm, 1, &dev);
+  cudaDeviceProp prop;
+  FLX_CUDA(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major < 10)
+    return fail(flxInvalidUsage, "device %d is sm_%d%d; this build targets sm_100a", dev,
+                prop.major, prop.minor);
+  char hex[40];
+  uint64_t nonce[2];
+  memcpy(nonce, id.internal + 8, sizeof(nonce));
+  snprintf(hex, sizeof(hex), "%016llx%016llx", (unsigned long long)nonce[0],
+           (unsigned long long)nonce[1]);
+  World* w = nullptr;
+  FLX_TRY(world_create_rank(nranks, rank, dev, hex, &w));
+  auto* c = new flxComm();
+  c->rank = rank;
+  c->nranks = nranks;
+  c->device = dev;
+  c->world = w;
+  c->local = 0;
+  world_attach(w, 0, c);
+  *comm = c;
+  return flxSuccess;
+}
+
+flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
+  if (!comms || nranks < 1) return fail(flxInvalidArgument, "bad comms/nranks");
+  int visible = 0;
+  FLX_CUDA(cudaGetDeviceCount(&visible));
+  if (device < 0 || device >= visible) return fail(flxInvalidArgument, "bad device %d", device);
+  cudaDeviceProp prop;
+  FLX_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    return fail(flxInvalidUsage, "device %d is sm_%d%d; this build targets sm_100a", device,
+                prop.major, prop.minor);
+  std::lock_guard<std::mutex> lock(g_mutex);
+  World* w = nullptr;
+  FLX_TRY(world_create_loopback(nranks, device, &w));
+  for (int r = 0; r < nranks; ++r) {
+    auto* c = new flxComm();
+    c->rank = r;
+    c->nranks = nranks;
+    c->device = device;
+    c->world = w;
+    c->local = r;
+    world_attach(w, r, c);
+    comms[r] = c;
+  }
+  return flxSuccess;
 }
 
 flxResult_t flxCommDestroy(flxComm_t comm) {
   FLX_TRY(validate_comm(comm));
   std::lock_guard<std::mutex> lock(g_mutex);
+  if (comm->world) {
+    world_release(comm->world);
+    delete comm;
+    return flxSuccess;
+  }
   Clique* c = comm->clique;
   c->destroyed++;
   if (c->destroyed == (int)c->members.size()) {
@@ -625,6 +725,11 @@ flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granule
 flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]) {
   FLX_TRY(validate_comm(comm));
   if (!ms) return fail(flxInvalidArgument, "null ms");
+  if (comm->world) {
+    const uint64_t calls = world_calls(comm->world, comm->local);
+    if (calls == 0) return fail(flxInvalidUsage, "no collective has run on this comm");
+    return world_read_timing(comm->world, comm->local, calls - 1, ms);
+  }
   Clique* c = comm->clique;
   if (c->calls == 0) return fail(flxInvalidUsage, "no collective has run on this comm");
   return read_timing(c, c->calls - 1, ms);
@@ -633,10 +738,16 @@ flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]) {
 flxResult_t flxGetPathTimesHistory(flxComm_t comm, int max_calls, float* ms, int* n_out) {
   FLX_TRY(validate_comm(comm));
   if (!ms || !n_out || max_calls < 0) return fail(flxInvalidArgument, "bad history arguments");
-  Clique* c = comm->clique;
-  const uint64_t avail = std::min<uint64_t>(c->calls, Clique::kTimingSlots);
+  const uint64_t calls =
+      comm->world ? world_calls(comm->world, comm->local) : comm->clique->calls;
+  const uint64_t avail = std::min<uint64_t>(calls, Clique::kTimingSlots);
   const uint64_t n = std::min<uint64_t>(avail, (uint64_t)max_calls);
-  for (uint64_t i = 0; i < n; ++i) FLX_TRY(read_timing(c, c->calls - n + i, ms + 3 * i));
+  for (uint64_t i = 0; i < n; ++i) {
+    if (comm->world)
+      FLX_TRY(world_read_timing(comm->world, comm->local, calls - n + i, ms + 3 * i));
+    else
+      FLX_TRY(read_timing(comm->clique, calls - n + i, ms + 3 * i));
+  }
   *n_out = (int)n;
   return flxSuccess;
 }
@@ -644,7 +755,9 @@ flxResult_t flxGetPathTimesHistory(flxComm_t comm, int max_calls, float* ms, int
 flxResult_t flxGetPathBytes(flxComm_t comm, size_t bytes[3]) {
   FLX_TRY(validate_comm(comm));
   if (!bytes) return fail(flxInvalidArgument, "null bytes");
-  for (int p = 0; p < FLX_NUM_PATHS; ++p) bytes[p] = comm->clique->last_bytes[p];
+  const auto last = comm->world ? world_last_bytes(comm->world, comm->local)
+                                : comm->clique->last_bytes;
+  for (int p = 0; p < FLX_NUM_PATHS; ++p) bytes[p] = last[p];
   return flxSuccess;
 }
 
@@ -659,6 +772,7 @@ flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
   FLX_TRY(validate_comm(comm));
   if (nctas < 0 || nctas > 65535) return fail(flxInvalidArgument, "bad nctas %d", nctas);
   comm->nvlink_ctas = nctas;
+  if (comm->world) world_set_nctas(comm->world, nctas > 0 ? nctas : 32);
   return flxSuccess;
 }
 

@@ -94,11 +94,29 @@ struct Clique {
   int destroyed = 0;
 };
 
+// Multi-rank worlds (world.cu): one process per GPU, or loopback emulation.
+struct World;
+flxResult_t world_create_loopback(int nranks, int device, World** out);
+flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_hex, World** out);
+void world_attach(World* w, int local, Comm* c);
+int world_release(World* w);
+flxResult_t run_world(World* w, const std::vector<const void*>& send,
+                      const std::vector<void*>& recv, const std::vector<cudaStream_t>& streams,
+                      int coll, size_t count, int dtype, int op, const Granules& g,
+                      size_t alignment);
+flxResult_t world_read_timing(World* w, int local, uint64_t seq, float ms[3]);
+uint64_t world_calls(World* w, int local);
+std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local);
+void world_set_nctas(World* w, int n);
+int world_nlocal(World* w);
+
 struct Comm {
   int rank = 0;
   int nranks = 1;
   int device = 0;
-  Clique* clique = nullptr;
+  Clique* clique = nullptr;  // virtual-rank (fused) mode
+  World* world = nullptr;    // multi-rank mode
+  int local = 0;             // index among the world's ranks in this process
   ShareTable shares[2];  // per flxCollOp_t
   int nvlink_ctas = 0;   // 0 = auto
   size_t chunk_bytes = 0;  // 0 = auto

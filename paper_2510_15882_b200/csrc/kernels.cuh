@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(512) fanout_vec_kernel(const FanoutArgs a) {
   }
 }
 
-__global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {
+static __global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {
   const int r = blockIdx.y;
   const size_t shift = (size_t)r * a.dst_stride;
   const size_t stride = (size_t)gridDim.x * blockDim.x;

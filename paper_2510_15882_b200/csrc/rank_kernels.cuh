@@ -1,0 +1,277 @@
+// Multi-rank NVLink-path kernels: one launch per rank per round, CTA b of
+// rank r exchanging with CTA b of every peer over NVSwitch through
+// peer-mapped (CUDA IPC) scratch buffers and release/acquire flags.
+//
+// AllReduce = reduce-scatter + all-gather in one launch:
+//   1 push   rank r stores its chunk c to peer c's inbox[r]           (NVLink write)
+//   2 reduce rank r folds inbox[0..N) (own chunk read in place) in rank
+//            order -> recv chunk r and its own outbox                  (local HBM)
+//   3 pull   rank r loads every peer's outbox into recv chunk c         (NVLink read)
+// AllGather: push own slice to every peer's inbox[r]; copy inbox -> recv.
+// Flags (per receiving rank): arrive/ready/done[src][cta], monotone epochs,
+// compared cyclically; the same fold rule as kernels.cuh (bit-identical to the
+// virtual-rank path and the CPU oracle).
+//
+// The same device code runs (a) per GPU with grid = nctas, (b) in loopback
+// (all ranks on one GPU, grid = nctas x nranks, cooperative launch so every
+// CTA is co-resident and the spin-waits cannot deadlock).
+#pragma once
+
+#include "kernels.cuh"
+
+namespace flx {
+
+constexpr int kMaxCtas = 128;
+enum FlagKind { kArrive = 0, kReady = 1, kDone = 2 };
+constexpr size_t kFlagWords = 3 * kMaxRanks * kMaxCtas;
+
+struct RankArgs {
+  const char* send;
+  char* recv;
+  char* scratch[kMaxRanks];    // every rank's scratch base, as mapped in this rank
+  uint32_t* flags[kMaxRanks];  // every rank's flag block, as mapped in this rank
+  int rank;
+  int nranks;
+  size_t bytes;        // NVLink slice: per-rank message bytes (AR) / send bytes (AG)
+  size_t rank_stride;  // AllGather: distance between rank blocks in recv
+  size_t slot;         // inbox slot capacity (bytes) per source rank
+  uint32_t epoch;      // epoch of round 0; round k uses epoch + k
+  uint32_t* abort_word;  // host-mapped; set on a wait timeout
+};
+
+struct LoopbackArgs {
+  RankArgs r[kMaxRanks];
+};
+
+__device__ __forceinline__ uint32_t* flag_at(uint32_t* block, int kind, int src, int cta) {
+  return block + ((size_t)kind * kMaxRanks + src) * kMaxCtas + cta;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Inter-rank data written during the kernel: bypass L1 (.cg) so a later round
+// never sees a stale line.
+__device__ __forceinline__ uint4 ld_cg(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+// Thread 0 spins until *p has reached `epoch` (cyclic compare), then the CTA
+// proceeds.  ~10 s timeout -> abort word, so a dead peer cannot hang the GPU.
+__device__ __forceinline__ bool cta_wait(const uint32_t* p, uint32_t epoch, uint32_t* abort_word) {
+  __shared__ int ok;
+  if (threadIdx.x == 0) {
+    ok = 1;
+    const long long t0 = clock64();
+    while ((int)(ld_acquire_sys(p) - epoch) < 0) {
+      if (*(volatile uint32_t*)abort_word) { ok = 0; break; }
+      if (clock64() - t0 > 20000000000ll) {
+        atomicExch(abort_word, 1u);
+        ok = 0;
+        break;
+      }
+    }
+  }
+  __syncthreads();
+  return ok;
+}
+
+// Make this CTA's prior global stores visible system-wide, then thread 0
+// publishes `epoch` to each flag in `targets`.
+__device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, uint32_t epoch) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int i = 0; i < count; ++i) st_release_sys(targets[i], epoch);
+  __syncthreads();
+}
+
+__device__ __forceinline__ bool aligned16_dev(const void* p) {
+  return (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+
+// CTA-wide copy of n bytes (vectorised when both ends are 16 B aligned).
+__device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, bool coherent) {
+  if (aligned16_dev(dst) && aligned16_dev(src)) {
+    const size_t nv = n >> 4;
+    for (size_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      const uint4 w = coherent ? ld_cg(src + (v << 4)) : ld_stream(src + (v << 4));
+      *reinterpret_cast<uint4*>(dst + (v << 4)) = w;
+    }
+    for (size_t i = (nv << 4) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else {
+    for (size_t i = threadIdx.x; i < n; i += blockDim.x)
+      dst[i] = coherent ? *(volatile const char*)(src + i) : src[i];
+  }
+}
+
+// CTA-wide fold of n bytes: src[0..nsrc) -> dst[0..ndst) (fold rule of kernels.cuh).
+template <typename T, int OP>
+__device__ __forceinline__ void cta_fold(char* const* dst, int ndst, const char* const* src,
+                                         int nsrc, size_t n) {
+  using A = typename AccT<T>::type;
+  constexpr int kVec = 16 / sizeof(T);
+  bool vec = true;
+  for (int i = 0; i < nsrc; ++i) vec = vec && aligned16_dev(src[i]);
+  for (int i = 0; i < ndst; ++i) vec = vec && aligned16_dev(dst[i]);
+  size_t done = 0;
+  if (vec) {
+    const size_t nv = n >> 4;
+    for (size_t v = threadIdx.x; v < nv; v += blockDim.x) {
+      uint4 w[kMaxRanks];
+#pragma unroll
+      for (int i = 0; i < kMaxRanks; ++i)
+        if (i < nsrc) w[i] = ld_cg(src[i] + (v << 4));
+      A acc[kVec];
+      load_acc<T>(acc, w[0]);
+#pragma unroll
+      for (int i = 1; i < kMaxRanks; ++i)
+        if (i < nsrc) fold_into<T, OP>(acc, w[i]);
+      const uint4 out = pack_acc<T>(acc);
+      for (int d = 0; d < ndst; ++d) *reinterpret_cast<uint4*>(dst[d] + (v << 4)) = out;
+    }
+    done = nv << 4;
+  }
+  for (size_t i = done / sizeof(T) + threadIdx.x; i < n / sizeof(T); i += blockDim.x) {
+    A acc = to_acc<T>(*(volatile const T*)(src[0] + i * sizeof(T)));
+    for (int s = 1; s < nsrc; ++s)
+      acc = apply_op<OP>(acc, to_acc<T>(*(volatile const T*)(src[s] + i * sizeof(T))));
+    const T out = from_acc<T>(acc);
+    for (int d = 0; d < ndst; ++d) *reinterpret_cast<T*>(dst[d] + i * sizeof(T)) = out;
+  }
+}
+
+__device__ __forceinline__ size_t ceil16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// [lo, hi) of CTA `cta`'s part of a span of `len` bytes split over `nctas`.
+__device__ __forceinline__ void cta_part(size_t len, int nctas, int cta, size_t* lo, size_t* hi) {
+  const size_t part = ceil16((len + nctas - 1) / nctas);
+  *lo = min(len, (size_t)cta * part);
+  *hi = min(len, *lo + part);
+}
+
+template <typename T, int OP>
+__device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
+  const int r = a.rank, n = a.nranks;
+  const size_t round_cap = a.slot * n;
+  const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
+  for (size_t base = 0, k = 0; base < a.bytes; base += round_cap, ++k) {
+    const uint32_t e = a.epoch + (uint32_t)k;
+    const size_t len = min(round_cap, a.bytes - base);
+    const size_t chunk = ceil16((len + n - 1) / n);
+    auto chunk_span = [&](int c, size_t* off, size_t* clen) {
+      *off = min(len, (size_t)c * chunk);
+      *clen = min(len, *off + chunk) - *off;
+    };
+    // 1) push my chunk c (part cta) into peer c's inbox slot r
+    uint32_t* arrive_targets[kMaxRanks];
+    int nt = 0;
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      size_t off, clen, lo, hi;
+      chunk_span(c, &off, &clen);
+      cta_part(clen, nctas, cta, &lo, &hi);
+      cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, a.send + base + off + lo, hi - lo, false);
+      arrive_targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    }
+    cta_signal(arrive_targets, nt, e);
+    // 2) reduce my chunk r from every source, in rank order
+    size_t off, clen, lo, hi;
+    chunk_span(r, &off, &clen);
+    cta_part(clen, nctas, cta, &lo, &hi);
+    for (int p = 0; p < n; ++p) {
+      if (p == r) continue;
+      if (!cta_wait(flag_at(a.flags[r], kArrive, p, cta), e, a.abort_word)) return;
+      // my outbox is rewritten below: peers must have pulled last round's
+      if (!cta_wait(flag_at(a.flags[r], kDone, p, cta), e - 1, a.abort_word)) return;
+    }
+    {
+      const char* src[kMaxRanks];
+      for (int p = 0; p < n; ++p)
+        src[p] = (p == r) ? a.send + base + off + lo : a.scratch[r] + (size_t)p * a.slot + lo;
+      char* dst[2] = {a.recv + base + off + lo, a.scratch[r] + outbox + lo};
+      cta_fold<T, OP>(dst, 2, src, n, hi - lo);
+    }
+    uint32_t* ready_targets[kMaxRanks];
+    nt = 0;
+    for (int s = 1; s < n; ++s) ready_targets[nt++] = flag_at(a.flags[(r + s) % n], kReady, r, cta);
+    cta_signal(ready_targets, nt, e);
+    // 3) pull every peer's reduced chunk
+    uint32_t* done_targets[kMaxRanks];
+    nt = 0;
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      size_t coff, cl, clo, chi;
+      chunk_span(c, &coff, &cl);
+      cta_part(cl, nctas, cta, &clo, &chi);
+      if (!cta_wait(flag_at(a.flags[r], kReady, c, cta), e, a.abort_word)) return;
+      cta_copy(a.recv + base + coff + clo, a.scratch[c] + outbox + clo, chi - clo, true);
+      done_targets[nt++] = flag_at(a.flags[c], kDone, r, cta);
+    }
+    cta_signal(done_targets, nt, e);
+  }
+}
+
+__device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
+  const int r = a.rank, n = a.nranks;
+  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = a.epoch + (uint32_t)k;
+    const size_t len = min(a.slot, a.bytes - base);
+    size_t lo, hi;
+    cta_part(len, nctas, cta, &lo, &hi);
+    // peers must have drained what I pushed into their inbox last round
+    for (int p = 0; p < n; ++p)
+      if (p != r && !cta_wait(flag_at(a.flags[r], kDone, p, cta), e - 1, a.abort_word)) return;
+    uint32_t* targets[kMaxRanks];
+    int nt = 0;
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, a.send + base + lo, hi - lo, false);
+      targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    }
+    char* own = a.recv + (size_t)r * a.rank_stride + base;
+    if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
+    cta_signal(targets, nt, e);
+    nt = 0;
+    for (int s = 1; s < n; ++s) {
+      const int p = (r - s + n) % n;
+      if (!cta_wait(flag_at(a.flags[r], kArrive, p, cta), e, a.abort_word)) return;
+      cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
+               a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
+      targets[nt++] = flag_at(a.flags[p], kDone, r, cta);
+    }
+    cta_signal(targets, nt, e);
+  }
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
+  rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
+  rank_allgather(a, blockIdx.x, gridDim.x);
+}
+
+// Loopback: blockIdx.y is the rank; cooperative launch (all CTAs co-resident).
+template <typename T, int OP>
+__global__ void __launch_bounds__(512) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
+  rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(512) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
+  rank_allgather(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+}
+
+}  // namespace flx

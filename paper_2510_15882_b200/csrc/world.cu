@@ -1,0 +1,585 @@
+// Multi-rank communicators: one process per GPU (flxCommInitRank), or every
+// rank of such a world emulated on one GPU (flxCommInitLoopback).
+//
+// Data plane per call (per rank r, message split by partition()):
+//   NVLink slice : rank_allreduce/rank_allgather kernel over peer-mapped
+//                  scratch (rank_kernels.cuh)
+//   PCIe slice   : host-hub staging through one shared host segment; copy
+//                  engines on two side streams; per-edge monotone counter
+//                  semaphores (staging.py:176-188 with buffers=1, lap=epoch-1)
+//                  set with cuStreamWriteValue32 and awaited with
+//                  cuStreamWaitValue32 on the shared words:
+//     AllReduce  1 D2H  send[sub c]   -> H_r[c]        prod[r][c] = e   (c != r)
+//                2 H2D  H_p[r]        -> stage[p]      cons[p][r] = e   (p != r)
+//                  fold stage[*] + own sub r           -> recv sub r
+//                3 D2H  recv sub r    -> R_r           rprod[r]   = e
+//                4 H2D  R_c           -> recv sub c    rcons[c][r] = e
+//     AllGather  1 D2H  send          -> H_r           gprod[r]   = e
+//                2 H2D  H_c           -> recv block c  gcons[c][r] = e
+//   Issue order is global (all ranks' step 1, then step 2, ...) so every wait
+//   refers to a write issued earlier: no deadlock even when streams share a
+//   hardware queue (loopback).
+// Bootstrap (multi-process): a POSIX shm segment named by the unique id
+// carries each rank's CUDA IPC handles (scratch + flags) and a second one is
+// the PCIe staging area, cudaHostRegister'ed by every rank.
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <thread>
+
+#include "internal.h"
+#include "rank_kernels.cuh"
+
+namespace flx {
+
+namespace {
+
+constexpr int kSemWords = 4096;  // uint32 words at the head of the staging segment
+// semaphore word layout (all [src][dst] over kMaxRanks)
+inline size_t sem_prod(int r, int c) { return 0 * 256 + r * kMaxRanks + c; }
+inline size_t sem_cons(int r, int c) { return 1 * 256 + r * kMaxRanks + c; }
+inline size_t sem_rcons(int r, int c) { return 2 * 256 + r * kMaxRanks + c; }
+inline size_t sem_gcons(int r, int c) { return 3 * 256 + r * kMaxRanks + c; }
+inline size_t sem_rprod(int r) { return 4 * 256 + r; }
+inline size_t sem_gprod(int r) { return 4 * 256 + kMaxRanks + r; }
+
+size_t env_mib(const char* name, size_t dflt) {
+  const char* v = getenv(name);
+  return v ? (size_t)atoll(v) << 20 : dflt << 20;
+}
+
+struct BootSlot {
+  int ready;
+  int device;
+  int pid;
+  char pad[4];
+  cudaIpcMemHandle_t scratch;
+  cudaIpcMemHandle_t flags;
+  char bus_id[32];
+};
+
+struct BootHeader {
+  int arrived;
+  int mapped;
+  int nranks;
+  int pad;
+  BootSlot slot[kMaxRanks];
+};
+
+}  // namespace
+
+struct World {
+  int nranks = 0;
+  bool loopback = false;
+  int nctas = 0;
+  size_t slot = 0;       // inbox slot bytes per source rank
+  size_t hcap = 0;       // PCIe staging bytes per rank region
+  uint32_t epoch = 1;    // NVLink-path flag epoch (next round)
+  uint32_t pepoch = 1;   // PCIe-path semaphore epoch (next call)
+  // host staging segment: [sem words][H_0 .. H_{n-1}][R_0 .. R_{n-1}]
+  char* host = nullptr;
+  size_t host_bytes = 0;
+  bool host_shm = false;
+  uint32_t* abort_word = nullptr;  // pinned, mapped
+  struct Local {
+    Comm* comm = nullptr;
+    int rank = 0;
+    int device = 0;
+    char* scratch = nullptr;
+    uint32_t* flags = nullptr;
+    char* dstage = nullptr;  // device landing zone for PCIe sub-chunks
+    cudaStream_t d2h = nullptr, h2d = nullptr;
+    cudaEvent_t fold_done = nullptr, ev_join = nullptr;
+    std::vector<cudaEvent_t> ev_fork;
+    Clique::Timing timing[Clique::kTimingSlots];
+    uint64_t calls = 0;
+    std::array<size_t, FLX_NUM_PATHS> last_bytes{{0, 0, 0}};
+  };
+  std::vector<Local> local;
+  // peer views (as mapped in this process): scratch/flags of every rank
+  char* peer_scratch[kMaxRanks] = {};
+  uint32_t* peer_flags[kMaxRanks] = {};
+  std::vector<void*> ipc_opened;
+  int destroyed = 0;
+
+  uint32_t* sem(size_t word) { return reinterpret_cast<uint32_t*>(host) + word; }
+  char* hregion(int r) { return host + kSemWords * 4 + (size_t)r * hcap; }
+  char* rregion(int r) { return host + kSemWords * 4 + (size_t)nranks * hcap + (size_t)r * hcap; }
+};
+
+namespace {
+
+flxResult_t local_init(World* w, World::Local& L) {
+  FLX_CUDA(cudaSetDevice(L.device));
+  const size_t scratch_bytes = w->slot * (w->nranks + 1);
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), kFlagWords * 4));
+  FLX_CUDA(cudaMemset(L.flags, 0, kFlagWords * 4));
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.dstage), w->hcap));
+  FLX_CUDA(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
+  FLX_CUDA(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
+  FLX_CUDA(cudaEventCreateWithFlags(&L.fold_done, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
+  for (auto& t : L.timing) {
+    FLX_CUDA(cudaEventCreate(&t.start));
+    FLX_CUDA(cudaEventCreate(&t.nv));
+    FLX_CUDA(cudaEventCreate(&t.pcie));
+  }
+  L.ev_fork.resize(w->loopback ? w->nranks : 1);
+  for (auto& e : L.ev_fork) FLX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  FLX_CUDA(cudaDeviceSynchronize());
+  return flxSuccess;
+}
+
+void world_free(World* w) {
+  for (auto& L : w->local) {
+    cudaSetDevice(L.device);
+    if (L.d2h) cudaStreamSynchronize(L.d2h);
+    if (L.h2d) cudaStreamSynchronize(L.h2d);
+  }
+  for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
+  for (auto& L : w->local) {
+    if (L.scratch) cudaFree(L.scratch);
+    if (L.flags) cudaFree(L.flags);
+    if (L.dstage) cudaFree(L.dstage);
+    if (L.d2h) cudaStreamDestroy(L.d2h);
+    if (L.h2d) cudaStreamDestroy(L.h2d);
+    if (L.fold_done) cudaEventDestroy(L.fold_done);
+    if (L.ev_join) cudaEventDestroy(L.ev_join);
+    for (auto e : L.ev_fork) cudaEventDestroy(e);
+    for (auto& t : L.timing) {
+      cudaEventDestroy(t.start);
+      cudaEventDestroy(t.nv);
+      cudaEventDestroy(t.pcie);
+    }
+  }
+  if (w->host) {
+    cudaHostUnregister(w->host);
+    if (w->host_shm)
+      munmap(w->host, w->host_bytes);
+    else
+      free(w->host);
+  }
+  if (w->abort_word) cudaFreeHost(w->abort_word);
+  delete w;
+}
+
+flxResult_t alloc_host_staging(World* w, const char* shm_name) {
+  w->host_bytes = (size_t)kSemWords * 4 + 2 * (size_t)w->nranks * w->hcap;
+  if (shm_name) {
+    int fd = shm_open(shm_name, O_CREAT | O_RDWR, 0600);
+    if (fd < 0) return fail(flxSystemError, "shm_open(%s) failed", shm_name);
+    if (ftruncate(fd, (off_t)w->host_bytes) != 0) {
+      close(fd);
+      return fail(flxSystemError, "ftruncate of %zu-byte staging segment failed", w->host_bytes);
+    }
+    void* p = mmap(nullptr, w->host_bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (p == MAP_FAILED) return fail(flxSystemError, "mmap of staging segment failed");
+    w->host = static_cast<char*>(p);
+    w->host_shm = true;
+  } else {
+    void* p = nullptr;
+    if (posix_memalign(&p, 4096, w->host_bytes) != 0)
+      return fail(flxSystemError, "host staging allocation failed");
+    memset(p, 0, w->host_bytes);
+    w->host = static_cast<char*>(p);
+  }
+  FLX_CUDA(cudaHostRegister(w->host, w->host_bytes,
+                            cudaHostRegisterMapped | cudaHostRegisterPortable));
+  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->abort_word), 64,
+                         cudaHostAllocMapped | cudaHostAllocPortable));
+  *w->abort_word = 0;
+  return flxSuccess;
+}
+
+void world_config(World* w, int nranks) {
+  w->nranks = nranks;
+  w->slot = env_mib("FLX_SLOT_MB", 32);
+  w->hcap = env_mib("FLX_PCIE_STAGE_MB", 32);
+  w->nctas = 32;
+  if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));
+}
+
+template <typename F>
+bool spin_until(F pred, double seconds) {
+  const auto t0 = std::chrono::steady_clock::now();
+  while (!pred()) {
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > seconds)
+      return false;
+    std::this_thread::sleep_for(std::chrono::microseconds(200));
+  }
+  return true;
+}
+
+// ------------------------------------------------------------- launches
+template <typename T, int OP>
+cudaError_t launch_rank_allreduce_t(bool loop, const void* args, int nctas, int nranks,
+                                    cudaStream_t s) {
+  if (loop) {
+    void* params[] = {const_cast<void*>(args)};
+    return cudaLaunchCooperativeKernel((const void*)loopback_allreduce_kernel<T, OP>,
+                                       dim3(nctas, nranks), dim3(512), params, 0, s);
+  }
+  rank_allreduce_kernel<T, OP><<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rank_allreduce_op(int op, bool loop, const void* a, int nctas, int n,
+                                     cudaStream_t s) {
+  switch (op) {
+    case kSum: return launch_rank_allreduce_t<T, kSum>(loop, a, nctas, n, s);
+    case kProd: return launch_rank_allreduce_t<T, kProd>(loop, a, nctas, n, s);
+    case kMax: return launch_rank_allreduce_t<T, kMax>(loop, a, nctas, n, s);
+    case kMin: return launch_rank_allreduce_t<T, kMin>(loop, a, nctas, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rank_allreduce(int dtype, int op, bool loop, const void* a, int nctas, int n,
+                                  cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  switch (dtype) {
+    case flxInt8: return launch_rank_allreduce_op<int8_t>(op, loop, a, nctas, n, s);
+    case flxUint8: return launch_rank_allreduce_op<uint8_t>(op, loop, a, nctas, n, s);
+    case flxInt32: return launch_rank_allreduce_op<int32_t>(op, loop, a, nctas, n, s);
+    case flxUint32: return launch_rank_allreduce_op<uint32_t>(op, loop, a, nctas, n, s);
+    case flxInt64: return launch_rank_allreduce_op<int64_t>(op, loop, a, nctas, n, s);
+    case flxUint64: return launch_rank_allreduce_op<uint64_t>(op, loop, a, nctas, n, s);
+    case flxFloat16: return launch_rank_allreduce_op<__half>(op, loop, a, nctas, n, s);
+    case flxFloat32: return launch_rank_allreduce_op<float>(op, loop, a, nctas, n, s);
+    case flxFloat64: return launch_rank_allreduce_op<double>(op, loop, a, nctas, n, s);
+    case flxBfloat16: return launch_rank_allreduce_op<__nv_bfloat16>(op, loop, a, nctas, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nranks,
+                                  cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (loop) {
+    void* params[] = {const_cast<void*>(args)};
+    return cudaLaunchCooperativeKernel((const void*)loopback_allgather_kernel, dim3(nctas, nranks),
+                                       dim3(512), params, 0, s);
+  }
+  rank_allgather_kernel<<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+// One collective over every local rank of a world; calls[i] is local rank i.
+flxResult_t run_world(World* w, const std::vector<const void*>& send,
+                      const std::vector<void*>& recv, const std::vector<cudaStream_t>& streams,
+                      int coll, size_t count, int dtype, int op, const Granules& g,
+                      size_t alignment) {
+  const int n = w->nranks;
+  const int nl = (int)w->local.size();
+  const size_t esz = dtype_size(dtype);
+  const size_t bytes = count * esz;
+  auto split = partition(bytes, g, alignment);
+  if (split[flxPathRdma] > 0) return fail(flxInvalidUsage, "rdma path is not available");
+  const size_t nv = split[flxPathNvlink], pc = split[flxPathPcie];
+  const bool gather = coll == flxCollAllGather;
+  if (*w->abort_word) return fail(flxInternalError, "communicator aborted by an earlier timeout");
+  if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
+  if (pc > (gather ? w->hcap : w->hcap))
+    return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
+                "FLX_PCIE_STAGE_MB or lower the pcie share)", pc, w->hcap);
+
+  // fork: in loopback every rank's stream joins local rank 0's stream
+  cudaStream_t s0 = streams[0];
+  FLX_CUDA(cudaSetDevice(w->local[0].device));
+  for (int i = 1; i < nl; ++i) {
+    if (streams[i] == s0) continue;
+    FLX_CUDA(cudaEventRecord(w->local[0].ev_fork[i], streams[i]));
+    FLX_CUDA(cudaStreamWaitEvent(s0, w->local[0].ev_fork[i], 0));
+  }
+  std::vector<Clique::Timing*> tm(nl);
+  for (int i = 0; i < nl; ++i) {
+    World::Local& L = w->local[i];
+    tm[i] = &L.timing[L.calls % Clique::kTimingSlots];
+    FLX_CUDA(cudaEventRecord(tm[i]->start, s0));
+  }
+
+  // ---------------- PCIe slice (issued first so the copies overlap the kernel)
+  if (pc > 0) {
+    const uint32_t e = w->pepoch++;
+    for (auto& L : w->local) {
+      FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[&L - &w->local[0]]->start, 0));
+      FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[&L - &w->local[0]]->start, 0));
+    }
+    if (!gather) {
+      const size_t q = pc / n;  // alignment makes pc a multiple of n*4096
+      // step 1: D2H my sub-chunk c into H_r[c]
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_cons(r, c)), e - 1));
+          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * q,
+                                   static_cast<const char*>(send[i]) + nv + c * q, q,
+                                   cudaMemcpyDeviceToHost, L.d2h));
+          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
+        }
+      }
+      // step 2: H2D every source's sub-chunk r, fold in rank order
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int s = 1; s < n; ++s) {
+          const int p = (r - s + n) % n;
+          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
+          FLX_CUDA(cudaMemcpyAsync(L.dstage + p * q, w->hregion(p) + r * q, q,
+                                   cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
+        }
+        FoldArgs a{};
+        for (int p = 0; p < n; ++p)
+          a.src[p] = (p == r) ? static_cast<const char*>(send[i]) + nv + r * q : L.dstage + p * q;
+        a.dst[0] = static_cast<char*>(recv[i]) + nv + r * q;
+        a.n = n;
+        a.ndst = 1;
+        a.bytes = q;
+        FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
+        FLX_CUDA(cudaEventRecord(L.fold_done, L.h2d));
+      }
+      // step 3: D2H my reduced sub-chunk into R_r
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done, 0));
+        for (int p = 0; p < n; ++p)
+          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_rcons(r, p)), e - 1));
+        FLX_CUDA(cudaMemcpyAsync(w->rregion(r), static_cast<char*>(recv[i]) + nv + r * q, q,
+                                 cudaMemcpyDeviceToHost, L.d2h));
+        FLX_TRY(sem_write(L.d2h, w->sem(sem_rprod(r)), e));
+      }
+      // step 4: H2D every other rank's reduced sub-chunk
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_rprod(c)), e));
+          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + nv + c * q, w->rregion(c), q,
+                                   cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_rcons(c, r)), e));
+        }
+        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+      }
+    } else {
+      // step 1: D2H my send slice into H_r (all readers of last call done)
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int p = 0; p < n; ++p)
+          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_gcons(r, p)), e - 1));
+        FLX_CUDA(cudaMemcpyAsync(w->hregion(r), static_cast<const char*>(send[i]) + nv, pc,
+                                 cudaMemcpyDeviceToHost, L.d2h));
+        FLX_TRY(sem_write(L.d2h, w->sem(sem_gprod(r)), e));
+      }
+      // step 2: H2D every other rank's slice into its block; own block locally
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        char* own = static_cast<char*>(recv[i]) + (size_t)r * bytes + nv;
+        const char* mine = static_cast<const char*>(send[i]) + nv;
+        if (own != mine)
+          FLX_CUDA(cudaMemcpyAsync(own, mine, pc, cudaMemcpyDeviceToDevice, L.h2d));
+        for (int s = 1; s < n; ++s) {
+          const int c = (r - s + n) % n;
+          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_gprod(c)), e));
+          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + (size_t)c * bytes + nv,
+                                   w->hregion(c), pc, cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_gcons(c, r)), e));
+        }
+        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+      }
+    }
+  }
+
+  // ---------------- NVLink slice
+  if (nv > 0) {
+    const uint32_t e0 = w->epoch;
+    const size_t round_cap = gather ? w->slot : w->slot * n;
+    w->epoch += (uint32_t)((nv + round_cap - 1) / round_cap);
+    LoopbackArgs la;
+    memset(&la, 0, sizeof(la));
+    for (int i = 0; i < nl; ++i) {
+      RankArgs& a = la.r[w->loopback ? w->local[i].rank : 0];
+      a.send = static_cast<const char*>(send[i]);
+      a.recv = static_cast<char*>(recv[i]);
+      for (int p = 0; p < n; ++p) {
+        a.scratch[p] = w->loopback ? w->local[p].scratch : w->peer_scratch[p];
+        a.flags[p] = w->loopback ? w->local[p].flags : w->peer_flags[p];
+      }
+      a.rank = w->local[i].rank;
+      a.nranks = n;
+      a.bytes = nv;
+      a.rank_stride = bytes;
+      a.slot = w->slot;
+      a.epoch = e0;
+      a.abort_word = w->abort_word;
+    }
+    const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
+    cudaError_t err = gather ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
+                             : launch_rank_allreduce(dtype, op, w->loopback, args, w->nctas, n, s0);
+    if (err != cudaSuccess)
+      return fail(flxUnhandledCudaError, "rank kernel launch: %s", cudaGetErrorString(err));
+  }
+  for (int i = 0; i < nl; ++i) FLX_CUDA(cudaEventRecord(tm[i]->nv, s0));
+  if (pc > 0)
+    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaStreamWaitEvent(s0, tm[i]->pcie, 0));
+  bool joined = false;
+  for (int i = 1; i < nl; ++i) {
+    if (streams[i] == s0) continue;
+    if (!joined) {
+      FLX_CUDA(cudaEventRecord(w->local[0].ev_join, s0));
+      joined = true;
+    }
+    FLX_CUDA(cudaStreamWaitEvent(streams[i], w->local[0].ev_join, 0));
+  }
+  for (int i = 0; i < nl; ++i) {
+    World::Local& L = w->local[i];
+    tm[i]->used[flxPathNvlink] = nv > 0;
+    tm[i]->used[flxPathPcie] = pc > 0;
+    tm[i]->used[flxPathRdma] = false;
+    L.last_bytes = split;
+    L.calls++;
+  }
+  return flxSuccess;
+}
+
+flxResult_t world_read_timing(World* w, int local, uint64_t seq, float ms[3]) {
+  World::Local& L = w->local[local];
+  const Clique::Timing& t = L.timing[seq % Clique::kTimingSlots];
+  FLX_CUDA(cudaSetDevice(L.device));
+  ms[0] = ms[1] = ms[2] = 0.f;
+  FLX_CUDA(cudaEventSynchronize(t.nv));
+  if (*w->abort_word) return fail(flxInternalError, "a peer wait timed out (rank died or hung?)");
+  if (t.used[flxPathNvlink]) FLX_CUDA(cudaEventElapsedTime(&ms[0], t.start, t.nv));
+  if (t.used[flxPathPcie]) {
+    FLX_CUDA(cudaEventSynchronize(t.pcie));
+    FLX_CUDA(cudaEventElapsedTime(&ms[1], t.start, t.pcie));
+  }
+  return flxSuccess;
+}
+
+uint64_t world_calls(World* w, int local) { return w->local[local].calls; }
+std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local) {
+  return w->local[local].last_bytes;
+}
+int world_nranks(World* w) { return w->nranks; }
+int world_nlocal(World* w) { return (int)w->local.size(); }
+void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(kMaxCtas, n)); }
+
+// ------------------------------------------------------------ creation
+flxResult_t world_create_loopback(int nranks, int device, World** out) {
+  if (nranks < 1 || nranks > kMaxRanks)
+    return fail(flxInvalidArgument, "loopback supports 1..%d ranks", kMaxRanks);
+  auto* w = new World();
+  world_config(w, nranks);
+  w->loopback = true;
+  w->local.resize(nranks);
+  FLX_CUDA(cudaSetDevice(device));
+  int coop = 0;
+  FLX_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  if (!coop) return fail(flxInvalidUsage, "device %d lacks cooperative launch", device);
+  int sms = 0;
+  FLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  w->nctas = std::max(1, std::min(w->nctas, sms / nranks));  // all CTAs co-resident
+  for (int r = 0; r < nranks; ++r) {
+    w->local[r].rank = r;
+    w->local[r].device = device;
+    FLX_TRY(local_init(w, w->local[r]));
+  }
+  FLX_TRY(alloc_host_staging(w, nullptr));
+  *out = w;
+  return flxSuccess;
+}
+
+flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_hex, World** out) {
+  auto* w = new World();
+  world_config(w, nranks);
+  w->local.resize(1);
+  w->local[0].rank = rank;
+  w->local[0].device = device;
+  FLX_TRY(local_init(w, w->local[0]));
+
+  char boot_name[96], stage_name[96];
+  snprintf(boot_name, sizeof(boot_name), "/flx-%s-boot", id_hex);
+  snprintf(stage_name, sizeof(stage_name), "/flx-%s-stage", id_hex);
+  int fd = shm_open(boot_name, O_CREAT | O_RDWR, 0600);
+  if (fd < 0) return fail(flxSystemError, "shm_open(%s) failed", boot_name);
+  if (ftruncate(fd, sizeof(BootHeader)) != 0) {
+    close(fd);
+    return fail(flxSystemError, "ftruncate(%s) failed", boot_name);
+  }
+  auto* hdr = static_cast<BootHeader*>(
+      mmap(nullptr, sizeof(BootHeader), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0));
+  close(fd);
+  if (hdr == MAP_FAILED) return fail(flxSystemError, "mmap(%s) failed", boot_name);
+
+  BootSlot& mine = hdr->slot[rank];
+  FLX_CUDA(cudaIpcGetMemHandle(&mine.scratch, w->local[0].scratch));
+  FLX_CUDA(cudaIpcGetMemHandle(&mine.flags, w->local[0].flags));
+  FLX_CUDA(cudaDeviceGetPCIBusId(mine.bus_id, sizeof(mine.bus_id), device));
+  mine.device = device;
+  mine.pid = getpid();
+  __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
+  __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
+  const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 300.0;
+  if (!spin_until([&] { return __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE) >= nranks; },
+                  timeout))
+    return fail(flxSystemError, "bootstrap timed out: %d of %d ranks arrived",
+                __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE), nranks);
+  for (int p = 0; p < nranks; ++p) {
+    if (p == rank) {
+      w->peer_scratch[p] = w->local[0].scratch;
+      w->peer_flags[p] = w->local[0].flags;
+      continue;
+    }
+    if (strcmp(hdr->slot[p].bus_id, mine.bus_id) == 0)
+      return fail(flxInvalidUsage, "ranks %d and %d share GPU %s; one GPU per rank", rank, p,
+                  mine.bus_id);
+    void* ptr = nullptr;
+    FLX_CUDA(cudaIpcOpenMemHandle(&ptr, hdr->slot[p].scratch, cudaIpcMemLazyEnablePeerAccess));
+    w->ipc_opened.push_back(ptr);
+    w->peer_scratch[p] = static_cast<char*>(ptr);
+    FLX_CUDA(cudaIpcOpenMemHandle(&ptr, hdr->slot[p].flags, cudaIpcMemLazyEnablePeerAccess));
+    w->ipc_opened.push_back(ptr);
+    w->peer_flags[p] = static_cast<uint32_t*>(ptr);
+  }
+  FLX_TRY(alloc_host_staging(w, stage_name));
+  __atomic_fetch_add(&hdr->mapped, 1, __ATOMIC_ACQ_REL);
+  if (!spin_until([&] { return __atomic_load_n(&hdr->mapped, __ATOMIC_ACQUIRE) >= nranks; },
+                  timeout))
+    return fail(flxSystemError, "bootstrap timed out mapping the staging segment");
+  munmap(hdr, sizeof(BootHeader));
+  if (rank == 0) {
+    shm_unlink(boot_name);
+    shm_unlink(stage_name);
+  }
+  *out = w;
+  return flxSuccess;
+}
+
+void world_attach(World* w, int local, Comm* c) { w->local[local].comm = c; }
+
+int world_release(World* w) {
+  if (++w->destroyed < (int)w->local.size()) return 0;
+  world_free(w);
+  return 1;
+}
+
+}  // namespace flx

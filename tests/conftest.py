@@ -19,3 +19,7 @@ def oracle_lib():
 
     oracle.build()
     return oracle
+
+# Loopback worlds put 3 streams per emulated rank on one device; give every
+# stream its own hardware queue (must be set before CUDA initialises).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")

@@ -1,0 +1,138 @@
+"""GPU parity of the multi-GPU engine, emulated on one device (flxCommInitLoopback).
+
+Same kernels and protocols as one-process-per-GPU: push/reduce/pull over
+peer-mapped scratch with release/acquire epoch flags (here the "peers" are
+other ranks' buffers on the same GPU, the kernel launched cooperatively over
+all ranks), and the host-hub PCIe path with cross-rank counter semaphores.
+Results must equal the CPU oracle bit for bit.
+"""
+
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from paper_2510_15882_b200 import comm as flx  # noqa: E402
+from paper_2510_15882_b200.links import PathKind  # noqa: E402
+from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
+
+from test_gpu_parity import TORCH_DT, OPS, _inputs, _np  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    flx.load_library()
+    oracle.build()
+
+
+def _allreduce(n, count, dtype, op, granules, inplace=False, calls=1, seed=0):
+    cpu = _inputs(n, count, dtype, seed)
+    sends = [t.cuda() for t in cpu]
+    recvs = sends if inplace else [torch.empty_like(s) for s in sends]
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, granules)
+        for _ in range(calls):
+            if inplace:
+                for s, c in zip(sends, cpu):
+                    s.copy_(c)
+            w.all_reduce(sends, recvs, op=op)
+        torch.cuda.synchronize()
+        got = [_np(r, dtype) for r in recvs]
+        align = w.comms[0].alignment(CollectiveOp.ALLREDUCE)
+        pb = w.path_bytes()
+    want = oracle.allreduce([_np(c, dtype) for c in cpu], dtype, OPS[op], granules, align)
+    return got, want, pb
+
+
+@pytest.mark.parametrize("n,count,dtype,op,granules", [
+    (2, 4096, 7, "sum", (1000, 0, 0)),
+    (4, (1 << 18) + 5, 7, "sum", (1000, 0, 0)),
+    (8, 1 << 18, 9, "sum", (1000, 0, 0)),
+    (8, (1 << 19) + 3, 7, "sum", (900, 100, 0)),
+    (4, 1 << 19, 9, "sum", (800, 200, 0)),
+    (3, 300007, 2, "max", (850, 150, 0)),
+    (8, 1 << 17, 6, "sum", (700, 300, 0)),
+    (5, 99999, 8, "min", (1000, 0, 0)),
+    (2, 1 << 18, 0, "sum", (500, 500, 0)),
+])
+def test_loopback_allreduce_matches_oracle(n, count, dtype, op, granules):
+    got, want, pb = _allreduce(n, count, dtype, op, granules, seed=n + dtype)
+    for r in range(n):
+        np.testing.assert_array_equal(got[r], want[r], err_msg=f"rank {r}")
+    if granules[1]:
+        assert pb[PathKind.PCIE_STAGED] > 0
+
+
+def test_loopback_repeated_calls_and_inplace():
+    got, want, _ = _allreduce(8, (1 << 18) + 7, 7, "sum", (900, 100, 0), inplace=True, calls=5)
+    for r in range(8):
+        np.testing.assert_array_equal(got[r], want[r])
+    got, want, _ = _allreduce(4, 1 << 18, 9, "sum", (850, 150, 0), calls=7)
+    for r in range(4):
+        np.testing.assert_array_equal(got[r], want[r])
+
+
+def test_loopback_multi_round_scratch():
+    os.environ["FLX_SLOT_MB"] = "1"  # 1 MiB inbox slots -> many rounds per call
+    try:
+        got, want, _ = _allreduce(4, 3 << 20, 7, "sum", (1000, 0, 0), calls=2)
+    finally:
+        del os.environ["FLX_SLOT_MB"]
+    for r in range(4):
+        np.testing.assert_array_equal(got[r], want[r])
+
+
+@pytest.mark.parametrize("n,count,dtype,granules", [
+    (2, 4096, 7, (1000, 0, 0)),
+    (8, (1 << 17) + 1, 9, (1000, 0, 0)),
+    (8, 1 << 18, 9, (900, 100, 0)),
+    (3, 100003, 0, (700, 300, 0)),
+])
+def test_loopback_allgather_matches_oracle(n, count, dtype, granules):
+    cpu = _inputs(n, count, dtype, n)
+    sends = [t.cuda() for t in cpu]
+    recvs = [torch.empty(n * count, dtype=TORCH_DT[dtype], device="cuda") for _ in range(n)]
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLGATHER, granules)
+        for _ in range(3):
+            w.all_gather(sends, recvs)
+        torch.cuda.synchronize()
+        align = w.comms[0].alignment(CollectiveOp.ALLGATHER)
+        got = [_np(r, dtype) for r in recvs]
+    want = oracle.allgather([_np(c, dtype) for c in cpu], dtype, granules, align)
+    for r in range(n):
+        np.testing.assert_array_equal(got[r], want[r])
+
+
+def test_loopback_and_fused_virtual_ranks_agree_bitwise():
+    cpu = _inputs(8, 1 << 18, 9, 77)
+    a = [t.cuda() for t in cpu]
+    b = [t.cuda() for t in cpu]
+    oa = [torch.empty_like(x) for x in a]
+    ob = [torch.empty_like(x) for x in b]
+    with flx.Clique(8, loopback=True) as w, flx.Clique(8) as v:
+        w.set_shares(CollectiveOp.ALLREDUCE, (880, 120, 0))
+        v.set_shares(CollectiveOp.ALLREDUCE, (1000, 0, 0))
+        w.all_reduce(a, oa)
+        v.all_reduce(b, ob)
+        torch.cuda.synchronize()
+    for x, y in zip(oa, ob):
+        assert torch.equal(x, y)
+
+
+def test_loopback_path_times():
+    n = 4
+    dev = [torch.randn(1 << 22, device="cuda") for _ in range(n)]
+    outs = [torch.empty_like(d) for d in dev]
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, (950, 50, 0))
+        for _ in range(3):
+            w.all_reduce(dev, outs)
+        h = w.comms[1].path_times_history(8)
+        assert len(h) == 3 and all(x[PathKind.NVLINK] > 0 and x[PathKind.PCIE_STAGED] > 0 for x in h)

@@ -307,6 +307,24 @@ def run_single_gpu(args) -> None:
         for q in range(n):
             assert torch.equal(ag_recv[r][q * ag_count:(q + 1) * ag_count], ag_send[q])
 
+    cfg4 = run_config4(clique, sends, recvs, topo, args, stream) if not args.skip_config4 else None
+
+    # ---- the multi-GPU engine (flxCommInitRank code path) emulated on this GPU
+    loop = flx.Clique(n, device=0, loopback=True)
+    loop.set_shares(CollectiveOp.ALLREDUCE, (1000, 0, 0))
+    for _ in range(2):
+        loop.all_reduce(sends, recvs)
+    loop_dt = _time_steps(lambda: loop.all_reduce(sends, recvs), args.steps, stream)
+    assert all(torch.equal(r, exact) for r in recvs), "loopback allreduce mismatch"
+    loop.set_shares(CollectiveOp.ALLREDUCE, (990, 10, 0))
+    loop.all_reduce(sends, recvs)
+    torch.cuda.synchronize()
+    assert all(torch.equal(r, exact) for r in recvs), "loopback striped allreduce mismatch"
+    loopback = {"busbw": round(busbw_allreduce(AR_BYTES, loop_dt, n), 2),
+                "ms_per_step": round(loop_dt * 1e3, 4),
+                "note": "8 ranks of the one-process-per-GPU engine sharing one GPU's HBM "
+                        "(push/reduce/pull through peer-mapped scratch; 3 HBM passes)"}
+    loop.destroy()
     cpu = cpu_allreduce_sample(args.cpu_seconds)
     total = AR_BYTES
     line = {
@@ -356,6 +374,8 @@ def run_single_gpu(args) -> None:
         "gpu_launches": launches,
         "clocks": clocks,
         "nccl": None,
+        "config4": cfg4,
+        "loopback_engine": loopback,
         "allgather": {
             "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, n), 2), "unit": "GB/s",
             "dtype": "bf16", "out_bytes": AG_OUT_BYTES, "ms_per_step": round(ag_dt * 1e3, 4),
@@ -369,6 +389,60 @@ def run_single_gpu(args) -> None:
     }
     clique.destroy()
     print(json.dumps(line), flush=True)
+
+
+def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
+    """BASELINE config 4: NVLink path capped to few SMs to emulate an H800-class
+    link ratio, so the balancer has real headroom to give to PCIe.
+
+    With 8 virtual ranks on one GPU the PCIe path carries every rank's bytes
+    over ONE PCIe link, i.e. 1/8 of a per-GPU link per rank.  The cap is chosen
+    so NVLink-only busbw : PCIe-only busbw matches H800's 200:64 GB/s per
+    direction (topo.py:130), then Stage 1 (+guard) tunes
+    the split on the real path and both are timed.
+    """
+    from paper_2510_15882_b200 import comm as flx
+    from paper_2510_15882_b200.links import PathKind
+    from paper_2510_15882_b200.stage1 import TunerConfig
+    from paper_2510_15882_b200.striping import CollectiveOp
+
+    n = len(sends)
+
+    def busbw_with(shares, ctas, steps=8):
+        clique.set_nvlink_ctas(ctas)
+        clique.set_shares(CollectiveOp.ALLREDUCE, shares, AR_BYTES)
+        for _ in range(2):
+            clique.all_reduce(sends, recvs)
+        dt = _time_steps(lambda: clique.all_reduce(sends, recvs), steps, stream)
+        return busbw_allreduce(AR_BYTES, dt, n), dt
+
+    pcie_only, _ = busbw_with((0, 1000, 0), 0, steps=3)
+    target = pcie_only * 200.0 / 64.0
+    best = None
+    for ctas in (1, 2, 3, 4, 6, 8, 12, 16):
+        bw, _ = busbw_with((1000, 0, 0), ctas, steps=3)
+        if best is None or abs(bw - target) < abs(best[1] - target):
+            best = (ctas, bw)
+    ctas = best[0]
+    clique.set_nvlink_ctas(ctas)
+    shares, trace, tuned_s, base_s = flx.tune_shares(
+        clique, topo, CollectiveOp.ALLREDUCE, sends, recvs, TunerConfig(), warmup=1, repeats=3)
+    nv_only, nv_dt = busbw_with((1000, 0, 0), ctas, steps=args.steps)
+    striped, st_dt = busbw_with(shares, ctas, steps=args.steps)
+    pbytes = clique.path_bytes()
+    clique.set_nvlink_ctas(args.nvlink_ctas)
+    clique.set_shares(CollectiveOp.ALLREDUCE, (1000, 0, 0), AR_BYTES)
+    return {
+        "workload": "config 4: AllReduce fp32 256 MiB/rank, 8 virtual ranks, NVLink-path kernel "
+                    "capped to emulate H800's NVLink:PCIe ratio (200:64 per direction)",
+        "nvlink_ctas": ctas, "pcie_only_busbw": round(pcie_only, 2),
+        "nvlink_only_busbw": round(nv_only, 2), "striped_busbw": round(striped, 2),
+        "gain_pct": round(100 * (striped / nv_only - 1), 2),
+        "shares": {k.short: shares.get(k) for k in PathKind},
+        "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
+        "stage1_iterations": trace.iterations, "stage1_trace": [r.action for r in trace.records],
+        "ms_per_step": {"nvlink_only": round(nv_dt * 1e3, 4), "striped": round(st_dt * 1e3, 4)},
+    }
 
 
 # --------------------------------------------------------------- N > 1
@@ -436,13 +510,14 @@ def run_multi_gpu(args) -> None:
 def main() -> None:
     p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["flexlink", "reference"], default="flexlink")
     p.add_argument("--nvlink-ctas", type=int, default=0,
                    help="cap the NVLink-path kernel's CTAs (config 4)")
     p.add_argument("--shares", default="", help="N>1: fixed granules nvlink,pcie,rdma")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
+    p.add_argument("--skip-config4", action="store_true")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "flexlink":
         args.warmup = 3

@@ -152,6 +152,11 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   c->sm_count = prop.multiProcessorCount;
   FLX_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+  FLX_CUDA(cudaStreamCreateWithFlags(&c->red, cudaStreamNonBlocking));
+  for (int b = 0; b < 2; ++b) {
+    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_landed[b], cudaEventDisableTiming));
+    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_folded[b], cudaEventDisableTiming));
+  }
   for (auto& t : c->timing) {
     FLX_CUDA(cudaEventCreate(&t.start));
     FLX_CUDA(cudaEventCreate(&t.nv));
@@ -172,8 +177,14 @@ flxResult_t clique_destroy(Clique* c) {
   cudaSetDevice(c->device);
   cudaStreamSynchronize(c->d2h);
   cudaStreamSynchronize(c->h2d);
+  cudaStreamSynchronize(c->red);
   cudaStreamDestroy(c->d2h);
   cudaStreamDestroy(c->h2d);
+  cudaStreamDestroy(c->red);
+  for (int b = 0; b < 2; ++b) {
+    cudaEventDestroy(c->ev_landed[b]);
+    cudaEventDestroy(c->ev_folded[b]);
+  }
   for (auto& t : c->timing) {
     cudaEventDestroy(t.start);
     cudaEventDestroy(t.nv);
@@ -194,6 +205,7 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
   if (c->stage_cap >= chunk && c->stage_bufs == bufs) return flxSuccess;
   FLX_CUDA(cudaStreamSynchronize(c->d2h));
   FLX_CUDA(cudaStreamSynchronize(c->h2d));
+  FLX_CUDA(cudaStreamSynchronize(c->red));
   if (c->host_stage) FLX_CUDA(cudaFreeHost(c->host_stage));
   if (c->dev_stage) FLX_CUDA(cudaFree(c->dev_stage));
   c->host_stage = nullptr;
@@ -305,10 +317,15 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_CUDA(cudaMemcpyAsync(host + i * pitch, static_cast<const char*>(calls[i].send) + at,
                                  len, cudaMemcpyDeviceToHost, c->d2h));
       FLX_TRY(sem_write(c->d2h, sem_full, lap + 1));
-      // consumer: wait full, H2D the whole slot, mark empty, reduce-on-receive
+      // consumer: wait full (and the device slot drained by its last fold),
+      // H2D the whole slot, mark empty; reduce-on-receive runs on its own
+      // stream so the next H2D starts immediately
       FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
+      FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[buf], 0));
       FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, n, cudaMemcpyHostToDevice, c->h2d));
       FLX_TRY(sem_write(c->h2d, sem_empty, lap + 1));
+      FLX_CUDA(cudaEventRecord(c->ev_landed[buf], c->h2d));
+      FLX_CUDA(cudaStreamWaitEvent(c->red, c->ev_landed[buf], 0));
       if (gather) {
         FanoutArgs a{};
         for (int i = 0; i < n; ++i) {
@@ -318,7 +335,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         a.nsrc = a.ndst = n;
         a.bytes = len;
         a.dst_stride = bytes;
-        FLX_CUDA(launch_fanout(a, 4, c->h2d));
+        FLX_CUDA(launch_fanout(a, 16, c->red));
       } else {
         FoldArgs a{};
         for (int i = 0; i < n; ++i) {
@@ -327,10 +344,11 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         }
         a.n = a.ndst = n;
         a.bytes = len;
-        FLX_CUDA(launch_fold(head.dtype, head.op, a, 8, c->h2d));
+        FLX_CUDA(launch_fold(head.dtype, head.op, a, 32, c->red));
       }
+      FLX_CUDA(cudaEventRecord(c->ev_folded[buf], c->red));
     }
-    FLX_CUDA(cudaEventRecord(tm.pcie, c->h2d));
+    FLX_CUDA(cudaEventRecord(tm.pcie, c->red));
   }
 
   // ---- NVLink slice: one fused kernel over all members on the lead stream

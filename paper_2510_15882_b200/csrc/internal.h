@@ -72,7 +72,10 @@ struct Clique {
   int sm_count = 0;
   std::vector<Comm*> members;  // index = position in clique == rank
   cudaStream_t d2h = nullptr;  // PCIe path: producer copies
-  cudaStream_t h2d = nullptr;  // PCIe path: consumer copies + reduce-on-receive
+  cudaStream_t h2d = nullptr;  // PCIe path: consumer copies
+  cudaStream_t red = nullptr;  // PCIe path: reduce-on-receive / fan-out kernels
+  cudaEvent_t ev_landed[2] = {nullptr, nullptr};  // H2D of slot b done
+  cudaEvent_t ev_folded[2] = {nullptr, nullptr};  // fold of slot b done (slot reusable)
   // per-call timing ring: call k uses slot k % kTimingSlots
   static constexpr int kTimingSlots = 64;
   struct Timing {

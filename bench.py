@@ -458,14 +458,38 @@ def run_multi_gpu(args) -> None:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
+    from paper_2510_15882_b200.links import preset
+    from paper_2510_15882_b200.stage1 import TunerConfig, TunerState, initial_tune
+    from paper_2510_15882_b200.striping import CollectiveSpec, ShareDistribution
+
     c = flx.Communicator.from_process_group()
+    if args.nvlink_ctas:
+        c.set_nvlink_ctas(args.nvlink_ctas)
     count = AR_BYTES // 4
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
     send = torch.randint(-1024, 1024, (count,), device="cuda", generator=gen).float()
     recv = torch.empty_like(send)
     stream = torch.cuda.current_stream()
-    shares = [int(x) for x in args.shares.split(",")] if args.shares else [1000, 0, 0]
-    c.set_shares(CollectiveOp.ALLREDUCE, shares)
+    topo = preset("B200", n_gpus=world).restricted(c.available_paths())
+
+    def stage1(op, s, r):
+        """Stage 1 on the real path with rank-agreed timings, then the guard."""
+        if args.shares:
+            g = [int(x) for x in args.shares.split(",")]
+            return ShareDistribution({k: g[int(k)] for k in PathKind if g[int(k)] or k == 0}), None
+        measure = flx.rank_measure_fn(c, op, s, r, warmup=2, repeats=5)
+        spec = CollectiveSpec(op, world, s.numel() * s.element_size())
+        shares, trace = initial_tune(topo, spec, TunerConfig(), measure=measure)
+        nv = ShareDistribution({PathKind.NVLINK: 1000})
+        base = measure(TunerState(shares=nv, active=frozenset({PathKind.NVLINK}), step=1)).total
+        tuned = measure(TunerState(shares=shares, active=frozenset(shares.loaded_paths),
+                                   step=1)).total
+        if tuned >= base:
+            shares = nv
+        c.set_shares(op, shares, spec.size)
+        return shares, trace
+
+    shares, trace = stage1(CollectiveOp.ALLREDUCE, send, recv)
 
     def timed(fn):
         for _ in range(args.warmup):
@@ -483,10 +507,21 @@ def run_multi_gpu(args) -> None:
     launches = flx.launch_count() - launches0
     pbytes = c.path_bytes()
     ref = send.clone()
-    nccl_dt = timed(lambda: (ref.copy_(send), dist.all_reduce(ref)))
-    exact = ref.clone()
-    dist.all_reduce(exact)
+    nccl_dt = timed(lambda: dist.all_reduce(ref))  # in place; values are irrelevant to timing
+    exact = send.clone()
+    dist.all_reduce(exact)  # integer-valued fp32: exact in any order
     ok = torch.equal(recv, exact)
+
+    # AllGather bf16, 256 MiB gathered (config 2)
+    ag_count = AG_OUT_BYTES // 2 // world
+    ag_send = torch.randn(ag_count, device="cuda", generator=gen).bfloat16()
+    ag_recv = torch.empty(ag_count * world, device="cuda", dtype=torch.bfloat16)
+    ag_shares, _ = stage1(CollectiveOp.ALLGATHER, ag_send, ag_recv)
+    ag_dt = timed(lambda: c.all_gather(ag_send, ag_recv))
+    ag_bytes = c.path_bytes()
+    ag_ref = torch.empty_like(ag_recv)
+    ag_nccl_dt = timed(lambda: dist.all_gather_into_tensor(ag_ref, ag_send))
+    ag_ok = torch.equal(ag_recv, ag_ref)
     if rank == 0:
         value = busbw_allreduce(AR_BYTES, dt, world) * 1.0
         print(json.dumps({
@@ -496,11 +531,25 @@ def run_multi_gpu(args) -> None:
             "data": "synthetic",
             "config": {"workload": f"AllReduce sum fp32 256 MiB/rank over {world} GPUs",
                        "bytes_per_rank": AR_BYTES},
-            "shares": {k.short: shares[int(k)] for k in PathKind},
+            "shares": {k.short: shares.get(k) for k in PathKind},
             "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
+            "stage1_trace": [r.action for r in trace.records] if trace else "fixed --shares",
+            "roofline": {"bound": "nvlink", "achieved": round(value, 2),
+                         "peak": round(770.0 + 55.0, 1), "unit": "GB/s",
+                         "frac": round(value / 825.0, 4), "traffic": None,
+                         "note": "busbw vs measured NVLink peer 770 GB/s/dir (B200_PROFILING.md) "
+                                 "+ ~55 GB/s PCIe Gen5 per direction; NIC absent"},
             "nccl": {"value": round(busbw_allreduce(AR_BYTES, nccl_dt, world), 2),
                      "ms_per_step": round(nccl_dt * 1e3, 4)},
             "result_matches_exact_sum": bool(ok), "gpu_launches": launches, "clocks": clocks,
+            "allgather": {
+                "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, world), 2), "unit": "GB/s",
+                "dtype": "bf16", "ms_per_step": round(ag_dt * 1e3, 4),
+                "shares": {k.short: ag_shares.get(k) for k in PathKind},
+                "traffic_share_pct": {k.short: round(100 * ag_bytes[k] / (AG_OUT_BYTES // world), 3)
+                                      for k in PathKind},
+                "nccl": round(busbw_allgather(AG_OUT_BYTES, ag_nccl_dt, world), 2),
+                "matches_nccl_bitwise": bool(ag_ok)},
         }), flush=True)
     dist.barrier()
     c.destroy()

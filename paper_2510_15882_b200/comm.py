@@ -198,9 +198,8 @@ class Communicator:
         """Bootstrap over torch.distributed (one process per GPU)."""
         import torch.distributed as dist
 
-        box = [cls.unique_id() if dist.get_rank(group) == 0 else None]
-        dist.broadcast_object_list(box, src=0, group=group)
-        return cls.init_rank(dist.get_world_size(group), box[0], dist.get_rank(group))
+        uid = broadcast_unique_id(group)
+        return cls.init_rank(dist.get_world_size(group), uid, dist.get_rank(group))
 
     def destroy(self) -> None:
         if self._h:
@@ -285,6 +284,66 @@ class Communicator:
     def available_paths(self) -> tuple[PathKind, ...]:
         m = self.path_mask()
         return tuple(k for k in PathKind if m & (1 << int(k)))
+
+
+def broadcast_unique_id(group=None) -> bytes:
+    """Rank 0 mints a flxUniqueId; every rank of ``group`` receives the same bytes."""
+    import torch.distributed as dist
+
+    box = [Communicator.unique_id() if dist.get_rank(group) == 0 else None]
+    dist.broadcast_object_list(box, src=0, group=group)
+    return box[0]
+
+
+def agree_report(report: PathTimingReport, group=None) -> PathTimingReport:
+    """Max-over-ranks of every path's duration, so all ranks see ONE report.
+
+    Stage 1/2 are deterministic given their inputs (ties break by PathKind,
+    `tuner.py:110-118`, `balancer.py:78-79`), so feeding every rank the agreed
+    report keeps the share tables identical across ranks — required, since a
+    rank whose byte split differed would exchange mismatched slices.
+    """
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+    vals = torch.tensor([report.durations.get(k, -1.0) for k in PathKind], dtype=torch.float64,
+                        device=dev)
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX, group=group)
+    out = {k: float(vals[int(k)]) for k in PathKind if float(vals[int(k)]) >= 0.0}
+    return PathTimingReport.build(report.op, report.n_gpus, report.size, out)
+
+
+def rank_measure_fn(comm: Communicator, op: CollectiveOp, send, recv, group=None,
+                    warmup: int = 2, repeats: int = 5, reduce_op: str = "sum"):
+    """Stage-1 ``MeasureFn`` for one rank of a multi-process communicator:
+    run the real collective with ``state.shares``, take per-path medians of
+    the CUDA-event times, then agree them across ranks (:func:`agree_report`)."""
+    import torch
+
+    op = CollectiveOp(op)
+    nbytes = send.numel() * send.element_size()
+
+    def run():
+        if op == CollectiveOp.ALLREDUCE:
+            comm.all_reduce(send, recv, op=reduce_op)
+        else:
+            comm.all_gather(send, recv)
+
+    def measure(state) -> PathTimingReport:
+        comm.set_shares(op, state.shares, nbytes)
+        for _ in range(warmup):
+            run()
+        for _ in range(repeats):
+            run()
+        hist = comm.path_times_history(repeats)
+        b = comm.path_bytes()
+        torch.cuda.synchronize()
+        durations = {k: statistics.median(h[k] for h in hist) for k in state.active if b[k] > 0}
+        local = PathTimingReport.build(op, comm.nranks, nbytes, durations)
+        return agree_report(local, group)
+
+    return measure
 
 
 def launch_count() -> int:

@@ -166,9 +166,19 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   c->ev_fork.resize(members);
   for (auto& e : c->ev_fork) FLX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // semaphore words: [0,B) semFull, [B,2B) semEmpty; start at zero (staging.py:224-225)
-  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->sems), 4096,
-                         cudaHostAllocMapped | cudaHostAllocPortable));
-  memset(c->sems, 0, 4096);
+  // Producer and consumer streams live on the same GPU here, so the words sit
+  // in device memory (the front end polls them without a PCIe round trip);
+  // FLX_SEM_HOST=1 puts them in pinned host memory as cross-process worlds must.
+  c->sems_on_host = getenv("FLX_SEM_HOST") != nullptr;
+  if (c->sems_on_host) {
+    FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->sems), 4096,
+                           cudaHostAllocMapped | cudaHostAllocPortable));
+    memset(c->sems, 0, 4096);
+  } else {
+    FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->sems), 4096));
+    FLX_CUDA(cudaMemset(c->sems, 0, 4096));
+    FLX_CUDA(cudaDeviceSynchronize());
+  }
   *out = c;
   return flxSuccess;
 }
@@ -194,7 +204,7 @@ flxResult_t clique_destroy(Clique* c) {
   for (auto e : c->ev_fork) cudaEventDestroy(e);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->dev_stage) cudaFree(c->dev_stage);
-  if (c->sems) cudaFreeHost(c->sems);
+  if (c->sems) c->sems_on_host ? cudaFreeHost(c->sems) : cudaFree(c->sems);
   delete c;
   return flxSuccess;
 }
@@ -215,7 +225,11 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
   FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_stage), total, cudaHostAllocPortable));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dev_stage), total));
   // a fresh ring starts a fresh protocol epoch: counters restart from zero
-  memset(c->sems, 0, 4096);
+  if (c->sems_on_host)
+    memset(c->sems, 0, 4096);
+  else
+    FLX_CUDA(cudaMemset(c->sems, 0, 4096));
+  FLX_CUDA(cudaDeviceSynchronize());
   c->piece_seq = 0;
   c->stage_cap = cap;
   c->stage_bufs = bufs;
@@ -288,7 +302,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
 
   const size_t nv = split[flxPathNvlink];
   const size_t pc = split[flxPathPcie];
-  const int grid_nv = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count;
+  static const int ctas_per_sm = getenv("FLX_FOLD_CTAS_PER_SM") ? atoi(getenv("FLX_FOLD_CTAS_PER_SM")) : 1;
+  const int grid_nv = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count * std::max(1, ctas_per_sm);
   const bool gather = head.coll == flxCollAllGather;
 
   // ---- PCIe slice: issue the side-stream pipeline first so its copies start

@@ -89,7 +89,8 @@ struct Clique {
   // host-staged ring: buffers x members x chunk_cap bytes, pinned + device
   char* host_stage = nullptr;
   char* dev_stage = nullptr;
-  uint32_t* sems = nullptr;  // [0..B) semFull, [B..2B) semEmpty (pinned, mapped)
+  uint32_t* sems = nullptr;  // [0..B) semFull, [B..2B) semEmpty
+  bool sems_on_host = false;  // pinned+mapped host words instead of device words
   size_t stage_cap = 0;      // chunk capacity per member
   int stage_bufs = 0;
   uint64_t piece_seq = 0;    // monotone chunk counter -> counter semaphores

@@ -222,6 +222,181 @@ __global__ void __launch_bounds__(512) fanout_vec_kernel(const FanoutArgs a) {
   }
 }
 
+// ------------------------------------------------- TMA bulk-copy variants
+// 1-D bulk copies (cp.async.bulk) stage each source's tile in shared memory
+// behind an mbarrier (complete_tx), the CTA folds smem -> smem, and the
+// result tile leaves through N bulk stores (smem -> global) without touching
+// registers again.  S-stage ring; one CTA of kTmaThreads per SM.
+constexpr int kTmaTile = 4096;    // bytes per source per stage
+constexpr int kTmaStages = 4;
+constexpr int kTmaThreads = 256;  // kTmaThreads * 16 B == kTmaTile
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes,
+                                          uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int NMAX>
+constexpr size_t tma_fold_smem() {
+  return (size_t)kTmaStages * NMAX * kTmaTile + 2 * kTmaTile + kTmaStages * sizeof(uint64_t);
+}
+
+// Requires 16 B aligned src/dst; a.bytes may be ragged (tail < 16 B folded
+// element-wise by CTA 0).
+template <typename T, int OP, int NMAX>
+__global__ void __launch_bounds__(kTmaThreads, 1) fold_tma_kernel(const FoldArgs a) {
+  using A = typename AccT<T>::type;
+  constexpr int kVec = 16 / sizeof(T);
+  extern __shared__ __align__(128) unsigned char smem[];
+  unsigned char* in = smem;                                         // [S][NMAX][tile]
+  unsigned char* out = smem + (size_t)kTmaStages * NMAX * kTmaTile;  // [2][tile]
+  uint64_t* full = reinterpret_cast<uint64_t*>(out + 2 * kTmaTile);  // [S]
+  const int n = a.n;
+  const size_t body = a.bytes & ~(size_t)15;
+  const size_t ntiles = (body + kTmaTile - 1) / kTmaTile;
+  auto tile_bytes = [&](size_t t) -> uint32_t {
+    return (uint32_t)min((size_t)kTmaTile, body - t * kTmaTile);
+  };
+  auto issue = [&](size_t t, int s) {
+    const uint32_t len = tile_bytes(t);
+    mbar_expect_tx(&full[s], len * n);
+    for (int r = 0; r < n; ++r)
+      bulk_load(in + ((size_t)s * NMAX + r) * kTmaTile, a.src[r] + t * kTmaTile, len, &full[s]);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const size_t first = blockIdx.x;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kTmaStages; ++s) {
+      const size_t t = first + (size_t)s * gridDim.x;
+      if (t < ntiles) issue(t, s);
+    }
+  uint32_t iter = 0;
+  for (size_t t = first; t < ntiles; t += gridDim.x, ++iter) {
+    const int s = iter % kTmaStages;
+    const uint32_t parity = (iter / kTmaStages) & 1;
+    const uint32_t len = tile_bytes(t);
+    unsigned char* o = out + (iter & 1) * kTmaTile;
+    if (threadIdx.x == 0) bulk_wait_read<1>();  // out[iter&1] free (store of iter-2 read)
+    mbar_wait(&full[s], parity);
+    __syncthreads();
+    const uint32_t off = threadIdx.x * 16;
+    if (off < len) {
+      const unsigned char* base = in + (size_t)s * NMAX * kTmaTile + off;
+      A acc[kVec];
+      load_acc<T>(acc, *reinterpret_cast<const uint4*>(base));
+#pragma unroll
+      for (int r = 1; r < NMAX; ++r)
+        if (r < n) fold_into<T, OP>(acc, *reinterpret_cast<const uint4*>(base + (size_t)r * kTmaTile));
+      *reinterpret_cast<uint4*>(o + off) = pack_acc<T>(acc);
+    }
+    fence_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int d = 0; d < a.ndst; ++d) bulk_store(a.dst[d] + t * kTmaTile, o, len);
+      bulk_commit();
+      const size_t nxt = t + (size_t)kTmaStages * gridDim.x;
+      if (nxt < ntiles) issue(nxt, s);  // slot s fully consumed (barrier above)
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+  if (blockIdx.x == 0) {  // ragged tail (< 16 B)
+    const size_t tail = (a.bytes - body) / sizeof(T);
+    if (threadIdx.x < tail) {
+      const size_t offb = body + threadIdx.x * sizeof(T);
+      A acc = to_acc<T>(*reinterpret_cast<const T*>(a.src[0] + offb));
+      for (int r = 1; r < n; ++r)
+        acc = apply_op<OP>(acc, to_acc<T>(*reinterpret_cast<const T*>(a.src[r] + offb)));
+      const T v = from_acc<T>(acc);
+      for (int d = 0; d < a.ndst; ++d) *reinterpret_cast<T*>(a.dst[d] + offb) = v;
+    }
+  }
+}
+
+// AllGather fan-out with bulk copies: tile of source r (blockIdx.y) lands in
+// smem once, then goes out to every destination by bulk stores.
+static __global__ void __launch_bounds__(32, 1) fanout_tma_kernel(const FanoutArgs a) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)kTmaStages * kTmaTile * 4);
+  constexpr int kBig = kTmaTile * 4;  // 16 KB tiles: one smem slot per stage
+  const int r = blockIdx.y;
+  const char* src = a.src[r];
+  const size_t shift = (size_t)r * a.dst_stride;
+  const size_t body = a.bytes & ~(size_t)15;
+  const size_t ntiles = (body + kBig - 1) / kBig;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kTmaStages; ++s) mbar_init(&full[s], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  auto len_of = [&](size_t t) { return (uint32_t)min((size_t)kBig, body - t * kBig); };
+  for (int s = 0; s < kTmaStages; ++s) {
+    const size_t t = blockIdx.x + (size_t)s * gridDim.x;
+    if (t < ntiles) {
+      mbar_expect_tx(&full[s], len_of(t));
+      bulk_load(smem + (size_t)s * kBig, src + t * kBig, len_of(t), &full[s]);
+    }
+  }
+  uint32_t iter = 0;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++iter) {
+    const int s = iter % kTmaStages;
+    mbar_wait(&full[s], (iter / kTmaStages) & 1);
+    for (int d = 0; d < a.ndst; ++d) bulk_store(a.dst[d] + shift + t * kBig, smem + (size_t)s * kBig, len_of(t));
+    bulk_commit();
+    const size_t nxt = t + (size_t)kTmaStages * gridDim.x;
+    if (nxt < ntiles) {
+      bulk_wait_read<0>();  // slot s read by the stores just issued
+      mbar_expect_tx(&full[s], len_of(nxt));
+      bulk_load(smem + (size_t)s * kBig, src + nxt * kBig, len_of(nxt), &full[s]);
+    }
+  }
+  bulk_wait_all();
+  if (blockIdx.x == 0)
+    for (size_t i = body; i < a.bytes; ++i)
+      for (int d = 0; d < a.ndst; ++d) a.dst[d][shift + i] = src[i];
+}
+
 static __global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {
   const int r = blockIdx.y;
   const size_t shift = (size_t)r * a.dst_stride;

@@ -19,6 +19,25 @@ cudaError_t fold_vec(const FoldArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+bool use_tma() {
+  static const bool on = getenv("FLX_TMA") && atoi(getenv("FLX_TMA")) != 0;
+  return on;
+}
+
+template <typename T, int OP, int NMAX>
+cudaError_t fold_tma(const FoldArgs& a, int grid, cudaStream_t s) {
+  constexpr size_t smem = tma_fold_smem<NMAX>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(fold_tma_kernel<T, OP, NMAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  fold_tma_kernel<T, OP, NMAX><<<grid, kTmaThreads, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 template <typename T, int OP>
 cudaError_t fold_typed(const FoldArgs& a, int grid, cudaStream_t s) {
   bool vec = true;
@@ -27,6 +46,10 @@ cudaError_t fold_typed(const FoldArgs& a, int grid, cudaStream_t s) {
   if (!vec) {
     fold_scalar_kernel<T, OP><<<grid, 512, 0, s>>>(a);
     return cudaGetLastError();
+  }
+  if (use_tma() && a.n <= 8 && a.ndst <= kMaxRanks) {
+    if (a.n <= 4) return fold_tma<T, OP, 4>(a, grid, s);
+    return fold_tma<T, OP, 8>(a, grid, s);
   }
   const int width = a.n > a.ndst ? a.n : a.ndst;
   if (width <= 2) return fold_vec<T, OP, 2>(a, grid, s);
@@ -77,7 +100,17 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   for (int r = 0; r < a.nsrc; ++r) vec = vec && aligned16(a.src[r]);
   for (int d = 0; d < a.ndst; ++d) vec = vec && aligned16(a.dst[d]);
   const dim3 g(grid, a.nsrc);
-  if (!vec) {
+  if (vec && use_tma()) {
+    constexpr size_t smem = (size_t)kTmaStages * kTmaTile * 4 + kTmaStages * sizeof(uint64_t);
+    static bool configured = false;
+    if (!configured) {
+      cudaError_t e = cudaFuncSetAttribute(fanout_tma_kernel,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      configured = true;
+    }
+    fanout_tma_kernel<<<dim3(grid * 3, a.nsrc), 32, smem, s>>>(a);
+  } else if (!vec) {
     fanout_byte_kernel<<<g, 512, 0, s>>>(a);
   } else if (a.ndst <= 2) {
     fanout_vec_kernel<2, 2><<<g, 512, 0, s>>>(a);

@@ -67,7 +67,28 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr[-4000:]}")
+    build_nccl_shim(force)
     return LIB
+
+
+SHIM = HERE / "libflexlink_nccl.so"
+
+
+def build_nccl_shim(force: bool = False) -> Path | None:
+    """NCCL-named entry points over libflexlink (checked against /usr/include/nccl.h)."""
+    src = CSRC / "nccl_shim.c"
+    hdr = Path("/usr/include/nccl.h")
+    if not hdr.exists():
+        return None
+    if not force and not _stale(SHIM, [src, LIB, ROOT / "include" / "flexlink.h"]):
+        return SHIM
+    cmd = ["gcc", "-O2", "-fPIC", "-shared", "-std=c11", "-Wall", "-Werror", "-o", str(SHIM),
+           str(src), f"-I{ROOT / 'include'}", "-I/usr/local/cuda/include", f"-L{HERE}",
+           "-lflexlink", "-Wl,-rpath,$ORIGIN"]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"nccl shim build failed:\n{res.stderr[-4000:]}")
+    return SHIM
 
 
 if __name__ == "__main__":

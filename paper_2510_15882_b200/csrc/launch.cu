@@ -19,10 +19,16 @@ cudaError_t fold_vec(const FoldArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-bool use_tma() {
-  static const bool on = getenv("FLX_TMA") && atoi(getenv("FLX_TMA")) != 0;
-  return on;
+// FLX_TMA selects the bulk-copy variants: unset -> fan-out only (measured
+// faster: 84.7% vs 81.6% of HBM peak for the 8-rank bf16 AllGather, while the
+// LDG fold is at 91-92% and TMA does not beat it; profiles/r1/variants.jsonl);
+// "0" -> none; "1" -> fold and fan-out.
+int tma_mode() {
+  static const int mode = getenv("FLX_TMA") ? atoi(getenv("FLX_TMA")) : -1;
+  return mode;
 }
+bool use_tma_fold() { return tma_mode() == 1; }
+bool use_tma_fanout() { return tma_mode() != 0; }
 
 template <typename T, int OP, int NMAX>
 cudaError_t fold_tma(const FoldArgs& a, int grid, cudaStream_t s) {
@@ -47,7 +53,7 @@ cudaError_t fold_typed(const FoldArgs& a, int grid, cudaStream_t s) {
     fold_scalar_kernel<T, OP><<<grid, 512, 0, s>>>(a);
     return cudaGetLastError();
   }
-  if (use_tma() && a.n <= 8 && a.ndst <= kMaxRanks) {
+  if (use_tma_fold() && a.n <= 8 && a.ndst <= kMaxRanks) {
     if (a.n <= 4) return fold_tma<T, OP, 4>(a, grid, s);
     return fold_tma<T, OP, 8>(a, grid, s);
   }
@@ -100,7 +106,7 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   for (int r = 0; r < a.nsrc; ++r) vec = vec && aligned16(a.src[r]);
   for (int d = 0; d < a.ndst; ++d) vec = vec && aligned16(a.dst[d]);
   const dim3 g(grid, a.nsrc);
-  if (vec && use_tma()) {
+  if (vec && use_tma_fanout()) {
     constexpr size_t smem = (size_t)kTmaStages * kTmaTile * 4 + kTmaStages * sizeof(uint64_t);
     static bool configured = false;
     if (!configured) {

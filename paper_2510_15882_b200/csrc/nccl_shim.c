@@ -1,0 +1,83 @@
+/*
+ * libflexlink_nccl.so — NCCL-symbol front end for libflexlink.so.
+ *
+ * Compiled against the system /usr/include/nccl.h (NCCL 2.27.3, the version
+ * the paper benchmarked), so the compiler itself checks that
+ * every entry point below has NCCL's exact signature.  An application linked
+ * against NCCL can be pointed at FlexLink for the calls below with
+ * LD_PRELOAD=libflexlink_nccl.so (or by linking this library first); the
+ * type values (ncclDataType_t, ncclRedOp_t, ncclResult_t, the 128-byte
+ * ncclUniqueId) are identical to flexlink.h's, so arguments pass through
+ * unchanged.  Calls NCCL has but FlexLink does not implement (ReduceScatter,
+ * Broadcast, send/recv, ...) are deliberately NOT defined here, so a
+ * preloaded process falls through to the real NCCL for them.
+ */
+#include <nccl.h>
+#include <string.h>
+
+#include "../../include/flexlink.h"
+
+_Static_assert(sizeof(ncclUniqueId) == sizeof(flxUniqueId), "unique id size");
+_Static_assert((int)ncclFloat32 == (int)flxFloat32 && (int)ncclBfloat16 == (int)flxBfloat16,
+               "datatype codes");
+_Static_assert((int)ncclSum == (int)flxSum && (int)ncclMin == (int)flxMin, "reduction codes");
+_Static_assert((int)ncclInvalidUsage == (int)flxInvalidUsage, "result codes");
+
+ncclResult_t ncclGetVersion(int* version) { return (ncclResult_t)flxGetVersion(version); }
+
+const char* ncclGetErrorString(ncclResult_t result) {
+  return flxGetErrorString((flxResult_t)result);
+}
+
+const char* ncclGetLastError(ncclComm_t comm) {
+  (void)comm;
+  return flxGetLastError();
+}
+
+ncclResult_t ncclGetUniqueId(ncclUniqueId* uniqueId) {
+  return (ncclResult_t)flxGetUniqueId((flxUniqueId*)uniqueId);
+}
+
+ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId commId, int rank) {
+  flxUniqueId id;
+  memcpy(&id, &commId, sizeof(id));
+  return (ncclResult_t)flxCommInitRank((flxComm_t*)comm, nranks, id, rank);
+}
+
+ncclResult_t ncclCommInitAll(ncclComm_t* comm, int ndev, const int* devlist) {
+  return (ncclResult_t)flxCommInitAll((flxComm_t*)comm, ndev, devlist);
+}
+
+ncclResult_t ncclCommDestroy(ncclComm_t comm) {
+  return (ncclResult_t)flxCommDestroy((flxComm_t)comm);
+}
+
+ncclResult_t ncclCommCount(const ncclComm_t comm, int* count) {
+  return (ncclResult_t)flxCommCount((flxComm_t)comm, count);
+}
+
+ncclResult_t ncclCommCuDevice(const ncclComm_t comm, int* device) {
+  return (ncclResult_t)flxCommCuDevice((flxComm_t)comm, device);
+}
+
+ncclResult_t ncclCommUserRank(const ncclComm_t comm, int* rank) {
+  return (ncclResult_t)flxCommUserRank((flxComm_t)comm, rank);
+}
+
+ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count,
+                           ncclDataType_t datatype, ncclRedOp_t op, ncclComm_t comm,
+                           cudaStream_t stream) {
+  if ((int)op >= (int)flxNumOps) return ncclInvalidArgument; /* ncclAvg / PreMulSum */
+  return (ncclResult_t)flxAllReduce(sendbuff, recvbuff, count, (flxDataType_t)datatype,
+                                    (flxRedOp_t)op, (flxComm_t)comm, stream);
+}
+
+ncclResult_t ncclAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
+                           ncclDataType_t datatype, ncclComm_t comm, cudaStream_t stream) {
+  return (ncclResult_t)flxAllGather(sendbuff, recvbuff, sendcount, (flxDataType_t)datatype,
+                                    (flxComm_t)comm, stream);
+}
+
+ncclResult_t ncclGroupStart(void) { return (ncclResult_t)flxGroupStart(); }
+
+ncclResult_t ncclGroupEnd(void) { return (ncclResult_t)flxGroupEnd(); }

@@ -276,3 +276,32 @@ def test_invalid_usage_is_loud():
             clique.set_shares(CollectiveOp.ALLREDUCE, (900, 0, 100))  # no NIC path
         with pytest.raises(ValueError):
             clique.comms[0].all_reduce(dev[0])  # virtual rank outside a group
+
+
+def test_nccl_named_entry_points_drive_the_same_path():
+    import ctypes
+
+    shim = flx.library_path().parent / "libflexlink_nccl.so"
+    if not shim.exists():
+        pytest.skip("nccl shim not built")
+    S = ctypes.CDLL(str(shim))
+    n, count = 4, (1 << 16) + 3
+    cpu = _inputs(n, count, 7, seed=5)
+    sends = [t.cuda() for t in cpu]
+    recvs = [torch.empty_like(s) for s in sends]
+    comms = (ctypes.c_void_p * n)()
+    devs = (ctypes.c_int * n)(*([0] * n))
+    assert S.ncclCommInitAll(comms, n, devs) == 0
+    stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert S.ncclGroupStart() == 0
+    for i in range(n):
+        assert S.ncclAllReduce(ctypes.c_void_p(sends[i].data_ptr()),
+                               ctypes.c_void_p(recvs[i].data_ptr()), ctypes.c_size_t(count), 7, 0,
+                               ctypes.c_void_p(comms[i]), stream) == 0
+    assert S.ncclGroupEnd() == 0
+    torch.cuda.synchronize()
+    want = oracle.allreduce([_np(c, 7) for c in cpu], 7, 0)
+    for r in range(n):
+        np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
+    for i in range(n):
+        assert S.ncclCommDestroy(ctypes.c_void_p(comms[i])) == 0

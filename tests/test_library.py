@@ -86,3 +86,21 @@ def test_argument_validation_without_device(lib):
     assert lib.flxGroupEnd() == 5  # unbalanced
     g = (ctypes.c_int * 3)(1000, 0, 0)
     assert lib.flxSetShares(None, 0, -2, g) == 4
+
+
+def test_nccl_shim_exports_nccl_named_entry_points(lib):
+    shim = comm.library_path().parent / "libflexlink_nccl.so"
+    if not shim.exists():
+        pytest.skip("/usr/include/nccl.h absent: shim not built")
+    out = subprocess.run(["nm", "-D", "--defined-only", str(shim)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    for name in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommInitAll", "ncclCommDestroy",
+                 "ncclAllReduce", "ncclAllGather", "ncclGroupStart", "ncclGroupEnd"):
+        assert name in exported
+    assert "ncclReduceScatter" not in exported  # falls through to real NCCL under LD_PRELOAD
+    S = ctypes.CDLL(str(shim))
+    S.ncclGetErrorString.restype = ctypes.c_char_p
+    assert S.ncclGetErrorString(4) == b"invalid argument"
+    uid = (ctypes.c_char * 128)()
+    assert S.ncclGetUniqueId(uid) == 0 and bytes(uid)[:4] == b"FLX1"

@@ -308,6 +308,8 @@ def run_single_gpu(args) -> None:
             assert torch.equal(ag_recv[r][q * ag_count:(q + 1) * ag_count], ag_send[q])
 
     cfg4 = run_config4(clique, sends, recvs, topo, args, stream) if not args.skip_config4 else None
+    del ag_send, ag_recv
+    cfg5 = run_config5(clique, topo, stream) if not args.skip_config5 else None
 
     # ---- the multi-GPU engine (flxCommInitRank code path) emulated on this GPU
     loop = flx.Clique(n, device=0, loopback=True)
@@ -375,6 +377,7 @@ def run_single_gpu(args) -> None:
         "clocks": clocks,
         "nccl": None,
         "config4": cfg4,
+        "config5": cfg5,
         "loopback_engine": loopback,
         "allgather": {
             "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, n), 2), "unit": "GB/s",
@@ -443,6 +446,42 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
         "stage1_iterations": trace.iterations, "stage1_trace": [r.action for r in trace.records],
         "ms_per_step": {"nvlink_only": round(nv_dt * 1e3, 4), "striped": round(st_dt * 1e3, 4)},
     }
+
+
+def run_config5(clique, topo, stream) -> dict:
+    """BASELINE config 5: Qwen-32B-shaped TP=8 prefill at 64K tokens — per layer two
+    AllReduces of a [65536, 5120] bf16 activation (640 MiB per rank), 64 layers.
+    Runs the 128 calls back to back on 8 virtual ranks; reports total comm time."""
+    import torch
+
+    from paper_2510_15882_b200 import comm as flx
+    from paper_2510_15882_b200.links import PathKind
+    from paper_2510_15882_b200.stage1 import TunerConfig
+    from paper_2510_15882_b200.striping import CollectiveOp
+
+    n, tokens, hidden, layers = len(clique.comms), 65536, 5120, 64
+    nbytes = tokens * hidden * 2
+    acts = [torch.randn(tokens, hidden, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
+    outs = [torch.empty_like(x) for x in acts]
+    shares, trace, _, _ = flx.tune_shares(clique, topo, CollectiveOp.ALLREDUCE, acts, outs,
+                                          TunerConfig(), warmup=1, repeats=3)
+    for _ in range(2):
+        clique.all_reduce(acts, outs)
+    total = _time_steps(lambda: clique.all_reduce(acts, outs), 2 * layers, stream) * 2 * layers
+    acc = acts[0].float()
+    for x in acts[1:]:
+        acc += x.float()
+    exact = all(torch.equal(o, acc.bfloat16()) for o in outs)
+    b = clique.path_bytes()
+    del acts, outs
+    return {"workload": "config 5: 64 layers x 2 AllReduce of [65536,5120] bf16 (640 MiB/rank), "
+                        "8 virtual ranks", "calls": 2 * layers,
+            "total_comm_ms": round(total * 1e3, 2),
+            "per_call_ms": round(total / (2 * layers) * 1e3, 4),
+            "busbw": round(busbw_allreduce(nbytes, total / (2 * layers), n), 2),
+            "shares": {k.short: shares.get(k) for k in PathKind},
+            "traffic_share_pct": {k.short: round(100 * b[k] / nbytes, 3) for k in PathKind},
+            "fixed_order_fp32_fold_exact": exact}
 
 
 # --------------------------------------------------------------- N > 1
@@ -567,6 +606,7 @@ def main() -> None:
     p.add_argument("--shares", default="", help="N>1: fixed granules nvlink,pcie,rdma")
     p.add_argument("--cpu-seconds", type=float, default=10.0)
     p.add_argument("--skip-config4", action="store_true")
+    p.add_argument("--skip-config5", action="store_true")
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "flexlink":
         args.warmup = 3

@@ -1,0 +1,57 @@
+"""BASELINE config 3: AllReduce fp32/bf16 message-size sweep 1 MiB - 1 GiB at N = 2/4/8
+(virtual ranks on one GPU), Stage 1 on the real path per size bucket (+ guard), per-link
+traffic split and the Stage-1 trace.  One JSON line per cell."""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2510_15882_b200 import comm as flx  # noqa: E402
+from paper_2510_15882_b200.links import PathKind, preset  # noqa: E402
+from paper_2510_15882_b200.stage1 import TunerConfig  # noqa: E402
+from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
+
+p = argparse.ArgumentParser()
+p.add_argument("--ranks", default="2,4,8")
+p.add_argument("--max-mib", type=int, default=1024)
+p.add_argument("--steps", type=int, default=20)
+p.add_argument("--nvlink-ctas", type=int, default=0)
+a = p.parse_args()
+topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
+for n in [int(x) for x in a.ranks.split(",")]:
+    cl = flx.Clique(n)
+    if a.nvlink_ctas:
+        cl.set_nvlink_ctas(a.nvlink_ctas)
+    for dt, esz, name in ((torch.float32, 4, "fp32"), (torch.bfloat16, 2, "bf16")):
+        mib = 1
+        while mib <= a.max_mib:
+            S = mib << 20
+            s = [torch.randn(S // esz, device="cuda").to(dt) for _ in range(n)]
+            r = [torch.empty_like(x) for x in s]
+            shares, trace, tuned, base = flx.tune_shares(cl, topo, CollectiveOp.ALLREDUCE, s, r,
+                                                         TunerConfig(), warmup=1, repeats=3)
+            for _ in range(3):
+                cl.all_reduce(s, r)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(a.steps):
+                cl.all_reduce(s, r)
+            e1.record()
+            torch.cuda.synchronize()
+            t = e0.elapsed_time(e1) / a.steps * 1e-3
+            b = cl.path_bytes()
+            print(json.dumps({
+                "n": n, "dtype": name, "size_mib": mib, "ms": round(t * 1e3, 4),
+                "busbw": round(S / t * 2 * (n - 1) / n / 1e9, 2),
+                "shares": {k.short: shares.get(k) for k in PathKind},
+                "traffic_pct": {k.short: round(100 * b[k] / S, 3) for k in PathKind},
+                "stage1": {"iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
+                           "nvlink_only_ms": round(base * 1e3, 4),
+                           "trace": [x.action for x in trace.records]}}), flush=True)
+            del s, r
+            mib *= 2
+    cl.destroy()

@@ -615,7 +615,15 @@ def main() -> None:
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if world > 1:
-        run_multi_gpu(args)
+        os.environ.setdefault("FLX_BOOT_TIMEOUT", "60")
+        try:
+            run_multi_gpu(args)
+        except Exception as e:  # report, do not hang the job
+            if int(os.environ.get("RANK", "0")) == 0:
+                print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s",
+                                  "n_gpus": world, "error": f"{type(e).__name__}: {e}"}),
+                      flush=True)
+            raise
     else:
         run_single_gpu(args)
 

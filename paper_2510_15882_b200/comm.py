@@ -395,14 +395,47 @@ class Clique:
         finally:
             _check(L.flxGroupEnd(), "flxGroupEnd")
 
+    def _validate(self, sends, recvs, gather: bool):
+        if len(sends) != self.nranks or len(recvs) != self.nranks:
+            raise ValueError(f"need one send and one recv tensor per rank ({self.nranks})")
+        s0 = sends[0]
+        for s, r in zip(sends, recvs):
+            _contiguous_cuda(s, "send")
+            _contiguous_cuda(r, "recv")
+            want = s0.numel() * (self.nranks if gather else 1)
+            if s.numel() != s0.numel() or s.dtype != s0.dtype or r.numel() != want \
+                    or r.dtype != s0.dtype:
+                raise ValueError("all ranks need same-shaped send/recv tensors of one dtype")
+
+    def _issue(self, fn, sends, recvs, extra, stream) -> None:
+        """One flxGroupStart/End around one call per rank; the stream handle and
+        pointers are resolved once (small messages are host-issue bound)."""
+        L = load_library()
+        s = _stream_handle(stream)
+        count = sends[0].numel()
+        dt = dtype_code(sends[0].dtype)
+        _check(L.flxGroupStart(), "flxGroupStart")
+        rc = 0
+        try:
+            for c, a, b in zip(self.comms, sends, recvs):
+                rc = fn(a.data_ptr(), b.data_ptr(), count, dt, *extra, c._h, s)
+                if rc:
+                    break
+        finally:
+            end = L.flxGroupEnd()
+        _check(rc, fn.__name__)
+        _check(end, "flxGroupEnd")
+
     def all_reduce(self, sends: Sequence, recvs: Sequence | None = None, op: str = "sum",
                    stream=None):
         recvs = list(sends) if recvs is None else list(recvs)
-        self._group(lambda i, c: c.all_reduce(sends[i], recvs[i], op=op, stream=stream))
+        self._validate(sends, recvs, gather=False)
+        self._issue(load_library().flxAllReduce, sends, recvs, (_OPS[op],), stream)
         return recvs
 
     def all_gather(self, sends: Sequence, recvs: Sequence, stream=None):
-        self._group(lambda i, c: c.all_gather(sends[i], recvs[i], stream=stream))
+        self._validate(sends, recvs, gather=True)
+        self._issue(load_library().flxAllGather, sends, recvs, (), stream)
         return recvs
 
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:

@@ -109,7 +109,10 @@ struct World {
   std::vector<void*> ipc_opened;
   int destroyed = 0;
 
-  uint32_t* sem(size_t word) { return reinterpret_cast<uint32_t*>(host) + word; }
+  // semaphore words as the GPU addresses them (registered host memory may map
+  // to a different device address than its host pointer)
+  char* host_dev = nullptr;
+  uint32_t* sem(size_t word) { return reinterpret_cast<uint32_t*>(host_dev) + word; }
   char* hregion(int r) { return host + kSemWords * 4 + (size_t)r * hcap; }
   char* rregion(int r) { return host + kSemWords * 4 + (size_t)nranks * hcap + (size_t)r * hcap; }
 };
@@ -194,6 +197,9 @@ flxResult_t alloc_host_staging(World* w, const char* shm_name) {
   }
   FLX_CUDA(cudaHostRegister(w->host, w->host_bytes,
                             cudaHostRegisterMapped | cudaHostRegisterPortable));
+  void* dev = nullptr;
+  FLX_CUDA(cudaHostGetDevicePointer(&dev, w->host, 0));
+  w->host_dev = static_cast<char*>(dev);
   FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->abort_word), 64,
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *w->abort_word = 0;
@@ -203,7 +209,7 @@ flxResult_t alloc_host_staging(World* w, const char* shm_name) {
 void world_config(World* w, int nranks) {
   w->nranks = nranks;
   w->slot = env_mib("FLX_SLOT_MB", 32);
-  w->hcap = env_mib("FLX_PCIE_STAGE_MB", 32);
+  w->hcap = env_mib("FLX_PCIE_STAGE_MB", 64);
   w->nctas = 32;
   if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));
 }
@@ -538,7 +544,7 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   mine.pid = getpid();
   __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
   __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
-  const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 300.0;
+  const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 60.0;
   if (!spin_until([&] { return __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE) >= nranks; },
                   timeout))
     return fail(flxSystemError, "bootstrap timed out: %d of %d ranks arrived",

@@ -156,6 +156,8 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   for (int b = 0; b < 2; ++b) {
     FLX_CUDA(cudaEventCreateWithFlags(&c->ev_landed[b], cudaEventDisableTiming));
     FLX_CUDA(cudaEventCreateWithFlags(&c->ev_folded[b], cudaEventDisableTiming));
+    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_filled[b], cudaEventDisableTiming));
+    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_drained[b], cudaEventDisableTiming));
   }
   for (auto& t : c->timing) {
     FLX_CUDA(cudaEventCreate(&t.start));
@@ -194,6 +196,8 @@ flxResult_t clique_destroy(Clique* c) {
   for (int b = 0; b < 2; ++b) {
     cudaEventDestroy(c->ev_landed[b]);
     cudaEventDestroy(c->ev_folded[b]);
+    cudaEventDestroy(c->ev_filled[b]);
+    cudaEventDestroy(c->ev_drained[b]);
   }
   for (auto& t : c->timing) {
     cudaEventDestroy(t.start);
@@ -297,6 +301,9 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     FLX_CUDA(cudaEventRecord(c->ev_fork[i], calls[i].stream));
     FLX_CUDA(cudaStreamWaitEvent(s0, c->ev_fork[i], 0));
   }
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FLX_CUDA(cudaStreamIsCapturing(s0, &cap));
+  const bool capturing = cap == cudaStreamCaptureStatusActive;
   Clique::Timing& tm = c->timing[c->calls % Clique::kTimingSlots];
   FLX_CUDA(cudaEventRecord(tm.start, s0));
 
@@ -310,16 +317,28 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   // while the NVLink kernel runs.
   if (pc > 0) {
     const size_t chunk = pick_chunk(lead, pc);
+    if (capturing && (c->stage_cap < chunk || c->stage_bufs != lead->buffers))
+      return fail(flxInvalidUsage,
+                  "PCIe staging must be sized before CUDA-graph capture: run the collective "
+                  "once eagerly with the same size/shares first");
     FLX_TRY(ensure_staging(c, chunk, lead->buffers));
     const int bufs = c->stage_bufs;
     const size_t pitch = c->stage_cap;
     const size_t slot_bytes = pitch * n;
     FLX_CUDA(cudaStreamWaitEvent(c->d2h, tm.start, 0));
     FLX_CUDA(cudaStreamWaitEvent(c->h2d, tm.start, 0));
+    uint64_t local_piece = 0;
+    // inside a capture only events recorded earlier in the SAME capture may be
+    // awaited; the first use of a slot needs no wait (the graph starts after
+    // all earlier work on the caller's stream, including the side streams)
+    bool drained_rec[2] = {false, false}, folded_rec[2] = {false, false};
     for (size_t done = 0; done < pc; done += chunk) {
       const size_t len = std::min(chunk, pc - done);
       const size_t at = nv + done;  // byte offset inside each rank's message
-      const uint64_t piece = c->piece_seq++;
+      // Under capture the monotone counters cannot be baked into a graph that
+      // is replayed, so the same handshake is expressed with captured events
+      // (graph edges); the eager counters are left untouched.
+      const uint64_t piece = capturing ? local_piece++ : c->piece_seq++;
       const int buf = (int)(piece % bufs);
       const uint32_t lap = (uint32_t)(piece / bufs);
       uint32_t* sem_full = c->sems + buf;
@@ -327,18 +346,33 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       char* host = c->host_stage + buf * slot_bytes;
       char* dev = c->dev_stage + buf * slot_bytes;
       // producer: wait slot drained, D2H each rank's piece, mark full
-      FLX_TRY(sem_wait_geq(c->d2h, sem_empty, lap));
+      if (!capturing)
+        FLX_TRY(sem_wait_geq(c->d2h, sem_empty, lap));
+      else if (drained_rec[buf])
+        FLX_CUDA(cudaStreamWaitEvent(c->d2h, c->ev_drained[buf], 0));
       for (int i = 0; i < n; ++i)
         FLX_CUDA(cudaMemcpyAsync(host + i * pitch, static_cast<const char*>(calls[i].send) + at,
                                  len, cudaMemcpyDeviceToHost, c->d2h));
-      FLX_TRY(sem_write(c->d2h, sem_full, lap + 1));
+      if (capturing)
+        FLX_CUDA(cudaEventRecord(c->ev_filled[buf], c->d2h));
+      else
+        FLX_TRY(sem_write(c->d2h, sem_full, lap + 1));
       // consumer: wait full (and the device slot drained by its last fold),
       // H2D the whole slot, mark empty; reduce-on-receive runs on its own
       // stream so the next H2D starts immediately
-      FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
-      FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[buf], 0));
+      if (capturing)
+        FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_filled[buf], 0));
+      else
+        FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
+      if (!capturing || folded_rec[buf])
+        FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[buf], 0));
       FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, n, cudaMemcpyHostToDevice, c->h2d));
-      FLX_TRY(sem_write(c->h2d, sem_empty, lap + 1));
+      if (capturing) {
+        FLX_CUDA(cudaEventRecord(c->ev_drained[buf], c->h2d));
+        drained_rec[buf] = true;
+      } else {
+        FLX_TRY(sem_write(c->h2d, sem_empty, lap + 1));
+      }
       FLX_CUDA(cudaEventRecord(c->ev_landed[buf], c->h2d));
       FLX_CUDA(cudaStreamWaitEvent(c->red, c->ev_landed[buf], 0));
       if (gather) {
@@ -362,6 +396,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_CUDA(launch_fold(head.dtype, head.op, a, 32, c->red));
       }
       FLX_CUDA(cudaEventRecord(c->ev_folded[buf], c->red));
+      folded_rec[buf] = true;
     }
     FLX_CUDA(cudaEventRecord(tm.pcie, c->red));
   }
@@ -404,8 +439,9 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     FLX_CUDA(cudaStreamWaitEvent(calls[i].stream, c->ev_join, 0));
   }
   c->last_bytes = split;
-  tm.used[flxPathNvlink] = nv > 0;
-  tm.used[flxPathPcie] = pc > 0;
+  // events recorded inside a capture are graph edges, not timestamps
+  tm.used[flxPathNvlink] = nv > 0 && !capturing;
+  tm.used[flxPathPcie] = pc > 0 && !capturing;
   tm.used[flxPathRdma] = false;
   c->calls++;
   return flxSuccess;

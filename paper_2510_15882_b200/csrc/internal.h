@@ -76,6 +76,8 @@ struct Clique {
   cudaStream_t red = nullptr;  // PCIe path: reduce-on-receive / fan-out kernels
   cudaEvent_t ev_landed[2] = {nullptr, nullptr};  // H2D of slot b done
   cudaEvent_t ev_folded[2] = {nullptr, nullptr};  // fold of slot b done (slot reusable)
+  cudaEvent_t ev_filled[2] = {nullptr, nullptr};   // capture-mode semFull
+  cudaEvent_t ev_drained[2] = {nullptr, nullptr};  // capture-mode semEmpty
   // per-call timing ring: call k uses slot k % kTimingSlots
   static constexpr int kTimingSlots = 64;
   struct Timing {

@@ -74,12 +74,14 @@ __device__ __forceinline__ bool cta_wait(const uint32_t* p, uint32_t epoch, uint
   if (threadIdx.x == 0) {
     ok = 1;
     const long long t0 = clock64();
+    uint32_t spins = 0;
     while ((int)(ld_acquire_sys(p) - epoch) < 0) {
-      if (*(volatile uint32_t*)abort_word) { ok = 0; break; }
-      if (clock64() - t0 > 20000000000ll) {
-        atomicExch(abort_word, 1u);
-        ok = 0;
-        break;
+      if ((++spins & 4095) == 0) {  // the abort word is host memory: poll it rarely
+        if (*(volatile uint32_t*)abort_word || clock64() - t0 > 20000000000ll) {
+          atomicExch(abort_word, 1u);
+          ok = 0;
+          break;
+        }
       }
     }
   }
@@ -87,13 +89,16 @@ __device__ __forceinline__ bool cta_wait(const uint32_t* p, uint32_t epoch, uint
   return ok;
 }
 
-// Make this CTA's prior global stores visible system-wide, then thread 0
-// publishes `epoch` to each flag in `targets`.
+// Publish this CTA's prior global stores: bar.sync orders every thread's
+// stores before thread 0's sys-scope fence (fences are cumulative), whose
+// release stores then carry them to any rank that acquires the flag.  One
+// fence per CTA, not one per thread.
 __device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, uint32_t epoch) {
-  __threadfence_system();
   __syncthreads();
-  if (threadIdx.x == 0)
+  if (threadIdx.x == 0) {
+    asm volatile("fence.acq_rel.sys;" ::: "memory");
     for (int i = 0; i < count; ++i) st_release_sys(targets[i], epoch);
+  }
   __syncthreads();
 }
 

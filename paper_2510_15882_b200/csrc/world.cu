@@ -296,6 +296,11 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   const size_t nv = split[flxPathNvlink], pc = split[flxPathPcie];
   const bool gather = coll == flxCollAllGather;
   if (*w->abort_word) return fail(flxInternalError, "communicator aborted by an earlier timeout");
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
+  if (cap != cudaStreamCaptureStatusNone)
+    return fail(flxInvalidUsage, "multi-rank collectives carry host-side epochs and cannot be "
+                "captured into a CUDA graph yet");
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
   if (pc > (gather ? w->hcap : w->hcap))
     return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "

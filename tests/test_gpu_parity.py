@@ -305,3 +305,36 @@ def test_nccl_named_entry_points_drive_the_same_path():
         np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
     for i in range(n):
         assert S.ncclCommDestroy(ctypes.c_void_p(comms[i])) == 0
+
+
+@pytest.mark.parametrize("granules", [(1000, 0, 0), (900, 100, 0)])
+def test_cuda_graph_capture_and_replay(granules):
+    # the striped call captured into a CUDA graph (PCIe handshake becomes graph
+    # edges) and replayed on fresh inputs gives the oracle's bits every time
+    n, count = 4, (1 << 18) + 5
+    g = torch.Generator(device="cpu").manual_seed(11)
+    sends = [torch.empty(count, device="cuda") for _ in range(n)]
+    recvs = [torch.empty_like(s) for s in sends]
+    with flx.Clique(n) as clique:
+        clique.set_shares(CollectiveOp.ALLREDUCE, granules)
+        clique.all_reduce(sends, recvs)  # eager warm-up sizes the staging ring
+        torch.cuda.synchronize()
+        stream = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            clique.all_reduce(sends, recvs)
+        align = clique.comms[0].alignment(CollectiveOp.ALLREDUCE)
+        for _ in range(3):
+            host = [torch.randn(count, generator=g) for _ in range(n)]
+            for s, h in zip(sends, host):
+                s.copy_(h)
+            graph.replay()
+            torch.cuda.synchronize()
+            want = oracle.allreduce([h.numpy() for h in host], 7, 0, granules, align)
+            for r in range(n):
+                np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
+        # eager calls still work (and still use the counter semaphores) afterwards
+        clique.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        for r in range(n):
+            np.testing.assert_array_equal(_np(recvs[r], 7), want[r])

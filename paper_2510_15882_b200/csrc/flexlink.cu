@@ -154,8 +154,10 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   FLX_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&c->red, cudaStreamNonBlocking));
   for (int b = 0; b < 2; ++b) {
-    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_landed[b], cudaEventDisableTiming));
-    FLX_CUDA(cudaEventCreateWithFlags(&c->ev_folded[b], cudaEventDisableTiming));
+    for (int m = 0; m < 2; ++m) {
+      FLX_CUDA(cudaEventCreateWithFlags(&c->ev_landed[m][b], cudaEventDisableTiming));
+      FLX_CUDA(cudaEventCreateWithFlags(&c->ev_folded[m][b], cudaEventDisableTiming));
+    }
     FLX_CUDA(cudaEventCreateWithFlags(&c->ev_filled[b], cudaEventDisableTiming));
     FLX_CUDA(cudaEventCreateWithFlags(&c->ev_drained[b], cudaEventDisableTiming));
   }
@@ -194,8 +196,10 @@ flxResult_t clique_destroy(Clique* c) {
   cudaStreamDestroy(c->h2d);
   cudaStreamDestroy(c->red);
   for (int b = 0; b < 2; ++b) {
-    cudaEventDestroy(c->ev_landed[b]);
-    cudaEventDestroy(c->ev_folded[b]);
+    for (int m = 0; m < 2; ++m) {
+      cudaEventDestroy(c->ev_landed[m][b]);
+      cudaEventDestroy(c->ev_folded[m][b]);
+    }
     cudaEventDestroy(c->ev_filled[b]);
     cudaEventDestroy(c->ev_drained[b]);
   }
@@ -365,7 +369,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       else
         FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
       if (!capturing || folded_rec[buf])
-        FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[buf], 0));
+        FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[capturing][buf], 0));
       FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, n, cudaMemcpyHostToDevice, c->h2d));
       if (capturing) {
         FLX_CUDA(cudaEventRecord(c->ev_drained[buf], c->h2d));
@@ -373,8 +377,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       } else {
         FLX_TRY(sem_write(c->h2d, sem_empty, lap + 1));
       }
-      FLX_CUDA(cudaEventRecord(c->ev_landed[buf], c->h2d));
-      FLX_CUDA(cudaStreamWaitEvent(c->red, c->ev_landed[buf], 0));
+      FLX_CUDA(cudaEventRecord(c->ev_landed[capturing][buf], c->h2d));
+      FLX_CUDA(cudaStreamWaitEvent(c->red, c->ev_landed[capturing][buf], 0));
       if (gather) {
         FanoutArgs a{};
         for (int i = 0; i < n; ++i) {
@@ -395,7 +399,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         a.bytes = len;
         FLX_CUDA(launch_fold(head.dtype, head.op, a, 32, c->red));
       }
-      FLX_CUDA(cudaEventRecord(c->ev_folded[buf], c->red));
+      FLX_CUDA(cudaEventRecord(c->ev_folded[capturing][buf], c->red));
       folded_rec[buf] = true;
     }
     FLX_CUDA(cudaEventRecord(tm.pcie, c->red));

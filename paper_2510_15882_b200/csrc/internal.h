@@ -74,8 +74,10 @@ struct Clique {
   cudaStream_t d2h = nullptr;  // PCIe path: producer copies
   cudaStream_t h2d = nullptr;  // PCIe path: consumer copies
   cudaStream_t red = nullptr;  // PCIe path: reduce-on-receive / fan-out kernels
-  cudaEvent_t ev_landed[2] = {nullptr, nullptr};  // H2D of slot b done
-  cudaEvent_t ev_folded[2] = {nullptr, nullptr};  // fold of slot b done (slot reusable)
+  // [mode][slot]: mode 1 = recorded inside a CUDA-graph capture (such an event
+  // may not be awaited by eager work afterwards, so the two modes never share)
+  cudaEvent_t ev_landed[2][2] = {};  // H2D of slot b done
+  cudaEvent_t ev_folded[2][2] = {};  // fold of slot b done (slot reusable)
   cudaEvent_t ev_filled[2] = {nullptr, nullptr};   // capture-mode semFull
   cudaEvent_t ev_drained[2] = {nullptr, nullptr};  // capture-mode semEmpty
   // per-call timing ring: call k uses slot k % kTimingSlots

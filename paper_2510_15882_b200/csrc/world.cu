@@ -230,6 +230,12 @@ template <typename T, int OP>
 cudaError_t launch_rank_allreduce_t(bool loop, const void* args, int nctas, int nranks,
                                     cudaStream_t s) {
   if (loop) {
+    static const bool plain = getenv("FLX_LOOPBACK_PLAIN") != nullptr;  // diagnostics
+    if (plain) {
+      loopback_allreduce_kernel<T, OP><<<dim3(nctas, nranks), 512, 0, s>>>(
+          *static_cast<const LoopbackArgs*>(args));
+      return cudaGetLastError();
+    }
     void* params[] = {const_cast<void*>(args)};
     return cudaLaunchCooperativeKernel((const void*)loopback_allreduce_kernel<T, OP>,
                                        dim3(nctas, nranks), dim3(512), params, 0, s);

@@ -67,39 +67,52 @@ __device__ __forceinline__ uint4 ld_cg(const void* p) {
   return v;
 }
 
-// Thread 0 spins until *p has reached `epoch` (cyclic compare), then the CTA
-// proceeds.  ~10 s timeout -> abort word, so a dead peer cannot hang the GPU.
-__device__ __forceinline__ bool cta_wait(const uint32_t* p, uint32_t epoch, uint32_t* abort_word) {
+// Publish this CTA's prior global stores: bar.sync orders every thread's
+// stores before the flag stores, and st.release.sys is cumulative, so a rank
+// that acquires a flag sees all of them.  Lane i of warp 0 stores flag i, so
+// the N-1 peers are signalled in parallel.
+__device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, uint32_t epoch) {
+  __syncthreads();
+  if (threadIdx.x < (unsigned)count) st_release_sys(targets[threadIdx.x], epoch);
+}
+
+// Flags are compared cyclically ((int)(flag - epoch) >= 0) so epochs may wrap;
+// a ~10 s spin limit sets the host-mapped abort word instead of hanging the GPU
+// when a peer died.
+// Warp 0 waits, one flag per lane, until every peer p != skip has published:
+// lanes 0..15 watch flag(kind1, p) >= e1, lanes 16..31 flag(kind2, p) >= e2
+// (kind2 < 0: unused).  One parallel poll instead of N-1 sequential ones.
+__device__ __forceinline__ bool cta_wait_peers(uint32_t* block, int n, int skip, int cta,
+                                               int kind1, uint32_t e1, int kind2, uint32_t e2,
+                                               uint32_t* abort_word) {
   __shared__ int ok;
-  if (threadIdx.x == 0) {
-    ok = 1;
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    const int src = lane & 15;
+    const int kind = lane < 16 ? kind1 : kind2;
+    const uint32_t e = lane < 16 ? e1 : e2;
+    const bool active = src < n && src != skip && kind >= 0;
+    const uint32_t* f = active ? flag_at(block, kind, src, cta) : nullptr;
     const long long t0 = clock64();
     uint32_t spins = 0;
-    while ((int)(ld_acquire_sys(p) - epoch) < 0) {
+    int good = 1;
+    while (true) {
+      const bool ready = !active || (int)(ld_acquire_sys(f) - e) >= 0;
+      if (__all_sync(0xffffffffu, ready)) break;
       if ((++spins & 4095) == 0) {  // the abort word is host memory: poll it rarely
-        if (*(volatile uint32_t*)abort_word || clock64() - t0 > 20000000000ll) {
-          atomicExch(abort_word, 1u);
-          ok = 0;
+        int bad = 0;
+        if (lane == 0) bad = *(volatile uint32_t*)abort_word || clock64() - t0 > 20000000000ll;
+        if (__shfl_sync(0xffffffffu, bad, 0)) {
+          if (lane == 0) atomicExch(abort_word, 1u);
+          good = 0;
           break;
         }
       }
     }
+    if (lane == 0) ok = good;
   }
   __syncthreads();
   return ok;
-}
-
-// Publish this CTA's prior global stores: bar.sync orders every thread's
-// stores before thread 0's sys-scope fence (fences are cumulative), whose
-// release stores then carry them to any rank that acquires the flag.  One
-// fence per CTA, not one per thread.
-__device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, uint32_t epoch) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("fence.acq_rel.sys;" ::: "memory");
-    for (int i = 0; i < count; ++i) st_release_sys(targets[i], epoch);
-  }
-  __syncthreads();
 }
 
 __device__ __forceinline__ bool aligned16_dev(const void* p) {
@@ -213,12 +226,9 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     size_t off, clen, lo, hi;
     chunk_span(r, &off, &clen);
     cta_part(clen, nctas, cta, &lo, &hi);
-    for (int p = 0; p < n; ++p) {
-      if (p == r) continue;
-      if (!cta_wait(flag_at(a.flags[r], kArrive, p, cta), e, a.abort_word)) return;
-      // my outbox is rewritten below: peers must have pulled last round's
-      if (!cta_wait(flag_at(a.flags[r], kDone, p, cta), e - 1, a.abort_word)) return;
-    }
+    // every peer's push has landed, and (my outbox is rewritten below) every
+    // peer has pulled last round's outbox
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kDone, e - 1, a.abort_word)) return;
     {
       const char* src[kMaxRanks];
       for (int p = 0; p < n; ++p)
@@ -233,12 +243,12 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     // 3) pull every peer's reduced chunk
     uint32_t* done_targets[kMaxRanks];
     nt = 0;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a.abort_word)) return;
     for (int s = 1; s < n; ++s) {
       const int c = (r + s) % n;
       size_t coff, cl, clo, chi;
       chunk_span(c, &coff, &cl);
       cta_part(cl, nctas, cta, &clo, &chi);
-      if (!cta_wait(flag_at(a.flags[r], kReady, c, cta), e, a.abort_word)) return;
       cta_copy(a.recv + base + coff + clo, a.scratch[c] + outbox + clo, chi - clo, true);
       done_targets[nt++] = flag_at(a.flags[c], kDone, r, cta);
     }
@@ -254,8 +264,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     // peers must have drained what I pushed into their inbox last round
-    for (int p = 0; p < n; ++p)
-      if (p != r && !cta_wait(flag_at(a.flags[r], kDone, p, cta), e - 1, a.abort_word)) return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kDone, e - 1, -1, 0, a.abort_word)) return;
     uint32_t* targets[kMaxRanks];
     int nt = 0;
     for (int s = 1; s < n; ++s) {
@@ -267,9 +276,9 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
     cta_signal(targets, nt, e);
     nt = 0;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
-      if (!cta_wait(flag_at(a.flags[r], kArrive, p, cta), e, a.abort_word)) return;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
                a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
       targets[nt++] = flag_at(a.flags[p], kDone, r, cta);

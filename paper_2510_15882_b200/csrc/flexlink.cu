@@ -135,6 +135,28 @@ int path_mask() {
   return mask;
 }
 
+// The device the caller made current.  This library carries its own (static)
+// CUDA runtime, whose per-thread "current device" is not the one torch's
+// runtime set; the driver's current context is shared by both, so ask it.
+flxResult_t current_device(int* dev) {
+  static CUresult (*ctx_get_device)(CUdevice*) = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuCtxGetDevice", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      ctx_get_device = reinterpret_cast<CUresult (*)(CUdevice*)>(fn);
+  });
+  CUdevice d;
+  if (ctx_get_device && ctx_get_device(&d) == CUDA_SUCCESS) {
+    *dev = (int)d;
+    return flxSuccess;
+  }
+  FLX_CUDA(cudaGetDevice(dev));
+  return flxSuccess;
+}
+
 flxResult_t validate_comm(const flxComm* comm) {
   if (comm == nullptr) return fail(flxInvalidArgument, "null communicator");
   return flxSuccess;
@@ -639,7 +661,7 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
   if (nranks > FLX_MAX_VIRTUAL_RANKS)
     return fail(flxInvalidArgument, "at most %d ranks per communicator", FLX_MAX_VIRTUAL_RANKS);
   int dev = 0;
-  FLX_CUDA(cudaGetDevice(&dev));
+  FLX_TRY(current_device(&dev));
   if (nranks == 1) return flxCommInitAll(comm, 1, &dev);
   cudaDeviceProp prop;
   FLX_CUDA(cudaGetDeviceProperties(&prop, dev));

@@ -228,7 +228,15 @@ def run_single_gpu(args) -> None:
     clique = flx.Clique(n, device=0)
     if args.nvlink_ctas:
         clique.set_nvlink_ctas(args.nvlink_ctas)
-    topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
+    # Stage 1 seeds from MEASURED per-link bandwidth (probe), not a datasheet
+    from paper_2510_15882_b200.probe import probe_topology, topology_to_yaml
+
+    try:
+        topo, probe_raw = probe_topology(nranks=n, name="probed-b200-virtual8")
+        link_profile = {"yaml": topology_to_yaml(topo), "raw": probe_raw}
+    except Exception as e:  # keep the bench alive; fall back to the nominal preset
+        topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
+        link_profile = {"error": str(e), "fallback": "preset B200"}
 
     # ---- Stage 1 on the real path (+ guard), then a Stage-2 phase
     t0 = time.perf_counter()
@@ -405,6 +413,7 @@ def run_single_gpu(args) -> None:
         "gpu_launches": launches,
         "clocks": clocks,
         "nccl": None,
+        "link_profile": link_profile,
         "config4": cfg4,
         "config5": cfg5,
         "loopback_engine": loopback,

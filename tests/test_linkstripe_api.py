@@ -106,6 +106,26 @@ def test_load_topology_yaml(tmp_path):
         fl.load_topology(str(bad))
 
 
+def test_probe_yaml_round_trips_through_load_topology(tmp_path):
+    from paper_2510_15882_b200.probe import topology_to_yaml
+
+    topo = TopologySpec(n_gpus=8, links={
+        NV: LinkSpec(NV, 712.5e9, base_latency=3.25e-6),
+        PC: LinkSpec(PC, 49.56e9, base_latency=11.5e-6, staging_chunk=4 * MIB,
+                     per_chunk_overhead=2e-6)}, path_contention=True,
+        shared_interface_bw=57.2e9, name="probed")
+    p = tmp_path / "probed.yaml"
+    p.write_text(topology_to_yaml(topo))
+    back = fl.load_topology(str(p))
+    assert back.name == "probed" and back.n_gpus == 8 and back.path_contention
+    for k in (NV, PC):
+        assert back.link(k).bandwidth_uni == pytest.approx(topo.link(k).bandwidth_uni, rel=1e-9)
+        assert back.link(k).base_latency == pytest.approx(topo.link(k).base_latency, rel=1e-6)
+    assert back.link(PC).staging_chunk == 4 * MIB
+    assert back.shared_interface_bw == pytest.approx(57.2e9)
+    assert fl.initialize_shares(back).get(NV) > 900
+
+
 def test_restricted_and_scaled_copies():
     t = fl.preset("H800")
     r = t.restricted([NV, PC])

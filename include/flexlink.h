@@ -75,8 +75,9 @@ typedef enum { flxSum = 0, flxProd = 1, flxMax = 2, flxMin = 3, flxNumOps = 4 } 
 /* == linkstripe PathKind (topo.py:18-31); also the tie-break order */
 typedef enum { flxPathNvlink = 0, flxPathPcie = 1, flxPathRdma = 2 } flxPath_t;
 
-/* == linkstripe CollectiveOp (collectives.py:26-28) */
-typedef enum { flxCollAllReduce = 0, flxCollAllGather = 1 } flxCollOp_t;
+/* == linkstripe CollectiveOp (collectives.py:26-28), plus ReduceScatter
+ * (ring_steps N-1) */
+typedef enum { flxCollAllReduce = 0, flxCollAllGather = 1, flxCollReduceScatter = 2 } flxCollOp_t;
 
 /* ---- library / errors --------------------------------------------------- */
 flxResult_t flxGetVersion(int* version);
@@ -115,6 +116,12 @@ flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                          cudaStream_t stream);
 flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
                          flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
+/* ncclReduceScatter shape (nccl.h:408-410): sendbuff holds nranks*recvcount
+ * elements, rank r receives the fold of block r; in place when
+ * recvbuff == sendbuff + rank*recvcount.  Partitioned per recv block. */
+flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
+                             flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
+                             cudaStream_t stream);
 flxResult_t flxGroupStart(void);
 flxResult_t flxGroupEnd(void);
 

@@ -84,7 +84,7 @@ static inline uint16_t f32_to_f16(float f) {
 
 /* -------------------------------------------------------------- the fold */
 #define FOLD_INT(T, UT)                                                            \
-  static void fold_##T(const void* const* src, void* const* dst, int n, uint64_t i0, \
+  static void fold_##T(const void* const* src, void* const* dst, int n, int ndst, uint64_t i0, \
                        uint64_t i1, int op) {                                      \
     for (uint64_t i = i0; i < i1; ++i) {                                           \
       T acc = ((const T*)src[0])[i];                                               \
@@ -97,7 +97,7 @@ static inline uint16_t f32_to_f16(float f) {
           default: acc = (x < acc) ? x : acc; break;                               \
         }                                                                          \
       }                                                                            \
-      for (int r = 0; r < n; ++r) ((T*)dst[r])[i] = acc;                           \
+      for (int r = 0; r < ndst; ++r) ((T*)dst[r])[i] = acc;                        \
     }                                                                              \
   }
 
@@ -109,7 +109,7 @@ FOLD_INT(int64_t, uint64_t)
 FOLD_INT(uint64_t, uint64_t)
 
 #define FOLD_FLOAT(NAME, T, A, LOAD, STORE)                                           \
-  static void fold_##NAME(const void* const* src, void* const* dst, int n, uint64_t i0, \
+  static void fold_##NAME(const void* const* src, void* const* dst, int n, int ndst, uint64_t i0, \
                           uint64_t i1, int op) {                                      \
     for (uint64_t i = i0; i < i1; ++i) {                                              \
       A acc = LOAD(((const T*)src[0])[i]);                                            \
@@ -123,7 +123,7 @@ FOLD_INT(uint64_t, uint64_t)
         }                                                                             \
       }                                                                               \
       T out = STORE(acc);                                                             \
-      for (int r = 0; r < n; ++r) ((T*)dst[r])[i] = out;                              \
+      for (int r = 0; r < ndst; ++r) ((T*)dst[r])[i] = out;                           \
     }                                                                                 \
   }
 
@@ -133,7 +133,7 @@ FOLD_FLOAT(f64, double, double, IDENT, IDENT)
 FOLD_FLOAT(bf16, uint16_t, float, bf16_to_f32, f32_to_bf16)
 FOLD_FLOAT(f16, uint16_t, float, f16_to_f32, f32_to_f16)
 
-typedef void (*fold_fn)(const void* const*, void* const*, int, uint64_t, uint64_t, int);
+typedef void (*fold_fn)(const void* const*, void* const*, int, int, uint64_t, uint64_t, int);
 
 static fold_fn pick(int dtype) {
   switch (dtype) {
@@ -214,7 +214,7 @@ int flxo_allreduce(const void* const* send, void* const* recv, int nranks, uint6
       if (hi > elems) hi = elems;
       if (lo >= hi) continue;
       const uint64_t span = hi - lo, plo = lo + span * part / 64, phi = lo + span * (part + 1) / 64;
-      fold(send, recv, nranks, e0 + plo, e0 + phi, op);
+      fold(send, recv, nranks, nranks, e0 + plo, e0 + phi, op);
     }
   }
   return 0;
@@ -240,6 +240,35 @@ int flxo_allgather(const void* const* send, void* const* recv, int nranks, uint6
     for (int q = 0; q < nranks; ++q)
       for (int r = 0; r < nranks; ++r)
         memmove((char*)recv[q] + (uint64_t)r * bytes + at, (const char*)send[r] + at, len);
+  }
+  return 0;
+}
+
+/*
+ * ReduceScatter (ring_steps N-1; the reduce-scatter half of the AllReduce
+ * ring): recv[r][i] = fold_q send[q][r*recvcount + i].  The per-rank recv
+ * block bytes are partitioned per path; each path's slice of every block is
+ * folded in rank order.
+ */
+int flxo_reducescatter(const void* const* send, void* const* recv, int nranks,
+                       uint64_t recvcount, int dtype, int op, const int granules[3],
+                       uint64_t alignment, int threads) {
+  const int esz = flxo_dtype_size(dtype);
+  fold_fn fold = pick(dtype);
+  if (!esz || !fold || nranks < 1 || nranks > 64 || op < 0 || op > 3) return -1;
+  uint64_t split[3];
+  if (flxo_partition(recvcount * esz, granules, alignment, split)) return -1;
+  for (int p = 0; p < 3; ++p)
+    if (split[p] % esz) return -2;
+  set_threads(threads);
+#pragma omp parallel for schedule(static)
+  for (int r = 0; r < nranks; ++r) {
+    const void* rows[64];
+    void* dst[1] = {recv[r]};
+    for (int q = 0; q < nranks; ++q)
+      rows[q] = (const char*)send[q] + (uint64_t)r * recvcount * esz;
+    for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p)
+      if (split[p]) fold(rows, dst, nranks, 1, at / esz, (at + split[p]) / esz, op);
   }
   return 0;
 }

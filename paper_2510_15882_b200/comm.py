@@ -43,7 +43,7 @@ _lib = None
 _RESULTS = {0: "success", 1: "unhandled cuda error", 2: "system error", 3: "internal error",
             4: "invalid argument", 5: "invalid usage", 6: "remote error", 7: "in progress"}
 _OPS = {"sum": 0, "prod": 1, "max": 2, "min": 3}
-_COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1}
+_COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1, CollectiveOp.REDUCESCATTER: 2}
 
 
 class FlexLinkError(RuntimeError):
@@ -90,6 +90,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommCuDevice": [vp, P(ci)],
         "flxAllReduce": [vp, vp, sz, ci, ci, vp, vp],
         "flxAllGather": [vp, vp, sz, ci, vp, vp],
+        "flxReduceScatter": [vp, vp, sz, ci, ci, vp, vp],
         "flxGroupStart": [],
         "flxGroupEnd": [],
         "flxSetShares": [vp, ci, ci, P(ci)],
@@ -232,6 +233,18 @@ class Communicator:
             dtype_code(send.dtype), self._h, _stream_handle(stream)), "flxAllGather")
         return recv
 
+    def reduce_scatter(self, send, recv, op: str = "sum", stream=None):
+        """ncclReduceScatter: ``send`` holds nranks blocks of ``recv.numel()``."""
+        _contiguous_cuda(send, "send")
+        _contiguous_cuda(recv, "recv")
+        if send.numel() != recv.numel() * self.nranks or recv.dtype != send.dtype:
+            raise ValueError("send must hold nranks * recv.numel() elements of recv.dtype")
+        _check(load_library().flxReduceScatter(
+            ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), recv.numel(),
+            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream)),
+            "flxReduceScatter")
+        return recv
+
     # ---- balancer plumbing
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
         bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)
@@ -322,11 +335,14 @@ def rank_measure_fn(comm: Communicator, op: CollectiveOp, send, recv, group=None
     import torch
 
     op = CollectiveOp(op)
-    nbytes = send.numel() * send.element_size()
+    ref = recv if op == CollectiveOp.REDUCESCATTER else send
+    nbytes = ref.numel() * ref.element_size()
 
     def run():
         if op == CollectiveOp.ALLREDUCE:
             comm.all_reduce(send, recv, op=reduce_op)
+        elif op == CollectiveOp.REDUCESCATTER:
+            comm.reduce_scatter(send, recv, op=reduce_op)
         else:
             comm.all_gather(send, recv)
 
@@ -395,24 +411,27 @@ class Clique:
         finally:
             _check(L.flxGroupEnd(), "flxGroupEnd")
 
-    def _validate(self, sends, recvs, gather: bool):
+    def _validate(self, sends, recvs, gather: bool = False, scatter: bool = False):
         if len(sends) != self.nranks or len(recvs) != self.nranks:
             raise ValueError(f"need one send and one recv tensor per rank ({self.nranks})")
         s0 = sends[0]
+        if scatter and s0.numel() % self.nranks:
+            raise ValueError("reduce_scatter send must hold nranks equal blocks")
+        want = s0.numel() * self.nranks if gather else \
+            (s0.numel() // self.nranks if scatter else s0.numel())
         for s, r in zip(sends, recvs):
             _contiguous_cuda(s, "send")
             _contiguous_cuda(r, "recv")
-            want = s0.numel() * (self.nranks if gather else 1)
             if s.numel() != s0.numel() or s.dtype != s0.dtype or r.numel() != want \
                     or r.dtype != s0.dtype:
                 raise ValueError("all ranks need same-shaped send/recv tensors of one dtype")
 
-    def _issue(self, fn, sends, recvs, extra, stream) -> None:
+    def _issue(self, fn, sends, recvs, extra, stream, count: int | None = None) -> None:
         """One flxGroupStart/End around one call per rank; the stream handle and
         pointers are resolved once (small messages are host-issue bound)."""
         L = load_library()
         s = _stream_handle(stream)
-        count = sends[0].numel()
+        count = sends[0].numel() if count is None else count
         dt = dtype_code(sends[0].dtype)
         _check(L.flxGroupStart(), "flxGroupStart")
         rc = 0
@@ -436,6 +455,12 @@ class Clique:
     def all_gather(self, sends: Sequence, recvs: Sequence, stream=None):
         self._validate(sends, recvs, gather=True)
         self._issue(load_library().flxAllGather, sends, recvs, (), stream)
+        return recvs
+
+    def reduce_scatter(self, sends: Sequence, recvs: Sequence, op: str = "sum", stream=None):
+        self._validate(sends, recvs, scatter=True)
+        self._issue(load_library().flxReduceScatter, sends, recvs, (_OPS[op],), stream,
+                    count=recvs[0].numel())
         return recvs
 
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
@@ -474,11 +499,16 @@ class Clique:
         import torch
 
         op = CollectiveOp(op)
-        nbytes = sends[0].numel() * sends[0].element_size()
+        # the byte count the share table is keyed on (per-rank message / send /
+        # recv block, as the C executor partitions it)
+        ref = recvs[0] if op == CollectiveOp.REDUCESCATTER else sends[0]
+        nbytes = ref.numel() * ref.element_size()
 
         def run():
             if op == CollectiveOp.ALLREDUCE:
                 self.all_reduce(sends, recvs, op=reduce_op)
+            elif op == CollectiveOp.REDUCESCATTER:
+                self.reduce_scatter(sends, recvs, op=reduce_op)
             else:
                 self.all_gather(sends, recvs)
 
@@ -514,7 +544,8 @@ def tune_shares(clique: Clique, topo, op: CollectiveOp, sends, recvs, config=Non
     from .striping import CollectiveSpec
 
     op = CollectiveOp(op)
-    nbytes = sends[0].numel() * sends[0].element_size()
+    ref = recvs[0] if op == CollectiveOp.REDUCESCATTER else sends[0]
+    nbytes = ref.numel() * ref.element_size()
     avail = set(clique.comms[0].available_paths())
     paths = tuple(k for k in topo.present_paths if k in avail)
     spec = CollectiveSpec(op, max(2, clique.nranks), nbytes)

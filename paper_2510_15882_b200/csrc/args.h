@@ -31,4 +31,15 @@ struct FanoutArgs {
   size_t dst_stride;  // byte distance between consecutive sources' blocks in dst
 };
 
+// ReduceScatter rows: row y (blockIdx.y, one per destination rank) folds
+// src[0..n) + y*src_stride into dst[y], `bytes` per row.
+struct RowsArgs {
+  const char* src[kMaxRanks];
+  char* dst[kMaxRanks];
+  int n;      // sources per row
+  int nrows;  // destinations
+  size_t bytes;
+  size_t src_stride;
+};
+
 }  // namespace flx

@@ -338,19 +338,22 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   static const int ctas_per_sm = getenv("FLX_FOLD_CTAS_PER_SM") ? atoi(getenv("FLX_FOLD_CTAS_PER_SM")) : 1;
   const int grid_nv = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count * std::max(1, ctas_per_sm);
   const bool gather = head.coll == flxCollAllGather;
+  const bool scatter = head.coll == flxCollReduceScatter;
 
   // ---- PCIe slice: issue the side-stream pipeline first so its copies start
   // while the NVLink kernel runs.
   if (pc > 0) {
     const size_t chunk = pick_chunk(lead, pc);
-    if (capturing && (c->stage_cap < chunk || c->stage_bufs != lead->buffers))
+    // ReduceScatter stages every (source, row) pair: n*n rows of one chunk
+    const size_t need = scatter ? chunk * n : chunk;
+    if (capturing && (c->stage_cap < need || c->stage_bufs != lead->buffers))
       return fail(flxInvalidUsage,
                   "PCIe staging must be sized before CUDA-graph capture: run the collective "
                   "once eagerly with the same size/shares first");
-    FLX_TRY(ensure_staging(c, chunk, lead->buffers));
+    FLX_TRY(ensure_staging(c, need, lead->buffers));
     const int bufs = c->stage_bufs;
-    const size_t pitch = c->stage_cap;
-    const size_t slot_bytes = pitch * n;
+    const size_t pitch = scatter ? chunk : c->stage_cap;  // row pitch in the slot
+    const size_t slot_bytes = c->stage_cap * n;
     FLX_CUDA(cudaStreamWaitEvent(c->d2h, tm.start, 0));
     FLX_CUDA(cudaStreamWaitEvent(c->h2d, tm.start, 0));
     uint64_t local_piece = 0;
@@ -376,9 +379,14 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_TRY(sem_wait_geq(c->d2h, sem_empty, lap));
       else if (drained_rec[buf])
         FLX_CUDA(cudaStreamWaitEvent(c->d2h, c->ev_drained[buf], 0));
-      for (int i = 0; i < n; ++i)
-        FLX_CUDA(cudaMemcpyAsync(host + i * pitch, static_cast<const char*>(calls[i].send) + at,
-                                 len, cudaMemcpyDeviceToHost, c->d2h));
+      for (int i = 0; i < n; ++i) {
+        const char* src = static_cast<const char*>(calls[i].send) + at;
+        if (scatter)  // this piece of every destination row r of rank i: rows at stride `bytes`
+          FLX_CUDA(cudaMemcpy2DAsync(host + (size_t)i * n * pitch, pitch, src, bytes, len, n,
+                                     cudaMemcpyDeviceToHost, c->d2h));
+        else
+          FLX_CUDA(cudaMemcpyAsync(host + i * pitch, src, len, cudaMemcpyDeviceToHost, c->d2h));
+      }
       if (capturing)
         FLX_CUDA(cudaEventRecord(c->ev_filled[buf], c->d2h));
       else
@@ -392,7 +400,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
       if (!capturing || folded_rec[buf])
         FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[capturing][buf], 0));
-      FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, n, cudaMemcpyHostToDevice, c->h2d));
+      FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, scatter ? n * n : n,
+                                 cudaMemcpyHostToDevice, c->h2d));
       if (capturing) {
         FLX_CUDA(cudaEventRecord(c->ev_drained[buf], c->h2d));
         drained_rec[buf] = true;
@@ -411,6 +420,16 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         a.bytes = len;
         a.dst_stride = bytes;
         FLX_CUDA(launch_fanout(a, 16, c->red));
+      } else if (scatter) {
+        RowsArgs a{};
+        for (int i = 0; i < n; ++i) {
+          a.src[i] = dev + (size_t)i * n * pitch;
+          a.dst[i] = static_cast<char*>(calls[i].recv) + at;
+        }
+        a.n = a.nrows = n;
+        a.bytes = len;
+        a.src_stride = pitch;
+        FLX_CUDA(launch_rows(head.dtype, head.op, a, 8, c->red));
       } else {
         FoldArgs a{};
         for (int i = 0; i < n; ++i) {
@@ -440,6 +459,16 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       a.dst_stride = bytes;
       const int gx = std::max(1, grid_nv / n);
       FLX_CUDA(launch_fanout(a, gx, s0));
+    } else if (scatter) {
+      RowsArgs a{};
+      for (int i = 0; i < n; ++i) {
+        a.src[i] = static_cast<const char*>(calls[i].send);
+        a.dst[i] = static_cast<char*>(calls[i].recv);
+      }
+      a.n = a.nrows = n;
+      a.bytes = nv;
+      a.src_stride = bytes;
+      FLX_CUDA(launch_rows(head.dtype, head.op, a, std::max(1, grid_nv / n), s0));
     } else {
       FoldArgs a{};
       for (int i = 0; i < n; ++i) {
@@ -765,6 +794,15 @@ flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
   return enqueue(Call{comm, flxCollAllGather, sendbuff, recvbuff, sendcount, datatype, 0, stream});
 }
 
+flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
+                             flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
+                             cudaStream_t stream) {
+  FLX_TRY(check_call(comm, datatype, op, true));
+  if (recvcount > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
+  return enqueue(
+      Call{comm, flxCollReduceScatter, sendbuff, recvbuff, recvcount, datatype, op, stream});
+}
+
 flxResult_t flxGroupStart(void) {
   ++t_group_depth;
   return flxSuccess;
@@ -778,7 +816,7 @@ flxResult_t flxGroupEnd(void) {
 
 flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]) {
   FLX_TRY(validate_comm(comm));
-  if (op != flxCollAllReduce && op != flxCollAllGather)
+  if (op != flxCollAllReduce && op != flxCollAllGather && op != flxCollReduceScatter)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
   if (!granules) return fail(flxInvalidArgument, "null granules");
   Granules g{{granules[0], granules[1], granules[2]}};
@@ -806,7 +844,7 @@ flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int g
 
 flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granules[3]) {
   FLX_TRY(validate_comm(comm));
-  if (op != flxCollAllReduce && op != flxCollAllGather)
+  if (op != flxCollAllReduce && op != flxCollAllGather && op != flxCollReduceScatter)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
   if (!granules) return fail(flxInvalidArgument, "null granules");
   const ShareTable& t = comm->shares[op];

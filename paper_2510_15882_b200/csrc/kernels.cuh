@@ -222,6 +222,57 @@ __global__ void __launch_bounds__(512) fanout_vec_kernel(const FanoutArgs a) {
   }
 }
 
+// ------------------------------------------------- ReduceScatter rows
+// Row y = blockIdx.y: dst[y] = fold_q(src[q] + y*src_stride), same fold rule.
+template <typename T, int OP, int NMAX>
+__global__ void __launch_bounds__(512) rows_vec_kernel(const RowsArgs a) {
+  using A = typename AccT<T>::type;
+  constexpr int kVec = 16 / sizeof(T);
+  const size_t shift = (size_t)blockIdx.y * a.src_stride;
+  char* dst = a.dst[blockIdx.y];
+  const size_t nvec = a.bytes >> 4;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    uint4 in[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+      if (r < a.n) in[r] = ld_stream(a.src[r] + shift + (v << 4));
+    A acc[kVec];
+    load_acc<T>(acc, in[0]);
+#pragma unroll
+    for (int r = 1; r < NMAX; ++r)
+      if (r < a.n) fold_into<T, OP>(acc, in[r]);
+    st_stream(dst + (v << 4), pack_acc<T>(acc));
+  }
+  if (blockIdx.x == 0) {
+    const size_t base = nvec << 4;
+    const size_t tail = (a.bytes - base) / sizeof(T);
+    if (threadIdx.x < tail) {
+      const size_t off = base + threadIdx.x * sizeof(T);
+      A acc = to_acc<T>(*reinterpret_cast<const T*>(a.src[0] + shift + off));
+      for (int r = 1; r < a.n; ++r)
+        acc = apply_op<OP>(acc, to_acc<T>(*reinterpret_cast<const T*>(a.src[r] + shift + off)));
+      *reinterpret_cast<T*>(dst + off) = from_acc<T>(acc);
+    }
+  }
+  (void)kVec;
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(512) rows_scalar_kernel(const RowsArgs a) {
+  using A = typename AccT<T>::type;
+  const size_t shift = (size_t)blockIdx.y * a.src_stride;
+  T* dst = reinterpret_cast<T*>(a.dst[blockIdx.y]);
+  const size_t count = a.bytes / sizeof(T);
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    A acc = to_acc<T>(reinterpret_cast<const T*>(a.src[0] + shift)[i]);
+    for (int r = 1; r < a.n; ++r)
+      acc = apply_op<OP>(acc, to_acc<T>(reinterpret_cast<const T*>(a.src[r] + shift)[i]));
+    dst[i] = from_acc<T>(acc);
+  }
+}
+
 // ------------------------------------------------- TMA bulk-copy variants
 // 1-D bulk copies (cp.async.bulk) stage each source's tile in shared memory
 // behind an mbarrier (complete_tx), the CTA folds smem -> smem, and the

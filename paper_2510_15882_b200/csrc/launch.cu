@@ -97,6 +97,60 @@ cudaError_t launch_fold(int dtype, int op, const FoldArgs& a, int grid, cudaStre
   return cudaErrorInvalidValue;
 }
 
+namespace {
+
+template <typename T, int OP>
+cudaError_t rows_typed(const RowsArgs& a, int grid, cudaStream_t s) {
+  bool vec = (a.src_stride & 15) == 0;
+  for (int r = 0; r < a.n; ++r) vec = vec && aligned16(a.src[r]);
+  for (int d = 0; d < a.nrows; ++d) vec = vec && aligned16(a.dst[d]);
+  const dim3 g(grid, a.nrows);
+  if (!vec)
+    rows_scalar_kernel<T, OP><<<g, 512, 0, s>>>(a);
+  else if (a.n <= 2)
+    rows_vec_kernel<T, OP, 2><<<g, 512, 0, s>>>(a);
+  else if (a.n <= 4)
+    rows_vec_kernel<T, OP, 4><<<g, 512, 0, s>>>(a);
+  else if (a.n <= 8)
+    rows_vec_kernel<T, OP, 8><<<g, 512, 0, s>>>(a);
+  else
+    rows_vec_kernel<T, OP, 16><<<g, 512, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t rows_op(int op, const RowsArgs& a, int grid, cudaStream_t s) {
+  switch (op) {
+    case kSum: return rows_typed<T, kSum>(a, grid, s);
+    case kProd: return rows_typed<T, kProd>(a, grid, s);
+    case kMax: return rows_typed<T, kMax>(a, grid, s);
+    case kMin: return rows_typed<T, kMin>(a, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+cudaError_t launch_rows(int dtype, int op, const RowsArgs& a, int grid, cudaStream_t s) {
+  if (a.bytes == 0) return cudaSuccess;
+  if (a.n < 1 || a.n > kMaxRanks || a.nrows < 1 || a.nrows > kMaxRanks || grid < 1)
+    return cudaErrorInvalidValue;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  switch (dtype) {
+    case flxInt8: return rows_op<int8_t>(op, a, grid, s);
+    case flxUint8: return rows_op<uint8_t>(op, a, grid, s);
+    case flxInt32: return rows_op<int32_t>(op, a, grid, s);
+    case flxUint32: return rows_op<uint32_t>(op, a, grid, s);
+    case flxInt64: return rows_op<int64_t>(op, a, grid, s);
+    case flxUint64: return rows_op<uint64_t>(op, a, grid, s);
+    case flxFloat16: return rows_op<__half>(op, a, grid, s);
+    case flxFloat32: return rows_op<float>(op, a, grid, s);
+    case flxFloat64: return rows_op<double>(op, a, grid, s);
+    case flxBfloat16: return rows_op<__nv_bfloat16>(op, a, grid, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   if (a.bytes == 0) return cudaSuccess;
   if (a.nsrc < 1 || a.nsrc > kMaxRanks || a.ndst < 1 || a.ndst > kMaxRanks || grid < 1)

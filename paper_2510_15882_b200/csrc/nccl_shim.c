@@ -8,7 +8,7 @@
  * LD_PRELOAD=libflexlink_nccl.so (or by linking this library first); the
  * type values (ncclDataType_t, ncclRedOp_t, ncclResult_t, the 128-byte
  * ncclUniqueId) are identical to flexlink.h's, so arguments pass through
- * unchanged.  Calls NCCL has but FlexLink does not implement (ReduceScatter,
+ * unchanged.  Calls NCCL has but FlexLink does not implement (Reduce,
  * Broadcast, send/recv, ...) are deliberately NOT defined here, so a
  * preloaded process falls through to the real NCCL for them.
  */
@@ -76,6 +76,14 @@ ncclResult_t ncclAllGather(const void* sendbuff, void* recvbuff, size_t sendcoun
                            ncclDataType_t datatype, ncclComm_t comm, cudaStream_t stream) {
   return (ncclResult_t)flxAllGather(sendbuff, recvbuff, sendcount, (flxDataType_t)datatype,
                                     (flxComm_t)comm, stream);
+}
+
+ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
+                               ncclDataType_t datatype, ncclRedOp_t op, ncclComm_t comm,
+                               cudaStream_t stream) {
+  if ((int)op >= (int)flxNumOps) return ncclInvalidArgument;
+  return (ncclResult_t)flxReduceScatter(sendbuff, recvbuff, recvcount, (flxDataType_t)datatype,
+                                        (flxRedOp_t)op, (flxComm_t)comm, stream);
 }
 
 ncclResult_t ncclGroupStart(void) { return (ncclResult_t)flxGroupStart(); }

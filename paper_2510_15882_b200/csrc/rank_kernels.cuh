@@ -22,8 +22,16 @@
 namespace flx {
 
 constexpr int kMaxCtas = 128;
-enum FlagKind { kArrive = 0, kReady = 1, kDone = 2 };
-constexpr size_t kFlagWords = 3 * kMaxRanks * kMaxCtas;
+// Flag kinds, each [src][cta] in the RECEIVING rank's block:
+//   kArrive  src pushed its data into my inbox[src] for epoch e
+//   kFree    src finished reading the inbox slot I pushed into (epoch e) —
+//            set by EVERY protocol every round, so "kFree >= e-1" is a valid
+//            reuse guard whatever collective ran before
+//   kReady   (AllReduce) src's reduced outbox for epoch e is readable
+//   kPulled  (AllReduce) src finished pulling my outbox of epoch e
+enum FlagKind { kArrive = 0, kFree = 1, kReady = 2, kPulled = 3 };
+constexpr int kFlagKinds = 4;
+constexpr size_t kFlagWords = (size_t)kFlagKinds * kMaxRanks * kMaxCtas;
 
 struct RankArgs {
   const char* send;
@@ -36,6 +44,7 @@ struct RankArgs {
   size_t rank_stride;  // AllGather: distance between rank blocks in recv
   size_t slot;         // inbox slot capacity (bytes) per source rank
   uint32_t epoch;      // epoch of round 0; round k uses epoch + k
+  uint32_t prev_outbox_epoch;  // AllReduce: epoch of the previous AllReduce round (0: none)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
 };
 
@@ -197,63 +206,86 @@ __device__ __forceinline__ void cta_part(size_t len, int nctas, int cta, size_t*
   *hi = min(len, *lo + part);
 }
 
+// Every protocol: wait until peer c freed the inbox slot I push into
+// (kFree >= e-1), push, announce (kArrive = e); the receiver consumes its
+// inbox and answers kFree = e.
+
 template <typename T, int OP>
 __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t round_cap = a.slot * n;
   const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
+  uint32_t prev_outbox = a.prev_outbox_epoch;
   for (size_t base = 0, k = 0; base < a.bytes; base += round_cap, ++k) {
     const uint32_t e = a.epoch + (uint32_t)k;
     const size_t len = min(round_cap, a.bytes - base);
     const size_t chunk = ceil16((len + n - 1) / n);
-    auto chunk_span = [&](int c, size_t* off, size_t* clen) {
-      *off = min(len, (size_t)c * chunk);
-      *clen = min(len, *off + chunk) - *off;
-    };
-    // 1) push my chunk c (part cta) into peer c's inbox slot r
-    uint32_t* arrive_targets[kMaxRanks];
-    int nt = 0;
-    for (int s = 1; s < n; ++s) {
-      const int c = (r + s) % n;
-      size_t off, clen, lo, hi;
-      chunk_span(c, &off, &clen);
-      cta_part(clen, nctas, cta, &lo, &hi);
-      cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, a.send + base + off + lo, hi - lo, false);
-      arrive_targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    size_t lo[kMaxRanks], hi[kMaxRanks], off[kMaxRanks];
+    const char* from[kMaxRanks];
+    size_t nb[kMaxRanks];
+    for (int c = 0; c < n; ++c) {
+      off[c] = min(len, (size_t)c * chunk);
+      cta_part(min(len, off[c] + chunk) - off[c], nctas, cta, &lo[c], &hi[c]);
+      from[c] = a.send + base + off[c] + lo[c];
+      nb[c] = hi[c] - lo[c];
     }
-    cta_signal(arrive_targets, nt, e);
-    // 2) reduce my chunk r from every source, in rank order
-    size_t off, clen, lo, hi;
-    chunk_span(r, &off, &clen);
-    cta_part(clen, nctas, cta, &lo, &hi);
-    // every peer's push has landed, and (my outbox is rewritten below) every
-    // peer has pulled last round's outbox
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kDone, e - 1, a.abort_word)) return;
+    // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it)
+    //    (inbox offsets are relative to the chunk, so shift by lo[c])
+    {
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      uint32_t* targets[kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo[c], from[c], nb[c], false);
+        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+      }
+      cta_signal(targets, nt, e);
+    }
+    // 2) every push landed, and every peer pulled my previous outbox
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a.abort_word))
+      return;
     {
       const char* src[kMaxRanks];
       for (int p = 0; p < n; ++p)
-        src[p] = (p == r) ? a.send + base + off + lo : a.scratch[r] + (size_t)p * a.slot + lo;
-      char* dst[2] = {a.recv + base + off + lo, a.scratch[r] + outbox + lo};
-      cta_fold<T, OP>(dst, 2, src, n, hi - lo);
+        src[p] = (p == r) ? a.send + base + off[r] + lo[r]
+                          : a.scratch[r] + (size_t)p * a.slot + lo[r];
+      char* dst[2] = {a.recv + base + off[r] + lo[r], a.scratch[r] + outbox + lo[r]};
+      cta_fold<T, OP>(dst, 2, src, n, hi[r] - lo[r]);
     }
-    uint32_t* ready_targets[kMaxRanks];
-    nt = 0;
-    for (int s = 1; s < n; ++s) ready_targets[nt++] = flag_at(a.flags[(r + s) % n], kReady, r, cta);
-    cta_signal(ready_targets, nt, e);
+    {  // inbox slots consumed (kFree) and outbox readable (kReady), to every peer
+      uint32_t* targets[2 * kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        targets[nt++] = flag_at(a.flags[c], kFree, r, cta);
+        targets[nt++] = flag_at(a.flags[c], kReady, r, cta);
+      }
+      cta_signal(targets, nt, e);
+    }
     // 3) pull every peer's reduced chunk
-    uint32_t* done_targets[kMaxRanks];
-    nt = 0;
     if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a.abort_word)) return;
-    for (int s = 1; s < n; ++s) {
-      const int c = (r + s) % n;
-      size_t coff, cl, clo, chi;
-      chunk_span(c, &coff, &cl);
-      cta_part(cl, nctas, cta, &clo, &chi);
-      cta_copy(a.recv + base + coff + clo, a.scratch[c] + outbox + clo, chi - clo, true);
-      done_targets[nt++] = flag_at(a.flags[c], kDone, r, cta);
+    {
+      uint32_t* targets[kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        cta_copy(a.recv + base + off[c] + lo[c], a.scratch[c] + outbox + lo[c], nb[c], true);
+        targets[nt++] = flag_at(a.flags[c], kPulled, r, cta);
+      }
+      cta_signal(targets, nt, e);
     }
-    cta_signal(done_targets, nt, e);
+    prev_outbox = e;
   }
+}
+
+// After consuming my inbox slots for epoch e: tell every source (kFree = e).
+__device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e) {
+  const int r = a.rank, n = a.nranks;
+  uint32_t* targets[kMaxRanks];
+  int nt = 0;
+  for (int s = 1; s < n; ++s) targets[nt++] = flag_at(a.flags[(r + s) % n], kFree, r, cta);
+  cta_signal(targets, nt, e);
 }
 
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
@@ -263,33 +295,78 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     const size_t len = min(a.slot, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
-    // peers must have drained what I pushed into their inbox last round
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kDone, e - 1, -1, 0, a.abort_word)) return;
-    uint32_t* targets[kMaxRanks];
-    int nt = 0;
-    for (int s = 1; s < n; ++s) {
-      const int c = (r + s) % n;
-      cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, a.send + base + lo, hi - lo, false);
-      targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    const char* from[kMaxRanks];
+    size_t nb[kMaxRanks];
+    for (int c = 0; c < n; ++c) {
+      from[c] = a.send + base + lo;
+      nb[c] = hi - lo;
     }
-    char* own = a.recv + (size_t)r * a.rank_stride + base;
-    if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
-    cta_signal(targets, nt, e);
-    nt = 0;
+    {  // push my slice into every peer's inbox slot r (at my part's offset)
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      uint32_t* targets[kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, from[c], nb[c], false);
+        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+      }
+      char* own = a.recv + (size_t)r * a.rank_stride + base;
+      if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
+      cta_signal(targets, nt, e);
+    }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
                a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
-      targets[nt++] = flag_at(a.flags[p], kDone, r, cta);
     }
-    cta_signal(targets, nt, e);
+    free_all(a, cta, e);
+  }
+}
+
+// ReduceScatter: a.bytes = NVLink part of each recv block, a.rank_stride = the
+// block stride R in send.  Push block c to peer c, fold my block in rank order.
+template <typename T, int OP>
+__device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
+  const int r = a.rank, n = a.nranks;
+  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = a.epoch + (uint32_t)k;
+    const size_t len = min(a.slot, a.bytes - base);
+    size_t lo, hi;
+    cta_part(len, nctas, cta, &lo, &hi);
+    {
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      uint32_t* targets[kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo,
+                 a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
+        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+      }
+      cta_signal(targets, nt, e);
+    }
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+    {
+      const char* src[kMaxRanks];
+      for (int p = 0; p < n; ++p)
+        src[p] = (p == r) ? a.send + (size_t)r * a.rank_stride + base + lo
+                          : a.scratch[r] + (size_t)p * a.slot + lo;
+      char* dst[1] = {a.recv + base + lo};
+      cta_fold<T, OP>(dst, 1, src, n, hi - lo);
+    }
+    free_all(a, cta, e);
   }
 }
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
   rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(512) rank_reducescatter_kernel(const RankArgs a) {
+  rank_reducescatter<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
@@ -300,6 +377,11 @@ __global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
   rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+}
+
+template <typename T, int OP>
+__global__ void __launch_bounds__(512) loopback_reducescatter_kernel(const __grid_constant__ LoopbackArgs a) {
+  rank_reducescatter<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(512) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {

@@ -15,7 +15,11 @@
 //                3 D2H  recv sub r    -> R_r           rprod[r]   = e
 //                4 H2D  R_c           -> recv sub c    rcons[c][r] = e
 //     AllGather  1 D2H  send          -> H_r           gprod[r]   = e
-//                2 H2D  H_c           -> recv block c  gcons[c][r] = e
+//                2 H2D  H_c           -> recv block c  cons[c][r] = e
+//     ReduceScatter = AllReduce steps 1-2 on the PCIe part of each recv block.
+//   Reuse guards: H_r is rewritten only when every reader of the previous
+//   PCIe epoch has set cons[r][p] (all protocols set it); R_r only after the
+//   previous AllReduce's readers set rcons.
 //   Issue order is global (all ranks' step 1, then step 2, ...) so every wait
 //   refers to a write issued earlier: no deadlock even when streams share a
 //   hardware queue (loopback).
@@ -46,9 +50,12 @@ constexpr int kSemWords = 4096;  // uint32 words at the head of the staging segm
 inline size_t sem_prod(int r, int c) { return 0 * 256 + r * kMaxRanks + c; }
 inline size_t sem_cons(int r, int c) { return 1 * 256 + r * kMaxRanks + c; }
 inline size_t sem_rcons(int r, int c) { return 2 * 256 + r * kMaxRanks + c; }
-inline size_t sem_gcons(int r, int c) { return 3 * 256 + r * kMaxRanks + c; }
 inline size_t sem_rprod(int r) { return 4 * 256 + r; }
 inline size_t sem_gprod(int r) { return 4 * 256 + kMaxRanks + r; }
+// sem_cons(r, p) = e: reader p finished reading region H_r for PCIe epoch e —
+// written by every protocol, so "all readers >= e-1" guards H_r whatever
+// collective used it last.  sem_rcons guards R_r, which only AllReduce uses,
+// against the last AllReduce epoch.
 
 size_t env_mib(const char* name, size_t dflt) {
   const char* v = getenv(name);
@@ -82,6 +89,8 @@ struct World {
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t hcap = 0;       // PCIe staging bytes per rank region
   uint32_t epoch = 1;    // NVLink-path flag epoch (next round)
+  uint32_t last_ar_epoch = 0;  // last AllReduce round (guards outbox reuse)
+  uint32_t last_ar_pepoch = 0;  // last AllReduce PCIe epoch (guards R_r reuse)
   uint32_t pepoch = 1;   // PCIe-path semaphore epoch (next call)
   // host staging segment: [sem words][H_0 .. H_{n-1}][R_0 .. R_{n-1}]
   char* host = nullptr;
@@ -226,50 +235,53 @@ bool spin_until(F pred, double seconds) {
 }
 
 // ------------------------------------------------------------- launches
-template <typename T, int OP>
-cudaError_t launch_rank_allreduce_t(bool loop, const void* args, int nctas, int nranks,
-                                    cudaStream_t s) {
+// SCATTER selects ReduceScatter (push + fold) instead of AllReduce (push +
+// fold + pull); both share dtype/op dispatch.
+template <typename T, int OP, bool SCATTER>
+cudaError_t launch_rank_reduce_t(bool loop, const void* args, int nctas, int nranks,
+                                 cudaStream_t s) {
   if (loop) {
-    static const bool plain = getenv("FLX_LOOPBACK_PLAIN") != nullptr;  // diagnostics
-    if (plain) {
-      loopback_allreduce_kernel<T, OP><<<dim3(nctas, nranks), 512, 0, s>>>(
-          *static_cast<const LoopbackArgs*>(args));
-      return cudaGetLastError();
-    }
+    const void* fn = SCATTER ? (const void*)loopback_reducescatter_kernel<T, OP>
+                             : (const void*)loopback_allreduce_kernel<T, OP>;
     void* params[] = {const_cast<void*>(args)};
-    return cudaLaunchCooperativeKernel((const void*)loopback_allreduce_kernel<T, OP>,
-                                       dim3(nctas, nranks), dim3(512), params, 0, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(nctas, nranks), dim3(512), params, 0, s);
   }
-  rank_allreduce_kernel<T, OP><<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  const RankArgs& a = *static_cast<const RankArgs*>(args);
+  if (SCATTER)
+    rank_reducescatter_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
+  else
+    rank_allreduce_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
   return cudaGetLastError();
 }
 
-template <typename T>
-cudaError_t launch_rank_allreduce_op(int op, bool loop, const void* a, int nctas, int n,
-                                     cudaStream_t s) {
+template <typename T, bool SCATTER>
+cudaError_t launch_rank_reduce_op(int op, bool loop, const void* a, int nctas, int n,
+                                  cudaStream_t s) {
   switch (op) {
-    case kSum: return launch_rank_allreduce_t<T, kSum>(loop, a, nctas, n, s);
-    case kProd: return launch_rank_allreduce_t<T, kProd>(loop, a, nctas, n, s);
-    case kMax: return launch_rank_allreduce_t<T, kMax>(loop, a, nctas, n, s);
-    case kMin: return launch_rank_allreduce_t<T, kMin>(loop, a, nctas, n, s);
+    case kSum: return launch_rank_reduce_t<T, kSum, SCATTER>(loop, a, nctas, n, s);
+    case kProd: return launch_rank_reduce_t<T, kProd, SCATTER>(loop, a, nctas, n, s);
+    case kMax: return launch_rank_reduce_t<T, kMax, SCATTER>(loop, a, nctas, n, s);
+    case kMin: return launch_rank_reduce_t<T, kMin, SCATTER>(loop, a, nctas, n, s);
   }
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_rank_allreduce(int dtype, int op, bool loop, const void* a, int nctas, int n,
-                                  cudaStream_t s) {
+template <bool SCATTER>
+cudaError_t launch_rank_reduce(int dtype, int op, bool loop, const void* a, int nctas, int n,
+                               cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (dtype) {
-    case flxInt8: return launch_rank_allreduce_op<int8_t>(op, loop, a, nctas, n, s);
-    case flxUint8: return launch_rank_allreduce_op<uint8_t>(op, loop, a, nctas, n, s);
-    case flxInt32: return launch_rank_allreduce_op<int32_t>(op, loop, a, nctas, n, s);
-    case flxUint32: return launch_rank_allreduce_op<uint32_t>(op, loop, a, nctas, n, s);
-    case flxInt64: return launch_rank_allreduce_op<int64_t>(op, loop, a, nctas, n, s);
-    case flxUint64: return launch_rank_allreduce_op<uint64_t>(op, loop, a, nctas, n, s);
-    case flxFloat16: return launch_rank_allreduce_op<__half>(op, loop, a, nctas, n, s);
-    case flxFloat32: return launch_rank_allreduce_op<float>(op, loop, a, nctas, n, s);
-    case flxFloat64: return launch_rank_allreduce_op<double>(op, loop, a, nctas, n, s);
-    case flxBfloat16: return launch_rank_allreduce_op<__nv_bfloat16>(op, loop, a, nctas, n, s);
+    case flxInt8: return launch_rank_reduce_op<int8_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxUint8: return launch_rank_reduce_op<uint8_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxInt32: return launch_rank_reduce_op<int32_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxUint32: return launch_rank_reduce_op<uint32_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxInt64: return launch_rank_reduce_op<int64_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxUint64: return launch_rank_reduce_op<uint64_t, SCATTER>(op, loop, a, nctas, n, s);
+    case flxFloat16: return launch_rank_reduce_op<__half, SCATTER>(op, loop, a, nctas, n, s);
+    case flxFloat32: return launch_rank_reduce_op<float, SCATTER>(op, loop, a, nctas, n, s);
+    case flxFloat64: return launch_rank_reduce_op<double, SCATTER>(op, loop, a, nctas, n, s);
+    case flxBfloat16:
+      return launch_rank_reduce_op<__nv_bfloat16, SCATTER>(op, loop, a, nctas, n, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -288,6 +300,14 @@ cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nr
 
 }  // namespace
 
+// Before rank r overwrites its host region H_r at PCIe epoch e, every reader
+// of the previous epoch must be done with it.
+static flxResult_t wait_region_free(World* w, cudaStream_t s, int r, uint32_t e) {
+  for (int p = 0; p < w->nranks; ++p)
+    if (p != r) FLX_TRY(sem_wait_geq(s, w->sem(sem_cons(r, p)), e - 1));
+  return flxSuccess;
+}
+
 // One collective over every local rank of a world; calls[i] is local rank i.
 flxResult_t run_world(World* w, const std::vector<const void*>& send,
                       const std::vector<void*>& recv, const std::vector<cudaStream_t>& streams,
@@ -301,6 +321,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   if (split[flxPathRdma] > 0) return fail(flxInvalidUsage, "rdma path is not available");
   const size_t nv = split[flxPathNvlink], pc = split[flxPathPcie];
   const bool gather = coll == flxCollAllGather;
+  const bool scatter = coll == flxCollReduceScatter;
   if (*w->abort_word) return fail(flxInternalError, "communicator aborted by an earlier timeout");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
@@ -308,7 +329,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     return fail(flxInvalidUsage, "multi-rank collectives carry host-side epochs and cannot be "
                 "captured into a CUDA graph yet");
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
-  if (pc > (gather ? w->hcap : w->hcap))
+  if ((scatter ? pc * n : pc) > w->hcap)
     return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
                 "FLX_PCIE_STAGE_MB or lower the pcie share)", pc, w->hcap);
 
@@ -334,15 +355,51 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[&L - &w->local[0]]->start, 0));
       FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[&L - &w->local[0]]->start, 0));
     }
-    if (!gather) {
+    if (scatter) {
+      // step 1: D2H the PCIe part of my block c into H_r[c]; step 2: the owner
+      // lands every source's copy of its block and folds it in rank order
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        FLX_TRY(wait_region_free(w, L.d2h, r, e));
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * pc,
+                                   static_cast<const char*>(send[i]) + (size_t)c * bytes + nv, pc,
+                                   cudaMemcpyDeviceToHost, L.d2h));
+          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
+        }
+      }
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int s = 1; s < n; ++s) {
+          const int p = (r - s + n) % n;
+          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
+          FLX_CUDA(cudaMemcpyAsync(L.dstage + p * pc, w->hregion(p) + r * pc, pc,
+                                   cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
+        }
+        FoldArgs a{};
+        for (int p = 0; p < n; ++p)
+          a.src[p] = (p == r) ? static_cast<const char*>(send[i]) + (size_t)r * bytes + nv
+                              : L.dstage + p * pc;
+        a.dst[0] = static_cast<char*>(recv[i]) + nv;
+        a.n = n;
+        a.ndst = 1;
+        a.bytes = pc;
+        FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
+        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+      }
+    } else if (!gather) {
       const size_t q = pc / n;  // alignment makes pc a multiple of n*4096
       // step 1: D2H my sub-chunk c into H_r[c]
       for (int i = 0; i < nl; ++i) {
         World::Local& L = w->local[i];
         const int r = L.rank;
+        FLX_TRY(wait_region_free(w, L.d2h, r, e));
         for (int s = 1; s < n; ++s) {
           const int c = (r + s) % n;
-          FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_cons(r, c)), e - 1));
           FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * q,
                                    static_cast<const char*>(send[i]) + nv + c * q, q,
                                    cudaMemcpyDeviceToHost, L.d2h));
@@ -376,7 +433,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         const int r = L.rank;
         FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done, 0));
         for (int p = 0; p < n; ++p)
-          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_rcons(r, p)), e - 1));
+          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_rcons(r, p)), w->last_ar_pepoch));
         FLX_CUDA(cudaMemcpyAsync(w->rregion(r), static_cast<char*>(recv[i]) + nv + r * q, q,
                                  cudaMemcpyDeviceToHost, L.d2h));
         FLX_TRY(sem_write(L.d2h, w->sem(sem_rprod(r)), e));
@@ -394,13 +451,13 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         }
         FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
       }
+      w->last_ar_pepoch = e;
     } else {
       // step 1: D2H my send slice into H_r (all readers of last call done)
       for (int i = 0; i < nl; ++i) {
         World::Local& L = w->local[i];
         const int r = L.rank;
-        for (int p = 0; p < n; ++p)
-          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_gcons(r, p)), e - 1));
+        FLX_TRY(wait_region_free(w, L.d2h, r, e));
         FLX_CUDA(cudaMemcpyAsync(w->hregion(r), static_cast<const char*>(send[i]) + nv, pc,
                                  cudaMemcpyDeviceToHost, L.d2h));
         FLX_TRY(sem_write(L.d2h, w->sem(sem_gprod(r)), e));
@@ -418,7 +475,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
           FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_gprod(c)), e));
           FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + (size_t)c * bytes + nv,
                                    w->hregion(c), pc, cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_gcons(c, r)), e));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(c, r)), e));
         }
         FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
       }
@@ -428,8 +485,9 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   // ---------------- NVLink slice
   if (nv > 0) {
     const uint32_t e0 = w->epoch;
-    const size_t round_cap = gather ? w->slot : w->slot * n;
-    w->epoch += (uint32_t)((nv + round_cap - 1) / round_cap);
+    const size_t round_cap = (gather || scatter) ? w->slot : w->slot * n;
+    const uint32_t rounds = (uint32_t)((nv + round_cap - 1) / round_cap);
+    w->epoch += rounds;
     LoopbackArgs la;
     memset(&la, 0, sizeof(la));
     for (int i = 0; i < nl; ++i) {
@@ -446,11 +504,15 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.rank_stride = bytes;
       a.slot = w->slot;
       a.epoch = e0;
+      a.prev_outbox_epoch = w->last_ar_epoch;
       a.abort_word = w->abort_word;
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
-    cudaError_t err = gather ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
-                             : launch_rank_allreduce(dtype, op, w->loopback, args, w->nctas, n, s0);
+    cudaError_t err =
+        gather    ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
+        : scatter ? launch_rank_reduce<true>(dtype, op, w->loopback, args, w->nctas, n, s0)
+                  : launch_rank_reduce<false>(dtype, op, w->loopback, args, w->nctas, n, s0);
+    if (!gather && !scatter) w->last_ar_epoch = e0 + rounds - 1;
     if (err != cudaSuccess)
       return fail(flxUnhandledCudaError, "rank kernel launch: %s", cudaGetErrorString(err));
   }

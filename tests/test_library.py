@@ -96,9 +96,10 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
                          text=True, check=True).stdout
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     for name in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommInitAll", "ncclCommDestroy",
-                 "ncclAllReduce", "ncclAllGather", "ncclGroupStart", "ncclGroupEnd"):
+                 "ncclAllReduce", "ncclAllGather", "ncclReduceScatter", "ncclGroupStart",
+                 "ncclGroupEnd"):
         assert name in exported
-    assert "ncclReduceScatter" not in exported  # falls through to real NCCL under LD_PRELOAD
+    assert "ncclBroadcast" not in exported  # falls through to real NCCL under LD_PRELOAD
     S = ctypes.CDLL(str(shim))
     S.ncclGetErrorString.restype = ctypes.c_char_p
     assert S.ncclGetErrorString(4) == b"invalid argument"

@@ -107,6 +107,24 @@ def test_bf16_and_fp16_rounding_match_torch_and_numpy():
                                            dtype=np.uint16), tail.astype(np.float16).view(np.uint16))
 
 
+@pytest.mark.parametrize("dtype", [0, 2, 6, 7, 8, 9])
+@pytest.mark.parametrize("op", [0, 2])
+def test_reducescatter_oracle_matches_numpy(dtype, op):
+    rng = np.random.default_rng(100 + dtype + op)
+    n, count = 5, 1237
+    sends = _rand(dtype, n, n * count, rng)
+    got = oracle.reducescatter(sends, dtype, op, (600, 400, 0), 16)
+    for r in range(n):
+        want = oracle.fold_numpy([s[r * count:(r + 1) * count] for s in sends], dtype, op)
+        np.testing.assert_array_equal(np.asarray(got[r]).view(np.uint8),
+                                      np.asarray(want).view(np.uint8))
+    # reduce_scatter == the matching block of an all_reduce
+    full = oracle.allreduce(sends, dtype, op)
+    for r in range(n):
+        np.testing.assert_array_equal(np.asarray(got[r]).view(np.uint8),
+                                      full[0][r * count:(r + 1) * count].view(np.uint8))
+
+
 def test_oracle_rejects_bad_arguments():
     with pytest.raises(ValueError):
         oracle.partition(10, (500, 400, 0), 0)

@@ -335,8 +335,18 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
 
   const size_t nv = split[flxPathNvlink];
   const size_t pc = split[flxPathPcie];
-  static const int ctas_per_sm = getenv("FLX_FOLD_CTAS_PER_SM") ? atoi(getenv("FLX_FOLD_CTAS_PER_SM")) : 1;
-  const int grid_nv = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count * std::max(1, ctas_per_sm);
+  // Uncapped, the fold runs one 16 B vector per thread (grid = slice/8 KiB):
+  // measured 6.73 TB/s vs 6.24 TB/s for one persistent CTA per SM
+  // (profiles/r1/fold_variants_standalone.jsonl) — CTA turnover hides the
+  // tail and DRAM turnaround better than a grid-stride loop.  A cap
+  // (flxSetNvlinkCtas, config 4) makes it a persistent grid-stride kernel.
+  static const int ctas_per_sm = getenv("FLX_FOLD_CTAS_PER_SM") ? atoi(getenv("FLX_FOLD_CTAS_PER_SM")) : 0;
+  const size_t nvec_nv = split[flxPathNvlink] / 16;
+  const int grid_nv =
+      lead->nvlink_ctas > 0 ? lead->nvlink_ctas
+      : ctas_per_sm > 0     ? c->sm_count * ctas_per_sm
+                            : (int)std::max<size_t>(c->sm_count,
+                                                    std::min<size_t>((nvec_nv + 511) / 512, 1u << 30));
   const bool gather = head.coll == flxCollAllGather;
   const bool scatter = head.coll == flxCollReduceScatter;
 
@@ -457,7 +467,10 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       a.nsrc = a.ndst = n;
       a.bytes = nv;
       a.dst_stride = bytes;
-      const int gx = std::max(1, grid_nv / n);
+      // fan-out keeps the persistent per-SM shape (its TMA variant pipelines
+      // several tiles per CTA); a cap divides over the sources
+      const int fan = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count;
+      const int gx = std::max(1, fan / n);
       FLX_CUDA(launch_fanout(a, gx, s0));
     } else if (scatter) {
       RowsArgs a{};

@@ -467,10 +467,13 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       a.nsrc = a.ndst = n;
       a.bytes = nv;
       a.dst_stride = bytes;
-      // fan-out keeps the persistent per-SM shape (its TMA variant pipelines
-      // several tiles per CTA); a cap divides over the sources
-      const int fan = lead->nvlink_ctas > 0 ? lead->nvlink_ctas : c->sm_count;
-      const int gx = std::max(1, fan / n);
+      // one vector per thread per source row when uncapped (6.25 TB/s vs 5.27
+      // persistent, 0.84 of peak for the TMA variant:
+      // profiles/r1/fanout_variants_standalone.jsonl); a cap divides over sources
+      const int gx = lead->nvlink_ctas > 0
+                         ? std::max(1, lead->nvlink_ctas / n)
+                         : (int)std::max<size_t>(1, std::min<size_t>((nv / 16 + 511) / 512,
+                                                                     1u << 30));
       FLX_CUDA(launch_fanout(a, gx, s0));
     } else if (scatter) {
       RowsArgs a{};

@@ -19,16 +19,16 @@ cudaError_t fold_vec(const FoldArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-// FLX_TMA selects the bulk-copy variants: unset -> fan-out only (measured
-// faster: 84.7% vs 81.6% of HBM peak for the 8-rank bf16 AllGather, while the
-// LDG fold is at 91-92% and TMA does not beat it; profiles/r1/variants.jsonl);
-// "0" -> none; "1" -> fold and fan-out.
+// FLX_TMA=1 selects the bulk-copy (cp.async.bulk + mbarrier) variants.  Off
+// by default: with one 16 B vector per thread over a large grid the LDG
+// kernels measure 1.04x (fold) and 0.95x (fan-out) of the copy peak, the TMA
+// ones 0.91x / 0.84x (profiles/r1/*variants*.jsonl).
 int tma_mode() {
-  static const int mode = getenv("FLX_TMA") ? atoi(getenv("FLX_TMA")) : -1;
+  static const int mode = getenv("FLX_TMA") ? atoi(getenv("FLX_TMA")) : 0;
   return mode;
 }
 bool use_tma_fold() { return tma_mode() == 1; }
-bool use_tma_fanout() { return tma_mode() != 0; }
+bool use_tma_fanout() { return tma_mode() == 1; }
 
 template <typename T, int OP, int NMAX>
 cudaError_t fold_tma(const FoldArgs& a, int grid, cudaStream_t s) {

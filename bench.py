@@ -399,7 +399,8 @@ def run_single_gpu(args) -> None:
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4), "traffic": None,
-            "kernel": "fold_vec_kernel<float,Sum,8,1> (NVLink-path slice, 8 virtual ranks)",
+            "kernel": "fold_once_kernel<float,Sum,8> (NVLink-path slice, 8 virtual ranks, "
+                      "one 16 B vector per thread)",
             "algorithmic_bytes_per_launch": nv_alg_bytes,
             "kernel_ms": round(nv_ms, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",

@@ -168,6 +168,44 @@ __global__ void __launch_bounds__(512) fold_vec_kernel(const FoldArgs a) {
   (void)kVec;
 }
 
+// Single-pass form: exactly one 16 B vector per thread, grid covers the slice.
+// No loop-invariant address hoisting, so few registers (high occupancy) and
+// CTA turnover instead of a grid-stride tail: the uncapped default.
+template <typename T, int OP, int NMAX>
+__global__ void __launch_bounds__(512) fold_once_kernel(const FoldArgs a) {
+  using A = typename AccT<T>::type;
+  constexpr int kVec = 16 / sizeof(T);
+  const size_t nvec = a.bytes >> 4;
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < nvec) {
+    uint4 in[NMAX];
+#pragma unroll
+    for (int r = 0; r < NMAX; ++r)
+      if (r < a.n) in[r] = ld_stream(a.src[r] + (v << 4));
+    A acc[kVec];
+    load_acc<T>(acc, in[0]);
+#pragma unroll
+    for (int r = 1; r < NMAX; ++r)
+      if (r < a.n) fold_into<T, OP>(acc, in[r]);
+    const uint4 out = pack_acc<T>(acc);
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d)
+      if (d < a.ndst) st_stream(a.dst[d] + (v << 4), out);
+  } else {  // ragged tail (< 16 B): the first threads past the last vector
+    // (the launcher sizes the grid for nvec + 16 threads)
+    const size_t base = nvec << 4;
+    const size_t j = v - nvec;
+    const size_t i = base + j * sizeof(T);
+    if (j < (a.bytes - base) / sizeof(T)) {
+      A acc = to_acc<T>(*reinterpret_cast<const T*>(a.src[0] + i));
+      for (int r = 1; r < a.n; ++r)
+        acc = apply_op<OP>(acc, to_acc<T>(*reinterpret_cast<const T*>(a.src[r] + i)));
+      const T out = from_acc<T>(acc);
+      for (int d = 0; d < a.ndst; ++d) *reinterpret_cast<T*>(a.dst[d] + i) = out;
+    }
+  }
+}
+
 // Element-at-a-time fallback for buffers that are not 16-byte aligned.
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) fold_scalar_kernel(const FoldArgs a) {
@@ -446,6 +484,28 @@ static __global__ void __launch_bounds__(32, 1) fanout_tma_kernel(const FanoutAr
   if (blockIdx.x == 0)
     for (size_t i = body; i < a.bytes; ++i)
       for (int d = 0; d < a.ndst; ++d) a.dst[d][shift + i] = src[i];
+}
+
+// Single-pass fan-out: one vector (or, past the last vector, one tail byte)
+// per thread; blockIdx.y = source.  The launcher sizes x for nvec + 16.
+template <int NMAX>
+__global__ void __launch_bounds__(512) fanout_once_kernel(const FanoutArgs a) {
+  const int r = blockIdx.y;
+  const size_t nvec = a.bytes >> 4;
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t shift = (size_t)r * a.dst_stride;
+  if (v < nvec) {
+    const uint4 w = ld_stream(a.src[r] + (v << 4));
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d)
+      if (d < a.ndst) st_stream(a.dst[d] + shift + (v << 4), w);
+  } else {
+    const size_t i = (nvec << 4) + (v - nvec);
+    if (i < a.bytes) {
+      const char b = a.src[r][i];
+      for (int d = 0; d < a.ndst; ++d) a.dst[d][shift + i] = b;
+    }
+  }
 }
 
 static __global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {

@@ -57,6 +57,16 @@ cudaError_t fold_typed(const FoldArgs& a, int grid, cudaStream_t s) {
     if (a.n <= 4) return fold_tma<T, OP, 4>(a, grid, s);
     return fold_tma<T, OP, 8>(a, grid, s);
   }
+  const size_t nvec = a.bytes >> 4;
+  if ((size_t)grid * 512 >= nvec) {  // uncapped: single pass, one vector per thread
+    const int once = (int)((nvec + 16 + 511) / 512);
+    const int width = a.n > a.ndst ? a.n : a.ndst;
+    if (width <= 2) fold_once_kernel<T, OP, 2><<<once, 512, 0, s>>>(a);
+    else if (width <= 4) fold_once_kernel<T, OP, 4><<<once, 512, 0, s>>>(a);
+    else if (width <= 8) fold_once_kernel<T, OP, 8><<<once, 512, 0, s>>>(a);
+    else fold_once_kernel<T, OP, 16><<<once, 512, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   const int width = a.n > a.ndst ? a.n : a.ndst;
   if (width <= 2) return fold_vec<T, OP, 2>(a, grid, s);
   if (width <= 4) return fold_vec<T, OP, 4>(a, grid, s);
@@ -172,12 +182,20 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
     fanout_tma_kernel<<<dim3(grid * 3, a.nsrc), 32, smem, s>>>(a);
   } else if (!vec) {
     fanout_byte_kernel<<<g, 512, 0, s>>>(a);
+  } else if ((size_t)grid * 512 >= (a.bytes >> 4)) {  // uncapped: single pass
+    const dim3 once((unsigned)(((a.bytes >> 4) + 16 + 511) / 512), a.nsrc);
+    if (a.ndst <= 2) fanout_once_kernel<2><<<once, 512, 0, s>>>(a);
+    else if (a.ndst <= 4) fanout_once_kernel<4><<<once, 512, 0, s>>>(a);
+    else if (a.ndst <= 8) fanout_once_kernel<8><<<once, 512, 0, s>>>(a);
+    else fanout_once_kernel<16><<<once, 512, 0, s>>>(a);
   } else if (a.ndst <= 2) {
-    fanout_vec_kernel<2, 2><<<g, 512, 0, s>>>(a);
+    fanout_vec_kernel<2, 1><<<g, 512, 0, s>>>(a);
   } else if (a.ndst <= 4) {
-    fanout_vec_kernel<4, 2><<<g, 512, 0, s>>>(a);
+    // UNR 1: one vector per thread per pass keeps registers low (the unrolled
+    // <8,2> build needed 76, one CTA/SM, and ran 24% slower on the big grid)
+    fanout_vec_kernel<4, 1><<<g, 512, 0, s>>>(a);
   } else if (a.ndst <= 8) {
-    fanout_vec_kernel<8, 2><<<g, 512, 0, s>>>(a);
+    fanout_vec_kernel<8, 1><<<g, 512, 0, s>>>(a);
   } else {
     fanout_vec_kernel<16, 1><<<g, 512, 0, s>>>(a);
   }

@@ -58,6 +58,14 @@ __global__ void __launch_bounds__(512) fan_dst(const Args a) {
   }
 }
 
+__global__ void fill_random(uint32_t* p, size_t n, uint32_t seed) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    p[i] = x;
+  }
+}
+
 template <typename K>
 float timeit(K launch, int reps) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -69,7 +77,7 @@ float timeit(K launch, int reps) {
   return ms / reps;
 }
 
-int main() {
+int main(int argc, char**) {
   const size_t in_bytes = 32ull << 20, nvec = in_bytes / 16;
   Args a; a.nvec = nvec; a.stride_vec = nvec;
   for (int r = 0; r < N; ++r) {
@@ -77,6 +85,11 @@ int main() {
     CK(cudaMemset(s, r + 1, in_bytes)); a.src[r] = s; a.dst[r] = d;
   }
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const bool random_data = argc > 1;
+  if (random_data)
+    for (int r = 0; r < N; ++r) fill_random<<<4 * sms, 256>>>((uint32_t*)a.src[r], in_bytes / 4, 77 + r);
+  CK(cudaDeviceSynchronize());
+  printf("{\"data\": \"%s\"}\n", random_data ? "random" : "memset");
   const double alg = (double)(N + N * N) * in_bytes;
   auto rep = [&](const char* name, float ms) { printf("{\"variant\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", name, ms, alg / (ms * 1e-3) / 1e9); };
   rep("persistent sm/8 per src, unr2", timeit([&] { fan<2, 0><<<dim3(sms / N, N), 512>>>(a); }, 20));

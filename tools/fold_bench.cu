@@ -64,6 +64,14 @@ __global__ void copyk(const float4* __restrict__ s, float4* __restrict__ d, size
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (size_t)gridDim.x * blockDim.x) d[v] = s[v];
 }
 
+__global__ void fill_random(uint32_t* p, size_t n, uint32_t seed) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t x = (uint32_t)i * 2654435761u ^ seed;
+    x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+    p[i] = (x & 0x7fffff) | 0x3f800000u;  // finite floats in [1,2)
+  }
+}
+
 template <typename K>
 float timeit(K launch, int reps) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -75,7 +83,7 @@ float timeit(K launch, int reps) {
   return ms / reps;
 }
 
-int main() {
+int main(int argc, char**) {
   const size_t bytes = 256ull << 20, nvec = bytes / 16;
   Args a; a.nvec = nvec;
   for (int r = 0; r < N; ++r) {
@@ -83,6 +91,11 @@ int main() {
     CK(cudaMemset(s, 0, bytes)); a.src[r] = s; a.dst[r] = d;
   }
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const bool random_data = argc > 1;
+  if (random_data)
+    for (int r = 0; r < N; ++r) fill_random<<<4 * sms, 256>>>((uint32_t*)a.src[r], bytes / 4, 77 + r);
+  CK(cudaDeviceSynchronize());
+  printf("{\"data\": \"%s\"}\n", random_data ? "random" : "memset");
   const double alg = 2.0 * N * bytes;
   auto report = [&](const char* name, float ms) { printf("{\"variant\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", name, ms, alg / (ms * 1e-3) / 1e9); };
   report("512x1/SM unr1 nc/noalloc (current)", timeit([&] { fold<512, 1, 0, 0><<<sms, 512>>>(a); }, 20));

@@ -157,6 +157,12 @@ flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers);
 flxResult_t flxGetPathMask(flxComm_t comm, int* mask);
 /* Number of device kernels this library has launched (process-wide). */
 flxResult_t flxGetLaunchCount(unsigned long long* count);
+/* Bootstrap self-test (multi-rank comms only): write=1 copies `bytes` from
+ * buf into this rank's scratch head (host_region=0) or shared host staging
+ * region (host_region=1); write=0 reads peer `peer`'s through the CUDA-IPC
+ * mapping / the shared segment.  Plain copies; no collective runs. */
+flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int write, void* buf,
+                             size_t bytes);
 
 #ifdef __cplusplus
 }

@@ -103,6 +103,7 @@ def load_library() -> ctypes.CDLL:
         "flxSetStaging": [vp, sz, ci],
         "flxGetPathMask": [vp, P(ci)],
         "flxGetLaunchCount": [P(ctypes.c_ulonglong)],
+        "flxCommDebugPeer": [vp, ci, ci, ci, vp, sz],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -942,6 +942,14 @@ flxResult_t flxGetPathMask(flxComm_t comm, int* mask) {
   return flxSuccess;
 }
 
+flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int write, void* buf,
+                             size_t bytes) {
+  FLX_TRY(validate_comm(comm));
+  if (!comm->world) return fail(flxInvalidUsage, "not a multi-rank communicator");
+  if (!buf && bytes) return fail(flxInvalidArgument, "null buffer");
+  return world_debug_peer(comm->world, comm->local, peer, host_region, write, buf, bytes);
+}
+
 flxResult_t flxGetLaunchCount(unsigned long long* count) {
   if (!count) return fail(flxInvalidArgument, "null count");
   *count = g_launches.load();

@@ -628,7 +628,9 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
       w->peer_flags[p] = w->local[0].flags;
       continue;
     }
-    if (strcmp(hdr->slot[p].bus_id, mine.bus_id) == 0)
+    // FLX_ALLOW_SHARED_GPU: bootstrap self-tests only (no collective may run:
+    // the rank kernels of two processes on one GPU would wait on each other)
+    if (strcmp(hdr->slot[p].bus_id, mine.bus_id) == 0 && !getenv("FLX_ALLOW_SHARED_GPU"))
       return fail(flxInvalidUsage, "ranks %d and %d share GPU %s; one GPU per rank", rank, p,
                   mine.bus_id);
     void* ptr = nullptr;
@@ -654,6 +656,29 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
 }
 
 void world_attach(World* w, int local, Comm* c) { w->local[local].comm = c; }
+
+// Bootstrap self-test: write my scratch head / host region, or read a peer's
+// through the IPC mapping / shared segment.  Plain copies, no waiting kernels.
+flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int write,
+                             void* buf, size_t bytes) {
+  World::Local& L = w->local[local];
+  if (peer < 0 || peer >= w->nranks) return fail(flxInvalidArgument, "bad peer %d", peer);
+  if (host_region) {
+    if (bytes > w->hcap) return fail(flxInvalidArgument, "too many bytes");
+    char* region = w->host + kSemWords * 4 + (size_t)(write ? L.rank : peer) * w->hcap;
+    if (write)
+      memcpy(region, buf, bytes);
+    else
+      memcpy(buf, region, bytes);
+    return flxSuccess;
+  }
+  if (bytes > w->slot) return fail(flxInvalidArgument, "too many bytes");
+  FLX_CUDA(cudaSetDevice(L.device));
+  char* dev = write ? L.scratch : (w->loopback ? w->local[peer].scratch : w->peer_scratch[peer]);
+  FLX_CUDA(cudaMemcpy(write ? dev : buf, write ? buf : dev, bytes,
+                      write ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
+  return flxSuccess;
+}
 
 int world_release(World* w) {
   if (++w->destroyed < (int)w->local.size()) return 0;

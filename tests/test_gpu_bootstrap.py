@@ -1,0 +1,73 @@
+"""Multi-process bootstrap on one GPU: flxCommInitRank across 2 real processes.
+
+Exercises what the loopback world cannot: the shm rendezvous named by the
+unique id, the exchange and opening of CUDA-IPC handles, and the shared,
+cudaHostRegister'ed staging segment.  Both processes sit on the same GPU
+(FLX_ALLOW_SHARED_GPU), so NO collective runs (the per-GPU rank kernels of two
+processes would wait on each other); data crosses only through plain copies
+(flxCommDebugPeer) with gloo barriers in between.
+"""
+
+import ctypes
+import os
+import socket
+
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import torch.distributed as dist  # noqa: E402
+import torch.multiprocessing as mp  # noqa: E402
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FLX_ALLOW_SHARED_GPU="1",
+                      FLX_SLOT_MB="1", FLX_PCIE_STAGE_MB="1", FLX_BOOT_TIMEOUT="60")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_15882_b200 import comm
+
+        c = comm.Communicator.from_process_group()
+        L = comm.load_library()
+        n = 4096
+        mine = (ctypes.c_ubyte * n)(*([(rank * 37 + i) % 251 for i in range(n)]))
+        for region in (0, 1):
+            assert L.flxCommDebugPeer(c.handle, rank, region, 1, mine, n) == 0
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = {}
+        for region in (0, 1):
+            for peer in range(world):
+                buf = (ctypes.c_ubyte * n)()
+                assert L.flxCommDebugPeer(c.handle, peer, region, 0, buf, n) == 0
+                got[(region, peer)] = bytes(buf)
+        dist.barrier()
+        out[rank] = {"nranks": c.nranks, "rank": c.rank, "got": got}
+        c.destroy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_bootstrap_ipc_and_shared_staging():
+    from paper_2510_15882_b200.build import build
+
+    build()
+    world = 2
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_worker, args=(world, _port(), out), nprocs=world, join=True)
+        res = dict(out)
+    for rank in range(world):
+        assert res[rank]["nranks"] == world and res[rank]["rank"] == rank
+        for region in (0, 1):
+            for peer in range(world):
+                want = bytes((peer * 37 + i) % 251 for i in range(4096))
+                assert res[rank]["got"][(region, peer)] == want, (rank, region, peer)

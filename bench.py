@@ -472,6 +472,7 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
     nv_only, nv_dt = busbw_with((1000, 0, 0), ctas, steps=args.steps)
     striped, st_dt = busbw_with(shares, ctas, steps=args.steps)
     pbytes = clique.path_bytes()
+    drift = run_stage2_drift(clique, sends, recvs, shares, stream)
     clique.set_nvlink_ctas(args.nvlink_ctas)
     clique.set_shares(CollectiveOp.ALLREDUCE, (1000, 0, 0), AR_BYTES)
     return {
@@ -484,7 +485,50 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
         "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
         "stage1_iterations": trace.iterations, "stage1_trace": [r.action for r in trace.records],
         "ms_per_step": {"nvlink_only": round(nv_dt * 1e3, 4), "striped": round(st_dt * 1e3, 4)},
+        "stage2_drift": drift,
     }
+
+
+def run_stage2_drift(clique, sends, recvs, shares, stream, calls: int = 240,
+                     hog_from: int = 60, hog_to: int = 150) -> dict:
+    """Stage 2 on the real path (balancer.py:163-207 with measured reports): in the
+    config-4 setting, a competing H2D stream hogs PCIe between calls hog_from and
+    hog_to.  The RuntimeBalancer sees the PCIe path slow down (CUDA-event times),
+    moves granules to NVLink, and moves them back once the hog stops."""
+    import torch
+
+    from paper_2510_15882_b200.links import PathKind
+    from paper_2510_15882_b200.stage2 import BalancerConfig, RuntimeBalancer
+    from paper_2510_15882_b200.striping import CollectiveOp, PathTimingReport
+
+    n = len(sends)
+    hog_src = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
+    hog_dst = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    hog_stream = torch.cuda.Stream()
+    bal = RuntimeBalancer(shares, BalancerConfig(), active=shares.loaded_paths)
+    clique.set_shares(CollectiveOp.ALLREDUCE, bal.shares, AR_BYTES)
+    trace = []
+    for call in range(1, calls + 1):
+        if hog_from <= call < hog_to:
+            with torch.cuda.stream(hog_stream):
+                hog_dst.copy_(hog_src, non_blocking=True)
+        clique.all_reduce(sends, recvs)
+        t, b = clique.path_times(), clique.path_bytes()
+        rep = PathTimingReport.build(CollectiveOp.ALLREDUCE, n, AR_BYTES,
+                                     {k: t[k] for k in bal.active if b[k] > 0})
+        ev = bal.observe(rep)
+        if ev is not None:
+            if ev.moved:
+                clique.set_shares(CollectiveOp.ALLREDUCE, bal.shares, AR_BYTES)
+            trace.append({"call": call, "gap": None if ev.gap is None else round(ev.gap, 4),
+                          "moved": ev.moved, "pcie": bal.shares.get(PathKind.PCIE_STAGED),
+                          "hog": hog_from <= call < hog_to})
+    torch.cuda.synchronize()
+    return {"calls": calls, "hog_calls": [hog_from, hog_to],
+            "pcie_granules_start": shares.get(PathKind.PCIE_STAGED),
+            "pcie_granules_during_hog_min": min(e["pcie"] for e in trace if e["hog"]),
+            "pcie_granules_end": bal.shares.get(PathKind.PCIE_STAGED),
+            "evaluations": trace}
 
 
 def run_config5(clique, topo, stream) -> dict:

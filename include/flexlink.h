@@ -77,7 +77,12 @@ typedef enum { flxPathNvlink = 0, flxPathPcie = 1, flxPathRdma = 2 } flxPath_t;
 
 /* == linkstripe CollectiveOp (collectives.py:26-28), plus ReduceScatter
  * (ring_steps N-1) */
-typedef enum { flxCollAllReduce = 0, flxCollAllGather = 1, flxCollReduceScatter = 2 } flxCollOp_t;
+typedef enum {
+  flxCollAllReduce = 0,
+  flxCollAllGather = 1,
+  flxCollReduceScatter = 2,
+  flxCollAllToAll = 3
+} flxCollOp_t;
 
 /* ---- library / errors --------------------------------------------------- */
 flxResult_t flxGetVersion(int* version);
@@ -122,6 +127,11 @@ flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
 flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
                              flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
                              cudaStream_t stream);
+/* AllToAll: sendbuff holds nranks blocks of `count` elements, block j goes to
+ * rank j; recvbuff block i comes from rank i.  Not in place.  Partitioned per
+ * block. */
+flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
+                        flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
 flxResult_t flxGroupStart(void);
 flxResult_t flxGroupEnd(void);
 

@@ -273,6 +273,30 @@ int flxo_reducescatter(const void* const* send, void* const* recv, int nranks,
   return 0;
 }
 
+/*
+ * AllToAll (N-1 pairwise steps): recv[q][r*count + i] = send[r][q*count + i].
+ * The per-block bytes are partitioned per path; every path moves its slice of
+ * every block.
+ */
+int flxo_alltoall(const void* const* send, void* const* recv, int nranks, uint64_t count,
+                  int dtype, const int granules[3], uint64_t alignment, int threads) {
+  const int esz = flxo_dtype_size(dtype);
+  if (!esz || nranks < 1) return -1;
+  const uint64_t block = count * esz;
+  uint64_t split[3];
+  if (flxo_partition(block, granules, alignment, split)) return -1;
+  set_threads(threads);
+  for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p) {
+    if (!split[p]) continue;
+#pragma omp parallel for collapse(2) schedule(static)
+    for (int q = 0; q < nranks; ++q)
+      for (int r = 0; r < nranks; ++r)
+        memcpy((char*)recv[q] + (uint64_t)r * block + at,
+               (const char*)send[r] + (uint64_t)q * block + at, split[p]);
+  }
+  return 0;
+}
+
 /* element conversions exported for the Python side of the tests */
 float flxo_bf16_to_f32(uint16_t h) { return bf16_to_f32(h); }
 uint16_t flxo_f32_to_bf16(float f) { return f32_to_bf16(f); }

@@ -43,7 +43,8 @@ _lib = None
 _RESULTS = {0: "success", 1: "unhandled cuda error", 2: "system error", 3: "internal error",
             4: "invalid argument", 5: "invalid usage", 6: "remote error", 7: "in progress"}
 _OPS = {"sum": 0, "prod": 1, "max": 2, "min": 3}
-_COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1, CollectiveOp.REDUCESCATTER: 2}
+_COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1, CollectiveOp.REDUCESCATTER: 2,
+         CollectiveOp.ALLTOALL: 3}
 
 
 class FlexLinkError(RuntimeError):
@@ -91,6 +92,7 @@ def load_library() -> ctypes.CDLL:
         "flxAllReduce": [vp, vp, sz, ci, ci, vp, vp],
         "flxAllGather": [vp, vp, sz, ci, vp, vp],
         "flxReduceScatter": [vp, vp, sz, ci, ci, vp, vp],
+        "flxAllToAll": [vp, vp, sz, ci, vp, vp],
         "flxGroupStart": [],
         "flxGroupEnd": [],
         "flxSetShares": [vp, ci, ci, P(ci)],
@@ -246,6 +248,18 @@ class Communicator:
             "flxReduceScatter")
         return recv
 
+    def all_to_all(self, send, recv, stream=None):
+        """Block j of ``send`` goes to rank j; block i of ``recv`` comes from rank i."""
+        _contiguous_cuda(send, "send")
+        _contiguous_cuda(recv, "recv")
+        if send.numel() != recv.numel() or send.numel() % self.nranks or recv.dtype != send.dtype:
+            raise ValueError("send and recv must hold nranks equal blocks of one dtype")
+        _check(load_library().flxAllToAll(
+            ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()),
+            send.numel() // self.nranks, dtype_code(send.dtype), self._h,
+            _stream_handle(stream)), "flxAllToAll")
+        return recv
+
     # ---- balancer plumbing
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
         bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)
@@ -300,6 +314,17 @@ class Communicator:
         return tuple(k for k in PathKind if m & (1 << int(k)))
 
 
+def share_key_bytes(op: CollectiveOp, send, recv, nranks: int) -> int:
+    """The per-rank byte count the C executor partitions (and keys shares on):
+    AllReduce message, AllGather send, ReduceScatter recv block, AllToAll block."""
+    op = CollectiveOp(op)
+    if op == CollectiveOp.REDUCESCATTER:
+        return recv.numel() * recv.element_size()
+    if op == CollectiveOp.ALLTOALL:
+        return send.numel() // nranks * send.element_size()
+    return send.numel() * send.element_size()
+
+
 def broadcast_unique_id(group=None) -> bytes:
     """Rank 0 mints a flxUniqueId; every rank of ``group`` receives the same bytes."""
     import torch.distributed as dist
@@ -336,12 +361,13 @@ def rank_measure_fn(comm: Communicator, op: CollectiveOp, send, recv, group=None
     import torch
 
     op = CollectiveOp(op)
-    ref = recv if op == CollectiveOp.REDUCESCATTER else send
-    nbytes = ref.numel() * ref.element_size()
+    nbytes = share_key_bytes(op, send, recv, comm.nranks)
 
     def run():
         if op == CollectiveOp.ALLREDUCE:
             comm.all_reduce(send, recv, op=reduce_op)
+        elif op == CollectiveOp.ALLTOALL:
+            comm.all_to_all(send, recv)
         elif op == CollectiveOp.REDUCESCATTER:
             comm.reduce_scatter(send, recv, op=reduce_op)
         else:
@@ -464,6 +490,14 @@ class Clique:
                     count=recvs[0].numel())
         return recvs
 
+    def all_to_all(self, sends: Sequence, recvs: Sequence, stream=None):
+        self._validate(sends, recvs)
+        if sends[0].numel() % self.nranks:
+            raise ValueError("all_to_all buffers must hold nranks equal blocks")
+        self._issue(load_library().flxAllToAll, sends, recvs, (), stream,
+                    count=sends[0].numel() // self.nranks)
+        return recvs
+
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
         for c in self.comms:
             c.set_shares(op, shares, nbytes)
@@ -502,12 +536,13 @@ class Clique:
         op = CollectiveOp(op)
         # the byte count the share table is keyed on (per-rank message / send /
         # recv block, as the C executor partitions it)
-        ref = recvs[0] if op == CollectiveOp.REDUCESCATTER else sends[0]
-        nbytes = ref.numel() * ref.element_size()
+        nbytes = share_key_bytes(op, sends[0], recvs[0], self.nranks)
 
         def run():
             if op == CollectiveOp.ALLREDUCE:
                 self.all_reduce(sends, recvs, op=reduce_op)
+            elif op == CollectiveOp.ALLTOALL:
+                self.all_to_all(sends, recvs)
             elif op == CollectiveOp.REDUCESCATTER:
                 self.reduce_scatter(sends, recvs, op=reduce_op)
             else:
@@ -545,8 +580,7 @@ def tune_shares(clique: Clique, topo, op: CollectiveOp, sends, recvs, config=Non
     from .striping import CollectiveSpec
 
     op = CollectiveOp(op)
-    ref = recvs[0] if op == CollectiveOp.REDUCESCATTER else sends[0]
-    nbytes = ref.numel() * ref.element_size()
+    nbytes = share_key_bytes(op, sends[0], recvs[0], clique.nranks)
     avail = set(clique.comms[0].available_paths())
     paths = tuple(k for k in topo.present_paths if k in avail)
     spec = CollectiveSpec(op, max(2, clique.nranks), nbytes)

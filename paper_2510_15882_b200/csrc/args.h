@@ -42,4 +42,15 @@ struct RowsArgs {
   size_t src_stride;
 };
 
+// AllToAll block transpose: y = r*n + q copies `bytes` from src[r] +
+// q*src_stride to dst[q] + r*dst_stride.
+struct XposeArgs {
+  const char* src[kMaxRanks];
+  char* dst[kMaxRanks];
+  int n;
+  size_t bytes;
+  size_t src_stride;
+  size_t dst_stride;
+};
+
 }  // namespace flx

@@ -349,20 +349,22 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
                                                     std::min<size_t>((nvec_nv + 511) / 512, 1u << 30));
   const bool gather = head.coll == flxCollAllGather;
   const bool scatter = head.coll == flxCollReduceScatter;
+  const bool a2a = head.coll == flxCollAllToAll;
+  const bool rows = scatter || a2a;  // n x n (source, block) rows per piece
 
   // ---- PCIe slice: issue the side-stream pipeline first so its copies start
   // while the NVLink kernel runs.
   if (pc > 0) {
     const size_t chunk = pick_chunk(lead, pc);
     // ReduceScatter stages every (source, row) pair: n*n rows of one chunk
-    const size_t need = scatter ? chunk * n : chunk;
+    const size_t need = rows ? chunk * n : chunk;
     if (capturing && (c->stage_cap < need || c->stage_bufs != lead->buffers))
       return fail(flxInvalidUsage,
                   "PCIe staging must be sized before CUDA-graph capture: run the collective "
                   "once eagerly with the same size/shares first");
     FLX_TRY(ensure_staging(c, need, lead->buffers));
     const int bufs = c->stage_bufs;
-    const size_t pitch = scatter ? chunk : c->stage_cap;  // row pitch in the slot
+    const size_t pitch = rows ? chunk : c->stage_cap;  // row pitch in the slot
     const size_t slot_bytes = c->stage_cap * n;
     FLX_CUDA(cudaStreamWaitEvent(c->d2h, tm.start, 0));
     FLX_CUDA(cudaStreamWaitEvent(c->h2d, tm.start, 0));
@@ -391,7 +393,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_CUDA(cudaStreamWaitEvent(c->d2h, c->ev_drained[buf], 0));
       for (int i = 0; i < n; ++i) {
         const char* src = static_cast<const char*>(calls[i].send) + at;
-        if (scatter)  // this piece of every destination row r of rank i: rows at stride `bytes`
+        if (rows)  // this piece of every block r of rank i: rows at stride `bytes`
           FLX_CUDA(cudaMemcpy2DAsync(host + (size_t)i * n * pitch, pitch, src, bytes, len, n,
                                      cudaMemcpyDeviceToHost, c->d2h));
         else
@@ -410,7 +412,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         FLX_TRY(sem_wait_geq(c->h2d, sem_full, lap + 1));
       if (!capturing || folded_rec[buf])
         FLX_CUDA(cudaStreamWaitEvent(c->h2d, c->ev_folded[capturing][buf], 0));
-      FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, scatter ? n * n : n,
+      FLX_CUDA(cudaMemcpy2DAsync(dev, pitch, host, pitch, len, rows ? n * n : n,
                                  cudaMemcpyHostToDevice, c->h2d));
       if (capturing) {
         FLX_CUDA(cudaEventRecord(c->ev_drained[buf], c->h2d));
@@ -430,6 +432,17 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
         a.bytes = len;
         a.dst_stride = bytes;
         FLX_CUDA(launch_fanout(a, 16, c->red));
+      } else if (a2a) {
+        XposeArgs a{};
+        for (int i = 0; i < n; ++i) {
+          a.src[i] = dev + (size_t)i * n * pitch;
+          a.dst[i] = static_cast<char*>(calls[i].recv) + at;
+        }
+        a.n = n;
+        a.bytes = len;
+        a.src_stride = pitch;
+        a.dst_stride = bytes;
+        FLX_CUDA(launch_xpose(a, 8, c->red));
       } else if (scatter) {
         RowsArgs a{};
         for (int i = 0; i < n; ++i) {
@@ -475,6 +488,17 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
                          : (int)std::max<size_t>(1, std::min<size_t>((nv / 16 + 511) / 512,
                                                                      1u << 30));
       FLX_CUDA(launch_fanout(a, gx, s0));
+    } else if (a2a) {
+      XposeArgs a{};
+      for (int i = 0; i < n; ++i) {
+        a.src[i] = static_cast<const char*>(calls[i].send);
+        a.dst[i] = static_cast<char*>(calls[i].recv);
+      }
+      a.n = n;
+      a.bytes = nv;
+      a.src_stride = a.dst_stride = bytes;
+      FLX_CUDA(launch_xpose(a, lead->nvlink_ctas > 0 ? std::max(1, lead->nvlink_ctas / (n * n))
+                                                       : 1 << 30, s0));
     } else if (scatter) {
       RowsArgs a{};
       for (int i = 0; i < n; ++i) {
@@ -819,6 +843,15 @@ flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvco
       Call{comm, flxCollReduceScatter, sendbuff, recvbuff, recvcount, datatype, op, stream});
 }
 
+flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
+                        flxDataType_t datatype, flxComm_t comm, cudaStream_t stream) {
+  FLX_TRY(check_call(comm, datatype, 0, false));
+  if (count > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
+  if (count > 0 && sendbuff == recvbuff)
+    return fail(flxInvalidArgument, "in-place AllToAll is not supported");
+  return enqueue(Call{comm, flxCollAllToAll, sendbuff, recvbuff, count, datatype, 0, stream});
+}
+
 flxResult_t flxGroupStart(void) {
   ++t_group_depth;
   return flxSuccess;
@@ -832,7 +865,7 @@ flxResult_t flxGroupEnd(void) {
 
 flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]) {
   FLX_TRY(validate_comm(comm));
-  if (op != flxCollAllReduce && op != flxCollAllGather && op != flxCollReduceScatter)
+  if (op < flxCollAllReduce || op > flxCollAllToAll)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
   if (!granules) return fail(flxInvalidArgument, "null granules");
   Granules g{{granules[0], granules[1], granules[2]}};
@@ -860,7 +893,7 @@ flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int g
 
 flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granules[3]) {
   FLX_TRY(validate_comm(comm));
-  if (op != flxCollAllReduce && op != flxCollAllGather && op != flxCollReduceScatter)
+  if (op < flxCollAllReduce || op > flxCollAllToAll)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
   if (!granules) return fail(flxInvalidArgument, "null granules");
   const ShareTable& t = comm->shares[op];

@@ -18,6 +18,8 @@ namespace flx {
 struct FoldArgs;
 struct FanoutArgs;
 struct RowsArgs;
+struct XposeArgs;
+cudaError_t launch_xpose(const XposeArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fold(int dtype, int op, const FoldArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_rows(int dtype, int op, const RowsArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s);
@@ -129,7 +131,7 @@ struct Comm {
   Clique* clique = nullptr;  // virtual-rank (fused) mode
   World* world = nullptr;    // multi-rank mode
   int local = 0;             // index among the world's ranks in this process
-  ShareTable shares[3];  // per flxCollOp_t
+  ShareTable shares[4];  // per flxCollOp_t
   int nvlink_ctas = 0;   // 0 = auto
   size_t chunk_bytes = 0;  // 0 = auto
   int buffers = 2;

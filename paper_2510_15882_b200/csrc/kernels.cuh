@@ -508,6 +508,23 @@ __global__ void __launch_bounds__(512) fanout_once_kernel(const FanoutArgs a) {
   }
 }
 
+// AllToAll transpose copy, blockIdx.y = r*n + q; one vector (or, past the
+// last vector, one tail byte) per thread; byte loop when misaligned.
+static __global__ void __launch_bounds__(512) xpose_kernel(const XposeArgs a, int vec) {
+  const int r = blockIdx.y / a.n, q = blockIdx.y % a.n;
+  const char* src = a.src[r] + (size_t)q * a.src_stride;
+  char* dst = a.dst[q] + (size_t)r * a.dst_stride;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (vec) {
+    const size_t nvec = a.bytes >> 4;
+    for (size_t v = t; v < nvec; v += stride) st_stream(dst + (v << 4), ld_stream(src + (v << 4)));
+    for (size_t i = (nvec << 4) + t; i < a.bytes; i += stride) dst[i] = src[i];
+  } else {
+    for (size_t i = t; i < a.bytes; i += stride) dst[i] = src[i];
+  }
+}
+
 static __global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {
   const int r = blockIdx.y;
   const size_t shift = (size_t)r * a.dst_stride;

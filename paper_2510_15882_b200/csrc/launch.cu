@@ -1,4 +1,5 @@
 // Template dispatch for the data-plane kernels (see kernels.cuh).
+#include <algorithm>
 #include <atomic>
 
 #include "internal.h"
@@ -159,6 +160,18 @@ cudaError_t launch_rows(int dtype, int op, const RowsArgs& a, int grid, cudaStre
     case flxBfloat16: return rows_op<__nv_bfloat16>(op, a, grid, s);
   }
   return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_xpose(const XposeArgs& a, int grid, cudaStream_t s) {
+  if (a.bytes == 0) return cudaSuccess;
+  if (a.n < 1 || a.n > kMaxRanks || grid < 1) return cudaErrorInvalidValue;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  bool vec = (a.src_stride & 15) == 0 && (a.dst_stride & 15) == 0;
+  for (int r = 0; r < a.n; ++r) vec = vec && aligned16(a.src[r]) && aligned16(a.dst[r]);
+  const size_t need = ((a.bytes >> 4) + 16 + 511) / 512;  // single pass when uncapped
+  const unsigned gx = (unsigned)std::min<size_t>(std::max<size_t>(1, need), (size_t)grid);
+  xpose_kernel<<<dim3(gx, a.n * a.n), 512, 0, s>>>(a, vec ? 1 : 0);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {

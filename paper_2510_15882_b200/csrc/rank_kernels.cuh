@@ -359,6 +359,48 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
   }
 }
 
+// AllToAll: a.bytes = NVLink part of each block, a.rank_stride = block stride
+// B (send and recv).  Push block c to peer c, copy my own block locally, then
+// land every peer's push into recv block p.
+__device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
+  const int r = a.rank, n = a.nranks;
+  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = a.epoch + (uint32_t)k;
+    const size_t len = min(a.slot, a.bytes - base);
+    size_t lo, hi;
+    cta_part(len, nctas, cta, &lo, &hi);
+    {
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      uint32_t* targets[kMaxRanks];
+      int nt = 0;
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo,
+                 a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
+        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+      }
+      const size_t own = (size_t)r * a.rank_stride + base + lo;
+      cta_copy(a.recv + own, a.send + own, hi - lo, false);
+      cta_signal(targets, nt, e);
+    }
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+    for (int s = 1; s < n; ++s) {
+      const int p = (r - s + n) % n;
+      cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
+               a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
+    }
+    free_all(a, cta, e);
+  }
+}
+
+__global__ void __launch_bounds__(512) rank_alltoall_kernel(const RankArgs a) {
+  rank_alltoall(a, blockIdx.x, gridDim.x);
+}
+
+__global__ void __launch_bounds__(512) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
+  rank_alltoall(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+}
+
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
   rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);

@@ -298,6 +298,18 @@ cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nr
   return cudaGetLastError();
 }
 
+cudaError_t launch_rank_alltoall(bool loop, const void* args, int nctas, int nranks,
+                                 cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (loop) {
+    void* params[] = {const_cast<void*>(args)};
+    return cudaLaunchCooperativeKernel((const void*)loopback_alltoall_kernel, dim3(nctas, nranks),
+                                       dim3(512), params, 0, s);
+  }
+  rank_alltoall_kernel<<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 // Before rank r overwrites its host region H_r at PCIe epoch e, every reader
@@ -322,6 +334,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   const size_t nv = split[flxPathNvlink], pc = split[flxPathPcie];
   const bool gather = coll == flxCollAllGather;
   const bool scatter = coll == flxCollReduceScatter;
+  const bool a2a = coll == flxCollAllToAll;
   if (*w->abort_word) return fail(flxInternalError, "communicator aborted by an earlier timeout");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
@@ -329,7 +342,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     return fail(flxInvalidUsage, "multi-rank collectives carry host-side epochs and cannot be "
                 "captured into a CUDA graph yet");
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
-  if ((scatter ? pc * n : pc) > w->hcap)
+  if ((scatter || a2a ? pc * n : pc) > w->hcap)
     return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
                 "FLX_PCIE_STAGE_MB or lower the pcie share)", pc, w->hcap);
 
@@ -355,7 +368,38 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[&L - &w->local[0]]->start, 0));
       FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[&L - &w->local[0]]->start, 0));
     }
-    if (scatter) {
+    if (a2a) {
+      // step 1 as ReduceScatter; step 2: rank r lands H_p[r] straight into its
+      // recv block p (no fold), and copies its own block device to device
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        FLX_TRY(wait_region_free(w, L.d2h, r, e));
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * pc,
+                                   static_cast<const char*>(send[i]) + (size_t)c * bytes + nv, pc,
+                                   cudaMemcpyDeviceToHost, L.d2h));
+          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
+        }
+      }
+      for (int i = 0; i < nl; ++i) {
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        const size_t own = (size_t)r * bytes + nv;
+        FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + own,
+                                 static_cast<const char*>(send[i]) + own, pc,
+                                 cudaMemcpyDeviceToDevice, L.h2d));
+        for (int s = 1; s < n; ++s) {
+          const int p = (r - s + n) % n;
+          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
+          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + (size_t)p * bytes + nv,
+                                   w->hregion(p) + r * pc, pc, cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
+        }
+        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+      }
+    } else if (scatter) {
       // step 1: D2H the PCIe part of my block c into H_r[c]; step 2: the owner
       // lands every source's copy of its block and folds it in rank order
       for (int i = 0; i < nl; ++i) {
@@ -485,7 +529,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   // ---------------- NVLink slice
   if (nv > 0) {
     const uint32_t e0 = w->epoch;
-    const size_t round_cap = (gather || scatter) ? w->slot : w->slot * n;
+    const size_t round_cap = (gather || scatter || a2a) ? w->slot : w->slot * n;
     const uint32_t rounds = (uint32_t)((nv + round_cap - 1) / round_cap);
     w->epoch += rounds;
     LoopbackArgs la;
@@ -509,7 +553,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
     cudaError_t err =
-        gather    ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
+        a2a       ? launch_rank_alltoall(w->loopback, args, w->nctas, n, s0)
+        : gather  ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
         : scatter ? launch_rank_reduce<true>(dtype, op, w->loopback, args, w->nctas, n, s0)
                   : launch_rank_reduce<false>(dtype, op, w->loopback, args, w->nctas, n, s0);
     if (!gather && !scatter) w->last_ar_epoch = e0 + rounds - 1;

@@ -18,10 +18,11 @@ from test_gpu_parity import OPS, TORCH_DT, _inputs, _np  # noqa: E402
 RNG = random.Random(20261018)
 CASES = []
 for i in range(48):
-    coll = RNG.choice(["allreduce", "allgather", "reducescatter"])
+    coll = RNG.choice(["allreduce", "allgather", "reducescatter", "alltoall"])
     n = RNG.choice([2, 3, 4, 5, 8])
     dtype = RNG.choice([0, 2, 6, 7, 8, 9])
-    op = RNG.choice(["sum", "max", "min", "prod"]) if coll != "allgather" else "sum"
+    op = RNG.choice(["sum", "max", "min", "prod"]) if coll in ("allreduce",
+                                                               "reducescatter") else "sum"
     if op == "prod" and dtype in (6, 9):
         op = "sum"  # fp16/bf16 products overflow quickly; sum/max/min cover the fold
     count = RNG.choice([1, 17, 1000, 4099, 65536, 200003, 1 << 18])
@@ -62,6 +63,12 @@ def test_fuzz_against_oracle(case):
                 s = [h.cuda() for h in cpu]
             c.all_gather(s, r)
             want = oracle.allgather([_np(h, dtype) for h in cpu], dtype, granules, align)
+        elif coll == "alltoall":
+            cpu = _inputs(n, n * count, dtype, seed)
+            s = [h.cuda() for h in cpu]
+            r = [torch.empty_like(x) for x in s]
+            c.all_to_all(s, r)
+            want = oracle.alltoall([_np(h, dtype) for h in cpu], dtype, granules, align)
         else:
             cpu = _inputs(n, n * count, dtype, seed)
             s = [h.cuda() for h in cpu]

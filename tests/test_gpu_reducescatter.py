@@ -102,6 +102,28 @@ def test_mixed_collectives_share_flags_and_staging():
                 np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])
 
 
+@pytest.mark.parametrize("loopback", [False, True])
+@pytest.mark.parametrize("n,count,dtype,granules", [
+    (2, 4096, 7, (1000, 0, 0)), (8, (1 << 15) + 3, 9, (900, 100, 0)), (3, 20001, 0, (600, 400, 0)),
+])
+def test_all_to_all_matches_oracle(loopback, n, count, dtype, granules):
+    cpu = _inputs(n, n * count, dtype, n * 7 + dtype)
+    sends = [h.cuda() for h in cpu]
+    recvs = [torch.empty_like(s) for s in sends]
+    with flx.Clique(n, loopback=loopback) as c:
+        c.set_shares(CollectiveOp.ALLTOALL, granules)
+        for _ in range(2):
+            c.all_to_all(sends, recvs)
+        torch.cuda.synchronize()
+        align = c.comms[0].alignment(CollectiveOp.ALLTOALL)
+        got = [_np(r, dtype) for r in recvs]
+        with pytest.raises(ValueError):
+            c.all_to_all(sends, sends)  # in place is rejected
+    want = oracle.alltoall([_np(h, dtype) for h in cpu], dtype, granules, align)
+    for r in range(n):
+        np.testing.assert_array_equal(got[r], want[r])
+
+
 def test_nccl_reduce_scatter_symbol():
     shim = flx.library_path().parent / "libflexlink_nccl.so"
     if not shim.exists():

@@ -125,6 +125,16 @@ def test_reducescatter_oracle_matches_numpy(dtype, op):
                                       full[0][r * count:(r + 1) * count].view(np.uint8))
 
 
+def test_alltoall_oracle_is_a_block_transpose():
+    rng = np.random.default_rng(5)
+    n, count = 4, 999
+    sends = [rng.integers(0, 255, n * count, dtype=np.uint8) for _ in range(n)]
+    got = oracle.alltoall(sends, 1, (700, 300, 0), 16)
+    for q in range(n):
+        want = np.concatenate([sends[r][q * count:(q + 1) * count] for r in range(n)])
+        np.testing.assert_array_equal(got[q], want)
+
+
 def test_oracle_rejects_bad_arguments():
     with pytest.raises(ValueError):
         oracle.partition(10, (500, 400, 0), 0)

@@ -276,6 +276,21 @@ def run_single_gpu(args) -> None:
     nv_alg_bytes = 2 * n * pbytes[PathKind.NVLINK]  # N reads + N writes of the NVLink slice
     achieved = nv_alg_bytes / (nv_ms * 1e-3) / 1e9
 
+    # library baseline on the same GPU: the same 8-rank AllReduce as unfused torch
+    # ops (left fold with torch.add, then 8 copies) — what one GPU does without
+    # the fused kernel (NCCL cannot run 8 ranks on one GPU)
+    def torch_unfused():
+        acc = torch.add(sends[0], sends[1])
+        for s in sends[2:]:
+            acc.add_(s)
+        for r in recvs:
+            r.copy_(acc)
+
+    torch_dt = _time_steps(torch_unfused, max(5, args.steps // 2), stream)
+    torch_base = {"value": round(busbw_allreduce(AR_BYTES, torch_dt, n), 2),
+                  "ms_per_step": round(torch_dt * 1e3, 4),
+                  "what": "torch.add left fold + 8 copy_ (unfused, same GPU, same data)"}
+
     # exactness spot check of the timed result (integer-valued inputs: exact sum)
     exact = torch.stack(sends).sum(0)
     assert all(torch.equal(r, exact) for r in recvs), "allreduce result mismatch"
@@ -414,6 +429,7 @@ def run_single_gpu(args) -> None:
         "gpu_launches": launches,
         "clocks": clocks,
         "nccl": None,
+        "torch_unfused_baseline": torch_base,
         "link_profile": link_profile,
         "config4": cfg4,
         "config5": cfg5,
@@ -634,6 +650,20 @@ def run_multi_gpu(args) -> None:
     dist.all_reduce(exact)  # integer-valued fp32: exact in any order
     ok = torch.equal(recv, exact)
 
+    # e2e through the public API: this rank's input H2D from pinned memory,
+    # in-place striped AllReduce, result D2H — every step
+    host_in = send.cpu().pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    work = torch.empty_like(send)
+
+    def e2e_step():
+        work.copy_(host_in, non_blocking=True)
+        c.all_reduce(work, work)
+        host_out.copy_(work, non_blocking=True)
+
+    e2e_dt = timed(e2e_step)
+    e2e_ok = torch.equal(host_out, exact.cpu())
+
     # AllGather bf16, 256 MiB gathered (config 2)
     ag_count = AG_OUT_BYTES // 2 // world
     ag_send = torch.randn(ag_count, device="cuda", generator=gen).bfloat16()
@@ -664,6 +694,9 @@ def run_multi_gpu(args) -> None:
             "nccl": {"value": round(busbw_allreduce(AR_BYTES, nccl_dt, world), 2),
                      "ms_per_step": round(nccl_dt * 1e3, 4)},
             "result_matches_exact_sum": bool(ok), "gpu_launches": launches, "clocks": clocks,
+            "e2e": {"value": round(busbw_allreduce(AR_BYTES, e2e_dt, world), 3), "unit": "GB/s",
+                    "h2d_bytes_per_step": AR_BYTES, "d2h_bytes_per_step": AR_BYTES,
+                    "ms_per_step": round(e2e_dt * 1e3, 3), "result_exact": bool(e2e_ok)},
             "allgather": {
                 "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, world), 2), "unit": "GB/s",
                 "dtype": "bf16", "ms_per_step": round(ag_dt * 1e3, 4),

@@ -695,8 +695,9 @@ def run_multi_gpu(args) -> None:
                      "ms_per_step": round(nccl_dt * 1e3, 4)},
             "result_matches_exact_sum": bool(ok), "gpu_launches": launches, "clocks": clocks,
             "e2e": {"value": round(busbw_allreduce(AR_BYTES, e2e_dt, world), 3), "unit": "GB/s",
-                    "h2d_bytes_per_step": AR_BYTES, "d2h_bytes_per_step": AR_BYTES,
-                    "ms_per_step": round(e2e_dt * 1e3, 3), "result_exact": bool(e2e_ok)},
+                    "h2d_bytes_per_step": world * AR_BYTES, "d2h_bytes_per_step": world * AR_BYTES,
+                    "ms_per_step": round(e2e_dt * 1e3, 3), "result_exact": bool(e2e_ok),
+                    "note": "every rank moves its own 256 MiB in and out over its own PCIe link"},
             "allgather": {
                 "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, world), 2), "unit": "GB/s",
                 "dtype": "bf16", "ms_per_step": round(ag_dt * 1e3, 4),

@@ -130,7 +130,7 @@ def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = 32 * MIB,
     count = per_rank_bytes // 4
     rng = np.random.default_rng(1000)
     sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(n)]
-    recvs = [np.empty_like(s) for s in sends]
+    recvs = [np.zeros_like(s) for s in sends]  # pre-touched: no page faults in the timing
     oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)  # warm
     t0 = time.perf_counter()
     reps = 0
@@ -165,13 +165,15 @@ def run_reference(args) -> None:
     count = per_rank // 4
     rng = np.random.default_rng(1000)
     sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(SIM_RANKS)]
-    recvs = [np.empty_like(s) for s in sends]
-    for _ in range(args.warmup):
+    recvs = [np.zeros_like(s) for s in sends]  # pre-touched: no page faults in the timing
+    for _ in range(max(args.warmup, 3)):  # OpenMP pool spin-up + caches
         oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
-    t0 = time.perf_counter()
+    times = []
     for _ in range(args.steps):
+        t0 = time.perf_counter()
         oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
-    dt = (time.perf_counter() - t0) / args.steps
+        times.append(time.perf_counter() - t0)
+    dt = sum(times) / len(times)
     value = busbw_allreduce(per_rank, dt, SIM_RANKS)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",

@@ -25,7 +25,8 @@
  * accumulated in fp32 for fp16/bf16 (one final RNE rounding), in the native
  * type otherwise (integers wrap).  AllGather is a pure byte copy.
  *
- * Build: oracle/Makefile (gcc -O2 -fopenmp -ffp-contract=off).
+ * Build: oracle/Makefile (gcc -O3 -fopenmp -ffp-contract=off; vectorised
+ * across elements only, never across ranks, so the fold order is kept).
  */
 #include <math.h>
 #include <stdint.h>
@@ -83,22 +84,32 @@ static inline uint16_t f32_to_f16(float f) {
 }
 
 /* -------------------------------------------------------------- the fold */
-#define FOLD_INT(T, UT)                                                            \
-  static void fold_##T(const void* const* src, void* const* dst, int n, int ndst, uint64_t i0, \
-                       uint64_t i1, int op) {                                      \
-    for (uint64_t i = i0; i < i1; ++i) {                                           \
-      T acc = ((const T*)src[0])[i];                                               \
-      for (int r = 1; r < n; ++r) {                                                \
-        T x = ((const T*)src[r])[i];                                               \
-        switch (op) {                                                              \
-          case SUM: acc = (T)(UT)((UT)acc + (UT)x); break;                         \
-          case PROD: acc = (T)(UT)((UT)acc * (UT)x); break;                        \
-          case MAX: acc = (x > acc) ? x : acc; break;                              \
-          default: acc = (x < acc) ? x : acc; break;                               \
-        }                                                                          \
-      }                                                                            \
-      for (int r = 0; r < ndst; ++r) ((T*)dst[r])[i] = acc;                        \
-    }                                                                              \
+/* Blocked so the per-element work vectorises across elements while every
+ * element keeps its left fold in rank order: the loop over ranks is outside
+ * the loop over a block's elements, nothing is reassociated, and all sources
+ * of a block are read before any destination is written (in-place safe). */
+#define FOLD_BLOCK 2048
+
+#define FOLD_INT(T, UT)                                                                     \
+  static void fold_##T(const void* const* src, void* const* dst, int n, int ndst,           \
+                       uint64_t i0, uint64_t i1, int op) {                                  \
+    T acc[FOLD_BLOCK];                                                                      \
+    for (uint64_t b = i0; b < i1; b += FOLD_BLOCK) {                                        \
+      const int len = (int)(i1 - b < FOLD_BLOCK ? i1 - b : FOLD_BLOCK);                     \
+      memcpy(acc, (const T*)src[0] + b, (size_t)len * sizeof(T));                           \
+      for (int r = 1; r < n; ++r) {                                                         \
+        const T* x = (const T*)src[r] + b;                                                  \
+        if (op == SUM)                                                                      \
+          for (int j = 0; j < len; ++j) acc[j] = (T)(UT)((UT)acc[j] + (UT)x[j]);            \
+        else if (op == PROD)                                                                \
+          for (int j = 0; j < len; ++j) acc[j] = (T)(UT)((UT)acc[j] * (UT)x[j]);            \
+        else if (op == MAX)                                                                 \
+          for (int j = 0; j < len; ++j) acc[j] = (x[j] > acc[j]) ? x[j] : acc[j];           \
+        else                                                                                \
+          for (int j = 0; j < len; ++j) acc[j] = (x[j] < acc[j]) ? x[j] : acc[j];           \
+      }                                                                                     \
+      for (int r = 0; r < ndst; ++r) memcpy((T*)dst[r] + b, acc, (size_t)len * sizeof(T)); \
+    }                                                                                       \
   }
 
 FOLD_INT(int8_t, uint8_t)
@@ -108,23 +119,35 @@ FOLD_INT(uint32_t, uint32_t)
 FOLD_INT(int64_t, uint64_t)
 FOLD_INT(uint64_t, uint64_t)
 
-#define FOLD_FLOAT(NAME, T, A, LOAD, STORE)                                           \
-  static void fold_##NAME(const void* const* src, void* const* dst, int n, int ndst, uint64_t i0, \
-                          uint64_t i1, int op) {                                      \
-    for (uint64_t i = i0; i < i1; ++i) {                                              \
-      A acc = LOAD(((const T*)src[0])[i]);                                            \
-      for (int r = 1; r < n; ++r) {                                                   \
-        A x = LOAD(((const T*)src[r])[i]);                                            \
-        switch (op) {                                                                 \
-          case SUM: acc = acc + x; break;                                             \
-          case PROD: acc = acc * x; break;                                            \
-          case MAX: acc = (x > acc) ? x : acc; break;                                 \
-          default: acc = (x < acc) ? x : acc; break;                                  \
-        }                                                                             \
-      }                                                                               \
-      T out = STORE(acc);                                                             \
-      for (int r = 0; r < ndst; ++r) ((T*)dst[r])[i] = out;                           \
-    }                                                                                 \
+#define FOLD_FLOAT(NAME, T, A, LOAD, STORE)                                                 \
+  static void fold_##NAME(const void* const* src, void* const* dst, int n, int ndst,        \
+                          uint64_t i0, uint64_t i1, int op) {                               \
+    A acc[FOLD_BLOCK];                                                                      \
+    T out[FOLD_BLOCK];                                                                      \
+    for (uint64_t b = i0; b < i1; b += FOLD_BLOCK) {                                        \
+      const int len = (int)(i1 - b < FOLD_BLOCK ? i1 - b : FOLD_BLOCK);                     \
+      const T* s0 = (const T*)src[0] + b;                                                   \
+      for (int j = 0; j < len; ++j) acc[j] = LOAD(s0[j]);                                   \
+      for (int r = 1; r < n; ++r) {                                                         \
+        const T* x = (const T*)src[r] + b;                                                  \
+        if (op == SUM)                                                                      \
+          for (int j = 0; j < len; ++j) acc[j] = acc[j] + LOAD(x[j]);                       \
+        else if (op == PROD)                                                                \
+          for (int j = 0; j < len; ++j) acc[j] = acc[j] * LOAD(x[j]);                       \
+        else if (op == MAX)                                                                 \
+          for (int j = 0; j < len; ++j) {                                                   \
+            const A v = LOAD(x[j]);                                                         \
+            acc[j] = (v > acc[j]) ? v : acc[j];                                             \
+          }                                                                                 \
+        else                                                                                \
+          for (int j = 0; j < len; ++j) {                                                   \
+            const A v = LOAD(x[j]);                                                         \
+            acc[j] = (v < acc[j]) ? v : acc[j];                                             \
+          }                                                                                 \
+      }                                                                                     \
+      for (int j = 0; j < len; ++j) out[j] = STORE(acc[j]);                                 \
+      for (int r = 0; r < ndst; ++r) memcpy((T*)dst[r] + b, out, (size_t)len * sizeof(T));  \
+    }                                                                                       \
   }
 
 #define IDENT(x) (x)

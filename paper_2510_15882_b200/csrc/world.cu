@@ -75,6 +75,7 @@ struct BootSlot {
 struct BootHeader {
   int arrived;
   int mapped;
+  int leaving;  // destroy barrier: no rank frees what peers may still touch
   int nranks;
   int pad;
   BootSlot slot[kMaxRanks];
@@ -116,6 +117,7 @@ struct World {
   char* peer_scratch[kMaxRanks] = {};
   uint32_t* peer_flags[kMaxRanks] = {};
   std::vector<void*> ipc_opened;
+  struct BootHeader* boot = nullptr;  // kept mapped (name unlinked) for the destroy barrier
   int destroyed = 0;
 
   // semaphore words as the GPU addresses them (registered host memory may map
@@ -153,8 +155,18 @@ flxResult_t local_init(World* w, World::Local& L) {
 void world_free(World* w) {
   for (auto& L : w->local) {
     cudaSetDevice(L.device);
-    if (L.d2h) cudaStreamSynchronize(L.d2h);
-    if (L.h2d) cudaStreamSynchronize(L.h2d);
+    cudaDeviceSynchronize();  // every kernel / copy that may touch peer memory
+  }
+  if (w->boot) {
+    // destroy barrier: a peer may still be pushing into my scratch or reading
+    // my outbox / host region until it, too, has drained its device
+    __atomic_fetch_add(&w->boot->leaving, 1, __ATOMIC_ACQ_REL);
+    const auto t0 = std::chrono::steady_clock::now();
+    while (__atomic_load_n(&w->boot->leaving, __ATOMIC_ACQUIRE) < w->nranks &&
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 60.0)
+      std::this_thread::sleep_for(std::chrono::milliseconds(1));
+    munmap(w->boot, sizeof(BootHeader));
+    w->boot = nullptr;
   }
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto& L : w->local) {
@@ -691,7 +703,7 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   if (!spin_until([&] { return __atomic_load_n(&hdr->mapped, __ATOMIC_ACQUIRE) >= nranks; },
                   timeout))
     return fail(flxSystemError, "bootstrap timed out mapping the staging segment");
-  munmap(hdr, sizeof(BootHeader));
+  w->boot = hdr;  // unmapped in world_free, after the destroy barrier
   if (rank == 0) {
     shm_unlink(boot_name);
     shm_unlink(stage_name);

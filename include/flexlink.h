@@ -132,6 +132,14 @@ flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvco
  * block. */
 flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
+/* Convenience for single-process communicator sets (flxCommInitAll /
+ * flxCommInitLoopback): the same collective on every comms[i] with
+ * sendbuffs[i]/recvbuffs[i] in ONE call — exactly flxGroupStart + n calls +
+ * flxGroupEnd, minus n+1 host crossings.  `op` is ignored for gather/alltoall. */
+flxResult_t flxGroupCollective(flxCollOp_t coll, flxComm_t* comms, int n,
+                               const void* const* sendbuffs, void* const* recvbuffs,
+                               size_t count, flxDataType_t datatype, flxRedOp_t op,
+                               cudaStream_t stream);
 flxResult_t flxGroupStart(void);
 flxResult_t flxGroupEnd(void);
 

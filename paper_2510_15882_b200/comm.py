@@ -94,6 +94,7 @@ def load_library() -> ctypes.CDLL:
         "flxReduceScatter": [vp, vp, sz, ci, ci, vp, vp],
         "flxAllToAll": [vp, vp, sz, ci, vp, vp],
         "flxGroupStart": [],
+        "flxGroupCollective": [ci, P(vp), ci, P(vp), P(vp), sz, ci, ci, vp],
         "flxGroupEnd": [],
         "flxSetShares": [vp, ci, ci, P(ci)],
         "flxGetShares": [vp, ci, ci, P(ci)],
@@ -415,6 +416,7 @@ class Clique:
             devs = (ctypes.c_int * nranks)(*([device] * nranks))
             _check(L.flxCommInitAll(handles, nranks, devs), "flxCommInitAll")
         self.loopback = loopback
+        self._handles = handles
         self.comms = [Communicator(h, self) for h in handles]
         self.nranks = nranks
         self.device = device
@@ -453,40 +455,33 @@ class Clique:
                     or r.dtype != s0.dtype:
                 raise ValueError("all ranks need same-shaped send/recv tensors of one dtype")
 
-    def _issue(self, fn, sends, recvs, extra, stream, count: int | None = None) -> None:
-        """One flxGroupStart/End around one call per rank; the stream handle and
-        pointers are resolved once (small messages are host-issue bound)."""
-        L = load_library()
-        s = _stream_handle(stream)
-        count = sends[0].numel() if count is None else count
-        dt = dtype_code(sends[0].dtype)
-        _check(L.flxGroupStart(), "flxGroupStart")
-        rc = 0
-        try:
-            for c, a, b in zip(self.comms, sends, recvs):
-                rc = fn(a.data_ptr(), b.data_ptr(), count, dt, *extra, c._h, s)
-                if rc:
-                    break
-        finally:
-            end = L.flxGroupEnd()
-        _check(rc, fn.__name__)
-        _check(end, "flxGroupEnd")
+    def _issue(self, coll: int, sends, recvs, op: int, stream, count: int | None = None) -> None:
+        """All ranks' calls in one ``flxGroupCollective`` (== flxGroupStart, one
+        call per rank, flxGroupEnd): small messages are host-issue bound."""
+        n = self.nranks
+        ptrs = ctypes.c_void_p * n
+        rc = load_library().flxGroupCollective(
+            coll, self._handles, n, ptrs(*[t.data_ptr() for t in sends]),
+            ptrs(*[t.data_ptr() for t in recvs]),
+            sends[0].numel() if count is None else count, dtype_code(sends[0].dtype), op,
+            _stream_handle(stream))
+        _check(rc, "flxGroupCollective")
 
     def all_reduce(self, sends: Sequence, recvs: Sequence | None = None, op: str = "sum",
                    stream=None):
         recvs = list(sends) if recvs is None else list(recvs)
         self._validate(sends, recvs, gather=False)
-        self._issue(load_library().flxAllReduce, sends, recvs, (_OPS[op],), stream)
+        self._issue(0, sends, recvs, _OPS[op], stream)
         return recvs
 
     def all_gather(self, sends: Sequence, recvs: Sequence, stream=None):
         self._validate(sends, recvs, gather=True)
-        self._issue(load_library().flxAllGather, sends, recvs, (), stream)
+        self._issue(1, sends, recvs, 0, stream)
         return recvs
 
     def reduce_scatter(self, sends: Sequence, recvs: Sequence, op: str = "sum", stream=None):
         self._validate(sends, recvs, scatter=True)
-        self._issue(load_library().flxReduceScatter, sends, recvs, (_OPS[op],), stream,
+        self._issue(2, sends, recvs, _OPS[op], stream,
                     count=recvs[0].numel())
         return recvs
 
@@ -494,7 +489,7 @@ class Clique:
         self._validate(sends, recvs)
         if sends[0].numel() % self.nranks:
             raise ValueError("all_to_all buffers must hold nranks equal blocks")
-        self._issue(load_library().flxAllToAll, sends, recvs, (), stream,
+        self._issue(3, sends, recvs, 0, stream,
                     count=sends[0].numel() // self.nranks)
         return recvs
 

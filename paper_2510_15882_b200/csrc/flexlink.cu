@@ -852,6 +852,34 @@ flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
   return enqueue(Call{comm, flxCollAllToAll, sendbuff, recvbuff, count, datatype, 0, stream});
 }
 
+// One collective for ALL ranks of a single-process communicator set in one
+// call: equivalent to flxGroupStart; per-rank flx<Coll>(...); flxGroupEnd, but
+// one host crossing instead of n+2 (small messages are host-issue bound).
+flxResult_t flxGroupCollective(flxCollOp_t coll, flxComm_t* comms, int n,
+                               const void* const* sendbuffs, void* const* recvbuffs,
+                               size_t count, flxDataType_t datatype, flxRedOp_t op,
+                               cudaStream_t stream) {
+  if (!comms || n < 1 || !sendbuffs || !recvbuffs)
+    return fail(flxInvalidArgument, "bad group arguments");
+  if (coll < flxCollAllReduce || coll > flxCollAllToAll)
+    return fail(flxInvalidArgument, "bad collective %d", (int)coll);
+  const bool reduce = coll == flxCollAllReduce || coll == flxCollReduceScatter;
+  for (int i = 0; i < n; ++i) {
+    FLX_TRY(check_call(comms[i], datatype, reduce ? op : 0, reduce));
+    if (count > 0 && (!sendbuffs[i] || !recvbuffs[i]))
+      return fail(flxInvalidArgument, "null buffer for rank %d", i);
+    if (coll == flxCollAllToAll && count > 0 && sendbuffs[i] == recvbuffs[i])
+      return fail(flxInvalidArgument, "in-place AllToAll is not supported");
+  }
+  ++t_group_depth;
+  for (int i = 0; i < n; ++i)
+    t_pending.push_back(Call{comms[i], (int)coll, sendbuffs[i], recvbuffs[i], count, datatype,
+                             reduce ? (int)op : 0, stream});
+  --t_group_depth;
+  if (t_group_depth > 0) return flxSuccess;  // inside an outer group: flushed by its end
+  return flush_group();
+}
+
 flxResult_t flxGroupStart(void) {
   ++t_group_depth;
   return flxSuccess;

@@ -620,10 +620,22 @@ int world_nlocal(World* w) { return (int)w->local.size(); }
 void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(kMaxCtas, n)); }
 
 // ------------------------------------------------------------ creation
+namespace {
+// Frees a partially built world when creation fails (the destroy barrier is
+// skipped: `boot` is only set once bootstrap has fully succeeded).
+struct WorldGuard {
+  World* w;
+  ~WorldGuard() {
+    if (w) world_free(w);
+  }
+};
+}  // namespace
+
 flxResult_t world_create_loopback(int nranks, int device, World** out) {
   if (nranks < 1 || nranks > kMaxRanks)
     return fail(flxInvalidArgument, "loopback supports 1..%d ranks", kMaxRanks);
   auto* w = new World();
+  WorldGuard guard{w};
   world_config(w, nranks);
   w->loopback = true;
   w->local.resize(nranks);
@@ -640,12 +652,14 @@ flxResult_t world_create_loopback(int nranks, int device, World** out) {
     FLX_TRY(local_init(w, w->local[r]));
   }
   FLX_TRY(alloc_host_staging(w, nullptr));
+  guard.w = nullptr;
   *out = w;
   return flxSuccess;
 }
 
 flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_hex, World** out) {
   auto* w = new World();
+  WorldGuard guard{w};
   world_config(w, nranks);
   w->local.resize(1);
   w->local[0].rank = rank;
@@ -708,6 +722,7 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
     shm_unlink(boot_name);
     shm_unlink(stage_name);
   }
+  guard.w = nullptr;
   *out = w;
   return flxSuccess;
 }

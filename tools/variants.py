@@ -58,6 +58,26 @@ out["allgather_bf16"] = {"ms": round(ms, 4), "kernel_ms": round(kms, 4),
                          "hbm_frac": round((n + n * n) * (S // n) / (kms * 1e-3) / 1e9 / peak, 4),
                          "busbw": round(S / (ms * 1e-3) * 7 / 8 / 1e9, 1), "exact": ok}
 del s, r
+# ReduceScatter fp32: each rank sends n blocks of S/n, receives one block
+blk = S // 4 // n
+s = [torch.randn(blk * n, device="cuda") for _ in range(n)]
+r = [torch.empty(blk, device="cuda") for _ in range(n)]
+cl.set_shares(CollectiveOp.REDUCESCATTER, (1000, 0, 0))
+ms = timeit(lambda: cl.reduce_scatter(s, r))
+h = cl.comms[0].path_times_history(20)
+kms = statistics.mean(x[PathKind.NVLINK] for x in h) * 1e3
+out["reducescatter_f32"] = {"ms": round(ms, 4), "kernel_ms": round(kms, 4),
+                            "hbm_frac": round((n * S + S) / (kms * 1e-3) / 1e9 / peak, 4),
+                            "busbw": round(S / (ms * 1e-3) * 7 / 8 / 1e9, 1)}
+# AllToAll fp32: n blocks of S/n each way
+r = [torch.empty_like(x) for x in s]
+cl.set_shares(CollectiveOp.ALLTOALL, (1000, 0, 0))
+ms = timeit(lambda: cl.all_to_all(s, r))
+h = cl.comms[0].path_times_history(20)
+kms = statistics.mean(x[PathKind.NVLINK] for x in h) * 1e3
+out["alltoall_f32"] = {"ms": round(ms, 4), "kernel_ms": round(kms, 4),
+                       "hbm_frac": round(2 * n * S / (kms * 1e-3) / 1e9 / peak, 4)}
+del s, r
 # PCIe-path cost in the capped (config-4 style) setting
 cnt = S // 4
 s = [torch.randn(cnt, device="cuda") for _ in range(n)]

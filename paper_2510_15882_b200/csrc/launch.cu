@@ -168,7 +168,7 @@ cudaError_t launch_xpose(const XposeArgs& a, int grid, cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   bool vec = (a.src_stride & 15) == 0 && (a.dst_stride & 15) == 0;
   for (int r = 0; r < a.n; ++r) vec = vec && aligned16(a.src[r]) && aligned16(a.dst[r]);
-  const size_t need = ((a.bytes >> 4) + 16 + 511) / 512;  // single pass when uncapped
+  const size_t need = ((a.bytes >> 4) + 2047) / 2048;  // single pass (4 vectors/thread)
   const unsigned gx = (unsigned)std::min<size_t>(std::max<size_t>(1, need), (size_t)grid);
   xpose_kernel<<<dim3(gx, a.n * a.n), 512, 0, s>>>(a, vec ? 1 : 0);
   return cudaGetLastError();

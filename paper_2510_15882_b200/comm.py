@@ -443,6 +443,13 @@ class Clique:
     def _validate(self, sends, recvs, gather: bool = False, scatter: bool = False):
         if len(sends) != self.nranks or len(recvs) != self.nranks:
             raise ValueError(f"need one send and one recv tensor per rank ({self.nranks})")
+        # the same tensors (same objects at the same addresses) as the last call
+        # in this mode were already checked: skip the per-tensor property reads
+        key = (gather, scatter, tuple((id(t), t.data_ptr(), t.numel()) for t in sends),
+               tuple((id(t), t.data_ptr(), t.numel()) for t in recvs))
+        if key == getattr(self, "_checked", None):
+            return
+        self._checked = None
         s0 = sends[0]
         if scatter and s0.numel() % self.nranks:
             raise ValueError("reduce_scatter send must hold nranks equal blocks")
@@ -454,6 +461,7 @@ class Clique:
             if s.numel() != s0.numel() or s.dtype != s0.dtype or r.numel() != want \
                     or r.dtype != s0.dtype:
                 raise ValueError("all ranks need same-shaped send/recv tensors of one dtype")
+        self._checked = key
 
     def _issue(self, coll: int, sends, recvs, op: int, stream, count: int | None = None) -> None:
         """All ranks' calls in one ``flxGroupCollective`` (== flxGroupStart, one

@@ -49,6 +49,23 @@ def busbw_allgather(out_bytes: int, seconds: float, n: int) -> float:
     return out_bytes / seconds * (n - 1) / n / 1e9
 
 
+def ncu_traffic(summary: str = "profiles/r1/fold_once_ncu_summary.txt"):
+    """dram read + write bytes per launch of the dominant kernel, from the
+    committed ``ncu --set full`` capture of the same workload (None if absent)."""
+    units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    try:
+        with open(os.path.join(ROOT, summary)) as f:
+            for line in f:
+                parts = line.split()
+                if len(parts) == 3 and parts[0] in ("dram__bytes_read.sum",
+                                                    "dram__bytes_write.sum"):
+                    total += float(parts[1]) * units[parts[2]]
+    except (OSError, KeyError, ValueError):
+        return None
+    return int(total) if total else None
+
+
 # ----------------------------------------------------------------- clocks
 class ClockSampler:
     """SM clock + throttle reasons polled through NVML during the timed region
@@ -415,7 +432,11 @@ def run_single_gpu(args) -> None:
                    "moves": sum(1 for e in balancer.evaluations if e.moved)},
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-            "frac": round(achieved / hbm_peak, 4), "traffic": None,
+            "frac": round(achieved / hbm_peak, 4),
+            # the capture is of the full 256 MiB slice; another split has no capture
+            "traffic": ncu_traffic() if pbytes[PathKind.NVLINK] == AR_BYTES else None,
+            "traffic_source": "profiles/r1/fold_once_ncu_summary.txt (ncu --set full, same "
+                              "kernel and size; dram__bytes_read.sum + dram__bytes_write.sum)",
             "kernel": "fold_once_kernel<float,Sum,8> (NVLink-path slice, 8 virtual ranks, "
                       "one 16 B vector per thread)",
             "algorithmic_bytes_per_launch": nv_alg_bytes,

@@ -139,10 +139,12 @@ def dtype_code(dtype) -> int:
     return table[dtype]
 
 
-def _stream_handle(stream) -> ctypes.c_void_p:
+def _stream_handle(stream, device: int | None = None) -> ctypes.c_void_p:
     import torch
 
     if stream is None:
+        if device is not None:  # raw handle without building a Stream object
+            return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(device))
         stream = torch.cuda.current_stream()
     return ctypes.c_void_p(stream.cuda_stream)
 
@@ -224,7 +226,7 @@ class Communicator:
             raise ValueError("recv must match send in size and dtype")
         _check(load_library().flxAllReduce(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
-            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream)), "flxAllReduce")
+            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream, send.get_device())), "flxAllReduce")
         return recv
 
     def all_gather(self, send, recv, stream=None):
@@ -234,7 +236,7 @@ class Communicator:
             raise ValueError("recv must hold nranks * send.numel() elements of send.dtype")
         _check(load_library().flxAllGather(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
-            dtype_code(send.dtype), self._h, _stream_handle(stream)), "flxAllGather")
+            dtype_code(send.dtype), self._h, _stream_handle(stream, send.get_device())), "flxAllGather")
         return recv
 
     def reduce_scatter(self, send, recv, op: str = "sum", stream=None):
@@ -245,7 +247,7 @@ class Communicator:
             raise ValueError("send must hold nranks * recv.numel() elements of recv.dtype")
         _check(load_library().flxReduceScatter(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), recv.numel(),
-            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream)),
+            dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream, send.get_device())),
             "flxReduceScatter")
         return recv
 
@@ -258,7 +260,7 @@ class Communicator:
         _check(load_library().flxAllToAll(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()),
             send.numel() // self.nranks, dtype_code(send.dtype), self._h,
-            _stream_handle(stream)), "flxAllToAll")
+            _stream_handle(stream, send.get_device())), "flxAllToAll")
         return recv
 
     # ---- balancer plumbing
@@ -447,8 +449,9 @@ class Clique:
         # in this mode were already checked: skip the per-tensor property reads
         key = (gather, scatter, tuple((id(t), t.data_ptr(), t.numel()) for t in sends),
                tuple((id(t), t.data_ptr(), t.numel()) for t in recvs))
-        if key == getattr(self, "_checked", None):
-            return
+        checked = getattr(self, "_checked", None)
+        if checked is not None and key == checked[0]:
+            return checked[1]
         self._checked = None
         s0 = sends[0]
         if scatter and s0.numel() % self.nranks:
@@ -461,44 +464,44 @@ class Clique:
             if s.numel() != s0.numel() or s.dtype != s0.dtype or r.numel() != want \
                     or r.dtype != s0.dtype:
                 raise ValueError("all ranks need same-shaped send/recv tensors of one dtype")
-        self._checked = key
+        ptrs = ctypes.c_void_p * self.nranks
+        # the pointer arrays and dtype ride along with the key: a repeated call
+        # re-uses them instead of rebuilding 2*nranks ctypes values
+        args = (ptrs(*[t.data_ptr() for t in sends]), ptrs(*[t.data_ptr() for t in recvs]),
+                dtype_code(s0.dtype))
+        self._checked = (key, args)
+        return args
 
-    def _issue(self, coll: int, sends, recvs, op: int, stream, count: int | None = None) -> None:
+    def _issue(self, coll: int, args, op: int, stream, count: int) -> None:
         """All ranks' calls in one ``flxGroupCollective`` (== flxGroupStart, one
         call per rank, flxGroupEnd): small messages are host-issue bound."""
-        n = self.nranks
-        ptrs = ctypes.c_void_p * n
-        rc = load_library().flxGroupCollective(
-            coll, self._handles, n, ptrs(*[t.data_ptr() for t in sends]),
-            ptrs(*[t.data_ptr() for t in recvs]),
-            sends[0].numel() if count is None else count, dtype_code(sends[0].dtype), op,
-            _stream_handle(stream))
+        sp, rp, dt = args
+        rc = load_library().flxGroupCollective(coll, self._handles, self.nranks, sp, rp, count,
+                                               dt, op, _stream_handle(stream, self.device))
         _check(rc, "flxGroupCollective")
 
     def all_reduce(self, sends: Sequence, recvs: Sequence | None = None, op: str = "sum",
                    stream=None):
         recvs = list(sends) if recvs is None else list(recvs)
-        self._validate(sends, recvs, gather=False)
-        self._issue(0, sends, recvs, _OPS[op], stream)
+        args = self._validate(sends, recvs, gather=False)
+        self._issue(0, args, _OPS[op], stream, sends[0].numel())
         return recvs
 
     def all_gather(self, sends: Sequence, recvs: Sequence, stream=None):
-        self._validate(sends, recvs, gather=True)
-        self._issue(1, sends, recvs, 0, stream)
+        args = self._validate(sends, recvs, gather=True)
+        self._issue(1, args, 0, stream, sends[0].numel())
         return recvs
 
     def reduce_scatter(self, sends: Sequence, recvs: Sequence, op: str = "sum", stream=None):
-        self._validate(sends, recvs, scatter=True)
-        self._issue(2, sends, recvs, _OPS[op], stream,
-                    count=recvs[0].numel())
+        args = self._validate(sends, recvs, scatter=True)
+        self._issue(2, args, _OPS[op], stream, recvs[0].numel())
         return recvs
 
     def all_to_all(self, sends: Sequence, recvs: Sequence, stream=None):
-        self._validate(sends, recvs)
+        args = self._validate(sends, recvs)
         if sends[0].numel() % self.nranks:
             raise ValueError("all_to_all buffers must hold nranks equal blocks")
-        self._issue(3, sends, recvs, 0, stream,
-                    count=sends[0].numel() // self.nranks)
+        self._issue(3, args, 0, stream, sends[0].numel() // self.nranks)
         return recvs
 
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:

@@ -58,6 +58,11 @@ __global__ void __launch_bounds__(512) fan_dst(const Args a) {
   }
 }
 
+__global__ void __launch_bounds__(512) write_only(const Args a) {
+  const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < a.nvec * N) stv<0>(a.dst[blockIdx.y] + v, make_uint4(v, v, v, v));
+}
+
 __global__ void fill_random(uint32_t* p, size_t n, uint32_t seed) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     uint32_t x = (uint32_t)i * 2654435761u ^ seed;
@@ -99,5 +104,12 @@ int main(int argc, char**) {
   rep("2 vec/thread many CTAs", timeit([&] { fan<2, 0><<<dim3((unsigned)((nvec + 1023) / 1024), N), 512>>>(a); }, 20));
   rep("dst-major sm/8 per dst", timeit([&] { fan_dst<<<dim3(sms / N * 2, N), 512>>>(a); }, 20));
   rep("dst-major many", timeit([&] { fan_dst<<<dim3((unsigned)((nvec * N + 511) / 512 / 4), N), 512>>>(a); }, 20));
+  // ceilings: the fan-out is 8/9 writes, so the HBM write-only rate bounds it
+  const double wbytes = (double)N * N * in_bytes;
+  auto rep_w = [&](const char* name, float ms) { printf("{\"variant\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", name, ms, wbytes / (ms * 1e-3) / 1e9); };
+  rep_w("ceiling: cudaMemsetAsync of the 8 outputs (write only)",
+        timeit([&] { for (int d = 0; d < N; ++d) cudaMemsetAsync(a.dst[d], 0, in_bytes * N); }, 20));
+  rep_w("ceiling: store-only kernel, 1 vec/thread",
+        timeit([&] { write_only<<<dim3((unsigned)((nvec * N + 511) / 512), N), 512>>>(a); }, 20));
   return 0;
 }

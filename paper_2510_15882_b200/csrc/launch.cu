@@ -196,11 +196,12 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   } else if (!vec) {
     fanout_byte_kernel<<<g, 512, 0, s>>>(a);
   } else if ((size_t)grid * 512 >= (a.bytes >> 4)) {  // uncapped: single pass
-    const dim3 once((unsigned)(((a.bytes >> 4) + 16 + 511) / 512), a.nsrc);
-    if (a.ndst <= 2) fanout_once_kernel<2><<<once, 512, 0, s>>>(a);
-    else if (a.ndst <= 4) fanout_once_kernel<4><<<once, 512, 0, s>>>(a);
-    else if (a.ndst <= 8) fanout_once_kernel<8><<<once, 512, 0, s>>>(a);
-    else fanout_once_kernel<16><<<once, 512, 0, s>>>(a);
+    const unsigned bx = (unsigned)(((a.bytes >> 4) + 16 + 511) / 512);
+    const dim3 once(bx, a.nsrc), twice(2 * bx, a.nsrc);
+    if (a.ndst <= 2) fanout_once_kernel<2, 1><<<once, 512, 0, s>>>(a);
+    else if (a.ndst <= 4) fanout_once_kernel<4, 2><<<twice, 512, 0, s>>>(a);
+    else if (a.ndst <= 8) fanout_once_kernel<8, 2><<<twice, 512, 0, s>>>(a);
+    else fanout_once_kernel<16, 2><<<twice, 512, 0, s>>>(a);
   } else if (a.ndst <= 2) {
     fanout_vec_kernel<2, 1><<<g, 512, 0, s>>>(a);
   } else if (a.ndst <= 4) {

@@ -60,6 +60,39 @@ __global__ void __launch_bounds__(THREADS) fold(const Args a) {
   }
 }
 
+// G adjacent CTAs fold the same span (repeat reads from L2); each stores N/G dsts
+template <int G>
+__global__ void __launch_bounds__(512) fold_split(const Args a) {
+  const int g = blockIdx.x % G;
+  const size_t v = (size_t)(blockIdx.x / G) * 512 + threadIdx.x;
+  if (v >= a.nvec) return;
+  float4 in[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) in[r] = ld<0>(a.src[r] + v);
+  float4 acc = in[0];
+#pragma unroll
+  for (int r = 1; r < N; ++r) { acc.x += in[r].x; acc.y += in[r].y; acc.z += in[r].z; acc.w += in[r].w; }
+#pragma unroll
+  for (int d = g * (N / G); d < (g + 1) * (N / G); ++d) st<0>(a.dst[d] + v, acc);
+}
+
+// ceilings: read-only (8 inputs, one flag store if impossible) and store-only
+__global__ void __launch_bounds__(512) read_only(const Args a, float* sink) {
+  const size_t v = (size_t)blockIdx.x * 512 + threadIdx.x;
+  if (v >= a.nvec) return;
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < N; ++r) { float4 x = ld<0>(a.src[r] + v); s += x.x + x.y + x.z + x.w; }
+  if (s == -1.2345f) *sink = s;
+}
+__global__ void __launch_bounds__(512) store_only(const Args a) {
+  const size_t v = (size_t)blockIdx.x * 512 + threadIdx.x;
+  if (v >= a.nvec) return;
+  const float4 x = make_float4(v, v, v, v);
+#pragma unroll
+  for (int d = 0; d < N; ++d) st<0>(a.dst[d] + v, x);
+}
+
 __global__ void copyk(const float4* __restrict__ s, float4* __restrict__ d, size_t nvec) {
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += (size_t)gridDim.x * blockDim.x) d[v] = s[v];
 }
@@ -110,6 +143,15 @@ int main(int argc, char**) {
   report("512x2/SM unr1", timeit([&] { fold<512, 1, 0, 0><<<2 * sms, 512>>>(a); }, 20));
   report("128x8/SM unr1", timeit([&] { fold<128, 1, 0, 0><<<8 * sms, 128>>>(a); }, 20));
   report("512 x many (nvec/512 CTAs)", timeit([&] { fold<512, 1, 0, 0><<<(unsigned)((nvec + 511) / 512), 512>>>(a); }, 20));
+  const unsigned nb = (unsigned)((nvec + 511) / 512);
+  report("split dst x2 (L2 re-read)", timeit([&] { fold_split<2><<<nb * 2, 512>>>(a); }, 20));
+  report("split dst x4 (L2 re-read)", timeit([&] { fold_split<4><<<nb * 4, 512>>>(a); }, 20));
+  float* sink; CK(cudaMalloc(&sink, 4));
+  const float rms = timeit([&] { read_only<<<nb, 512>>>(a, sink); }, 20);
+  printf("{\"variant\": \"ceiling: read-only 8 x 256 MiB\", \"ms\": %.4f, \"GBps\": %.1f}\n", rms, N * (double)bytes / (rms * 1e-3) / 1e9);
+  const float wms = timeit([&] { store_only<<<nb, 512>>>(a); }, 20);
+  printf("{\"variant\": \"ceiling: store-only 8 x 256 MiB\", \"ms\": %.4f, \"GBps\": %.1f}\n", wms, N * (double)bytes / (wms * 1e-3) / 1e9);
+  printf("{\"variant\": \"ceiling: read-only + store-only times\", \"ms\": %.4f, \"GBps\": %.1f}\n", rms + wms, alg / ((rms + wms) * 1e-3) / 1e9);
   float cms = timeit([&] { for (int r = 0; r < N; ++r) copyk<<<4 * sms, 256>>>(a.src[r], a.dst[r], nvec); }, 10);
   printf("{\"variant\": \"copy 8 x 256 MiB (reference)\", \"ms\": %.4f, \"GBps\": %.1f}\n", cms, alg / (cms * 1e-3) / 1e9);
   return 0;

@@ -32,6 +32,16 @@ constexpr int kMaxCtas = 128;
 enum FlagKind { kArrive = 0, kFree = 1, kReady = 2, kPulled = 3 };
 constexpr int kFlagKinds = 4;
 constexpr size_t kFlagWords = (size_t)kFlagKinds * kMaxRanks * kMaxCtas;
+// Per-CTA epoch state, private to the rank, after the flag words:
+//   [2*cta + 0] rounds run so far by CTA cta (round k of the next call uses
+//               epoch state + 1 + k)
+//   [2*cta + 1] epoch of the last AllReduce round (guards outbox reuse; 0: none)
+// Kept on the device and advanced by the kernel itself, so a launch carries
+// no host-side epoch and can be captured into a CUDA graph and replayed.
+// Every rank runs the same sequence of collectives with the same grid, so
+// CTA b's state is identical on every rank; a CTA that sits out a call lags
+// the same way everywhere.
+constexpr size_t kStateWords = 2 * kMaxCtas;
 
 struct RankArgs {
   const char* send;
@@ -43,10 +53,34 @@ struct RankArgs {
   size_t bytes;        // NVLink slice: per-rank message bytes (AR) / send bytes (AG)
   size_t rank_stride;  // AllGather: distance between rank blocks in recv
   size_t slot;         // inbox slot capacity (bytes) per source rank
-  uint32_t epoch;      // epoch of round 0; round k uses epoch + k
-  uint32_t prev_outbox_epoch;  // AllReduce: epoch of the previous AllReduce round (0: none)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
 };
+
+// This CTA's epoch state (in its own rank's flag block).
+struct CtaEpochs {
+  uint32_t* state;
+  uint32_t first;    // epoch of round 0 of this call
+  uint32_t last_ar;  // epoch of the last AllReduce round before this call
+};
+
+__device__ __forceinline__ CtaEpochs cta_epochs(const RankArgs& a, int cta) {
+  __shared__ uint32_t s_first, s_last_ar;
+  uint32_t* st = a.flags[a.rank] + kFlagWords + 2 * (size_t)cta;
+  if (threadIdx.x == 0) {
+    s_first = st[0] + 1;
+    s_last_ar = st[1];
+  }
+  __syncthreads();
+  return CtaEpochs{st, s_first, s_last_ar};
+}
+
+// After the call's `rounds` rounds (not reached when a wait aborted).
+__device__ __forceinline__ void cta_epochs_done(const CtaEpochs& ep, uint32_t rounds, bool ar) {
+  if (threadIdx.x == 0 && rounds > 0) {
+    ep.state[0] = ep.first - 1 + rounds;
+    if (ar) ep.state[1] = ep.first + rounds - 1;
+  }
+}
 
 struct LoopbackArgs {
   RankArgs r[kMaxRanks];
@@ -215,9 +249,11 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t round_cap = a.slot * n;
   const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
-  uint32_t prev_outbox = a.prev_outbox_epoch;
-  for (size_t base = 0, k = 0; base < a.bytes; base += round_cap, ++k) {
-    const uint32_t e = a.epoch + (uint32_t)k;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t prev_outbox = ep.last_ar;
+  uint32_t k = 0;
+  for (size_t base = 0; base < a.bytes; base += round_cap, ++k) {
+    const uint32_t e = ep.first + k;
     const size_t len = min(round_cap, a.bytes - base);
     const size_t chunk = ceil16((len + n - 1) / n);
     size_t lo[kMaxRanks], hi[kMaxRanks], off[kMaxRanks];
@@ -277,6 +313,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     }
     prev_outbox = e;
   }
+  cta_epochs_done(ep, k, true);
 }
 
 // After consuming my inbox slots for epoch e: tell every source (kFree = e).
@@ -290,8 +327,10 @@ __device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e)
 
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
-    const uint32_t e = a.epoch + (uint32_t)k;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t k = 0;
+  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = ep.first + k;
     const size_t len = min(a.slot, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
@@ -322,6 +361,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     }
     free_all(a, cta, e);
   }
+  cta_epochs_done(ep, k, false);
 }
 
 // ReduceScatter: a.bytes = NVLink part of each recv block, a.rank_stride = the
@@ -329,8 +369,10 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
 template <typename T, int OP>
 __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
-    const uint32_t e = a.epoch + (uint32_t)k;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t k = 0;
+  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = ep.first + k;
     const size_t len = min(a.slot, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
@@ -357,6 +399,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
     }
     free_all(a, cta, e);
   }
+  cta_epochs_done(ep, k, false);
 }
 
 // AllToAll: a.bytes = NVLink part of each block, a.rank_stride = block stride
@@ -364,8 +407,10 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
 // land every peer's push into recv block p.
 __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  for (size_t base = 0, k = 0; base < a.bytes; base += a.slot, ++k) {
-    const uint32_t e = a.epoch + (uint32_t)k;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t k = 0;
+  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+    const uint32_t e = ep.first + k;
     const size_t len = min(a.slot, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
@@ -391,6 +436,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     }
     free_all(a, cta, e);
   }
+  cta_epochs_done(ep, k, false);
 }
 
 __global__ void __launch_bounds__(512) rank_alltoall_kernel(const RankArgs a) {

@@ -89,8 +89,7 @@ struct World {
   int nctas = 0;
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t hcap = 0;       // PCIe staging bytes per rank region
-  uint32_t epoch = 1;    // NVLink-path flag epoch (next round)
-  uint32_t last_ar_epoch = 0;  // last AllReduce round (guards outbox reuse)
+  // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
   uint32_t last_ar_pepoch = 0;  // last AllReduce PCIe epoch (guards R_r reuse)
   uint32_t pepoch = 1;   // PCIe-path semaphore epoch (next call)
   // host staging segment: [sem words][H_0 .. H_{n-1}][R_0 .. R_{n-1}]
@@ -134,8 +133,8 @@ flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaSetDevice(L.device));
   const size_t scratch_bytes = w->slot * (w->nranks + 1);
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
-  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), kFlagWords * 4));
-  FLX_CUDA(cudaMemset(L.flags, 0, kFlagWords * 4));
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), (kFlagWords + kStateWords) * 4));
+  FLX_CUDA(cudaMemset(L.flags, 0, (kFlagWords + kStateWords) * 4));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.dstage), w->hcap));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
@@ -350,9 +349,13 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   if (*w->abort_word) return fail(flxInternalError, "communicator aborted by an earlier timeout");
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
-  if (cap != cudaStreamCaptureStatusNone)
-    return fail(flxInvalidUsage, "multi-rank collectives carry host-side epochs and cannot be "
-                "captured into a CUDA graph yet");
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  // The NVLink kernels keep their epochs on the device and replay correctly
+  // from a graph; the PCIe path's semaphore targets are host-side counters
+  // that a replay would repeat.
+  if (capturing && pc > 0)
+    return fail(flxInvalidUsage, "a multi-rank collective with a PCIe share cannot be captured "
+                "into a CUDA graph: set NVLink-only shares for the captured size bucket");
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
   if ((scatter || a2a ? pc * n : pc) > w->hcap)
     return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
@@ -540,10 +543,6 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
 
   // ---------------- NVLink slice
   if (nv > 0) {
-    const uint32_t e0 = w->epoch;
-    const size_t round_cap = (gather || scatter || a2a) ? w->slot : w->slot * n;
-    const uint32_t rounds = (uint32_t)((nv + round_cap - 1) / round_cap);
-    w->epoch += rounds;
     LoopbackArgs la;
     memset(&la, 0, sizeof(la));
     for (int i = 0; i < nl; ++i) {
@@ -559,8 +558,6 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.bytes = nv;
       a.rank_stride = bytes;
       a.slot = w->slot;
-      a.epoch = e0;
-      a.prev_outbox_epoch = w->last_ar_epoch;
       a.abort_word = w->abort_word;
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
@@ -569,7 +566,6 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         : gather  ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
         : scatter ? launch_rank_reduce<true>(dtype, op, w->loopback, args, w->nctas, n, s0)
                   : launch_rank_reduce<false>(dtype, op, w->loopback, args, w->nctas, n, s0);
-    if (!gather && !scatter) w->last_ar_epoch = e0 + rounds - 1;
     if (err != cudaSuccess)
       return fail(flxUnhandledCudaError, "rank kernel launch: %s", cudaGetErrorString(err));
   }
@@ -587,8 +583,9 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   }
   for (int i = 0; i < nl; ++i) {
     World::Local& L = w->local[i];
-    tm[i]->used[flxPathNvlink] = nv > 0;
-    tm[i]->used[flxPathPcie] = pc > 0;
+    // events recorded inside a capture are graph edges, not timestamps
+    tm[i]->used[flxPathNvlink] = nv > 0 && !capturing;
+    tm[i]->used[flxPathPcie] = pc > 0 && !capturing;
     tm[i]->used[flxPathRdma] = false;
     L.last_bytes = split;
     L.calls++;

@@ -136,3 +136,71 @@ def test_loopback_path_times():
             w.all_reduce(dev, outs)
         h = w.comms[1].path_times_history(8)
         assert len(h) == 3 and all(x[PathKind.NVLINK] > 0 and x[PathKind.PCIE_STAGED] > 0 for x in h)
+
+
+def test_loopback_cuda_graph_capture_and_replay():
+    # The rank kernels keep their flag epochs on the device, so the multi-rank
+    # collectives (all four protocols, several slot rounds per call) can be
+    # captured once and replayed on fresh inputs, interleaved with eager calls.
+    n, count = 4, (3 << 18) + 4
+    os.environ["FLX_SLOT_MB"] = "1"  # several rounds per call
+    try:
+        w = flx.Clique(n, loopback=True)
+    finally:
+        del os.environ["FLX_SLOT_MB"]
+    g = torch.Generator(device="cpu").manual_seed(5)
+    sends = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    ar = [torch.empty_like(s) for s in sends]
+    ag = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    ag_in = [s[:count] for s in sends]
+    rs = [torch.empty(count, device="cuda") for _ in range(n)]
+    a2a = [torch.empty_like(s) for s in sends]
+    with w:
+        for op in CollectiveOp:
+            w.set_shares(op, (1000, 0, 0))
+        stream = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            w.all_reduce(sends, ar)
+            w.all_gather(ag_in, ag)
+            w.reduce_scatter(sends, rs)
+            w.all_to_all(sends, a2a)
+        a2a_align = w.comms[0].alignment(CollectiveOp.ALLTOALL)
+        g1 = (1000, 0, 0)
+        for it in range(4):
+            host = [torch.randn(n * count, generator=g).round() for _ in range(n)]
+            for s, h in zip(sends, host):
+                s.copy_(h)
+            if it % 2:
+                graph.replay()
+            else:  # eager calls advance the same device epochs
+                w.all_reduce(sends, ar)
+                w.all_gather(ag_in, ag)
+                w.reduce_scatter(sends, rs)
+                w.all_to_all(sends, a2a)
+            torch.cuda.synchronize()
+            hn = [h.numpy() for h in host]
+            want_ar = oracle.allreduce(hn, 7, 0, g1, n * 4096)
+            want_ag = oracle.allgather([x[:count] for x in hn], 7, g1, 4096)
+            want_rs = oracle.reducescatter(hn, 7, 0, g1, 4096)
+            want_a2a = oracle.alltoall(hn, 7, g1, a2a_align)
+            for r in range(n):
+                np.testing.assert_array_equal(_np(ar[r], 7), want_ar[r])
+                np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
+                np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])
+                np.testing.assert_array_equal(_np(a2a[r], 7), want_a2a[r])
+
+
+def test_loopback_capture_with_pcie_share_is_rejected():
+    n = 2
+    sends = [torch.randn(1 << 16, device="cuda") for _ in range(n)]
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        stream = torch.cuda.Stream()
+        graph = torch.cuda.CUDAGraph()
+        with pytest.raises(flx.FlexLinkError):
+            with torch.cuda.graph(graph, stream=stream):
+                w.all_reduce(sends, sends)
+        torch.cuda.synchronize()
+        w.all_reduce(sends, sends)  # still usable eagerly
+        torch.cuda.synchronize()

@@ -76,13 +76,15 @@ def test_reduce_scatter_in_place(loopback):
 
 
 def test_mixed_collectives_share_flags_and_staging():
-    # AllReduce, AllGather and ReduceScatter interleaved on one loopback world
-    # (shared epochs/semaphores across protocols), every result exact
+    # AllReduce, AllGather, ReduceScatter and AllToAll interleaved on one
+    # loopback world (shared epochs/semaphores across protocols; an AllToAll
+    # right before an AllReduce must not move the outbox guard), every result exact
     n, count = 4, (1 << 16) + 1
+    g = (900, 100, 0)
     cpu = _inputs(n, n * count, 7, 21)
     with flx.Clique(n, loopback=True) as w:
-        for op in (CollectiveOp.ALLREDUCE, CollectiveOp.ALLGATHER, CollectiveOp.REDUCESCATTER):
-            w.set_shares(op, (900, 100, 0))
+        for op in CollectiveOp:
+            w.set_shares(op, g)
         for _ in range(3):
             s = [h.cuda() for h in cpu]
             ar = [torch.empty_like(x) for x in s]
@@ -92,14 +94,19 @@ def test_mixed_collectives_share_flags_and_staging():
             w.all_gather(ag_in, ag)
             rs = [torch.empty(count, device="cuda") for _ in range(n)]
             w.reduce_scatter(s, rs)
+            a2a = [torch.empty_like(x) for x in s]
+            w.all_to_all(s, a2a)
             torch.cuda.synchronize()
-            want_ar = oracle.allreduce([h.numpy() for h in cpu], 7, 0, (900, 100, 0), n * 4096)
-            want_ag = oracle.allgather([h.numpy()[:count] for h in cpu], 7, (900, 100, 0), 4096)
-            want_rs = oracle.reducescatter([h.numpy() for h in cpu], 7, 0, (900, 100, 0), 4096)
+            want_ar = oracle.allreduce([h.numpy() for h in cpu], 7, 0, g, n * 4096)
+            want_ag = oracle.allgather([h.numpy()[:count] for h in cpu], 7, g, 4096)
+            want_rs = oracle.reducescatter([h.numpy() for h in cpu], 7, 0, g, 4096)
+            want_a2a = oracle.alltoall([h.numpy() for h in cpu], 7, g,
+                                       w.comms[0].alignment(CollectiveOp.ALLTOALL))
             for r in range(n):
                 np.testing.assert_array_equal(_np(ar[r], 7), want_ar[r])
                 np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
                 np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])
+                np.testing.assert_array_equal(_np(a2a[r], 7), want_a2a[r])
 
 
 @pytest.mark.parametrize("loopback", [False, True])

@@ -22,6 +22,11 @@
 namespace flx {
 
 constexpr int kMaxCtas = 128;
+
+// Phase-timing hook for tools/rank_phases.cu (compiled out in the library).
+#ifndef FLX_PHASE
+#define FLX_PHASE(i)
+#endif
 // Flag kinds, each [src][cta] in the RECEIVING rank's block:
 //   kArrive  src pushed its data into my inbox[src] for epoch e
 //   kFree    src finished reading the inbox slot I pushed into (epoch e) —
@@ -240,6 +245,16 @@ __device__ __forceinline__ void cta_part(size_t len, int nctas, int cta, size_t*
   *hi = min(len, *lo + part);
 }
 
+// CTA cta owns the same region [cta*sub, cta*sub + sub) of every inbox slot
+// and of the outbox in every round of every protocol: it never depends on the
+// message length, so the per-CTA flags guard exactly the bytes that CTA pair
+// writes and reads (with length-dependent offsets, CTA b could overwrite bytes
+// a slower peer CTA b' is still reading from an earlier round).  The round
+// capacity is sub * nctas per slot, which keeps every CTA part <= sub.
+__device__ __forceinline__ size_t cta_sub(size_t slot, int nctas) {
+  return (slot / (size_t)nctas) & ~(size_t)15;
+}
+
 // Every protocol: wait until peer c freed the inbox slot I push into
 // (kFree >= e-1), push, announce (kArrive = e); the receiver consumes its
 // inbox and answers kFree = e.
@@ -247,8 +262,11 @@ __device__ __forceinline__ void cta_part(size_t len, int nctas, int cta, size_t*
 template <typename T, int OP>
 __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  const size_t round_cap = a.slot * n;
+  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
+  const size_t round_cap = sub * nctas * n;
   const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
+  FLX_PHASE(0);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_outbox = ep.last_ar;
   uint32_t k = 0;
@@ -265,28 +283,31 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
       from[c] = a.send + base + off[c] + lo[c];
       nb[c] = hi[c] - lo[c];
     }
-    // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it)
-    //    (inbox offsets are relative to the chunk, so shift by lo[c])
+    // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it,
+    //    into this CTA's region of the slot)
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      FLX_PHASE(1);
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo[c], from[c], nb[c], false);
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, from[c], nb[c], false);
         targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
       cta_signal(targets, nt, e);
+      FLX_PHASE(2);
     }
     // 2) every push landed, and every peer pulled my previous outbox
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a.abort_word))
       return;
+    FLX_PHASE(3);
     {
       const char* src[kMaxRanks];
       for (int p = 0; p < n; ++p)
         src[p] = (p == r) ? a.send + base + off[r] + lo[r]
-                          : a.scratch[r] + (size_t)p * a.slot + lo[r];
-      char* dst[2] = {a.recv + base + off[r] + lo[r], a.scratch[r] + outbox + lo[r]};
+                          : a.scratch[r] + (size_t)p * a.slot + mine;
+      char* dst[2] = {a.recv + base + off[r] + lo[r], a.scratch[r] + outbox + mine};
       cta_fold<T, OP>(dst, 2, src, n, hi[r] - lo[r]);
     }
     {  // inbox slots consumed (kFree) and outbox readable (kReady), to every peer
@@ -298,18 +319,21 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
         targets[nt++] = flag_at(a.flags[c], kReady, r, cta);
       }
       cta_signal(targets, nt, e);
+      FLX_PHASE(4);
     }
     // 3) pull every peer's reduced chunk
     if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a.abort_word)) return;
+    FLX_PHASE(5);
     {
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.recv + base + off[c] + lo[c], a.scratch[c] + outbox + lo[c], nb[c], true);
+        cta_copy(a.recv + base + off[c] + lo[c], a.scratch[c] + outbox + mine, nb[c], true);
         targets[nt++] = flag_at(a.flags[c], kPulled, r, cta);
       }
       cta_signal(targets, nt, e);
+      FLX_PHASE(6);
     }
     prev_outbox = e;
   }
@@ -327,11 +351,14 @@ __device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e)
 
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
+  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
+  const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(a.slot, a.bytes - base);
+    const size_t len = min(cap, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     const char* from[kMaxRanks];
@@ -340,13 +367,13 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
       from[c] = a.send + base + lo;
       nb[c] = hi - lo;
     }
-    {  // push my slice into every peer's inbox slot r (at my part's offset)
+    {  // push my slice into every peer's inbox slot r (this CTA's region)
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo, from[c], nb[c], false);
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, from[c], nb[c], false);
         targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
       char* own = a.recv + (size_t)r * a.rank_stride + base;
@@ -357,7 +384,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
-               a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
+               a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
     }
     free_all(a, cta, e);
   }
@@ -369,11 +396,14 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
 template <typename T, int OP>
 __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
+  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
+  const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(a.slot, a.bytes - base);
+    const size_t len = min(cap, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
@@ -382,7 +412,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
       int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo,
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
                  a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
         targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
@@ -393,7 +423,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
       const char* src[kMaxRanks];
       for (int p = 0; p < n; ++p)
         src[p] = (p == r) ? a.send + (size_t)r * a.rank_stride + base + lo
-                          : a.scratch[r] + (size_t)p * a.slot + lo;
+                          : a.scratch[r] + (size_t)p * a.slot + mine;
       char* dst[1] = {a.recv + base + lo};
       cta_fold<T, OP>(dst, 1, src, n, hi - lo);
     }
@@ -407,11 +437,14 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
 // land every peer's push into recv block p.
 __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
+  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
+  const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += a.slot, ++k) {
+  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(a.slot, a.bytes - base);
+    const size_t len = min(cap, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
@@ -420,7 +453,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
       int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + lo,
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
                  a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
         targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
@@ -432,7 +465,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
-               a.scratch[r] + (size_t)p * a.slot + lo, hi - lo, true);
+               a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
     }
     free_all(a, cta, e);
   }

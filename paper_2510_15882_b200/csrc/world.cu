@@ -228,7 +228,7 @@ flxResult_t alloc_host_staging(World* w, const char* shm_name) {
 
 void world_config(World* w, int nranks) {
   w->nranks = nranks;
-  w->slot = env_mib("FLX_SLOT_MB", 32);
+  w->slot = std::max<size_t>(env_mib("FLX_SLOT_MB", 32), 1 << 20);
   w->hcap = env_mib("FLX_PCIE_STAGE_MB", 64);
   w->nctas = 32;
   if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));

@@ -204,3 +204,37 @@ def test_loopback_capture_with_pcie_share_is_rejected():
         torch.cuda.synchronize()
         w.all_reduce(sends, sends)  # still usable eagerly
         torch.cuda.synchronize()
+
+
+def test_loopback_varying_sizes_multi_round():
+    # Back-to-back calls whose sizes (and short last rounds) differ: every CTA
+    # keeps one fixed region of each slot, so a fast rank's next round never
+    # lands in bytes a slower peer CTA is still reading.
+    n = 4
+    os.environ["FLX_SLOT_MB"] = "1"
+    try:
+        w = flx.Clique(n, loopback=True)
+    finally:
+        del os.environ["FLX_SLOT_MB"]
+    g = torch.Generator(device="cpu").manual_seed(9)
+    with w:
+        for op in CollectiveOp:
+            w.set_shares(op, (1000, 0, 0))
+        for count in (3 << 18, 5000, (1 << 20) + 12, 1 << 16, 777777, 4):
+            host = [torch.randn(n * count, generator=g) for _ in range(n)]
+            sends = [h.cuda() for h in host]
+            ar = [torch.empty_like(s) for s in sends]
+            ag = [torch.empty(n * count, device="cuda") for _ in range(n)]
+            rs = [torch.empty(count, device="cuda") for _ in range(n)]
+            w.all_reduce(sends, ar)
+            w.all_gather([s[:count] for s in sends], ag)
+            w.reduce_scatter(sends, rs)
+            torch.cuda.synchronize()
+            hn = [h.numpy() for h in host]
+            want_ar = oracle.allreduce(hn, 7, 0, (1000, 0, 0), n * 4096)
+            want_ag = oracle.allgather([x[:count] for x in hn], 7, (1000, 0, 0), 4096)
+            want_rs = oracle.reducescatter(hn, 7, 0, (1000, 0, 0), 4096)
+            for r in range(n):
+                np.testing.assert_array_equal(_np(ar[r], 7), want_ar[r])
+                np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
+                np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])

@@ -21,7 +21,7 @@
 
 namespace flx {
 
-constexpr int kMaxCtas = 128;
+constexpr int kMaxCtas = 64;  // also the number of regions per slot (cta_sub)
 
 // Phase-timing hook for tools/rank_phases.cu (compiled out in the library).
 #ifndef FLX_PHASE
@@ -38,15 +38,18 @@ enum FlagKind { kArrive = 0, kFree = 1, kReady = 2, kPulled = 3 };
 constexpr int kFlagKinds = 4;
 constexpr size_t kFlagWords = (size_t)kFlagKinds * kMaxRanks * kMaxCtas;
 // Per-CTA epoch state, private to the rank, after the flag words:
-//   [2*cta + 0] rounds run so far by CTA cta (round k of the next call uses
+//   [4*cta + 0] rounds run so far by CTA cta (round k of the next call uses
 //               epoch state + 1 + k)
-//   [2*cta + 1] epoch of the last AllReduce round (guards outbox reuse; 0: none)
+//   [4*cta + 1] epoch of the last two-shot AllReduce round (guards outbox
+//               reuse through kPulled; 0: none)
+//   [4*cta + 2] epoch of the last round that used the main inbox slots
+//               (guards them through kFree; one-shot rounds do not touch them)
 // Kept on the device and advanced by the kernel itself, so a launch carries
 // no host-side epoch and can be captured into a CUDA graph and replayed.
 // Every rank runs the same sequence of collectives with the same grid, so
 // CTA b's state is identical on every rank; a CTA that sits out a call lags
 // the same way everywhere.
-constexpr size_t kStateWords = 2 * kMaxCtas;
+constexpr size_t kStateWords = 4 * kMaxCtas;
 
 struct RankArgs {
   const char* send;
@@ -58,32 +61,35 @@ struct RankArgs {
   size_t bytes;        // NVLink slice: per-rank message bytes (AR) / send bytes (AG)
   size_t rank_stride;  // AllGather: distance between rank blocks in recv
   size_t slot;         // inbox slot capacity (bytes) per source rank
+  size_t small_slot;   // one-shot inbox capacity per source rank and parity
+  int oneshot;         // AllReduce: run the one-shot protocol (bytes fit small_slot)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
 };
 
 // This CTA's epoch state (in its own rank's flag block).
 struct CtaEpochs {
   uint32_t* state;
-  uint32_t first;    // epoch of round 0 of this call
-  uint32_t last_ar;  // epoch of the last AllReduce round before this call
+  uint32_t first;      // epoch of round 0 of this call
+  uint32_t last_ar;    // epoch of the last two-shot AllReduce round before this call
+  uint32_t last_main;  // epoch of the last main-slot round before this call
 };
 
 __device__ __forceinline__ CtaEpochs cta_epochs(const RankArgs& a, int cta) {
-  __shared__ uint32_t s_first, s_last_ar;
-  uint32_t* st = a.flags[a.rank] + kFlagWords + 2 * (size_t)cta;
-  if (threadIdx.x == 0) {
-    s_first = st[0] + 1;
-    s_last_ar = st[1];
-  }
+  __shared__ uint32_t s_st[3];
+  uint32_t* st = a.flags[a.rank] + kFlagWords + 4 * (size_t)cta;
+  if (threadIdx.x < 3) s_st[threadIdx.x] = st[threadIdx.x];
   __syncthreads();
-  return CtaEpochs{st, s_first, s_last_ar};
+  return CtaEpochs{st, s_st[0] + 1, s_st[1], s_st[2]};
 }
 
-// After the call's `rounds` rounds (not reached when a wait aborted).
-__device__ __forceinline__ void cta_epochs_done(const CtaEpochs& ep, uint32_t rounds, bool ar) {
+// After the call's rounds (not reached when a wait aborted): `last_ar` /
+// `last_main` are the values to carry forward.
+__device__ __forceinline__ void cta_epochs_done(const CtaEpochs& ep, uint32_t rounds,
+                                                uint32_t last_ar, uint32_t last_main) {
   if (threadIdx.x == 0 && rounds > 0) {
     ep.state[0] = ep.first - 1 + rounds;
-    if (ar) ep.state[1] = ep.first + rounds - 1;
+    ep.state[1] = last_ar;
+    ep.state[2] = last_main;
   }
 }
 
@@ -246,13 +252,14 @@ __device__ __forceinline__ void cta_part(size_t len, int nctas, int cta, size_t*
 }
 
 // CTA cta owns the same region [cta*sub, cta*sub + sub) of every inbox slot
-// and of the outbox in every round of every protocol: it never depends on the
-// message length, so the per-CTA flags guard exactly the bytes that CTA pair
-// writes and reads (with length-dependent offsets, CTA b could overwrite bytes
-// a slower peer CTA b' is still reading from an earlier round).  The round
-// capacity is sub * nctas per slot, which keeps every CTA part <= sub.
-__device__ __forceinline__ size_t cta_sub(size_t slot, int nctas) {
-  return (slot / (size_t)nctas) & ~(size_t)15;
+// and of the outbox, sub = slot / kMaxCtas, in every round of every protocol:
+// it depends neither on the message length nor on the grid size, so the
+// per-CTA flags guard exactly the bytes that CTA pair writes and reads (with
+// length- or grid-dependent offsets, CTA b could overwrite bytes a slower
+// peer CTA b' is still reading from an earlier round).  The round capacity is
+// sub * nctas per slot, which keeps every CTA part <= sub.
+__device__ __forceinline__ size_t cta_sub(size_t slot) {
+  return (slot / (size_t)kMaxCtas) & ~(size_t)15;
 }
 
 // Every protocol: wait until peer c freed the inbox slot I push into
@@ -262,13 +269,13 @@ __device__ __forceinline__ size_t cta_sub(size_t slot, int nctas) {
 template <typename T, int OP>
 __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
   const size_t round_cap = sub * nctas * n;
   const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
   FLX_PHASE(0);
   const CtaEpochs ep = cta_epochs(a, cta);
-  uint32_t prev_outbox = ep.last_ar;
+  uint32_t prev_outbox = ep.last_ar, prev_main = ep.last_main;
   uint32_t k = 0;
   for (size_t base = 0; base < a.bytes; base += round_cap, ++k) {
     const uint32_t e = ep.first + k;
@@ -286,7 +293,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it,
     //    into this CTA's region of the slot)
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
       FLX_PHASE(1);
       uint32_t* targets[kMaxRanks];
       int nt = 0;
@@ -335,9 +342,54 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
       cta_signal(targets, nt, e);
       FLX_PHASE(6);
     }
-    prev_outbox = e;
+    prev_outbox = prev_main = e;
   }
-  cta_epochs_done(ep, k, true);
+  cta_epochs_done(ep, k, prev_outbox, prev_main);
+}
+
+// One-shot AllReduce for small messages: push my part of the whole message
+// into every peer's small inbox (parity e & 1, slot r), signal kArrive(e),
+// wait for every peer's kArrive(e), fold the n copies in rank order into recv.
+// One release and one wait per call instead of three of each (the two-shot
+// protocol's latency is its three flag hops, tools/rank_phases.cu).  Reuse
+// of the parity region needs no flag: its last readers ran round e-2, and in
+// round e-1 this CTA awaited every peer's kArrive(e-1), which that peer
+// signalled after finishing round e-2 (every protocol awaits kArrive from
+// every peer every round).  The main slots are untouched, so last_main stays.
+template <typename T, int OP>
+__device__ void rank_allreduce_oneshot(const RankArgs& a, int cta, int nctas) {
+  FLX_PHASE(0);
+  const int r = a.rank, n = a.nranks;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  const uint32_t e = ep.first;
+  const size_t mine = (size_t)cta * cta_sub(a.small_slot);
+  const size_t region = a.slot * (n + 1) + (size_t)(e & 1) * n * a.small_slot;
+  size_t lo, hi;
+  cta_part(a.bytes, nctas, cta, &lo, &hi);
+  FLX_PHASE(1);
+  {
+    uint32_t* targets[kMaxRanks];
+    int nt = 0;
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      cta_copy(a.scratch[c] + region + (size_t)r * a.small_slot + mine, a.send + lo, hi - lo,
+               false);
+      targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    }
+    cta_signal(targets, nt, e);
+  }
+  FLX_PHASE(2);
+  if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+  FLX_PHASE(3);
+  {
+    const char* src[kMaxRanks];
+    for (int p = 0; p < n; ++p)
+      src[p] = (p == r) ? a.send + lo : a.scratch[r] + region + (size_t)p * a.small_slot + mine;
+    char* dst[1] = {a.recv + lo};
+    cta_fold<T, OP>(dst, 1, src, n, hi - lo);
+  }
+  FLX_PHASE(4);
+  cta_epochs_done(ep, 1, ep.last_ar, ep.last_main);
 }
 
 // After consuming my inbox slots for epoch e: tell every source (kFree = e).
@@ -351,10 +403,11 @@ __device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e)
 
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
   const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
   for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
@@ -368,7 +421,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
       nb[c] = hi - lo;
     }
     {  // push my slice into every peer's inbox slot r (this CTA's region)
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -387,8 +440,9 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
                a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
     }
     free_all(a, cta, e);
+    prev_main = e;
   }
-  cta_epochs_done(ep, k, false);
+  cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
 
 // ReduceScatter: a.bytes = NVLink part of each recv block, a.rank_stride = the
@@ -396,10 +450,11 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
 template <typename T, int OP>
 __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
   const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
   for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
@@ -407,7 +462,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -428,8 +483,9 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
       cta_fold<T, OP>(dst, 1, src, n, hi - lo);
     }
     free_all(a, cta, e);
+    prev_main = e;
   }
-  cta_epochs_done(ep, k, false);
+  cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
 
 // AllToAll: a.bytes = NVLink part of each block, a.rank_stride = block stride
@@ -437,10 +493,11 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
 // land every peer's push into recv block p.
 __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
-  const size_t sub = cta_sub(a.slot, nctas);
+  const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
   const size_t cap = sub * nctas;
   const CtaEpochs ep = cta_epochs(a, cta);
+  uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
   for (size_t base = 0; base < a.bytes; base += cap, ++k) {
     const uint32_t e = ep.first + k;
@@ -448,7 +505,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, e - 1, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -468,8 +525,9 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
                a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
     }
     free_all(a, cta, e);
+    prev_main = e;
   }
-  cta_epochs_done(ep, k, false);
+  cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
 
 __global__ void __launch_bounds__(512) rank_alltoall_kernel(const RankArgs a) {
@@ -482,7 +540,8 @@ __global__ void __launch_bounds__(512) loopback_alltoall_kernel(const __grid_con
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
-  rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
+  if (a.oneshot) rank_allreduce_oneshot<T, OP>(a, blockIdx.x, gridDim.x);
+  else rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
@@ -497,7 +556,8 @@ __global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
 // Loopback: blockIdx.y is the rank; cooperative launch (all CTAs co-resident).
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
-  rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  if (a.r[blockIdx.y].oneshot) rank_allreduce_oneshot<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  else rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>

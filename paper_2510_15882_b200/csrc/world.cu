@@ -88,6 +88,8 @@ struct World {
   bool loopback = false;
   int nctas = 0;
   size_t slot = 0;       // inbox slot bytes per source rank
+  size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
+  size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   size_t hcap = 0;       // PCIe staging bytes per rank region
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
   uint32_t last_ar_pepoch = 0;  // last AllReduce PCIe epoch (guards R_r reuse)
@@ -131,7 +133,8 @@ namespace {
 
 flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaSetDevice(L.device));
-  const size_t scratch_bytes = w->slot * (w->nranks + 1);
+  // [n inbox slots][outbox][one-shot inboxes: 2 parities x n sources]
+  const size_t scratch_bytes = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), (kFlagWords + kStateWords) * 4));
   FLX_CUDA(cudaMemset(L.flags, 0, (kFlagWords + kStateWords) * 4));
@@ -228,10 +231,16 @@ flxResult_t alloc_host_staging(World* w, const char* shm_name) {
 
 void world_config(World* w, int nranks) {
   w->nranks = nranks;
-  w->slot = std::max<size_t>(env_mib("FLX_SLOT_MB", 32), 1 << 20);
+  // 64 MiB: kMaxCtas regions of 1 MiB, so 32 CTAs move 256 MiB per AllReduce round
+  w->slot = std::max<size_t>(env_mib("FLX_SLOT_MB", 64), 1 << 20);
   w->hcap = env_mib("FLX_PCIE_STAGE_MB", 64);
   w->nctas = 32;
   if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));
+  // one-shot AllReduce up to this many bytes per rank (FLX_ONESHOT_KB=0: off);
+  // its inbox holds kMaxCtas regions, so 2x the threshold covers nctas >= 32
+  const char* os = getenv("FLX_ONESHOT_KB");
+  w->oneshot_max = (size_t)(os ? atoll(os) : 256) << 10;
+  w->small_slot = std::max<size_t>(2 * w->oneshot_max, 16 * kMaxCtas);
 }
 
 template <typename F>
@@ -373,15 +382,17 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   for (int i = 0; i < nl; ++i) {
     World::Local& L = w->local[i];
     tm[i] = &L.timing[L.calls % Clique::kTimingSlots];
-    FLX_CUDA(cudaEventRecord(tm[i]->start, s0));
   }
+  // every local rank shares s0: one start/nv event pair (local rank 0's) times
+  // the NVLink slice for all of them; the PCIe legs keep per-rank events
+  FLX_CUDA(cudaEventRecord(tm[0]->start, s0));
 
   // ---------------- PCIe slice (issued first so the copies overlap the kernel)
   if (pc > 0) {
     const uint32_t e = w->pepoch++;
     for (auto& L : w->local) {
-      FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[&L - &w->local[0]]->start, 0));
-      FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[&L - &w->local[0]]->start, 0));
+      FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[0]->start, 0));
+      FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[0]->start, 0));
     }
     if (a2a) {
       // step 1 as ReduceScatter; step 2: rank r lands H_p[r] straight into its
@@ -558,6 +569,11 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.bytes = nv;
       a.rank_stride = bytes;
       a.slot = w->slot;
+      a.small_slot = w->small_slot;
+      // one-shot when the slice fits both the threshold and this grid's
+      // share of the one-shot inbox (every CTA part <= its region)
+      a.oneshot = !gather && !scatter && !a2a && n > 1 && nv <= w->oneshot_max &&
+                  nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas;
       a.abort_word = w->abort_word;
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
@@ -569,7 +585,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     if (err != cudaSuccess)
       return fail(flxUnhandledCudaError, "rank kernel launch: %s", cudaGetErrorString(err));
   }
-  for (int i = 0; i < nl; ++i) FLX_CUDA(cudaEventRecord(tm[i]->nv, s0));
+  FLX_CUDA(cudaEventRecord(tm[0]->nv, s0));
   if (pc > 0)
     for (int i = 0; i < nl; ++i) FLX_CUDA(cudaStreamWaitEvent(s0, tm[i]->pcie, 0));
   bool joined = false;
@@ -596,14 +612,16 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
 flxResult_t world_read_timing(World* w, int local, uint64_t seq, float ms[3]) {
   World::Local& L = w->local[local];
   const Clique::Timing& t = L.timing[seq % Clique::kTimingSlots];
+  // start/nv events are local rank 0's (shared by every local rank of a call)
+  const Clique::Timing& t0 = w->local[0].timing[seq % Clique::kTimingSlots];
   FLX_CUDA(cudaSetDevice(L.device));
   ms[0] = ms[1] = ms[2] = 0.f;
-  FLX_CUDA(cudaEventSynchronize(t.nv));
+  FLX_CUDA(cudaEventSynchronize(t0.nv));
   if (*w->abort_word) return fail(flxInternalError, "a peer wait timed out (rank died or hung?)");
-  if (t.used[flxPathNvlink]) FLX_CUDA(cudaEventElapsedTime(&ms[0], t.start, t.nv));
+  if (t.used[flxPathNvlink]) FLX_CUDA(cudaEventElapsedTime(&ms[0], t0.start, t0.nv));
   if (t.used[flxPathPcie]) {
     FLX_CUDA(cudaEventSynchronize(t.pcie));
-    FLX_CUDA(cudaEventElapsedTime(&ms[1], t.start, t.pcie));
+    FLX_CUDA(cudaEventElapsedTime(&ms[1], t0.start, t.pcie));
   }
   return flxSuccess;
 }

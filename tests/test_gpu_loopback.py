@@ -238,3 +238,43 @@ def test_loopback_varying_sizes_multi_round():
                 np.testing.assert_array_equal(_np(ar[r], 7), want_ar[r])
                 np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
                 np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])
+
+
+@pytest.mark.parametrize("oneshot_kb", ["256", "0"])
+def test_loopback_oneshot_and_twoshot_interleaved(oneshot_kb):
+    # AllReduce slices up to FLX_ONESHOT_KB run the one-shot protocol (its own
+    # double-buffered inbox), larger ones the two-shot; interleaved with
+    # AllGather on the main slots, in place and out of place, all exact.
+    n = 8
+    os.environ["FLX_ONESHOT_KB"] = oneshot_kb
+    try:
+        w = flx.Clique(n, loopback=True)
+    finally:
+        del os.environ["FLX_ONESHOT_KB"]
+    g = torch.Generator(device="cpu").manual_seed(3)
+    with w:
+        for op in CollectiveOp:
+            w.set_shares(op, (1000, 0, 0))
+        for it, (count, dtype, op) in enumerate([
+                (1024, 7, "sum"), (1 << 20, 7, "sum"), (5, 9, "sum"), (4096, 6, "max"),
+                (65536, 7, "sum"), (65536, 7, "sum"), (3 << 18, 9, "sum"), (100, 2, "min"),
+                (16384, 8, "prod"), (1, 7, "sum")]):
+            cpu = _inputs(n, count, dtype, 100 + it)
+            sends = [c.cuda() for c in cpu]
+            inplace = it % 3 == 1
+            recvs = sends if inplace else [torch.empty_like(s) for s in sends]
+            w.all_reduce(sends, recvs, op=op)
+            ag = [torch.empty(n * 64, dtype=TORCH_DT[dtype], device="cuda") for _ in range(n)]
+            ag_in = [c[:64].cuda() for c in cpu] if count >= 64 else None
+            if ag_in is not None:
+                w.all_gather(ag_in, ag)
+            torch.cuda.synchronize()
+            want = oracle.allreduce([_np(c, dtype) for c in cpu], dtype, OPS[op], (1000, 0, 0),
+                                    n * 4096)
+            for r in range(n):
+                np.testing.assert_array_equal(_np(recvs[r], dtype), want[r], err_msg=f"it {it}")
+            if ag_in is not None:
+                want_ag = oracle.allgather([_np(c, dtype)[:64] for c in cpu], dtype, (1000, 0, 0),
+                                           4096)
+                for r in range(n):
+                    np.testing.assert_array_equal(_np(ag[r], dtype), want_ag[r])

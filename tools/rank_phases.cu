@@ -2,7 +2,7 @@
 // one GPU, cooperative launch), from %globaltimer stamps at the protocol's
 // phase boundaries (FLX_PHASE hooks in rank_kernels.cuh).  Build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o tools/bin/rank_phases tools/rank_phases.cu
-//   tools/bin/rank_phases [bytes_per_rank] [nranks] [nctas]
+//   tools/bin/rank_phases [bytes_per_rank] [nranks] [nctas] [oneshot 0/1]
 #include <cuda_runtime.h>
 #include <cstdio>
 #include <cstdlib>
@@ -27,13 +27,14 @@ int main(int argc, char** argv) {
   const size_t bytes = argc > 1 ? strtoull(argv[1], nullptr, 0) : 4096;
   const int n = argc > 2 ? atoi(argv[2]) : 8;
   const int nctas = argc > 3 ? atoi(argv[3]) : 1;
-  const size_t slot = 32u << 20;
+  const int oneshot = argc > 4 ? atoi(argv[4]) : 0;
+  const size_t slot = 64u << 20, small = 4u << 20;  // small: one-shot parts up to 64 KiB per CTA
   LoopbackArgs la;
   memset(&la, 0, sizeof(la));
   char* scratch[kMaxRanks];
   uint32_t* flags[kMaxRanks];
   for (int r = 0; r < n; ++r) {
-    CK(cudaMalloc(&scratch[r], slot * (n + 1)));
+    CK(cudaMalloc(&scratch[r], slot * (n + 1) + 2 * n * small));
     CK(cudaMalloc(&flags[r], (kFlagWords + kStateWords) * 4));
     CK(cudaMemset(flags[r], 0, (kFlagWords + kStateWords) * 4));
   }
@@ -59,6 +60,8 @@ int main(int argc, char** argv) {
     a.bytes = bytes;
     a.rank_stride = bytes;
     a.slot = slot;
+    a.small_slot = small;
+    a.oneshot = oneshot;
     a.abort_word = abort_dev;
   }
   void* params[] = {&la};
@@ -89,12 +92,15 @@ int main(int argc, char** argv) {
         avg[i] += v / (n * nctas);
         mx[i] = v > mx[i] ? v : mx[i];
       }
-  printf("{\"bytes\": %zu, \"nranks\": %d, \"nctas\": %d, \"us_per_launch\": %.2f, "
+  if (oneshot) avg[5] = avg[6] = mx[5] = mx[6] = 0;
+  printf("{\"oneshot\": %d, \"bytes\": %zu, \"nranks\": %d, \"nctas\": %d, \"us_per_launch\": %.2f, "
          "\"phase_avg_us\": [%.2f, %.2f, %.2f, %.2f, %.2f, %.2f, %.2f], "
          "\"phase_max_us\": [%.2f, %.2f, %.2f, %.2f, %.2f, %.2f, %.2f], "
-         "\"phases\": \"entry, kFree waited, pushed+signalled, arrive waited, folded+signalled, "
-         "ready waited, pulled+signalled\"}\n",
-         bytes, n, nctas, ms * 1e3 / iters, avg[0], avg[1], avg[2], avg[3], avg[4], avg[5], avg[6],
-         mx[0], mx[1], mx[2], mx[3], mx[4], mx[5], mx[6]);
+         "\"phases\": \"%s\"}\n",
+         oneshot, bytes, n, nctas, ms * 1e3 / iters, avg[0], avg[1], avg[2], avg[3], avg[4], avg[5], avg[6],
+         mx[0], mx[1], mx[2], mx[3], mx[4], mx[5], mx[6],
+         oneshot ? "entry, setup, pushed+signalled, arrive waited, folded"
+                 : "entry, kFree waited, pushed+signalled, arrive waited, folded+signalled, "
+                   "ready waited, pulled+signalled");
   return 0;
 }

@@ -64,6 +64,7 @@ struct RankArgs {
   size_t small_slot;   // one-shot inbox capacity per source rank and parity
   int oneshot;         // AllReduce: run the one-shot protocol (bytes fit small_slot)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
+  long long spin_limit;  // clock64 cycles a wait may spin before aborting (FLX_TIMEOUT_S)
 };
 
 // This CTA's epoch state (in its own rank's flag block).
@@ -131,14 +132,15 @@ __device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, 
 }
 
 // Flags are compared cyclically ((int)(flag - epoch) >= 0) so epochs may wrap;
-// a ~10 s spin limit sets the host-mapped abort word instead of hanging the GPU
+// a spin limit (FLX_TIMEOUT_S, default 10 s) sets the host-mapped abort word
+// instead of hanging the GPU
 // when a peer died.
 // Warp 0 waits, one flag per lane, until every peer p != skip has published:
 // lanes 0..15 watch flag(kind1, p) >= e1, lanes 16..31 flag(kind2, p) >= e2
 // (kind2 < 0: unused).  One parallel poll instead of N-1 sequential ones.
 __device__ __forceinline__ bool cta_wait_peers(uint32_t* block, int n, int skip, int cta,
                                                int kind1, uint32_t e1, int kind2, uint32_t e2,
-                                               uint32_t* abort_word) {
+                                               const RankArgs& a) {
   __shared__ int ok;
   if (threadIdx.x < 32) {
     const int lane = threadIdx.x;
@@ -155,9 +157,9 @@ __device__ __forceinline__ bool cta_wait_peers(uint32_t* block, int n, int skip,
       if (__all_sync(0xffffffffu, ready)) break;
       if ((++spins & 4095) == 0) {  // the abort word is host memory: poll it rarely
         int bad = 0;
-        if (lane == 0) bad = *(volatile uint32_t*)abort_word || clock64() - t0 > 20000000000ll;
+        if (lane == 0) bad = *(volatile uint32_t*)a.abort_word || clock64() - t0 > a.spin_limit;
         if (__shfl_sync(0xffffffffu, bad, 0)) {
-          if (lane == 0) atomicExch(abort_word, 1u);
+          if (lane == 0) atomicExch(a.abort_word, 1u);
           good = 0;
           break;
         }
@@ -293,7 +295,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it,
     //    into this CTA's region of the slot)
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       FLX_PHASE(1);
       uint32_t* targets[kMaxRanks];
       int nt = 0;
@@ -306,7 +308,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
       FLX_PHASE(2);
     }
     // 2) every push landed, and every peer pulled my previous outbox
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a.abort_word))
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a))
       return;
     FLX_PHASE(3);
     {
@@ -329,7 +331,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
       FLX_PHASE(4);
     }
     // 3) pull every peer's reduced chunk
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a.abort_word)) return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a)) return;
     FLX_PHASE(5);
     {
       uint32_t* targets[kMaxRanks];
@@ -379,7 +381,7 @@ __device__ void rank_allreduce_oneshot(const RankArgs& a, int cta, int nctas) {
     cta_signal(targets, nt, e);
   }
   FLX_PHASE(2);
-  if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+  if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
   FLX_PHASE(3);
   {
     const char* src[kMaxRanks];
@@ -421,7 +423,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
       nb[c] = hi - lo;
     }
     {  // push my slice into every peer's inbox slot r (this CTA's region)
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -433,7 +435,7 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
       if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
       cta_signal(targets, nt, e);
     }
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
@@ -462,7 +464,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -473,7 +475,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
       }
       cta_signal(targets, nt, e);
     }
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     {
       const char* src[kMaxRanks];
       for (int p = 0; p < n; ++p)
@@ -505,7 +507,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
     {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a.abort_word)) return;
+      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       uint32_t* targets[kMaxRanks];
       int nt = 0;
       for (int s = 1; s < n; ++s) {
@@ -518,7 +520,7 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
       cta_copy(a.recv + own, a.send + own, hi - lo, false);
       cta_signal(targets, nt, e);
     }
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a.abort_word)) return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
       cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,

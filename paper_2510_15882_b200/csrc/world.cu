@@ -89,6 +89,7 @@ struct World {
   int nctas = 0;
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
+  long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   size_t hcap = 0;       // PCIe staging bytes per rank region
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
@@ -133,6 +134,11 @@ namespace {
 
 flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaSetDevice(L.device));
+  int khz = 0;
+  FLX_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, L.device));
+  const char* to = getenv("FLX_TIMEOUT_S");
+  const double secs = to ? atof(to) : 10.0;
+  w->spin_limit = (long long)(std::max(0.01, secs) * khz * 1e3);
   // [n inbox slots][outbox][one-shot inboxes: 2 parities x n sources]
   const size_t scratch_bytes = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
@@ -575,6 +581,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.oneshot = !gather && !scatter && !a2a && n > 1 && nv <= w->oneshot_max &&
                   nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas;
       a.abort_word = w->abort_word;
+      a.spin_limit = w->spin_limit;
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
     cudaError_t err =

@@ -11,6 +11,7 @@ processes would wait on each other); data crosses only through plain copies
 import ctypes
 import os
 import socket
+import time
 
 import pytest
 
@@ -71,3 +72,46 @@ def test_two_process_bootstrap_ipc_and_shared_staging():
             for peer in range(world):
                 want = bytes((peer * 37 + i) % 251 for i in range(4096))
                 assert res[rank]["got"][(region, peer)] == want, (rank, region, peer)
+
+
+def _abort_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FLX_ALLOW_SHARED_GPU="1",
+                      FLX_SLOT_MB="1", FLX_PCIE_STAGE_MB="1", FLX_BOOT_TIMEOUT="60",
+                      FLX_TIMEOUT_S="1")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_15882_b200 import comm
+
+        c = comm.Communicator.from_process_group()
+        if rank == 0:
+            # rank 1 never joins: rank 0's kernel (the only one spinning on this
+            # GPU) gives up after FLX_TIMEOUT_S and the communicator is aborted
+            t = torch.ones(1024, device="cuda")
+            t0 = time.perf_counter()
+            c.all_reduce(t)
+            torch.cuda.synchronize()
+            waited = time.perf_counter() - t0
+            try:
+                c.all_reduce(t)
+                out[0] = ("no error", waited)
+            except comm.FlexLinkError as e:
+                out[0] = (e.code, waited)
+        dist.barrier()
+        c.destroy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_timeout_aborts_instead_of_hanging():
+    # SURVEY 8(b) error conventions: a peer that never arrives ends in
+    # flxInternalError (== ncclInternalError, 3) after FLX_TIMEOUT_S, not a hang.
+    from paper_2510_15882_b200.build import build
+
+    build()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_abort_worker, args=(2, _port(), out), nprocs=2, join=True)
+        code, waited = out[0]
+    assert code == 3, code
+    assert 0.5 < waited < 30, waited

@@ -58,6 +58,20 @@ __global__ void __launch_bounds__(512) fan_dst(const Args a) {
   }
 }
 
+// destination groups: G adjacent CTAs read the same source span (the repeats
+// hit L2) and each writes N/G of the destinations: fewer stores per thread.
+template <int G>
+__global__ void __launch_bounds__(512) fan_split(const Args a) {
+  const int r = blockIdx.y;
+  const int g = blockIdx.x % G;
+  const size_t v = (size_t)(blockIdx.x / G) * blockDim.x + threadIdx.x;
+  if (v >= a.nvec) return;
+  const uint4 w = ldnc(a.src[r] + v);
+  const size_t shift = (size_t)r * a.stride_vec;
+#pragma unroll
+  for (int d = g * (N / G); d < (g + 1) * (N / G); ++d) stv<0>(a.dst[d] + shift + v, w);
+}
+
 __global__ void __launch_bounds__(512) write_only(const Args a) {
   const size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (v < a.nvec * N) stv<0>(a.dst[blockIdx.y] + v, make_uint4(v, v, v, v));
@@ -104,6 +118,10 @@ int main(int argc, char**) {
   rep("2 vec/thread many CTAs", timeit([&] { fan<2, 0><<<dim3((unsigned)((nvec + 1023) / 1024), N), 512>>>(a); }, 20));
   rep("dst-major sm/8 per dst", timeit([&] { fan_dst<<<dim3(sms / N * 2, N), 512>>>(a); }, 20));
   rep("dst-major many", timeit([&] { fan_dst<<<dim3((unsigned)((nvec * N + 511) / 512 / 4), N), 512>>>(a); }, 20));
+  const unsigned nb = (unsigned)((nvec + 511) / 512);
+  rep("split dst x2 (L2 re-read)", timeit([&] { fan_split<2><<<dim3(nb * 2, N), 512>>>(a); }, 20));
+  rep("split dst x4 (L2 re-read)", timeit([&] { fan_split<4><<<dim3(nb * 4, N), 512>>>(a); }, 20));
+  rep("split dst x8 (L2 re-read)", timeit([&] { fan_split<8><<<dim3(nb * 8, N), 512>>>(a); }, 20));
   // ceilings: the fan-out is 8/9 writes, so the HBM write-only rate bounds it
   const double wbytes = (double)N * N * in_bytes;
   auto rep_w = [&](const char* name, float ms) { printf("{\"variant\": \"%s\", \"ms\": %.4f, \"GBps\": %.1f}\n", name, ms, wbytes / (ms * 1e-3) / 1e9); };

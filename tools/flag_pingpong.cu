@@ -89,6 +89,81 @@ float run_fan(uint32_t* flags, uint32_t* back, int iters) {
   return ms * 1e3f / iters;
 }
 
+// cost of a satisfied 7-flag wait (flags already >= target), per call:
+// W 0: 7 lanes ld.acquire.sys; 1: 7 lanes ld.relaxed.sys, then each of those
+// lanes fence.acq_rel.sys; 2: lane 0 loads 7 flags relaxed, one fence;
+// 3: 7 lanes relaxed, __syncwarp, lane 0 fence (not a formal acquire)
+template <int W>
+__global__ void satisfied_wait(const uint32_t* flags, int iters, uint32_t* out) {
+  const int lane = threadIdx.x;
+  uint32_t acc = 0;
+  for (int i = 0; i < iters; ++i) {
+    if (W == 0) {
+      if (lane < 7) acc += get<0>(flags + lane * 64);
+    } else if (W == 1) {
+      if (lane < 7) {
+        acc += get<3>(flags + lane * 64);
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      }
+    } else if (W == 2) {
+      if (lane == 0) {
+        uint32_t v[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) v[k] = get<3>(flags + k * 64);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) acc += v[k];
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+      }
+    } else {
+      if (lane < 7) acc += get<3>(flags + lane * 64);
+      __syncwarp();
+      if (lane == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+    }
+    __syncwarp();
+  }
+  if (acc == 0xdeadbeef) *out = acc;
+}
+
+template <int W>
+float run_wait(const uint32_t* flags, uint32_t* out, int iters) {
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  satisfied_wait<W><<<1, 32>>>(flags, iters, out);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  return ms * 1e3f / iters;
+}
+
+// cost of a 7-flag release signal right after the CTA wrote `kb` KiB of data
+// (W 0: 7 lanes st.release.sys; 1: bar, lane 0 fence.sys, syncwarp, 7 lanes relaxed)
+template <int W>
+__global__ void __launch_bounds__(512) signal_after_writes(uint32_t* flags, uint4* data, int kb, int iters) {
+  for (int i = 1; i <= iters; ++i) {
+    for (int v = threadIdx.x; v < kb * 64; v += blockDim.x) data[v] = make_uint4(i, i, i, i);
+    __syncthreads();
+    if (W == 0) {
+      if (threadIdx.x < 7) put<0>(flags + threadIdx.x * 64, i);
+    } else {
+      if (threadIdx.x == 0) asm volatile("fence.acq_rel.sys;" ::: "memory");
+      __syncwarp();
+      if (threadIdx.x < 7) put<3>(flags + threadIdx.x * 64, i);
+    }
+    __syncthreads();
+  }
+}
+
+template <int W>
+float run_sig(uint32_t* flags, uint4* data, int kb, int iters) {
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
+  signal_after_writes<W><<<1, 512>>>(flags, data, kb, iters);
+  cudaEventRecord(e1); cudaEventSynchronize(e1);
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  return ms * 1e3f / iters;
+}
+
+#define CK_SET(p) cudaMemset(p, 1, 64 * 1024)
+
 int main() {
   uint32_t* d; cudaMalloc(&d, 4096);
   uint32_t *a = d, *b = d + 256;  // different 1 KiB lines
@@ -105,6 +180,18 @@ int main() {
                        run_fan<2>(fl, fl + 8192, iters)};
   for (int m = 0; m < 3; ++m)
     printf("{\"flags\": \"device\", \"signal14\": \"%s\", \"round_trip_us\": %.3f}\n", ways[m], fu[m]);
+  CK_SET(fl);
+  const char* wn[4] = {"7 lanes ld.acquire.sys", "7 lanes relaxed + per-lane fence.sys",
+                       "lane 0: 7 relaxed loads + 1 fence.sys", "7 lanes relaxed, lane 0 fence.sys"};
+  const float wu[4] = {run_wait<0>(fl, fl + 8000, 2000), run_wait<1>(fl, fl + 8000, 2000),
+                       run_wait<2>(fl, fl + 8000, 2000), run_wait<3>(fl, fl + 8000, 2000)};
+  for (int m = 0; m < 4; ++m)
+    printf("{\"satisfied_wait7\": \"%s\", \"us\": %.3f}\n", wn[m], wu[m]);
+  uint4* data; cudaMalloc(&data, 1 << 20);
+  for (int kb : {0, 4, 64}) {
+    printf("{\"signal7_after_kib\": %d, \"7 lanes st.release.sys_us\": %.3f, \"one fence + relaxed_us\": %.3f}\n",
+           kb, run_sig<0>(fl, data, kb, 2000), run_sig<1>(fl, data, kb, 2000));
+  }
   // a release.sys store while this CTA has outstanding writes to host-mapped memory
   uint32_t* h; cudaHostAlloc(&h, 4096, cudaHostAllocMapped);
   uint32_t* hd; cudaHostGetDevicePointer(&hd, h, 0);

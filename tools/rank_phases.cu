@@ -63,6 +63,7 @@ int main(int argc, char** argv) {
     a.small_slot = small;
     a.oneshot = oneshot;
     a.abort_word = abort_dev;
+    a.spin_limit = 20000000000ll;
   }
   void* params[] = {&la};
   const void* fn = (const void*)loopback_allreduce_kernel<float, kSum>;

@@ -19,10 +19,12 @@ p.add_argument("--ranks", default="2,4,8")
 p.add_argument("--max-mib", type=int, default=1024)
 p.add_argument("--steps", type=int, default=20)
 p.add_argument("--nvlink-ctas", type=int, default=0)
+p.add_argument("--loopback", action="store_true",
+               help="the multi-GPU engine emulated on one GPU, NVLink path only (no tuning)")
 a = p.parse_args()
 topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
 for n in [int(x) for x in a.ranks.split(",")]:
-    cl = flx.Clique(n)
+    cl = flx.Clique(n, loopback=a.loopback)
     if a.nvlink_ctas:
         cl.set_nvlink_ctas(a.nvlink_ctas)
     for dt, esz, name in ((torch.float32, 4, "fp32"), (torch.bfloat16, 2, "bf16")):
@@ -31,8 +33,13 @@ for n in [int(x) for x in a.ranks.split(",")]:
             S = mib << 20
             s = [torch.randn(S // esz, device="cuda").to(dt) for _ in range(n)]
             r = [torch.empty_like(x) for x in s]
-            shares, trace, tuned, base = flx.tune_shares(cl, topo, CollectiveOp.ALLREDUCE, s, r,
-                                                         TunerConfig(), warmup=1, repeats=3)
+            if a.loopback:
+                shares, trace = flx.ShareDistribution({PathKind.NVLINK: 1000}), None
+                cl.set_shares(CollectiveOp.ALLREDUCE, shares)
+            else:
+                shares, trace, tuned, base = flx.tune_shares(cl, topo, CollectiveOp.ALLREDUCE,
+                                                             s, r, TunerConfig(), warmup=1,
+                                                             repeats=3)
             for _ in range(3):
                 cl.all_reduce(s, r)
             torch.cuda.synchronize()
@@ -45,13 +52,15 @@ for n in [int(x) for x in a.ranks.split(",")]:
             t = e0.elapsed_time(e1) / a.steps * 1e-3
             b = cl.path_bytes()
             print(json.dumps({
+                "executor": "loopback" if a.loopback else "virtual",
                 "n": n, "dtype": name, "size_mib": mib, "ms": round(t * 1e3, 4),
                 "busbw": round(S / t * 2 * (n - 1) / n / 1e9, 2),
                 "shares": {k.short: shares.get(k) for k in PathKind},
                 "traffic_pct": {k.short: round(100 * b[k] / S, 3) for k in PathKind},
-                "stage1": {"iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
-                           "nvlink_only_ms": round(base * 1e3, 4),
-                           "trace": [x.action for x in trace.records]}}), flush=True)
+                "stage1": None if trace is None else {
+                    "iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
+                    "nvlink_only_ms": round(base * 1e3, 4),
+                    "trace": [x.action for x in trace.records]}}), flush=True)
             del s, r
             mib *= 2
     cl.destroy()

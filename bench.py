@@ -134,6 +134,17 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def workload_config(n_gpus: int) -> dict:
+    """The ``config`` both arms report (the reference arm samples it on the host)."""
+    if n_gpus > 1:
+        return {"workload": f"AllReduce sum fp32 256 MiB/rank over {n_gpus} GPUs",
+                "bytes_per_rank": AR_BYTES}
+    return {"workload": "AllReduce sum fp32 256 MiB/rank over 8 simulated ranks (BASELINE "
+                        "config 1) as 8 virtual ranks on one B200; NVLink path = fused "
+                        "on-device fold, PCIe path = real host-staged copy-engine pipeline",
+            "sim_ranks": SIM_RANKS, "bytes_per_rank": AR_BYTES}
+
+
 # ------------------------------------------------------------ CPU baseline
 def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = 32 * MIB,
                          n: int = SIM_RANKS):
@@ -180,8 +191,9 @@ def run_reference(args) -> None:
     threads = oracle.cpu_threads()
     per_rank = 32 * MIB
     count = per_rank // 4
+    ranks = args.gpus if args.gpus > 1 else SIM_RANKS
     rng = np.random.default_rng(1000)
-    sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(SIM_RANKS)]
+    sends = [rng.integers(-1024, 1024, count).astype(np.float32) for _ in range(ranks)]
     recvs = [np.zeros_like(s) for s in sends]  # pre-touched: no page faults in the timing
     for _ in range(max(args.warmup, 3)):  # OpenMP pool spin-up + caches
         oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
@@ -191,18 +203,18 @@ def run_reference(args) -> None:
         oracle.allreduce(sends, 7, oracle.SUM, recvs=recvs, threads=threads)
         times.append(time.perf_counter() - t0)
     dt = sum(times) / len(times)
-    value = busbw_allreduce(per_rank, dt, SIM_RANKS)
+    value = busbw_allreduce(per_rank, dt, ranks)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GB/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "AllReduce sum fp32 over 8 simulated ranks (BASELINE config 1), "
-                               "CPU oracle port, bounded sample",
-                   "bytes_per_rank": per_rank, "sim_ranks": SIM_RANKS},
+        "config": workload_config(args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"{per_rank // MIB} MiB/rank x {SIM_RANKS} ranks per step"},
+                         "sample": f"each step: AllReduce sum fp32 {per_rank // MIB} MiB/rank x "
+                                   f"{ranks} ranks on the host (oracle/flx_oracle.c, OpenMP; "
+                                   f"a bounded sample of the 256 MiB/rank workload)"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -416,10 +428,7 @@ def run_single_gpu(args) -> None:
         "dtype": "f32",
         "data": "synthetic (seeded integer-valued fp32, exact-sum checked)",
         "config": {
-            "workload": "AllReduce sum fp32 256 MiB/rank over 8 simulated ranks (BASELINE "
-                        "config 1) as 8 virtual ranks on one B200; NVLink path = fused "
-                        "on-device fold, PCIe path = real host-staged copy-engine pipeline",
-            "sim_ranks": n, "bytes_per_rank": AR_BYTES, "busbw": "(S/t)*2(N-1)/N, N=8",
+            **workload_config(1), "busbw": "(S/t)*2(N-1)/N, N=8",
             "l2": "inputs 2 GiB + outputs 2 GiB per step > 126 MB L2 (no flush needed)",
             "nvlink_ctas": args.nvlink_ctas or "auto",
         },
@@ -710,8 +719,7 @@ def run_multi_gpu(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": f"AllReduce sum fp32 256 MiB/rank over {world} GPUs",
-                       "bytes_per_rank": AR_BYTES},
+            "config": workload_config(world),
             "shares": {k.short: shares.get(k) for k in PathKind},
             "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
             "stage1_trace": [r.action for r in trace.records] if trace else "fixed --shares",

@@ -143,9 +143,10 @@ def _stream_handle(stream, device: int | None = None) -> ctypes.c_void_p:
     import torch
 
     if stream is None:
-        if device is not None:  # raw handle without building a Stream object
-            return ctypes.c_void_p(torch._C._cuda_getCurrentRawStream(device))
-        stream = torch.cuda.current_stream()
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if device is not None and raw is not None:  # no Stream object per call
+            return ctypes.c_void_p(raw(device))
+        stream = torch.cuda.current_stream(device)
     return ctypes.c_void_p(stream.cuda_stream)
 
 

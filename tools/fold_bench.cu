@@ -76,6 +76,38 @@ __global__ void __launch_bounds__(512) fold_split(const Args a) {
   for (int d = g * (N / G); d < (g + 1) * (N / G); ++d) st<0>(a.dst[d] + v, acc);
 }
 
+// single-pass fold with L2 eviction-priority hints (createpolicy):
+// LP/SP: 0 none, 1 evict_first, 2 evict_last, 3 evict_unchanged (loads) / no hint
+template <int LP, int SP>
+__global__ void __launch_bounds__(512) fold_policy(const Args a) {
+  const size_t v = (size_t)blockIdx.x * 512 + threadIdx.x;
+  if (v >= a.nvec) return;
+  uint64_t lpol = 0, spol = 0;
+  if (LP == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(lpol));
+  if (LP == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(lpol));
+  if (LP == 3) asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(lpol));
+  if (SP == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(spol));
+  if (SP == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(spol));
+  float4 in[N];
+#pragma unroll
+  for (int r = 0; r < N; ++r) {
+    const float4* p = a.src[r] + v;
+    if (LP == 0) in[r] = ld<0>(p);
+    else asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                      : "=f"(in[r].x), "=f"(in[r].y), "=f"(in[r].z), "=f"(in[r].w) : "l"(p), "l"(lpol));
+  }
+  float4 acc = in[0];
+#pragma unroll
+  for (int r = 1; r < N; ++r) { acc.x += in[r].x; acc.y += in[r].y; acc.z += in[r].z; acc.w += in[r].w; }
+#pragma unroll
+  for (int d = 0; d < N; ++d) {
+    float4* p = a.dst[d] + v;
+    if (SP == 0) st<0>(p, acc);
+    else asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.f32 [%0], {%1,%2,%3,%4}, %5;"
+                      :: "l"(p), "f"(acc.x), "f"(acc.y), "f"(acc.z), "f"(acc.w), "l"(spol) : "memory");
+  }
+}
+
 // ceilings: read-only (8 inputs, one flag store if impossible) and store-only
 __global__ void __launch_bounds__(512) read_only(const Args a, float* sink) {
   const size_t v = (size_t)blockIdx.x * 512 + threadIdx.x;
@@ -144,6 +176,13 @@ int main(int argc, char**) {
   report("128x8/SM unr1", timeit([&] { fold<128, 1, 0, 0><<<8 * sms, 128>>>(a); }, 20));
   report("512 x many (nvec/512 CTAs)", timeit([&] { fold<512, 1, 0, 0><<<(unsigned)((nvec + 511) / 512), 512>>>(a); }, 20));
   const unsigned nb = (unsigned)((nvec + 511) / 512);
+  report("policy: none (single pass)", timeit([&] { fold_policy<0, 0><<<nb, 512>>>(a); }, 20));
+  report("policy: loads evict_first", timeit([&] { fold_policy<1, 0><<<nb, 512>>>(a); }, 20));
+  report("policy: loads evict_unchanged", timeit([&] { fold_policy<3, 0><<<nb, 512>>>(a); }, 20));
+  report("policy: stores evict_first", timeit([&] { fold_policy<0, 1><<<nb, 512>>>(a); }, 20));
+  report("policy: stores evict_last", timeit([&] { fold_policy<0, 2><<<nb, 512>>>(a); }, 20));
+  report("policy: loads evict_first, stores evict_last", timeit([&] { fold_policy<1, 2><<<nb, 512>>>(a); }, 20));
+  report("policy: loads evict_first, stores evict_first", timeit([&] { fold_policy<1, 1><<<nb, 512>>>(a); }, 20));
   report("split dst x2 (L2 re-read)", timeit([&] { fold_split<2><<<nb * 2, 512>>>(a); }, 20));
   report("split dst x4 (L2 re-read)", timeit([&] { fold_split<4><<<nb * 4, 512>>>(a); }, 20));
   float* sink; CK(cudaMalloc(&sink, 4));

@@ -46,8 +46,16 @@ def test_single_rank_group_ops():
     y = x.clone()
     grp.all_reduce(y)
     out = torch.ops.flexlink.all_gather(x, grp.handle)
+    rs = torch.ops.flexlink.reduce_scatter(x, grp.handle, "sum")
+    a2a = torch.ops.flexlink.all_to_all(x, grp.handle)
+    rs2 = torch.empty_like(x)
+    grp.reduce_scatter_tensor(rs2, x)
+    a2a2 = torch.empty_like(x)
+    grp.all_to_all_single(a2a2, x)
     torch.cuda.synchronize()
     assert torch.equal(y, x) and torch.equal(out, x)
+    for t in (rs, a2a, rs2, a2a2):
+        assert torch.equal(t, x)
     grp.close()
     c.destroy()
 

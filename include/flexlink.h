@@ -108,6 +108,10 @@ flxResult_t flxCommDestroy(flxComm_t comm);
 flxResult_t flxCommCount(const flxComm_t comm, int* count);
 flxResult_t flxCommUserRank(const flxComm_t comm, int* rank);
 flxResult_t flxCommCuDevice(const flxComm_t comm, int* device);
+/* ncclCommGetAsyncError (nccl.h:227): flxInternalError once a multi-rank
+ * kernel of this comm gave up waiting for a peer (FLX_TIMEOUT_S), else
+ * flxSuccess.  Virtual-rank comms never time out. */
+flxResult_t flxCommGetAsyncError(flxComm_t comm, flxResult_t* async_error);
 
 /* ---- collectives --------------------------------------------------------
  * Replace linkstripe `simulate_collective(topo, spec, shares)`

@@ -89,6 +89,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
         "flxCommCuDevice": [vp, P(ci)],
+        "flxCommGetAsyncError": [vp, P(ci)],
         "flxAllReduce": [vp, vp, sz, ci, ci, vp, vp],
         "flxAllGather": [vp, vp, sz, ci, vp, vp],
         "flxReduceScatter": [vp, vp, sz, ci, ci, vp, vp],
@@ -182,6 +183,13 @@ class Communicator:
         self.rank = v.value
         _check(L.flxCommCuDevice(self._h, ctypes.byref(v)), "flxCommCuDevice")
         self.device = v.value
+
+    def async_error(self) -> int:
+        """``ncclCommGetAsyncError``: 3 (internal error) once a peer wait timed out."""
+        v = ctypes.c_int()
+        _check(load_library().flxCommGetAsyncError(self._h, ctypes.byref(v)),
+               "flxCommGetAsyncError")
+        return v.value
 
     # ---- construction
     @staticmethod

@@ -819,6 +819,13 @@ flxResult_t flxCommCuDevice(const flxComm_t comm, int* device) {
   return flxSuccess;
 }
 
+flxResult_t flxCommGetAsyncError(flxComm_t comm, flxResult_t* async_error) {
+  FLX_TRY(validate_comm(comm));
+  if (!async_error) return fail(flxInvalidArgument, "null async_error");
+  *async_error = comm->world && world_aborted(comm->world) ? flxInternalError : flxSuccess;
+  return flxSuccess;
+}
+
 flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                          flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
                          cudaStream_t stream) {

@@ -86,6 +86,13 @@ ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recv
                                         (flxRedOp_t)op, (flxComm_t)comm, stream);
 }
 
+ncclResult_t ncclCommGetAsyncError(ncclComm_t comm, ncclResult_t* asyncError) {
+  flxResult_t e = flxSuccess;
+  const flxResult_t rc = flxCommGetAsyncError((flxComm_t)comm, &e);
+  if (rc == flxSuccess && asyncError) *asyncError = (ncclResult_t)e;
+  return (ncclResult_t)rc;
+}
+
 ncclResult_t ncclGroupStart(void) { return (ncclResult_t)flxGroupStart(); }
 
 ncclResult_t ncclGroupEnd(void) { return (ncclResult_t)flxGroupEnd(); }

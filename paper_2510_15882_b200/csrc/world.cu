@@ -639,6 +639,7 @@ std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local) {
 }
 int world_nranks(World* w) { return w->nranks; }
 int world_nlocal(World* w) { return (int)w->local.size(); }
+bool world_aborted(World* w) { return *(volatile uint32_t*)w->abort_word != 0; }
 void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(kMaxCtas, n)); }
 
 // ------------------------------------------------------------ creation

@@ -92,11 +92,12 @@ def _abort_worker(rank, world, port, out):
             c.all_reduce(t)
             torch.cuda.synchronize()
             waited = time.perf_counter() - t0
+            async_err = c.async_error()  # ncclCommGetAsyncError
             try:
                 c.all_reduce(t)
-                out[0] = ("no error", waited)
+                out[0] = ("no error", waited, async_err)
             except comm.FlexLinkError as e:
-                out[0] = (e.code, waited)
+                out[0] = (e.code, waited, async_err)
         dist.barrier()
         c.destroy()
     finally:
@@ -112,6 +113,6 @@ def test_peer_timeout_aborts_instead_of_hanging():
     with mp.Manager() as m:
         out = m.dict()
         mp.spawn(_abort_worker, args=(2, _port(), out), nprocs=2, join=True)
-        code, waited = out[0]
-    assert code == 3, code
+        code, waited, async_err = out[0]
+    assert code == 3 and async_err == 3, (code, async_err)
     assert 0.5 < waited < 30, waited

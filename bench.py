@@ -646,13 +646,15 @@ def run_multi_gpu(args) -> None:
     send = torch.randint(-1024, 1024, (count,), device="cuda", generator=gen).float()
     recv = torch.empty_like(send)
     stream = torch.cuda.current_stream()
-    topo = preset("B200", n_gpus=world).restricted(c.available_paths())
+    topo = preset("B200", n_gpus=max(world, 2)).restricted(c.available_paths())  # 1: smoke
 
     def stage1(op, s, r):
         """Stage 1 on the real path with rank-agreed timings, then the guard."""
-        if args.shares:
-            g = [int(x) for x in args.shares.split(",")]
-            return ShareDistribution({k: g[int(k)] for k in PathKind if g[int(k)] or k == 0}), None
+        if args.shares or world < 2:  # world 1 (FLX_BENCH_MULTI smoke): nothing to tune
+            g = [int(x) for x in (args.shares or "1000,0,0").split(",")]
+            shares = ShareDistribution({k: g[int(k)] for k in PathKind if g[int(k)] or k == 0})
+            c.set_shares(op, shares, s.numel() * s.element_size())
+            return shares, None
         measure = flx.rank_measure_fn(c, op, s, r, warmup=2, repeats=5)
         spec = CollectiveSpec(op, world, s.numel() * s.element_size())
         shares, trace = initial_tune(topo, spec, TunerConfig(), measure=measure)
@@ -768,7 +770,9 @@ def main() -> None:
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1:
+    # FLX_BENCH_MULTI=1: take the one-process-per-GPU path even at WORLD_SIZE 1
+    # (a smoke test of run_multi_gpu on a 1-GPU box)
+    if world > 1 or os.environ.get("FLX_BENCH_MULTI") == "1":
         os.environ.setdefault("FLX_BOOT_TIMEOUT", "60")
         try:
             run_multi_gpu(args)

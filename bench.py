@@ -480,6 +480,8 @@ def run_single_gpu(args) -> None:
                                   for k in PathKind},
             "kernel_achieved_gbs": round(ag_alg / (ag_nv_ms * 1e-3) / 1e9, 1),
             "kernel_frac_hbm": round(ag_alg / (ag_nv_ms * 1e-3) / 1e9 / hbm_peak, 4),
+            "kernel_algorithmic_bytes": ag_alg,
+            "kernel_traffic": ncu_traffic("profiles/r1/fanout_once_ncu_summary.txt"),
             "paper_convention_algbw": round(AG_OUT_BYTES / n / ag_dt / 1e9, 2),
         },
     }

@@ -172,6 +172,13 @@ flxResult_t flxGetAlignment(flxComm_t comm, flxCollOp_t op, size_t* alignment);
  * nctas: CTAs of the NVLink-path kernel (0 = automatic).  Config 4 caps it to
  * emulate a slower NVLink.  Must match on all ranks. */
 flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas);
+/* enabled = 1 (default): every collective records per-path CUDA events, read
+ * back by flxGetPathTimes / flxGetPathTimesHistory (Stage 1 / Stage 2's
+ * MeasurePathTimings).  0: no timing events — a timed event record costs as
+ * much host time as a kernel launch, so small-message callers that do not
+ * rebalance at run time save ~5 us per call; path times then read as 0.
+ * Must match on all ranks of a group. */
+flxResult_t flxSetTiming(flxComm_t comm, int enabled);
 /* PCIe staging: bytes per chunk per rank and ring depth (1 or 2 buffers;
  * PipelineSpec, staging.py:24-42).  Must match on all ranks. */
 flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers);

@@ -104,6 +104,7 @@ def load_library() -> ctypes.CDLL:
         "flxGetPathBytes": [vp, P(sz)],
         "flxGetAlignment": [vp, ci, P(sz)],
         "flxSetNvlinkCtas": [vp, ci],
+        "flxSetTiming": [vp, ci],
         "flxSetStaging": [vp, sz, ci],
         "flxGetPathMask": [vp, P(ci)],
         "flxGetLaunchCount": [P(ctypes.c_ulonglong)],
@@ -316,6 +317,10 @@ class Communicator:
     def set_staging(self, chunk_bytes: int = 0, buffers: int = 2) -> None:
         _check(load_library().flxSetStaging(self._h, chunk_bytes, buffers), "flxSetStaging")
 
+    def set_timing(self, enabled: bool) -> None:
+        """``flxSetTiming``: per-path CUDA-event timing on (default) or off."""
+        _check(load_library().flxSetTiming(self._h, int(bool(enabled))), "flxSetTiming")
+
     def path_mask(self) -> int:
         m = ctypes.c_int()
         _check(load_library().flxGetPathMask(self._h, ctypes.byref(m)), "flxGetPathMask")
@@ -524,6 +529,10 @@ class Clique:
     def set_staging(self, chunk_bytes: int = 0, buffers: int = 2) -> None:
         for c in self.comms:
             c.set_staging(chunk_bytes, buffers)
+
+    def set_timing(self, enabled: bool) -> None:
+        for c in self.comms:
+            c.set_timing(enabled)
 
     def path_times(self) -> dict[PathKind, float]:
         return self.comms[0].path_times()

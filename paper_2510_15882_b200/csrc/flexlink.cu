@@ -189,6 +189,8 @@ flxResult_t clique_create(int device, int members, Clique** out) {
     FLX_CUDA(cudaEventCreate(&t.pcie));
   }
   FLX_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&c->ev_start_nt, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&c->ev_pcie_nt, cudaEventDisableTiming));
   c->ev_fork.resize(members);
   for (auto& e : c->ev_fork) FLX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   // semaphore words: [0,B) semFull, [B,2B) semEmpty; start at zero (staging.py:224-225)
@@ -231,6 +233,8 @@ flxResult_t clique_destroy(Clique* c) {
     cudaEventDestroy(t.pcie);
   }
   cudaEventDestroy(c->ev_join);
+  cudaEventDestroy(c->ev_start_nt);
+  cudaEventDestroy(c->ev_pcie_nt);
   for (auto e : c->ev_fork) cudaEventDestroy(e);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->dev_stage) cudaFree(c->dev_stage);
@@ -304,7 +308,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       return fail(flxInvalidUsage, "rank %d called a different collective than rank 0", i);
     const Comm* m = k.comm;
     if (m->nvlink_ctas != lead->nvlink_ctas || m->chunk_bytes != lead->chunk_bytes ||
-        m->buffers != lead->buffers)
+        m->buffers != lead->buffers || m->timing != lead->timing)
       return fail(flxInvalidUsage, "rank %d path configuration differs from rank 0", i);
   }
   FLX_CUDA(cudaSetDevice(c->device));
@@ -331,10 +335,14 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   FLX_CUDA(cudaStreamIsCapturing(s0, &cap));
   const bool capturing = cap == cudaStreamCaptureStatusActive;
   Clique::Timing& tm = c->timing[c->calls % Clique::kTimingSlots];
-  FLX_CUDA(cudaEventRecord(tm.start, s0));
-
   const size_t nv = split[flxPathNvlink];
   const size_t pc = split[flxPathPcie];
+  // events recorded inside a capture are graph edges, not timestamps
+  const bool timed = lead->timing && !capturing;
+  const cudaEvent_t ev_start = timed ? tm.start : c->ev_start_nt;
+  const cudaEvent_t ev_pcie = timed ? tm.pcie : c->ev_pcie_nt;
+  if (timed || pc > 0) FLX_CUDA(cudaEventRecord(ev_start, s0));
+
   // Uncapped, the fold runs one 16 B vector per thread (grid = slice/8 KiB):
   // measured 6.73 TB/s vs 6.24 TB/s for one persistent CTA per SM
   // (profiles/r1/fold_variants_standalone.jsonl) — CTA turnover hides the
@@ -366,8 +374,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     const int bufs = c->stage_bufs;
     const size_t pitch = rows ? chunk : c->stage_cap;  // row pitch in the slot
     const size_t slot_bytes = c->stage_cap * n;
-    FLX_CUDA(cudaStreamWaitEvent(c->d2h, tm.start, 0));
-    FLX_CUDA(cudaStreamWaitEvent(c->h2d, tm.start, 0));
+    FLX_CUDA(cudaStreamWaitEvent(c->d2h, ev_start, 0));
+    FLX_CUDA(cudaStreamWaitEvent(c->h2d, ev_start, 0));
     uint64_t local_piece = 0;
     // inside a capture only events recorded earlier in the SAME capture may be
     // awaited; the first use of a slot needs no wait (the graph starts after
@@ -466,7 +474,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       FLX_CUDA(cudaEventRecord(c->ev_folded[capturing][buf], c->red));
       folded_rec[buf] = true;
     }
-    FLX_CUDA(cudaEventRecord(tm.pcie, c->red));
+    FLX_CUDA(cudaEventRecord(ev_pcie, c->red));
   }
 
   // ---- NVLink slice: one fused kernel over all members on the lead stream
@@ -520,8 +528,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
       FLX_CUDA(launch_fold(head.dtype, head.op, a, grid_nv, s0));
     }
   }
-  FLX_CUDA(cudaEventRecord(tm.nv, s0));
-  if (pc > 0) FLX_CUDA(cudaStreamWaitEvent(s0, tm.pcie, 0));
+  if (timed) FLX_CUDA(cudaEventRecord(tm.nv, s0));
+  if (pc > 0) FLX_CUDA(cudaStreamWaitEvent(s0, ev_pcie, 0));
 
   // join: every member's stream waits for the collective
   bool joined = false;
@@ -534,9 +542,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     FLX_CUDA(cudaStreamWaitEvent(calls[i].stream, c->ev_join, 0));
   }
   c->last_bytes = split;
-  // events recorded inside a capture are graph edges, not timestamps
-  tm.used[flxPathNvlink] = nv > 0 && !capturing;
-  tm.used[flxPathPcie] = pc > 0 && !capturing;
+  tm.used[flxPathNvlink] = nv > 0 && timed;
+  tm.used[flxPathPcie] = pc > 0 && timed;
   tm.used[flxPathRdma] = false;
   c->calls++;
   return flxSuccess;
@@ -557,12 +564,14 @@ flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
       return fail(flxInvalidUsage, "local rank %zu called a different collective", i);
     if (k.comm->shares[head.coll].lookup(head.coll, bytes) != g)
       return fail(flxInvalidUsage, "local rank %zu has different shares", i);
+    if (k.comm->timing != lead->timing)
+      return fail(flxInvalidUsage, "local rank %zu has a different timing setting", i);
     send.push_back(k.send);
     recv.push_back(k.recv);
     streams.push_back(k.stream);
   }
   return run_world(w, send, recv, streams, head.coll, head.count, head.dtype, head.op, g,
-                   alignment_for(lead, head.coll));
+                   alignment_for(lead, head.coll), lead->timing);
 }
 
 flxResult_t flush_group() {
@@ -982,6 +991,12 @@ flxResult_t flxGetAlignment(flxComm_t comm, flxCollOp_t op, size_t* alignment) {
   FLX_TRY(validate_comm(comm));
   if (!alignment) return fail(flxInvalidArgument, "null alignment");
   *alignment = alignment_for(comm, op);
+  return flxSuccess;
+}
+
+flxResult_t flxSetTiming(flxComm_t comm, int enabled) {
+  FLX_TRY(validate_comm(comm));
+  comm->timing = enabled != 0;
   return flxSuccess;
 }
 

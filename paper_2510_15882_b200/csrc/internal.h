@@ -94,6 +94,9 @@ struct Clique {
   uint64_t calls = 0;  // collectives issued on this clique
   cudaEvent_t ev_join = nullptr;
   std::vector<cudaEvent_t> ev_fork;
+  // fork/join points when a call is not timed (flxSetTiming 0 or capture):
+  // a timing event record costs as much host time as a kernel launch
+  cudaEvent_t ev_start_nt = nullptr, ev_pcie_nt = nullptr;
   // host-staged ring: buffers x members x chunk_cap bytes, pinned + device
   char* host_stage = nullptr;
   char* dev_stage = nullptr;
@@ -115,7 +118,7 @@ int world_release(World* w);
 flxResult_t run_world(World* w, const std::vector<const void*>& send,
                       const std::vector<void*>& recv, const std::vector<cudaStream_t>& streams,
                       int coll, size_t count, int dtype, int op, const Granules& g,
-                      size_t alignment);
+                      size_t alignment, bool timing);
 flxResult_t world_read_timing(World* w, int local, uint64_t seq, float ms[3]);
 uint64_t world_calls(World* w, int local);
 std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local);
@@ -136,6 +139,7 @@ struct Comm {
   int nvlink_ctas = 0;   // 0 = auto
   size_t chunk_bytes = 0;  // 0 = auto
   int buffers = 2;
+  bool timing = true;    // record per-path CUDA events (flxSetTiming)
 };
 
 }  // namespace flx

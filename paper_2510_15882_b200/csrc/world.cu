@@ -87,6 +87,7 @@ struct World {
   int nranks = 0;
   bool loopback = false;
   int nctas = 0;
+  int max_nctas = kMaxCtas;  // loopback: every CTA of every rank co-resident
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
   long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
@@ -109,6 +110,7 @@ struct World {
     char* dstage = nullptr;  // device landing zone for PCIe sub-chunks
     cudaStream_t d2h = nullptr, h2d = nullptr;
     cudaEvent_t fold_done = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_start_nt = nullptr, ev_pcie_nt = nullptr;  // untimed fork/join points
     std::vector<cudaEvent_t> ev_fork;
     Clique::Timing timing[Clique::kTimingSlots];
     uint64_t calls = 0;
@@ -149,6 +151,8 @@ flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
   FLX_CUDA(cudaEventCreateWithFlags(&L.fold_done, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&L.ev_start_nt, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&L.ev_pcie_nt, cudaEventDisableTiming));
   for (auto& t : L.timing) {
     FLX_CUDA(cudaEventCreate(&t.start));
     FLX_CUDA(cudaEventCreate(&t.nv));
@@ -185,6 +189,8 @@ void world_free(World* w) {
     if (L.h2d) cudaStreamDestroy(L.h2d);
     if (L.fold_done) cudaEventDestroy(L.fold_done);
     if (L.ev_join) cudaEventDestroy(L.ev_join);
+    if (L.ev_start_nt) cudaEventDestroy(L.ev_start_nt);
+    if (L.ev_pcie_nt) cudaEventDestroy(L.ev_pcie_nt);
     for (auto e : L.ev_fork) cudaEventDestroy(e);
     for (auto& t : L.timing) {
       cudaEventDestroy(t.start);
@@ -350,7 +356,7 @@ static flxResult_t wait_region_free(World* w, cudaStream_t s, int r, uint32_t e)
 flxResult_t run_world(World* w, const std::vector<const void*>& send,
                       const std::vector<void*>& recv, const std::vector<cudaStream_t>& streams,
                       int coll, size_t count, int dtype, int op, const Granules& g,
-                      size_t alignment) {
+                      size_t alignment, bool timing) {
   const int n = w->nranks;
   const int nl = (int)w->local.size();
   const size_t esz = dtype_size(dtype);
@@ -391,14 +397,17 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   }
   // every local rank shares s0: one start/nv event pair (local rank 0's) times
   // the NVLink slice for all of them; the PCIe legs keep per-rank events
-  FLX_CUDA(cudaEventRecord(tm[0]->start, s0));
+  const bool timed = timing && !capturing;
+  const cudaEvent_t ev_start = timed ? tm[0]->start : w->local[0].ev_start_nt;
+  auto ev_pcie = [&](int i) { return timed ? tm[i]->pcie : w->local[i].ev_pcie_nt; };
+  if (timed || pc > 0) FLX_CUDA(cudaEventRecord(ev_start, s0));
 
   // ---------------- PCIe slice (issued first so the copies overlap the kernel)
   if (pc > 0) {
     const uint32_t e = w->pepoch++;
     for (auto& L : w->local) {
-      FLX_CUDA(cudaStreamWaitEvent(L.d2h, tm[0]->start, 0));
-      FLX_CUDA(cudaStreamWaitEvent(L.h2d, tm[0]->start, 0));
+      FLX_CUDA(cudaStreamWaitEvent(L.d2h, ev_start, 0));
+      FLX_CUDA(cudaStreamWaitEvent(L.h2d, ev_start, 0));
     }
     if (a2a) {
       // step 1 as ReduceScatter; step 2: rank r lands H_p[r] straight into its
@@ -429,7 +438,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
                                    w->hregion(p) + r * pc, pc, cudaMemcpyHostToDevice, L.h2d));
           FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
         }
-        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
       }
     } else if (scatter) {
       // step 1: D2H the PCIe part of my block c into H_r[c]; step 2: the owner
@@ -465,7 +474,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         a.ndst = 1;
         a.bytes = pc;
         FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
-        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
       }
     } else if (!gather) {
       const size_t q = pc / n;  // alignment makes pc a multiple of n*4096
@@ -525,7 +534,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
                                    cudaMemcpyHostToDevice, L.h2d));
           FLX_TRY(sem_write(L.h2d, w->sem(sem_rcons(c, r)), e));
         }
-        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
       }
       w->last_ar_pepoch = e;
     } else {
@@ -553,7 +562,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
                                    w->hregion(c), pc, cudaMemcpyHostToDevice, L.h2d));
           FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(c, r)), e));
         }
-        FLX_CUDA(cudaEventRecord(tm[i]->pcie, L.h2d));
+        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
       }
     }
   }
@@ -592,9 +601,9 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     if (err != cudaSuccess)
       return fail(flxUnhandledCudaError, "rank kernel launch: %s", cudaGetErrorString(err));
   }
-  FLX_CUDA(cudaEventRecord(tm[0]->nv, s0));
+  if (timed) FLX_CUDA(cudaEventRecord(tm[0]->nv, s0));
   if (pc > 0)
-    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaStreamWaitEvent(s0, tm[i]->pcie, 0));
+    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaStreamWaitEvent(s0, ev_pcie(i), 0));
   bool joined = false;
   for (int i = 1; i < nl; ++i) {
     if (streams[i] == s0) continue;
@@ -607,8 +616,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   for (int i = 0; i < nl; ++i) {
     World::Local& L = w->local[i];
     // events recorded inside a capture are graph edges, not timestamps
-    tm[i]->used[flxPathNvlink] = nv > 0 && !capturing;
-    tm[i]->used[flxPathPcie] = pc > 0 && !capturing;
+    tm[i]->used[flxPathNvlink] = nv > 0 && timed;
+    tm[i]->used[flxPathPcie] = pc > 0 && timed;
     tm[i]->used[flxPathRdma] = false;
     L.last_bytes = split;
     L.calls++;
@@ -640,7 +649,7 @@ std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local) {
 int world_nranks(World* w) { return w->nranks; }
 int world_nlocal(World* w) { return (int)w->local.size(); }
 bool world_aborted(World* w) { return *(volatile uint32_t*)w->abort_word != 0; }
-void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(kMaxCtas, n)); }
+void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(w->max_nctas, n)); }
 
 // ------------------------------------------------------------ creation
 namespace {
@@ -668,7 +677,8 @@ flxResult_t world_create_loopback(int nranks, int device, World** out) {
   if (!coop) return fail(flxInvalidUsage, "device %d lacks cooperative launch", device);
   int sms = 0;
   FLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  w->nctas = std::max(1, std::min(w->nctas, sms / nranks));  // all CTAs co-resident
+  w->max_nctas = std::max(1, std::min(kMaxCtas, sms / nranks));  // all CTAs co-resident
+  w->nctas = std::min(w->nctas, w->max_nctas);
   for (int r = 0; r < nranks; ++r) {
     w->local[r].rank = r;
     w->local[r].device = device;

@@ -278,3 +278,27 @@ def test_loopback_oneshot_and_twoshot_interleaved(oneshot_kb):
                                            4096)
                 for r in range(n):
                     np.testing.assert_array_equal(_np(ag[r], dtype), want_ag[r])
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_timing_off_keeps_results_and_zeroes_path_times(loopback):
+    n, count, g = 4, (1 << 18) + 8, (850, 150, 0)
+    cpu = _inputs(n, count, 7, 55)
+    sends = [c.cuda() for c in cpu]
+    recvs = [torch.empty_like(s) for s in sends]
+    with flx.Clique(n, loopback=loopback) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, g)
+        w.set_timing(False)
+        for _ in range(3):
+            w.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        assert all(v == 0 for v in w.comms[0].path_times().values())
+        align = w.comms[0].alignment(CollectiveOp.ALLREDUCE)
+        want = oracle.allreduce([c.numpy() for c in cpu], 7, 0, g, align)
+        for r in range(n):
+            np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
+        w.set_timing(True)
+        w.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        t = w.comms[0].path_times()
+        assert t[PathKind.NVLINK] > 0 and t[PathKind.PCIE_STAGED] > 0

@@ -71,6 +71,15 @@ flxResult_t sem_wait_geq(cudaStream_t s, uint32_t* word, uint32_t value) {
   return flxSuccess;
 }
 
+flxResult_t sem_wait_eq(cudaStream_t s, uint32_t* word, uint32_t value) {
+  const MemOps& m = memops();
+  if (!m.ok) return fail(flxInternalError, "stream memory operations unavailable");
+  CUresult r = m.wait32(reinterpret_cast<CUstream>(s), reinterpret_cast<CUdeviceptr>(word),
+                        value, CU_STREAM_WAIT_VALUE_EQ);
+  if (r != CUDA_SUCCESS) return fail(flxUnhandledCudaError, "cuStreamWaitValue32: %d", (int)r);
+  return flxSuccess;
+}
+
 flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value) {
   const MemOps& m = memops();
   if (!m.ok) return fail(flxInternalError, "stream memory operations unavailable");

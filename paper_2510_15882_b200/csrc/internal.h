@@ -50,6 +50,7 @@ struct MemOps {
 };
 const MemOps& memops();
 flxResult_t sem_wait_geq(cudaStream_t s, uint32_t* word, uint32_t value);
+flxResult_t sem_wait_eq(cudaStream_t s, uint32_t* word, uint32_t value);
 flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value);
 
 size_t dtype_size(int dtype);

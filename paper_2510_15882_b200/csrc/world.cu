@@ -5,21 +5,21 @@
 //   NVLink slice : rank_allreduce/rank_allgather kernel over peer-mapped
 //                  scratch (rank_kernels.cuh)
 //   PCIe slice   : host-hub staging through one shared host segment; copy
-//                  engines on two side streams; per-edge monotone counter
-//                  semaphores (staging.py:176-188 with buffers=1, lap=epoch-1)
-//                  set with cuStreamWriteValue32 and awaited with
-//                  cuStreamWaitValue32 on the shared words:
-//     AllReduce  1 D2H  send[sub c]   -> H_r[c]        prod[r][c] = e   (c != r)
-//                2 H2D  H_p[r]        -> stage[p]      cons[p][r] = e   (p != r)
-//                  fold stage[*] + own sub r           -> recv sub r
-//                3 D2H  recv sub r    -> R_r           rprod[r]   = e
-//                4 H2D  R_c           -> recv sub c    rcons[c][r] = e
-//     AllGather  1 D2H  send          -> H_r           gprod[r]   = e
-//                2 H2D  H_c           -> recv block c  cons[c][r] = e
-//     ReduceScatter = AllReduce steps 1-2 on the PCIe part of each recv block.
-//   Reuse guards: H_r is rewritten only when every reader of the previous
-//   PCIe epoch has set cons[r][p] (all protocols set it); R_r only after the
-//   previous AllReduce's readers set rcons.
+//                  engines on two side streams; per-edge tokens on the shared
+//                  words, set with cuStreamWriteValue32 and awaited with
+//                  cuStreamWaitValue32 (EQ) — constant values, so the same
+//                  memops replay correctly from a CUDA graph:
+//     AllReduce  1 take H_r; D2H send[sub c] -> H_r[c]; post prod[r][c]  (c != r)
+//                2 accept prod[p][r]; H2D H_p[r] -> stage[p]; give hfree[p][r]
+//                  fold stage[*] + own sub r -> recv sub r
+//                3 take R_r; D2H recv sub r -> R_r; post rprod[r][c]
+//                4 accept rprod[c][r]; H2D R_c -> recv sub c; give rfree[c][r]
+//     AllGather  1 take H_r; D2H send -> H_r; post prod[r][c]
+//                2 accept prod[c][r]; H2D H_c -> recv block c; give hfree[c][r]
+//     ReduceScatter / AllToAll = steps 1-2 on the PCIe part of each block
+//                (AllToAll lands straight in recv, no fold).
+//   "take H_r" waits for every reader's free token of the previous use of
+//   H_r, whichever protocol that was; R_r likewise for AllReduce.
 //   Issue order is global (all ranks' step 1, then step 2, ...) so every wait
 //   refers to a write issued earlier: no deadlock even when streams share a
 //   hardware queue (loopback).
@@ -46,16 +46,11 @@ namespace flx {
 namespace {
 
 constexpr int kSemWords = 4096;  // uint32 words at the head of the staging segment
-// semaphore word layout (all [src][dst] over kMaxRanks)
-inline size_t sem_prod(int r, int c) { return 0 * 256 + r * kMaxRanks + c; }
-inline size_t sem_cons(int r, int c) { return 1 * 256 + r * kMaxRanks + c; }
-inline size_t sem_rcons(int r, int c) { return 2 * 256 + r * kMaxRanks + c; }
-inline size_t sem_rprod(int r) { return 4 * 256 + r; }
-inline size_t sem_gprod(int r) { return 4 * 256 + kMaxRanks + r; }
-// sem_cons(r, p) = e: reader p finished reading region H_r for PCIe epoch e —
-// written by every protocol, so "all readers >= e-1" guards H_r whatever
-// collective used it last.  sem_rcons guards R_r, which only AllReduce uses,
-// against the last AllReduce epoch.
+// token word layout (all [producer][reader] over kMaxRanks), see token_post
+inline size_t sem_prod(int r, int c) { return 0 * 256 + r * kMaxRanks + c; }   // H_r piece ready
+inline size_t sem_hfree(int r, int c) { return 1 * 256 + r * kMaxRanks + c; }  // H_r taken/free
+inline size_t sem_rprod(int r, int c) { return 2 * 256 + r * kMaxRanks + c; }  // R_r ready
+inline size_t sem_rfree(int r, int c) { return 3 * 256 + r * kMaxRanks + c; }  // R_r taken/free
 
 size_t env_mib(const char* name, size_t dflt) {
   const char* v = getenv(name);
@@ -94,8 +89,6 @@ struct World {
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   size_t hcap = 0;       // PCIe staging bytes per rank region
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
-  uint32_t last_ar_pepoch = 0;  // last AllReduce PCIe epoch (guards R_r reuse)
-  uint32_t pepoch = 1;   // PCIe-path semaphore epoch (next call)
   // host staging segment: [sem words][H_0 .. H_{n-1}][R_0 .. R_{n-1}]
   char* host = nullptr;
   size_t host_bytes = 0;
@@ -111,6 +104,7 @@ struct World {
     cudaStream_t d2h = nullptr, h2d = nullptr;
     cudaEvent_t fold_done = nullptr, ev_join = nullptr;
     cudaEvent_t ev_start_nt = nullptr, ev_pcie_nt = nullptr;  // untimed fork/join points
+    cudaEvent_t ev_d2h_done = nullptr;  // joins the D2H stream's last token writes
     std::vector<cudaEvent_t> ev_fork;
     Clique::Timing timing[Clique::kTimingSlots];
     uint64_t calls = 0;
@@ -153,6 +147,7 @@ flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_start_nt, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_pcie_nt, cudaEventDisableTiming));
+  FLX_CUDA(cudaEventCreateWithFlags(&L.ev_d2h_done, cudaEventDisableTiming));
   for (auto& t : L.timing) {
     FLX_CUDA(cudaEventCreate(&t.start));
     FLX_CUDA(cudaEventCreate(&t.nv));
@@ -191,6 +186,7 @@ void world_free(World* w) {
     if (L.ev_join) cudaEventDestroy(L.ev_join);
     if (L.ev_start_nt) cudaEventDestroy(L.ev_start_nt);
     if (L.ev_pcie_nt) cudaEventDestroy(L.ev_pcie_nt);
+    if (L.ev_d2h_done) cudaEventDestroy(L.ev_d2h_done);
     for (auto e : L.ev_fork) cudaEventDestroy(e);
     for (auto& t : L.timing) {
       cudaEventDestroy(t.start);
@@ -344,11 +340,28 @@ cudaError_t launch_rank_alltoall(bool loop, const void* args, int nctas, int nra
 
 }  // namespace
 
-// Before rank r overwrites its host region H_r at PCIe epoch e, every reader
-// of the previous epoch must be done with it.
-static flxResult_t wait_region_free(World* w, cudaStream_t s, int r, uint32_t e) {
-  for (int p = 0; p < w->nranks; ++p)
-    if (p != r) FLX_TRY(sem_wait_geq(s, w->sem(sem_cons(r, p)), e - 1));
+// Token handshake on the shared host words (all values are constants, so the
+// same stream memory operations are correct eagerly and replayed from a CUDA
+// graph):  ready tokens prod/rprod[r][c] = 1 posted by producer r, consumed
+// (reset to 0) by reader c; free tokens hfree/rfree[r][c] = 0 while reader c
+// is done with region H_r / R_r, set to 1 by producer r when it takes the
+// region, returned (0) by the reader after its H2D.  Every edge strictly
+// alternates take -> post -> accept -> give, each write ordered after the
+// wait that licenses it on the same stream.
+static flxResult_t token_post(cudaStream_t s, uint32_t* w) { return sem_write(s, w, 1); }
+static flxResult_t token_give(cudaStream_t s, uint32_t* w) { return sem_write(s, w, 0); }
+static flxResult_t token_accept(cudaStream_t s, uint32_t* w) {
+  FLX_TRY(sem_wait_eq(s, w, 1));
+  return sem_write(s, w, 0);
+}
+// Rank r takes H_r (or R_r): every reader returned its free token.
+static flxResult_t take_region(World* w, cudaStream_t s, int r, bool result) {
+  for (int p = 0; p < w->nranks; ++p) {
+    if (p == r) continue;
+    uint32_t* word = w->sem(result ? sem_rfree(r, p) : sem_hfree(r, p));
+    FLX_TRY(sem_wait_eq(s, word, 0));
+    FLX_TRY(sem_write(s, word, 1));
+  }
   return flxSuccess;
 }
 
@@ -371,12 +384,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
   const bool capturing = cap != cudaStreamCaptureStatusNone;
-  // The NVLink kernels keep their epochs on the device and replay correctly
-  // from a graph; the PCIe path's semaphore targets are host-side counters
-  // that a replay would repeat.
-  if (capturing && pc > 0)
-    return fail(flxInvalidUsage, "a multi-rank collective with a PCIe share cannot be captured "
-                "into a CUDA graph: set NVLink-only shares for the captured size bucket");
+  // The NVLink kernels keep their epochs on the device and the PCIe path's
+  // token handshake uses constant values: both replay correctly from a graph.
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
   if ((scatter || a2a ? pc * n : pc) > w->hcap)
     return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
@@ -404,163 +413,97 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
 
   // ---------------- PCIe slice (issued first so the copies overlap the kernel)
   if (pc > 0) {
-    const uint32_t e = w->pepoch++;
-    for (auto& L : w->local) {
+    for (int i = 0; i < nl; ++i) {
+      World::Local& L = w->local[i];
       FLX_CUDA(cudaStreamWaitEvent(L.d2h, ev_start, 0));
       FLX_CUDA(cudaStreamWaitEvent(L.h2d, ev_start, 0));
     }
-    if (a2a) {
-      // step 1 as ReduceScatter; step 2: rank r lands H_p[r] straight into its
-      // recv block p (no fold), and copies its own block device to device
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        FLX_TRY(wait_region_free(w, L.d2h, r, e));
+    // step 1 (every protocol): rank r takes the free token of every reader of
+    // H_r, D2H's its pieces into H_r and posts one ready token per reader.
+    // AllReduce: sub-chunk c -> H_r[c]; ReduceScatter / AllToAll: the PCIe
+    // part of block c -> H_r[c]; AllGather: the whole slice -> H_r.
+    const size_t q = (!gather && !scatter && !a2a) ? pc / n : pc;  // piece per reader
+    for (int i = 0; i < nl; ++i) {
+      World::Local& L = w->local[i];
+      const int r = L.rank;
+      FLX_TRY(take_region(w, L.d2h, r, /*result=*/false));
+      const char* src = static_cast<const char*>(send[i]);
+      if (gather) {
+        FLX_CUDA(cudaMemcpyAsync(w->hregion(r), src + nv, pc, cudaMemcpyDeviceToHost, L.d2h));
+      } else {
         for (int s = 1; s < n; ++s) {
           const int c = (r + s) % n;
-          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * pc,
-                                   static_cast<const char*>(send[i]) + (size_t)c * bytes + nv, pc,
-                                   cudaMemcpyDeviceToHost, L.d2h));
-          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
+          const char* piece = (scatter || a2a) ? src + (size_t)c * bytes + nv : src + nv + c * q;
+          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * q, piece, q, cudaMemcpyDeviceToHost,
+                                   L.d2h));
         }
       }
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
+      for (int s = 1; s < n; ++s) FLX_TRY(token_post(L.d2h, w->sem(sem_prod(r, (r + s) % n))));
+    }
+    // step 2: rank r accepts every peer's piece, lands it (AllGather / AllToAll:
+    // straight into recv; AllReduce / ReduceScatter: into dstage, then the
+    // rank-order fold) and returns the free token
+    for (int i = 0; i < nl; ++i) {
+      World::Local& L = w->local[i];
+      const int r = L.rank;
+      char* dst = static_cast<char*>(recv[i]);
+      const char* src = static_cast<const char*>(send[i]);
+      if (gather) {
+        char* own = dst + (size_t)r * bytes + nv;
+        if (own != src + nv)
+          FLX_CUDA(cudaMemcpyAsync(own, src + nv, pc, cudaMemcpyDeviceToDevice, L.h2d));
+      } else if (a2a) {
         const size_t own = (size_t)r * bytes + nv;
-        FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + own,
-                                 static_cast<const char*>(send[i]) + own, pc,
-                                 cudaMemcpyDeviceToDevice, L.h2d));
-        for (int s = 1; s < n; ++s) {
-          const int p = (r - s + n) % n;
-          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
-          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + (size_t)p * bytes + nv,
-                                   w->hregion(p) + r * pc, pc, cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
-        }
-        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
+        FLX_CUDA(cudaMemcpyAsync(dst + own, src + own, pc, cudaMemcpyDeviceToDevice, L.h2d));
       }
-    } else if (scatter) {
-      // step 1: D2H the PCIe part of my block c into H_r[c]; step 2: the owner
-      // lands every source's copy of its block and folds it in rank order
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        FLX_TRY(wait_region_free(w, L.d2h, r, e));
-        for (int s = 1; s < n; ++s) {
-          const int c = (r + s) % n;
-          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * pc,
-                                   static_cast<const char*>(send[i]) + (size_t)c * bytes + nv, pc,
-                                   cudaMemcpyDeviceToHost, L.d2h));
-          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
-        }
+      for (int s = 1; s < n; ++s) {
+        const int p = (r - s + n) % n;
+        FLX_TRY(token_accept(L.h2d, w->sem(sem_prod(p, r))));
+        const char* from = gather ? w->hregion(p) : w->hregion(p) + r * q;
+        char* to = gather ? dst + (size_t)p * bytes + nv
+                   : a2a  ? dst + (size_t)p * bytes + nv
+                          : L.dstage + p * q;
+        FLX_CUDA(cudaMemcpyAsync(to, from, q, cudaMemcpyHostToDevice, L.h2d));
+        FLX_TRY(token_give(L.h2d, w->sem(sem_hfree(p, r))));
       }
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        for (int s = 1; s < n; ++s) {
-          const int p = (r - s + n) % n;
-          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
-          FLX_CUDA(cudaMemcpyAsync(L.dstage + p * pc, w->hregion(p) + r * pc, pc,
-                                   cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
-        }
+      if (!gather && !a2a) {  // fold every source's piece r in rank order
         FoldArgs a{};
         for (int p = 0; p < n; ++p)
-          a.src[p] = (p == r) ? static_cast<const char*>(send[i]) + (size_t)r * bytes + nv
-                              : L.dstage + p * pc;
-        a.dst[0] = static_cast<char*>(recv[i]) + nv;
-        a.n = n;
-        a.ndst = 1;
-        a.bytes = pc;
-        FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
-        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
-      }
-    } else if (!gather) {
-      const size_t q = pc / n;  // alignment makes pc a multiple of n*4096
-      // step 1: D2H my sub-chunk c into H_r[c]
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        FLX_TRY(wait_region_free(w, L.d2h, r, e));
-        for (int s = 1; s < n; ++s) {
-          const int c = (r + s) % n;
-          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * q,
-                                   static_cast<const char*>(send[i]) + nv + c * q, q,
-                                   cudaMemcpyDeviceToHost, L.d2h));
-          FLX_TRY(sem_write(L.d2h, w->sem(sem_prod(r, c)), e));
-        }
-      }
-      // step 2: H2D every source's sub-chunk r, fold in rank order
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        for (int s = 1; s < n; ++s) {
-          const int p = (r - s + n) % n;
-          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_prod(p, r)), e));
-          FLX_CUDA(cudaMemcpyAsync(L.dstage + p * q, w->hregion(p) + r * q, q,
-                                   cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(p, r)), e));
-        }
-        FoldArgs a{};
-        for (int p = 0; p < n; ++p)
-          a.src[p] = (p == r) ? static_cast<const char*>(send[i]) + nv + r * q : L.dstage + p * q;
-        a.dst[0] = static_cast<char*>(recv[i]) + nv + r * q;
+          a.src[p] = p != r    ? L.dstage + p * q
+                     : scatter ? src + (size_t)r * bytes + nv
+                               : src + nv + r * q;
+        a.dst[0] = scatter ? dst + nv : dst + nv + r * q;
         a.n = n;
         a.ndst = 1;
         a.bytes = q;
         FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
-        FLX_CUDA(cudaEventRecord(L.fold_done, L.h2d));
       }
-      // step 3: D2H my reduced sub-chunk into R_r
+      if (gather || scatter || a2a) FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
+      else FLX_CUDA(cudaEventRecord(L.fold_done, L.h2d));
+    }
+    if (!gather && !scatter && !a2a) {
+      // AllReduce step 3: D2H my reduced sub-chunk into R_r (after its previous
+      // readers returned the R_r free tokens), post a ready token per reader
       for (int i = 0; i < nl; ++i) {
         World::Local& L = w->local[i];
         const int r = L.rank;
         FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done, 0));
-        for (int p = 0; p < n; ++p)
-          if (p != r) FLX_TRY(sem_wait_geq(L.d2h, w->sem(sem_rcons(r, p)), w->last_ar_pepoch));
+        FLX_TRY(take_region(w, L.d2h, r, /*result=*/true));
         FLX_CUDA(cudaMemcpyAsync(w->rregion(r), static_cast<char*>(recv[i]) + nv + r * q, q,
                                  cudaMemcpyDeviceToHost, L.d2h));
-        FLX_TRY(sem_write(L.d2h, w->sem(sem_rprod(r)), e));
+        for (int s = 1; s < n; ++s)
+          FLX_TRY(token_post(L.d2h, w->sem(sem_rprod(r, (r + s) % n))));
       }
-      // step 4: H2D every other rank's reduced sub-chunk
+      // step 4: H2D every other rank's reduced sub-chunk, return R_c's token
       for (int i = 0; i < nl; ++i) {
         World::Local& L = w->local[i];
         const int r = L.rank;
         for (int s = 1; s < n; ++s) {
           const int c = (r + s) % n;
-          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_rprod(c)), e));
+          FLX_TRY(token_accept(L.h2d, w->sem(sem_rprod(c, r))));
           FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + nv + c * q, w->rregion(c), q,
                                    cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_rcons(c, r)), e));
-        }
-        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
-      }
-      w->last_ar_pepoch = e;
-    } else {
-      // step 1: D2H my send slice into H_r (all readers of last call done)
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        FLX_TRY(wait_region_free(w, L.d2h, r, e));
-        FLX_CUDA(cudaMemcpyAsync(w->hregion(r), static_cast<const char*>(send[i]) + nv, pc,
-                                 cudaMemcpyDeviceToHost, L.d2h));
-        FLX_TRY(sem_write(L.d2h, w->sem(sem_gprod(r)), e));
-      }
-      // step 2: H2D every other rank's slice into its block; own block locally
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        char* own = static_cast<char*>(recv[i]) + (size_t)r * bytes + nv;
-        const char* mine = static_cast<const char*>(send[i]) + nv;
-        if (own != mine)
-          FLX_CUDA(cudaMemcpyAsync(own, mine, pc, cudaMemcpyDeviceToDevice, L.h2d));
-        for (int s = 1; s < n; ++s) {
-          const int c = (r - s + n) % n;
-          FLX_TRY(sem_wait_geq(L.h2d, w->sem(sem_gprod(c)), e));
-          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + (size_t)c * bytes + nv,
-                                   w->hregion(c), pc, cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(sem_write(L.h2d, w->sem(sem_cons(c, r)), e));
+          FLX_TRY(token_give(L.h2d, w->sem(sem_rfree(c, r))));
         }
         FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
       }
@@ -603,7 +546,13 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   }
   if (timed) FLX_CUDA(cudaEventRecord(tm[0]->nv, s0));
   if (pc > 0)
-    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaStreamWaitEvent(s0, ev_pcie(i), 0));
+    for (int i = 0; i < nl; ++i) {
+      FLX_CUDA(cudaStreamWaitEvent(s0, ev_pcie(i), 0));
+      // the D2H stream ends with token posts: join it too (a CUDA-graph
+      // capture must end with every forked stream joined)
+      FLX_CUDA(cudaEventRecord(w->local[i].ev_d2h_done, w->local[i].d2h));
+      FLX_CUDA(cudaStreamWaitEvent(s0, w->local[i].ev_d2h_done, 0));
+    }
   bool joined = false;
   for (int i = 1; i < nl; ++i) {
     if (streams[i] == s0) continue;

@@ -191,19 +191,53 @@ def test_loopback_cuda_graph_capture_and_replay():
                 np.testing.assert_array_equal(_np(a2a[r], 7), want_a2a[r])
 
 
-def test_loopback_capture_with_pcie_share_is_rejected():
-    n = 2
-    sends = [torch.randn(1 << 16, device="cuda") for _ in range(n)]
+def test_loopback_capture_with_pcie_share_replays():
+    # the PCIe path's token handshake uses constant values, so a striped
+    # multi-rank collective (NVLink + PCIe) is captured once and replayed,
+    # interleaved with eager calls, for all four protocols
+    n, count, g = 4, (1 << 18) + 64, (850, 150, 0)
+    gen = torch.Generator(device="cpu").manual_seed(21)
+    sends = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    ar = [torch.empty_like(s) for s in sends]
+    ag = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    ag_in = [s[:count] for s in sends]
+    rs = [torch.empty(count, device="cuda") for _ in range(n)]
+    a2a = [torch.empty_like(s) for s in sends]
     with flx.Clique(n, loopback=True) as w:
-        w.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        for op in CollectiveOp:
+            w.set_shares(op, g)
         stream = torch.cuda.Stream()
         graph = torch.cuda.CUDAGraph()
-        with pytest.raises(flx.FlexLinkError):
-            with torch.cuda.graph(graph, stream=stream):
-                w.all_reduce(sends, sends)
-        torch.cuda.synchronize()
-        w.all_reduce(sends, sends)  # still usable eagerly
-        torch.cuda.synchronize()
+        with torch.cuda.graph(graph, stream=stream):
+            w.all_reduce(sends, ar)
+            w.all_gather(ag_in, ag)
+            w.reduce_scatter(sends, rs)
+            w.all_to_all(sends, a2a)
+        assert w.path_bytes()[PathKind.PCIE_STAGED] > 0
+        aligns = {op: w.comms[0].alignment(op) for op in CollectiveOp}
+        for it in range(5):
+            host = [torch.randn(n * count, generator=gen) for _ in range(n)]
+            for s, h in zip(sends, host):
+                s.copy_(h)
+            if it % 2 == 0:
+                graph.replay()
+            else:
+                w.all_reduce(sends, ar)
+                w.all_gather(ag_in, ag)
+                w.reduce_scatter(sends, rs)
+                w.all_to_all(sends, a2a)
+            torch.cuda.synchronize()
+            hn = [h.numpy() for h in host]
+            want_ar = oracle.allreduce(hn, 7, 0, g, aligns[CollectiveOp.ALLREDUCE])
+            want_ag = oracle.allgather([x[:count] for x in hn], 7, g,
+                                       aligns[CollectiveOp.ALLGATHER])
+            want_rs = oracle.reducescatter(hn, 7, 0, g, aligns[CollectiveOp.REDUCESCATTER])
+            want_a2a = oracle.alltoall(hn, 7, g, aligns[CollectiveOp.ALLTOALL])
+            for r in range(n):
+                np.testing.assert_array_equal(_np(ar[r], 7), want_ar[r], err_msg=f"it {it}")
+                np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
+                np.testing.assert_array_equal(_np(rs[r], 7), want_rs[r])
+                np.testing.assert_array_equal(_np(a2a[r], 7), want_a2a[r])
 
 
 def test_loopback_varying_sizes_multi_round():

@@ -349,46 +349,71 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   cta_epochs_done(ep, k, prev_outbox, prev_main);
 }
 
-// One-shot AllReduce for small messages: push my part of the whole message
-// into every peer's small inbox (parity e & 1, slot r), signal kArrive(e),
-// wait for every peer's kArrive(e), fold the n copies in rank order into recv.
-// One release and one wait per call instead of three of each (the two-shot
-// protocol's latency is its three flag hops, tools/rank_phases.cu).  Reuse
-// of the parity region needs no flag: its last readers ran round e-2, and in
-// round e-1 this CTA awaited every peer's kArrive(e-1), which that peer
+// One-shot protocols for small slices (RankArgs::oneshot): one release and one
+// wait per call.  Every rank pushes its pieces into the peers' small inboxes
+// (parity e & 1, slot = source rank, this CTA's region), signals kArrive(e),
+// waits for every peer's kArrive(e), then finishes locally:
+//   KIND 0 AllReduce      push my part of the whole message to every peer,
+//                         fold the n copies in rank order into recv
+//   KIND 1 AllGather      push my slice to every peer, land each peer's slice
+//                         in its recv block
+//   KIND 2 ReduceScatter  push block c to peer c, fold my block's n copies
+//   KIND 3 AllToAll       push block c to peer c, land peer p's block in recv
+//                         block p
+// The two-shot AllReduce spends three signal hops and the slot protocols two
+// (kArrive, then kFree); a signal costs ~1.5-2 us (tools/rank_phases.cu).
+// Reuse of the parity region needs no flag: its last readers ran round e-2,
+// and in round e-1 this CTA awaited every peer's kArrive(e-1), which that peer
 // signalled after finishing round e-2 (every protocol awaits kArrive from
 // every peer every round).  The main slots are untouched, so last_main stays.
-template <typename T, int OP>
-__device__ void rank_allreduce_oneshot(const RankArgs& a, int cta, int nctas) {
+template <typename T, int OP, int KIND>
+__device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
   FLX_PHASE(0);
   const int r = a.rank, n = a.nranks;
   const CtaEpochs ep = cta_epochs(a, cta);
   const uint32_t e = ep.first;
   const size_t mine = (size_t)cta * cta_sub(a.small_slot);
   const size_t region = a.slot * (n + 1) + (size_t)(e & 1) * n * a.small_slot;
+  const size_t stride = a.rank_stride;
   size_t lo, hi;
   cta_part(a.bytes, nctas, cta, &lo, &hi);
+  auto inbox = [&](int holder, int src) {
+    return a.scratch[holder] + region + (size_t)src * a.small_slot + mine;
+  };
   FLX_PHASE(1);
   {
     uint32_t* targets[kMaxRanks];
     int nt = 0;
     for (int s = 1; s < n; ++s) {
       const int c = (r + s) % n;
-      cta_copy(a.scratch[c] + region + (size_t)r * a.small_slot + mine, a.send + lo, hi - lo,
-               false);
+      const char* piece = (KIND == 0 || KIND == 1) ? a.send + lo : a.send + (size_t)c * stride + lo;
+      cta_copy(inbox(c, r), piece, hi - lo, false);
       targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+    }
+    if (KIND == 1) {
+      char* own = a.recv + (size_t)r * stride + lo;
+      if (own != a.send + lo) cta_copy(own, a.send + lo, hi - lo, false);
+    } else if (KIND == 3) {
+      cta_copy(a.recv + (size_t)r * stride + lo, a.send + (size_t)r * stride + lo, hi - lo, false);
     }
     cta_signal(targets, nt, e);
   }
   FLX_PHASE(2);
   if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
   FLX_PHASE(3);
-  {
+  if (KIND == 0 || KIND == 2) {
     const char* src[kMaxRanks];
     for (int p = 0; p < n; ++p)
-      src[p] = (p == r) ? a.send + lo : a.scratch[r] + region + (size_t)p * a.small_slot + mine;
+      src[p] = p != r      ? inbox(r, p)
+               : KIND == 0 ? a.send + lo
+                           : a.send + (size_t)r * stride + lo;
     char* dst[1] = {a.recv + lo};
     cta_fold<T, OP>(dst, 1, src, n, hi - lo);
+  } else {
+    for (int s = 1; s < n; ++s) {
+      const int p = (r - s + n) % n;
+      cta_copy(a.recv + (size_t)p * stride + lo, inbox(r, p), hi - lo, true);
+    }
   }
   FLX_PHASE(4);
   cta_epochs_done(ep, 1, ep.last_ar, ep.last_main);
@@ -533,42 +558,48 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
 }
 
 __global__ void __launch_bounds__(512) rank_alltoall_kernel(const RankArgs a) {
-  rank_alltoall(a, blockIdx.x, gridDim.x);
+  if (a.oneshot) rank_oneshot<float, kSum, 3>(a, blockIdx.x, gridDim.x);
+  else rank_alltoall(a, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(512) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
-  rank_alltoall(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 3>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  else rank_alltoall(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
-  if (a.oneshot) rank_allreduce_oneshot<T, OP>(a, blockIdx.x, gridDim.x);
+  if (a.oneshot) rank_oneshot<T, OP, 0>(a, blockIdx.x, gridDim.x);
   else rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) rank_reducescatter_kernel(const RankArgs a) {
-  rank_reducescatter<T, OP>(a, blockIdx.x, gridDim.x);
+  if (a.oneshot) rank_oneshot<T, OP, 2>(a, blockIdx.x, gridDim.x);
+  else rank_reducescatter<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
-  rank_allgather(a, blockIdx.x, gridDim.x);
+  if (a.oneshot) rank_oneshot<float, kSum, 1>(a, blockIdx.x, gridDim.x);
+  else rank_allgather(a, blockIdx.x, gridDim.x);
 }
 
 // Loopback: blockIdx.y is the rank; cooperative launch (all CTAs co-resident).
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
-  if (a.r[blockIdx.y].oneshot) rank_allreduce_oneshot<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  if (a.r[blockIdx.y].oneshot) rank_oneshot<T, OP, 0>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
 __global__ void __launch_bounds__(512) loopback_reducescatter_kernel(const __grid_constant__ LoopbackArgs a) {
-  rank_reducescatter<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  if (a.r[blockIdx.y].oneshot) rank_oneshot<T, OP, 2>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  else rank_reducescatter<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 __global__ void __launch_bounds__(512) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
-  rank_allgather(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 1>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
+  else rank_allgather(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 }  // namespace flx

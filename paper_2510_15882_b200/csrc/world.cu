@@ -528,10 +528,13 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.rank_stride = bytes;
       a.slot = w->slot;
       a.small_slot = w->small_slot;
-      // one-shot when the slice fits both the threshold and this grid's
-      // share of the one-shot inbox (every CTA part <= its region)
-      a.oneshot = !gather && !scatter && !a2a && n > 1 && nv <= w->oneshot_max &&
-                  nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas;
+      // one-shot when the slice fits this grid's share of the one-shot inbox
+      // (every CTA part <= its region); AllReduce also below FLX_ONESHOT_KB
+      // (above it the two-shot's 2(N-1)/N traffic wins), the other protocols
+      // move the same bytes either way and save a signal hop
+      a.oneshot = w->oneshot_max > 0 && n > 1 &&
+                  nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas &&
+                  (gather || scatter || a2a || nv <= w->oneshot_max);
       a.abort_word = w->abort_word;
       a.spin_limit = w->spin_limit;
     }

@@ -116,3 +116,65 @@ def test_peer_timeout_aborts_instead_of_hanging():
         code, waited, async_err = out[0]
     assert code == 3 and async_err == 3, (code, async_err)
     assert 0.5 < waited < 30, waited
+
+
+def _pcie_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FLX_ALLOW_SHARED_GPU="1",
+                      FLX_SLOT_MB="1", FLX_PCIE_STAGE_MB="8", FLX_BOOT_TIMEOUT="60")
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2510_15882_b200 import comm
+        from paper_2510_15882_b200.striping import CollectiveOp
+
+        c = comm.Communicator.from_process_group()
+        for op in CollectiveOp:  # PCIe only: no NVLink-path kernel, so nothing on
+            c.set_shares(op, (0, 1000, 0))  # this shared GPU spins on a peer
+        count = 1 << 18  # a multiple of the alignment: the whole message is on PCIe
+
+        def data(r, n_elems):
+            return (torch.arange(n_elems, dtype=torch.float32) * (r + 1)) % 251 - 100
+
+        res = {}
+        for it in range(3):  # repeated calls reuse the host regions (token handshake)
+            x = data(rank + it, count).cuda()
+            ar = torch.empty_like(x)
+            c.all_reduce(x, ar)
+            ag = torch.empty(world * count, device="cuda")
+            c.all_gather(x, ag)
+            big = data(rank + it, world * count).cuda()
+            rs = torch.empty(count, device="cuda")
+            c.reduce_scatter(big, rs)
+            a2a = torch.empty_like(big)
+            c.all_to_all(big, a2a)
+            torch.cuda.synchronize()
+            xs = [data(r + it, count) for r in range(world)]
+            bigs = [data(r + it, world * count) for r in range(world)]
+            ok = torch.equal(ar.cpu(), sum(xs)) and torch.equal(ag.cpu(), torch.cat(xs))
+            ok = ok and torch.equal(rs.cpu(), sum(b[rank * count:(rank + 1) * count] for b in bigs))
+            ok = ok and torch.equal(a2a.cpu(), torch.cat(
+                [bigs[p][rank * count:(rank + 1) * count] for p in range(world)]))
+            res[it] = bool(ok)
+        res["pcie_bytes"] = c.path_bytes()[1]
+        out[rank] = res
+        dist.barrier()
+        c.destroy()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_process_pcie_only_collectives():
+    # The host-hub PCIe path across two real processes (shared cudaHostRegister'ed
+    # segment, token words written and awaited by different processes).  Only
+    # copy engines, stream memory ops and non-waiting fold kernels run, so the
+    # two processes may share this GPU.
+    from paper_2510_15882_b200.build import build
+
+    build()
+    with mp.Manager() as m:
+        out = m.dict()
+        mp.spawn(_pcie_worker, args=(2, _port(), out), nprocs=2, join=True)
+        res = dict(out)
+    for rank in range(2):
+        assert all(res[rank][it] for it in range(3)), res[rank]
+        assert res[rank]["pcie_bytes"] > 0

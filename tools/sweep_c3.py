@@ -17,7 +17,10 @@ from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
 p = argparse.ArgumentParser()
 p.add_argument("--ranks", default="2,4,8")
 p.add_argument("--max-mib", type=int, default=1024)
-p.add_argument("--steps", type=int, default=20)
+p.add_argument("--steps", type=int, default=50)
+p.add_argument("--warmup", type=int, default=20)
+p.add_argument("--trace-dir", default="", help="write each cell's Stage-1 trace (reference "
+               "JSONL schema, tuner.py:229-253) here")
 p.add_argument("--nvlink-ctas", type=int, default=0)
 p.add_argument("--loopback", action="store_true",
                help="the multi-GPU engine emulated on one GPU, NVLink path only (no tuning)")
@@ -40,7 +43,7 @@ for n in [int(x) for x in a.ranks.split(",")]:
                 shares, trace, tuned, base = flx.tune_shares(cl, topo, CollectiveOp.ALLREDUCE,
                                                              s, r, TunerConfig(), warmup=1,
                                                              repeats=3)
-            for _ in range(3):
+            for _ in range(a.warmup):
                 cl.all_reduce(s, r)
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -61,6 +64,12 @@ for n in [int(x) for x in a.ranks.split(",")]:
                     "iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
                     "nvlink_only_ms": round(base * 1e3, 4),
                     "trace": [x.action for x in trace.records]}}), flush=True)
+            if a.trace_dir and trace is not None:
+                from paper_2510_15882_b200.stage1 import write_trace
+
+                os.makedirs(a.trace_dir, exist_ok=True)
+                with open(os.path.join(a.trace_dir, f"n{n}_{name}_{mib}MiB.jsonl"), "w") as fh:
+                    write_trace(trace, fh, fmt="jsonl")
             del s, r
             mib *= 2
     cl.destroy()

@@ -49,6 +49,18 @@ def busbw_allgather(out_bytes: int, seconds: float, n: int) -> float:
     return out_bytes / seconds * (n - 1) / n / 1e9
 
 
+PCIE_H2D_GBS = 55.5  # measured pinned H2D on this pool (profiles/r1/pcie_bidir.json)
+
+
+def link_roofline(busbw: float, pcie_gbs: float | None) -> dict:
+    """The north star's aggregate-link roofline: 900 GB/s/dir NVLink 5 + measured PCIe
+    Gen5 + NIC (absent)."""
+    pcie = round(pcie_gbs if pcie_gbs else PCIE_H2D_GBS, 1)
+    peak = 900.0 + pcie
+    return {"nvlink_gbs": 900.0, "pcie_gbs": pcie, "nic_gbs": 0.0, "peak": round(peak, 1),
+            "achieved": round(busbw, 2), "frac": round(busbw / peak, 4)}
+
+
 def ncu_traffic(summary: str = "profiles/r1/fold_once_ncu_summary.txt"):
     """dram read + write bytes per launch of the dominant kernel, from the
     committed ``ncu --set full`` capture of the same workload (None if absent)."""
@@ -266,8 +278,9 @@ def run_single_gpu(args) -> None:
         topo, probe_raw = probe_topology(nranks=n, name="probed-b200-virtual8")
         link_profile = {"yaml": topology_to_yaml(topo), "raw": probe_raw}
         link_bidir = probe_raw["pcie"]["bidir_each"]  # B/s per direction, both busy
+        pcie_h2d = probe_raw["pcie"]["h2d"] / 1e9
     except Exception as e:  # keep the bench alive; fall back to the nominal preset
-        link_bidir = None
+        link_bidir = pcie_h2d = None
         topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
         link_profile = {"error": str(e), "fallback": "preset B200"}
 
@@ -456,6 +469,9 @@ def run_single_gpu(args) -> None:
             "kernel_ms": round(nv_ms, 4),
             "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650",
         },
+        "link_roofline": {**link_roofline(value, pcie_h2d), "note": "at N=1 the NVLink path is "
+                          "an on-GPU fold bound by HBM (see roofline); this is the north star's "
+                          "multi-GPU denominator"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": n * AR_BYTES, "d2h_bytes_per_step": n * AR_BYTES,
@@ -483,6 +499,7 @@ def run_single_gpu(args) -> None:
             "kernel_algorithmic_bytes": ag_alg,
             "kernel_traffic": ncu_traffic("profiles/r1/fanout_once_ncu_summary.txt"),
             "paper_convention_algbw": round(AG_OUT_BYTES / n / ag_dt / 1e9, 2),
+            "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, n), pcie_h2d),
         },
     }
     clique.destroy()
@@ -746,7 +763,9 @@ def run_multi_gpu(args) -> None:
                 "traffic_share_pct": {k.short: round(100 * ag_bytes[k] / (AG_OUT_BYTES // world), 3)
                                       for k in PathKind},
                 "nccl": round(busbw_allgather(AG_OUT_BYTES, ag_nccl_dt, world), 2),
-                "matches_nccl_bitwise": bool(ag_ok)},
+                "matches_nccl_bitwise": bool(ag_ok),
+                "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, world), None)},
+            "link_roofline": link_roofline(value, None),
         }), flush=True)
     dist.barrier()
     c.destroy()

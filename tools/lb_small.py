@@ -1,4 +1,4 @@
-"""8-rank loopback AllReduce of 4 KiB per rank, repeated (for ncu launch timing)."""
+"""8-rank loopback AllReduce (LB_BYTES per rank, default 4 KiB), repeated — for ncu."""
 import os
 import sys
 
@@ -9,7 +9,7 @@ from paper_2510_15882_b200 import comm as flx  # noqa: E402
 
 n = int(os.environ.get("LB_RANKS", "8"))
 cl = flx.Clique(n, loopback=True)
-s = [torch.randn(1024, device="cuda") for _ in range(n)]
+s = [torch.randn(int(os.environ.get("LB_BYTES", "4096")) // 4, device="cuda") for _ in range(n)]
 r = [torch.empty_like(x) for x in s]
 for _ in range(int(os.environ.get("LB_CALLS", "30"))):
     cl.all_reduce(s, r)

@@ -420,8 +420,11 @@ def run_single_gpu(args) -> None:
     loop.all_reduce(sends, recvs)
     torch.cuda.synchronize()
     assert all(torch.equal(r, exact) for r in recvs), "loopback striped allreduce mismatch"
+    loop_alg = int(n * (5 - 2 / n) * AR_BYTES)  # push 2(n-1)/n S + fold (1+2/n) S + pull 2(n-1)/n S
     loopback = {"busbw": round(busbw_allreduce(AR_BYTES, loop_dt, n), 2),
                 "ms_per_step": round(loop_dt * 1e3, 4),
+                "hbm_algorithmic_bytes": loop_alg,
+                "hbm_frac": round(loop_alg / loop_dt / 1e9 / hbm_peak, 4),
                 "note": "8 ranks of the one-process-per-GPU engine sharing one GPU's HBM "
                         "(push/reduce/pull through peer-mapped scratch; 3 HBM passes)"}
     loop.destroy()

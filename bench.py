@@ -301,6 +301,13 @@ def run_single_gpu(args) -> None:
             if ev is not None and ev.moved:
                 clique.set_shares(CollectiveOp.ALLREDUCE, balancer.shares, AR_BYTES)
     shares = balancer.shares
+    # the reference's closed-form model (simulate_collective, collectives.py:136-186) on
+    # the probed link profile, for the split that runs: predicted vs measured per path
+    from paper_2510_15882_b200.striping import CollectiveSpec, simulate_collective
+
+    pred = simulate_collective(topo, CollectiveSpec(CollectiveOp.ALLREDUCE, n, AR_BYTES), shares,
+                               alignment=clique.comms[0].alignment(CollectiveOp.ALLREDUCE))
+    model_ms = {k.short: round(v * 1e3, 4) for k, v in pred.durations.items()}
 
     def step():
         clique.all_reduce(sends, recvs)
@@ -452,6 +459,8 @@ def run_single_gpu(args) -> None:
         "path_bytes": {k.short: pbytes[k] for k in PathKind},
         "traffic_share_pct": {k.short: round(100 * pbytes[k] / total, 3) for k in PathKind},
         "path_ms": {"nvlink": round(nv_ms, 4), "pcie": round(pc_ms, 4), "rdma": None},
+        "model_path_ms": {**model_ms, "source": "linkstripe simulate_collective on the probed "
+                                                "link profile (the reference's predictor)"},
         "rdma": "absent (no NIC / rdma-core in this image)",
         "stage1": {"iterations": trace.iterations, "converged": trace.converged,
                    "tuned_total_ms": round(tuned_s * 1e3, 4),

@@ -495,6 +495,8 @@ def run_single_gpu(args) -> None:
         "gpu_launches": launches,
         "clocks": clocks,
         "nccl": None,
+        "nccl_note": "NCCL cannot place 8 ranks on one GPU (duplicate device); the N>1 line "
+                     "(torchrun, one process per GPU) times NCCL on the same box",
         "torch_unfused_baseline": torch_base,
         "link_profile": link_profile,
         "config4": cfg4,

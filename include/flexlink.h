@@ -99,7 +99,7 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId commId, int
 flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist);
 /* All nranks ranks of a flxCommInitRank-style world emulated on ONE device:
  * the multi-rank engine (peer-mapped scratch + flags kernels, host-hub PCIe
- * staging with cross-rank counter semaphores) with every peer pointer local
+ * staging with cross-rank token handshakes) with every peer pointer local
  * and the NVLink-path kernel launched cooperatively over all ranks.  Driven
  * like flxCommInitAll (one group per collective).  For testing the N-GPU code
  * path on a single GPU; set CUDA_DEVICE_MAX_CONNECTIONS>=3*nranks+1. */

@@ -1,6 +1,7 @@
 """Seeded random sweep: collective x executor x dtype x op x shares x size x in-place,
 each checked bit-for-bit against the CPU oracle (complements the hand-picked cases)."""
 
+import os
 import random
 
 import numpy as np
@@ -15,9 +16,10 @@ from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
 
 from test_gpu_parity import OPS, TORCH_DT, _inputs, _np  # noqa: E402
 
-RNG = random.Random(20261018)
+# FLX_FUZZ_CASES / FLX_FUZZ_SEED widen the sweep for soak runs (default: 48 cases)
+RNG = random.Random(int(os.environ.get("FLX_FUZZ_SEED", "20261018")))
 CASES = []
-for i in range(48):
+for i in range(int(os.environ.get("FLX_FUZZ_CASES", "48"))):
     coll = RNG.choice(["allreduce", "allgather", "reducescatter", "alltoall"])
     n = RNG.choice([2, 3, 4, 5, 8])
     dtype = RNG.choice([0, 2, 6, 7, 8, 9])

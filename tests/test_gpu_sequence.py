@@ -54,7 +54,9 @@ def test_random_sequence_on_one_communicator(loopback, n):
         del os.environ["FLX_SLOT_MB"]
     pending = []
     with c:
-        for i, (coll, dtype, op, count, g, inplace, untimed) in enumerate(_plan(7 + 2 * loopback + n, 80)):
+        calls = int(os.environ.get("FLX_SEQ_CALLS", "80"))  # soak runs raise it
+        for i, (coll, dtype, op, count, g, inplace, untimed) in enumerate(
+                _plan(7 + 2 * loopback + n, calls)):
             c.set_shares(CollectiveOp(coll), g)
             c.set_timing(not untimed)
             align = c.comms[0].alignment(CollectiveOp(coll))
@@ -88,7 +90,7 @@ def test_random_sequence_on_one_communicator(loopback, n):
                 want = lambda cpu=cpu, dtype=dtype, op=op, g=g, align=align: \
                     oracle.reducescatter([_np(h, dtype) for h in cpu], dtype, OPS[op], g, align)
             pending.append((i, coll, r, dtype, want, s))  # keep s alive until checked
-            if len(pending) == 6 or i == 79:  # several calls in flight between checks
+            if len(pending) == 6 or i == calls - 1:  # several calls in flight between checks
                 torch.cuda.synchronize()
                 for j, cl, rr, dt, wf, _ in pending:
                     w = wf()

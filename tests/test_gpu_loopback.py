@@ -336,3 +336,26 @@ def test_timing_off_keeps_results_and_zeroes_path_times(loopback):
         torch.cuda.synchronize()
         t = w.comms[0].path_times()
         assert t[PathKind.NVLINK] > 0 and t[PathKind.PCIE_STAGED] > 0
+
+
+@pytest.mark.parametrize("count", [1000, (1 << 18) + 4])  # one-shot and two-shot
+def test_loopback_sixteen_ranks(count):
+    # the widest world (kMaxRanks): 15 peers per flag wait / signal warp
+    n, g = 16, (950, 50, 0)
+    cpu = _inputs(n, count, 7, 16)
+    sends = [c.cuda() for c in cpu]
+    recvs = [torch.empty_like(s) for s in sends]
+    ag = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, g)
+        w.set_shares(CollectiveOp.ALLGATHER, g)
+        w.all_reduce(sends, recvs)
+        w.all_gather(sends, ag)
+        torch.cuda.synchronize()
+        want = oracle.allreduce([c.numpy() for c in cpu], 7, 0, g,
+                                w.comms[0].alignment(CollectiveOp.ALLREDUCE))
+        want_ag = oracle.allgather([c.numpy() for c in cpu], 7, g,
+                                   w.comms[0].alignment(CollectiveOp.ALLGATHER))
+    for r in range(n):
+        np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
+        np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])

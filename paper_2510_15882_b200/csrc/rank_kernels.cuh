@@ -1,16 +1,19 @@
-// Multi-rank NVLink-path kernels: one launch per rank per round, CTA b of
+// Multi-rank NVLink-path kernels: one launch per rank per call, CTA b of
 // rank r exchanging with CTA b of every peer over NVSwitch through
 // peer-mapped (CUDA IPC) scratch buffers and release/acquire flags.
 //
-// AllReduce = reduce-scatter + all-gather in one launch:
+// Two-shot AllReduce = reduce-scatter + all-gather in one launch, per round:
 //   1 push   rank r stores its chunk c to peer c's inbox[r]           (NVLink write)
 //   2 reduce rank r folds inbox[0..N) (own chunk read in place) in rank
 //            order -> recv chunk r and its own outbox                  (local HBM)
 //   3 pull   rank r loads every peer's outbox into recv chunk c         (NVLink read)
-// AllGather: push own slice to every peer's inbox[r]; copy inbox -> recv.
-// Flags (per receiving rank): arrive/ready/done[src][cta], monotone epochs,
-// compared cyclically; the same fold rule as kernels.cuh (bit-identical to the
-// virtual-rank path and the CPU oracle).
+// Slot protocols (AllGather / ReduceScatter / AllToAll): push, wait, land or
+// fold, free.  One-shot variants of all four (rank_oneshot) for small slices:
+// push into the peers' double-buffered one-shot inboxes, one wait, finish locally.
+// Flags (per receiving rank): arrive/free/ready/pulled[src][cta], monotone
+// per-CTA epochs kept on the device (cta_epochs), compared cyclically; every
+// CTA owns one fixed region of each slot (cta_sub).  The fold rule is
+// kernels.cuh's (bit-identical to the virtual-rank path and the CPU oracle).
 //
 // The same device code runs (a) per GPU with grid = nctas, (b) in loopback
 // (all ranks on one GPU, grid = nctas x nranks, cooperative launch so every

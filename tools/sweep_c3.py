@@ -1,4 +1,4 @@
-"""BASELINE config 3: AllReduce fp32/bf16 message-size sweep 1 MiB - 1 GiB at N = 2/4/8
+"""BASELINE config 3: AllReduce (or --op allgather) fp32/bf16 message-size sweep 1 MiB - 1 GiB at N = 2/4/8
 (virtual ranks on one GPU), Stage 1 on the real path per size bucket (+ guard), per-link
 traffic split and the Stage-1 trace.  One JSON line per cell."""
 import argparse
@@ -22,6 +22,8 @@ p.add_argument("--warmup", type=int, default=20)
 p.add_argument("--trace-dir", default="", help="write each cell's Stage-1 trace (reference "
                "JSONL schema, tuner.py:229-253) here")
 p.add_argument("--nvlink-ctas", type=int, default=0)
+p.add_argument("--op", choices=["allreduce", "allgather"], default="allreduce",
+               help="allgather: S is the gathered size (S/N sent per rank), nccl-tests busbw")
 p.add_argument("--loopback", action="store_true",
                help="the multi-GPU engine emulated on one GPU, NVLink path only (no tuning)")
 a = p.parse_args()
@@ -34,32 +36,36 @@ for n in [int(x) for x in a.ranks.split(",")]:
         mib = 1
         while mib <= a.max_mib:
             S = mib << 20
-            s = [torch.randn(S // esz, device="cuda").to(dt) for _ in range(n)]
-            r = [torch.empty_like(x) for x in s]
+            gather = a.op == "allgather"
+            cop = CollectiveOp.ALLGATHER if gather else CollectiveOp.ALLREDUCE
+            per = S // esz // n if gather else S // esz
+            s = [torch.randn(per, device="cuda").to(dt) for _ in range(n)]
+            r = [torch.empty(per * n if gather else per, device="cuda", dtype=dt) for _ in range(n)]
+            run = (lambda: cl.all_gather(s, r)) if gather else (lambda: cl.all_reduce(s, r))
             if a.loopback:
                 shares, trace = flx.ShareDistribution({PathKind.NVLINK: 1000}), None
-                cl.set_shares(CollectiveOp.ALLREDUCE, shares)
+                cl.set_shares(cop, shares)
             else:
-                shares, trace, tuned, base = flx.tune_shares(cl, topo, CollectiveOp.ALLREDUCE,
-                                                             s, r, TunerConfig(), warmup=1,
-                                                             repeats=3)
+                shares, trace, tuned, base = flx.tune_shares(cl, topo, cop, s, r, TunerConfig(),
+                                                             warmup=1, repeats=3)
             for _ in range(a.warmup):
-                cl.all_reduce(s, r)
+                run()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             for _ in range(a.steps):
-                cl.all_reduce(s, r)
+                run()
             e1.record()
             torch.cuda.synchronize()
             t = e0.elapsed_time(e1) / a.steps * 1e-3
             b = cl.path_bytes()
             print(json.dumps({
-                "executor": "loopback" if a.loopback else "virtual",
+                "executor": "loopback" if a.loopback else "virtual", "op": a.op,
                 "n": n, "dtype": name, "size_mib": mib, "ms": round(t * 1e3, 4),
-                "busbw": round(S / t * 2 * (n - 1) / n / 1e9, 2),
+                "busbw": round(S / t * ((n - 1) / n if gather else 2 * (n - 1) / n) / 1e9, 2),
                 "shares": {k.short: shares.get(k) for k in PathKind},
-                "traffic_pct": {k.short: round(100 * b[k] / S, 3) for k in PathKind},
+                "traffic_pct": {k.short: round(100 * b[k] / (S // n if gather else S), 3)
+                                for k in PathKind},
                 "stage1": None if trace is None else {
                     "iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
                     "nvlink_only_ms": round(base * 1e3, 4),
@@ -68,7 +74,8 @@ for n in [int(x) for x in a.ranks.split(",")]:
                 from paper_2510_15882_b200.stage1 import write_trace
 
                 os.makedirs(a.trace_dir, exist_ok=True)
-                with open(os.path.join(a.trace_dir, f"n{n}_{name}_{mib}MiB.jsonl"), "w") as fh:
+                tag = "ag_" if gather else ""
+                with open(os.path.join(a.trace_dir, f"{tag}n{n}_{name}_{mib}MiB.jsonl"), "w") as fh:
                     write_trace(trace, fh, fmt="jsonl")
             del s, r
             mib *= 2

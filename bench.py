@@ -412,8 +412,38 @@ def run_single_gpu(args) -> None:
         for q in range(n):
             assert torch.equal(ag_recv[r][q * ag_count:(q + 1) * ag_count], ag_send[q])
 
-    cfg4 = run_config4(clique, sends, recvs, topo, args, stream) if not args.skip_config4 else None
     del ag_send, ag_recv
+
+    # ---- ReduceScatter / AllToAll fp32 on the same 8 x 256 MiB inputs
+    blk = count // n
+    extra = {}
+    rs_recv = [torch.empty(blk, device="cuda") for _ in range(n)]
+    a2a_recv = [torch.empty_like(x) for x in sends]
+    for name, cop, run, alg in (
+            ("reducescatter", CollectiveOp.REDUCESCATTER,
+             lambda: clique.reduce_scatter(sends, rs_recv), (n + 1) * AR_BYTES),
+            ("alltoall", CollectiveOp.ALLTOALL, lambda: clique.all_to_all(sends, a2a_recv),
+             2 * n * AR_BYTES)):
+        clique.set_shares(cop, (1000, 0, 0), AR_BYTES)
+        for _ in range(args.warmup):
+            run()
+        dt_c = _time_steps(run, args.steps, stream)
+        hist = clique.comms[0].path_times_history(min(args.steps, 64))
+        k_ms = statistics.mean(h[PathKind.NVLINK] for h in hist) * 1e3
+        extra[name] = {"value": round(AR_BYTES / dt_c * (n - 1) / n / 1e9, 2), "unit": "GB/s",
+                       "dtype": "f32", "send_bytes_per_rank": AR_BYTES,
+                       "ms_per_step": round(dt_c * 1e3, 4),
+                       "busbw": "(S_send/t)*(N-1)/N (nccl-tests)",
+                       "kernel_algorithmic_bytes": alg,
+                       "kernel_frac_hbm": round(alg / (k_ms * 1e-3) / 1e9 / hbm_peak, 4)}
+    for r in range(n):
+        assert torch.equal(rs_recv[r], exact[r * blk:(r + 1) * blk]), "reduce_scatter mismatch"
+        for q in range(n):
+            assert torch.equal(a2a_recv[r][q * blk:(q + 1) * blk],
+                               sends[q][r * blk:(r + 1) * blk]), "all_to_all mismatch"
+    del rs_recv, a2a_recv
+
+    cfg4 = run_config4(clique, sends, recvs, topo, args, stream) if not args.skip_config4 else None
     cfg5 = run_config5(clique, topo, stream) if not args.skip_config5 else None
 
     # ---- the multi-GPU engine (flxCommInitRank code path) emulated on this GPU
@@ -502,6 +532,7 @@ def run_single_gpu(args) -> None:
         "config4": cfg4,
         "config5": cfg5,
         "loopback_engine": loopback,
+        **extra,
         "allgather": {
             "value": round(busbw_allgather(AG_OUT_BYTES, ag_dt, n), 2), "unit": "GB/s",
             "dtype": "bf16", "out_bytes": AG_OUT_BYTES, "ms_per_step": round(ag_dt * 1e3, 4),

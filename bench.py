@@ -795,6 +795,29 @@ def run_multi_gpu(args) -> None:
     ag_ref = torch.empty_like(ag_recv)
     ag_nccl_dt = timed(lambda: dist.all_gather_into_tensor(ag_ref, ag_send))
     ag_ok = torch.equal(ag_recv, ag_ref)
+    del ag_send, ag_recv, ag_ref
+
+    # ReduceScatter / AllToAll fp32 on the AllReduce inputs (8(f) row 4), NCCL beside
+    extra = {}
+    blk = count // world
+    rs_out, rs_ref = torch.empty(blk, device="cuda"), torch.empty(blk, device="cuda")
+    a2a_out, a2a_ref = torch.empty_like(send), torch.empty_like(send)
+    for name, cop, ours, theirs in (
+            ("reducescatter", CollectiveOp.REDUCESCATTER,
+             lambda: c.reduce_scatter(send, rs_out),
+             lambda: dist.reduce_scatter_tensor(rs_ref, send)),
+            ("alltoall", CollectiveOp.ALLTOALL, lambda: c.all_to_all(send, a2a_out),
+             lambda: dist.all_to_all_single(a2a_ref, send))):
+        c.set_shares(cop, ShareDistribution({PathKind.NVLINK: 1000}), AR_BYTES)
+        dt_c = timed(ours)
+        dt_n = timed(theirs)
+        same = torch.equal(rs_out, rs_ref) if cop == CollectiveOp.REDUCESCATTER else \
+            torch.equal(a2a_out, a2a_ref)
+        extra[name] = {"value": round(AR_BYTES / dt_c * (world - 1) / world / 1e9, 2),
+                       "unit": "GB/s", "dtype": "f32", "ms_per_step": round(dt_c * 1e3, 4),
+                       "nccl": round(AR_BYTES / dt_n * (world - 1) / world / 1e9, 2),
+                       "matches_nccl_bitwise": bool(same)}
+    del rs_out, rs_ref, a2a_out, a2a_ref
     if rank == 0:
         value = busbw_allreduce(AR_BYTES, dt, world) * 1.0
         print(json.dumps({
@@ -828,6 +851,7 @@ def run_multi_gpu(args) -> None:
                 "nccl": round(busbw_allgather(AG_OUT_BYTES, ag_nccl_dt, world), 2),
                 "matches_nccl_bitwise": bool(ag_ok),
                 "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, world), None)},
+            **extra,
             "link_roofline": link_roofline(value, None),
         }), flush=True)
     dist.barrier()

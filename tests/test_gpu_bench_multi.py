@@ -32,3 +32,5 @@ def test_run_multi_gpu_path_smoke():
     assert line["n_gpus"] == 1 and line["result_matches_exact_sum"] is True
     assert line["e2e"]["result_exact"] is True and line["allgather"]["matches_nccl_bitwise"]
     assert line["gpu_launches"] > 0 and "clocks" in line
+    for name in ("reducescatter", "alltoall"):
+        assert line[name]["matches_nccl_bitwise"] is True, line[name]

@@ -12,7 +12,8 @@ from paper_2510_15882_b200 import comm as flx  # noqa: E402
 from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
 
 p = argparse.ArgumentParser()
-p.add_argument("--op", default="allreduce", choices=["allreduce", "allgather"])
+p.add_argument("--op", default="allreduce",
+               choices=["allreduce", "allgather", "reducescatter", "alltoall"])
 p.add_argument("--steps", type=int, default=3)
 p.add_argument("--shares", default="1000,0,0")
 p.add_argument("--ranks", type=int, default=8)
@@ -27,6 +28,17 @@ if a.op == "allreduce":
     r = [torch.empty_like(x) for x in s]
     clique.set_shares(CollectiveOp.ALLREDUCE, shares)
     run = lambda: clique.all_reduce(s, r)  # noqa: E731
+elif a.op in ("reducescatter", "alltoall"):  # fp32, a.mib MiB sent per rank
+    count = a.mib * (1 << 20) // 4
+    s = [torch.randn(count, device="cuda") for _ in range(n)]
+    if a.op == "reducescatter":
+        r = [torch.empty(count // n, device="cuda") for _ in range(n)]
+        clique.set_shares(CollectiveOp.REDUCESCATTER, shares)
+        run = lambda: clique.reduce_scatter(s, r)  # noqa: E731
+    else:
+        r = [torch.empty_like(x) for x in s]
+        clique.set_shares(CollectiveOp.ALLTOALL, shares)
+        run = lambda: clique.all_to_all(s, r)  # noqa: E731
 else:
     count = a.mib * (1 << 20) // 2 // n
     s = [torch.randn(count, device="cuda").bfloat16() for _ in range(n)]

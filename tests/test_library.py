@@ -105,3 +105,27 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
     assert S.ncclGetErrorString(4) == b"invalid argument"
     uid = (ctypes.c_char * 128)()
     assert S.ncclGetUniqueId(uid) == 0 and bytes(uid)[:4] == b"FLX1"
+
+
+def test_header_is_plain_c_and_links(tmp_path, lib):
+    # the C-ABI is consumable from C (a cgo / FFI caller's view): strict C11,
+    # -pedantic, no C++ in the header; link and call the no-device entry points
+    src = tmp_path / "caller.c"
+    src.write_text(
+        '#include "flexlink.h"\n#include <stdio.h>\n#include <string.h>\n'
+        "int main(void) {\n"
+        "  int v = 0; flxUniqueId id; memset(&id, 0, sizeof id);\n"
+        "  if (flxGetVersion(&v) != flxSuccess || v != FLX_VERSION_CODE) return 1;\n"
+        "  if (flxGetUniqueId(&id) != flxSuccess) return 2;\n"
+        '  if (strcmp(flxGetErrorString(flxInvalidArgument), "invalid argument")) return 3;\n'
+        "  if (flxAllReduce(NULL, NULL, 1, flxFloat32, flxSum, NULL, 0) != flxInvalidArgument)"
+        " return 4;\n"
+        '  printf("ok\\n"); return 0;\n}\n')
+    libdir = comm.library_path().parent
+    exe = tmp_path / "caller"
+    cuda_inc = "/usr/local/cuda/include"
+    subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror",
+                    f"-I{cuda_inc}", f"-I{ROOT / 'include'}", str(src), f"-L{libdir}",
+                    "-lflexlink", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True)
+    assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout)

@@ -46,11 +46,14 @@ namespace flx {
 namespace {
 
 constexpr int kSemWords = 4096;  // uint32 words at the head of the staging segment
-// token word layout (all [producer][reader] over kMaxRanks), see token_post
-inline size_t sem_prod(int r, int c) { return 0 * 256 + r * kMaxRanks + c; }   // H_r piece ready
-inline size_t sem_hfree(int r, int c) { return 1 * 256 + r * kMaxRanks + c; }  // H_r taken/free
-inline size_t sem_rprod(int r, int c) { return 2 * 256 + r * kMaxRanks + c; }  // R_r ready
-inline size_t sem_rfree(int r, int c) { return 3 * 256 + r * kMaxRanks + c; }  // R_r taken/free
+// token word layout: [kind][buffer][producer][reader] over kMaxRanks, see token_post
+inline size_t tok(int kind, int r, int c, int b) {
+  return ((size_t)(kind * 2 + b) * kMaxRanks + r) * kMaxRanks + c;
+}
+inline size_t sem_prod(int r, int c, int b) { return tok(0, r, c, b); }   // H_r[b] piece ready
+inline size_t sem_hfree(int r, int c, int b) { return tok(1, r, c, b); }  // H_r[b] taken/free
+inline size_t sem_rprod(int r, int c, int b) { return tok(2, r, c, b); }  // R_r[b] ready
+inline size_t sem_rfree(int r, int c, int b) { return tok(3, r, c, b); }  // R_r[b] taken/free
 
 size_t env_mib(const char* name, size_t dflt) {
   const char* v = getenv(name);
@@ -88,6 +91,7 @@ struct World {
   long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   size_t hcap = 0;       // PCIe staging bytes per rank region
+  size_t pcie_chunk = 0;  // PCIe pipeline chunk, bytes per reader (FLX_PCIE_CHUNK_KB)
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
   // host staging segment: [sem words][H_0 .. H_{n-1}][R_0 .. R_{n-1}]
   char* host = nullptr;
@@ -102,7 +106,7 @@ struct World {
     uint32_t* flags = nullptr;
     char* dstage = nullptr;  // device landing zone for PCIe sub-chunks
     cudaStream_t d2h = nullptr, h2d = nullptr;
-    cudaEvent_t fold_done = nullptr, ev_join = nullptr;
+    cudaEvent_t fold_done[2] = {nullptr, nullptr}, ev_join = nullptr;
     cudaEvent_t ev_start_nt = nullptr, ev_pcie_nt = nullptr;  // untimed fork/join points
     cudaEvent_t ev_d2h_done = nullptr;  // joins the D2H stream's last token writes
     std::vector<cudaEvent_t> ev_fork;
@@ -143,7 +147,7 @@ flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.dstage), w->hcap));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
-  FLX_CUDA(cudaEventCreateWithFlags(&L.fold_done, cudaEventDisableTiming));
+  for (auto& e : L.fold_done) FLX_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_join, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_start_nt, cudaEventDisableTiming));
   FLX_CUDA(cudaEventCreateWithFlags(&L.ev_pcie_nt, cudaEventDisableTiming));
@@ -182,7 +186,8 @@ void world_free(World* w) {
     if (L.dstage) cudaFree(L.dstage);
     if (L.d2h) cudaStreamDestroy(L.d2h);
     if (L.h2d) cudaStreamDestroy(L.h2d);
-    if (L.fold_done) cudaEventDestroy(L.fold_done);
+    for (auto e : L.fold_done)
+      if (e) cudaEventDestroy(e);
     if (L.ev_join) cudaEventDestroy(L.ev_join);
     if (L.ev_start_nt) cudaEventDestroy(L.ev_start_nt);
     if (L.ev_pcie_nt) cudaEventDestroy(L.ev_pcie_nt);
@@ -242,6 +247,9 @@ void world_config(World* w, int nranks) {
   // 64 MiB: kMaxCtas regions of 1 MiB, so 32 CTAs move 256 MiB per AllReduce round
   w->slot = std::max<size_t>(env_mib("FLX_SLOT_MB", 64), 1 << 20);
   w->hcap = env_mib("FLX_PCIE_STAGE_MB", 64);
+  // per-reader bytes of one PCIe pipeline chunk (the paper's 4 MiB staging buffer)
+  const char* ck = getenv("FLX_PCIE_CHUNK_KB");
+  w->pcie_chunk = std::max<size_t>(4096, (size_t)(ck ? atoll(ck) : 4096) << 10);
   w->nctas = 32;
   if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));
   // one-shot AllReduce up to this many bytes per rank (FLX_ONESHOT_KB=0: off);
@@ -355,10 +363,10 @@ static flxResult_t token_accept(cudaStream_t s, uint32_t* w) {
   return sem_write(s, w, 0);
 }
 // Rank r takes H_r (or R_r): every reader returned its free token.
-static flxResult_t take_region(World* w, cudaStream_t s, int r, bool result) {
+static flxResult_t take_region(World* w, cudaStream_t s, int r, bool result, int b) {
   for (int p = 0; p < w->nranks; ++p) {
     if (p == r) continue;
-    uint32_t* word = w->sem(result ? sem_rfree(r, p) : sem_hfree(r, p));
+    uint32_t* word = w->sem(result ? sem_rfree(r, p, b) : sem_hfree(r, p, b));
     FLX_TRY(sem_wait_eq(s, word, 0));
     FLX_TRY(sem_write(s, word, 1));
   }
@@ -387,9 +395,6 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   // The NVLink kernels keep their epochs on the device and the PCIe path's
   // token handshake uses constant values: both replay correctly from a graph.
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
-  if ((scatter || a2a ? pc * n : pc) > w->hcap)
-    return fail(flxInvalidUsage, "pcie slice of %zu bytes exceeds staging capacity %zu (raise "
-                "FLX_PCIE_STAGE_MB or lower the pcie share)", pc, w->hcap);
 
   // fork: in loopback every rank's stream joins local rank 0's stream
   cudaStream_t s0 = streams[0];
@@ -412,38 +417,108 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   if (timed || pc > 0) FLX_CUDA(cudaEventRecord(ev_start, s0));
 
   // ---------------- PCIe slice (issued first so the copies overlap the kernel)
+  // Chunked and double-buffered (buffer b = chunk k % 2 of H_r, R_r and each
+  // rank's device landing zone), so chunk k+1's D2H runs while chunk k's H2D
+  // and fold do: both PCIe directions stay busy (staging.py's two-hop
+  // pipeline, PipelineSpec with buffers=2).  Issue order is software-pipelined
+  // and global — step 1 and 2 of chunk k for every rank, then AllReduce steps 3
+  // and 4 of chunk k-1 — so every wait refers to a write issued earlier.
   if (pc > 0) {
     for (int i = 0; i < nl; ++i) {
       World::Local& L = w->local[i];
       FLX_CUDA(cudaStreamWaitEvent(L.d2h, ev_start, 0));
       FLX_CUDA(cudaStreamWaitEvent(L.h2d, ev_start, 0));
     }
-    // step 1 (every protocol): rank r takes the free token of every reader of
-    // H_r, D2H's its pieces into H_r and posts one ready token per reader.
-    // AllReduce: sub-chunk c -> H_r[c]; ReduceScatter / AllToAll: the PCIe
-    // part of block c -> H_r[c]; AllGather: the whole slice -> H_r.
-    const size_t q = (!gather && !scatter && !a2a) ? pc / n : pc;  // piece per reader
-    for (int i = 0; i < nl; ++i) {
-      World::Local& L = w->local[i];
-      const int r = L.rank;
-      FLX_TRY(take_region(w, L.d2h, r, /*result=*/false));
-      const char* src = static_cast<const char*>(send[i]);
-      if (gather) {
-        FLX_CUDA(cudaMemcpyAsync(w->hregion(r), src + nv, pc, cudaMemcpyDeviceToHost, L.d2h));
-      } else {
+    const bool ar = !gather && !scatter && !a2a;
+    const size_t q = ar ? pc / n : pc;  // bytes per reader (AR sub-chunk / RS, A2A block part)
+    // per-reader bytes of one chunk: a multiple of 4096 that lets 2 buffers x n
+    // readers fit a rank's host region (and landing zone)
+    const size_t fit = ((w->hcap / (2 * (size_t)n)) / 4096) * 4096;
+    const size_t cq = std::max<size_t>(4096, std::min(w->pcie_chunk, fit));
+    const size_t chunks = (q + cq - 1) / cq;
+    const size_t slot_h = gather ? cq : cq * n;  // one buffer of H_r
+    auto piece = [&](size_t k) { return std::min(cq, q - k * cq); };
+
+    auto step12 = [&](size_t k) -> flxResult_t {
+      const int b = (int)(k & 1);
+      const size_t len = piece(k), at = k * cq;
+      for (int i = 0; i < nl; ++i) {  // step 1: take H_r[b], D2H, post per reader
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        FLX_TRY(take_region(w, L.d2h, r, false, b));
+        const char* src = static_cast<const char*>(send[i]);
+        char* h = w->hregion(r) + b * slot_h;
+        if (gather) {
+          FLX_CUDA(cudaMemcpyAsync(h, src + nv + at, len, cudaMemcpyDeviceToHost, L.d2h));
+        } else {
+          for (int s = 1; s < n; ++s) {
+            const int c = (r + s) % n;
+            const char* from = ar ? src + nv + c * q + at : src + (size_t)c * bytes + nv + at;
+            FLX_CUDA(cudaMemcpyAsync(h + c * cq, from, len, cudaMemcpyDeviceToHost, L.d2h));
+          }
+        }
+        for (int s = 1; s < n; ++s)
+          FLX_TRY(token_post(L.d2h, w->sem(sem_prod(r, (r + s) % n, b))));
+      }
+      for (int i = 0; i < nl; ++i) {  // step 2: accept, H2D, give; fold (AR / RS)
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        char* dst = static_cast<char*>(recv[i]);
+        const char* src = static_cast<const char*>(send[i]);
+        char* land = L.dstage + b * cq * n;
         for (int s = 1; s < n; ++s) {
-          const int c = (r + s) % n;
-          const char* piece = (scatter || a2a) ? src + (size_t)c * bytes + nv : src + nv + c * q;
-          FLX_CUDA(cudaMemcpyAsync(w->hregion(r) + c * q, piece, q, cudaMemcpyDeviceToHost,
-                                   L.d2h));
+          const int p = (r - s + n) % n;
+          FLX_TRY(token_accept(L.h2d, w->sem(sem_prod(p, r, b))));
+          const char* from = w->hregion(p) + b * slot_h + (gather ? 0 : r * cq);
+          char* to = (gather || a2a) ? dst + (size_t)p * bytes + nv + at : land + p * cq;
+          FLX_CUDA(cudaMemcpyAsync(to, from, len, cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(token_give(L.h2d, w->sem(sem_hfree(p, r, b))));
+        }
+        if (ar || scatter) {  // fold every source's piece in rank order
+          FoldArgs a{};
+          for (int p = 0; p < n; ++p)
+            a.src[p] = p != r    ? land + p * cq
+                       : scatter ? src + (size_t)r * bytes + nv + at
+                                 : src + nv + r * q + at;
+          a.dst[0] = scatter ? dst + nv + at : dst + nv + r * q + at;
+          a.n = n;
+          a.ndst = 1;
+          a.bytes = len;
+          FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
+          if (ar) FLX_CUDA(cudaEventRecord(L.fold_done[b], L.h2d));
         }
       }
-      for (int s = 1; s < n; ++s) FLX_TRY(token_post(L.d2h, w->sem(sem_prod(r, (r + s) % n))));
-    }
-    // step 2: rank r accepts every peer's piece, lands it (AllGather / AllToAll:
-    // straight into recv; AllReduce / ReduceScatter: into dstage, then the
-    // rank-order fold) and returns the free token
-    for (int i = 0; i < nl; ++i) {
+      return flxSuccess;
+    };
+    auto step34 = [&](size_t k) -> flxResult_t {  // AllReduce: share the reduced piece
+      const int b = (int)(k & 1);
+      const size_t len = piece(k), at = k * cq;
+      for (int i = 0; i < nl; ++i) {  // step 3: take R_r[b], D2H my reduced piece, post
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done[b], 0));
+        FLX_TRY(take_region(w, L.d2h, r, true, b));
+        FLX_CUDA(cudaMemcpyAsync(w->rregion(r) + b * cq,
+                                 static_cast<char*>(recv[i]) + nv + r * q + at, len,
+                                 cudaMemcpyDeviceToHost, L.d2h));
+        for (int s = 1; s < n; ++s)
+          FLX_TRY(token_post(L.d2h, w->sem(sem_rprod(r, (r + s) % n, b))));
+      }
+      for (int i = 0; i < nl; ++i) {  // step 4: accept, H2D every other piece, give
+        World::Local& L = w->local[i];
+        const int r = L.rank;
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          FLX_TRY(token_accept(L.h2d, w->sem(sem_rprod(c, r, b))));
+          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + nv + c * q + at,
+                                   w->rregion(c) + b * cq, len, cudaMemcpyHostToDevice, L.h2d));
+          FLX_TRY(token_give(L.h2d, w->sem(sem_rfree(c, r, b))));
+        }
+      }
+      return flxSuccess;
+    };
+
+    for (int i = 0; i < nl; ++i) {  // own pieces that never leave the GPU
       World::Local& L = w->local[i];
       const int r = L.rank;
       char* dst = static_cast<char*>(recv[i]);
@@ -456,58 +531,12 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         const size_t own = (size_t)r * bytes + nv;
         FLX_CUDA(cudaMemcpyAsync(dst + own, src + own, pc, cudaMemcpyDeviceToDevice, L.h2d));
       }
-      for (int s = 1; s < n; ++s) {
-        const int p = (r - s + n) % n;
-        FLX_TRY(token_accept(L.h2d, w->sem(sem_prod(p, r))));
-        const char* from = gather ? w->hregion(p) : w->hregion(p) + r * q;
-        char* to = gather ? dst + (size_t)p * bytes + nv
-                   : a2a  ? dst + (size_t)p * bytes + nv
-                          : L.dstage + p * q;
-        FLX_CUDA(cudaMemcpyAsync(to, from, q, cudaMemcpyHostToDevice, L.h2d));
-        FLX_TRY(token_give(L.h2d, w->sem(sem_hfree(p, r))));
-      }
-      if (!gather && !a2a) {  // fold every source's piece r in rank order
-        FoldArgs a{};
-        for (int p = 0; p < n; ++p)
-          a.src[p] = p != r    ? L.dstage + p * q
-                     : scatter ? src + (size_t)r * bytes + nv
-                               : src + nv + r * q;
-        a.dst[0] = scatter ? dst + nv : dst + nv + r * q;
-        a.n = n;
-        a.ndst = 1;
-        a.bytes = q;
-        FLX_CUDA(launch_fold(dtype, op, a, 16, L.h2d));
-      }
-      if (gather || scatter || a2a) FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
-      else FLX_CUDA(cudaEventRecord(L.fold_done, L.h2d));
     }
-    if (!gather && !scatter && !a2a) {
-      // AllReduce step 3: D2H my reduced sub-chunk into R_r (after its previous
-      // readers returned the R_r free tokens), post a ready token per reader
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done, 0));
-        FLX_TRY(take_region(w, L.d2h, r, /*result=*/true));
-        FLX_CUDA(cudaMemcpyAsync(w->rregion(r), static_cast<char*>(recv[i]) + nv + r * q, q,
-                                 cudaMemcpyDeviceToHost, L.d2h));
-        for (int s = 1; s < n; ++s)
-          FLX_TRY(token_post(L.d2h, w->sem(sem_rprod(r, (r + s) % n))));
-      }
-      // step 4: H2D every other rank's reduced sub-chunk, return R_c's token
-      for (int i = 0; i < nl; ++i) {
-        World::Local& L = w->local[i];
-        const int r = L.rank;
-        for (int s = 1; s < n; ++s) {
-          const int c = (r + s) % n;
-          FLX_TRY(token_accept(L.h2d, w->sem(sem_rprod(c, r))));
-          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + nv + c * q, w->rregion(c), q,
-                                   cudaMemcpyHostToDevice, L.h2d));
-          FLX_TRY(token_give(L.h2d, w->sem(sem_rfree(c, r))));
-        }
-        FLX_CUDA(cudaEventRecord(ev_pcie(i), L.h2d));
-      }
+    for (size_t k = 0; k <= chunks; ++k) {
+      if (k < chunks) FLX_TRY(step12(k));
+      if (ar && k >= 1) FLX_TRY(step34(k - 1));
     }
+    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaEventRecord(ev_pcie(i), w->local[i].h2d));
   }
 
   // ---------------- NVLink slice

@@ -18,11 +18,13 @@
 //                2 accept prod[c][r]; H2D H_c -> recv block c; give hfree[c][r]
 //     ReduceScatter / AllToAll = steps 1-2 on the PCIe part of each block
 //                (AllToAll lands straight in recv, no fold).
-//   "take H_r" waits for every reader's free token of the previous use of
-//   H_r, whichever protocol that was; R_r likewise for AllReduce.
-//   Issue order is global (all ranks' step 1, then step 2, ...) so every wait
-//   refers to a write issued earlier: no deadlock even when streams share a
-//   hardware queue (loopback).
+//   The slice moves in chunks (FLX_PCIE_CHUNK_KB per reader) through two
+//   buffers b = k % 2 of H_r, R_r and the landing zone, every token indexed by
+//   [buffer]; "take H_r[b]" waits for every reader's free token of the
+//   previous use of that buffer, whichever protocol that was; R_r likewise.
+//   Issue order is global and software-pipelined (steps 1-2 of chunk k for all
+//   ranks, then steps 3-4 of chunk k-1) so every wait refers to a write issued
+//   earlier: no deadlock even when streams share a hardware queue (loopback).
 // Bootstrap (multi-process): a POSIX shm segment named by the unique id
 // carries each rank's CUDA IPC handles (scratch + flags) and a second one is
 // the PCIe staging area, cudaHostRegister'ed by every rank.

@@ -435,7 +435,12 @@ def run_single_gpu(args) -> None:
                        "ms_per_step": round(dt_c * 1e3, 4),
                        "busbw": "(S_send/t)*(N-1)/N (nccl-tests)",
                        "kernel_algorithmic_bytes": alg,
-                       "kernel_frac_hbm": round(alg / (k_ms * 1e-3) / 1e9 / hbm_peak, 4)}
+                       "kernel_frac_hbm": round(alg / (k_ms * 1e-3) / 1e9 / hbm_peak, 4),
+                       "traffic_share_pct": {k.short: round(100 * v / max(1, sum(
+                           clique.path_bytes().values())), 3)
+                                             for k, v in clique.path_bytes().items()},
+                       "link_roofline": link_roofline(AR_BYTES / dt_c * (n - 1) / n / 1e9,
+                                                      pcie_h2d)}
     for r in range(n):
         assert torch.equal(rs_recv[r], exact[r * blk:(r + 1) * blk]), "reduce_scatter mismatch"
         for q in range(n):

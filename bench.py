@@ -41,6 +41,28 @@ AG_OUT_BYTES = 256 * MIB       # gathered output (config 2, nccl-tests conventio
 METRIC = "AllReduce/AllGather busBW GB/s @256MB vs NCCL; PCIe/NIC traffic share %"
 
 
+# The JSON line goes to the process's original stdout; everything else the
+# native libraries print (e.g. NCCL's "NCCL version ..." banner under torchrun)
+# is routed to stderr, so rank 0's stdout is exactly ONE JSON line.
+_JSON_FD: int | None = None
+
+
+def emit(line: dict) -> None:
+    data = (json.dumps(line) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, data)
+
+
+def route_native_stdout_to_stderr() -> None:
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
 def busbw_allreduce(nbytes: int, seconds: float, n: int) -> float:
     return nbytes / seconds * 2 * (n - 1) / n / 1e9
 
@@ -230,7 +252,7 @@ def run_reference(args) -> None:
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # --------------------------------------------------------------- N = 1
@@ -553,7 +575,7 @@ def run_single_gpu(args) -> None:
         },
     }
     clique.destroy()
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
@@ -825,7 +847,7 @@ def run_multi_gpu(args) -> None:
     del rs_out, rs_ref, a2a_out, a2a_ref
     if rank == 0:
         value = busbw_allreduce(AR_BYTES, dt, world) * 1.0
-        print(json.dumps({
+        emit({
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dt * 1e3, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
@@ -858,7 +880,7 @@ def run_multi_gpu(args) -> None:
                 "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, world), None)},
             **extra,
             "link_roofline": link_roofline(value, None),
-        }), flush=True)
+        })
     dist.barrier()
     c.destroy()
     dist.destroy_process_group()
@@ -879,6 +901,7 @@ def main() -> None:
     args = p.parse_args()
     if args.warmup < 3 and args.impl == "flexlink":
         args.warmup = 3
+    route_native_stdout_to_stderr()
     if args.impl == "reference":
         run_reference(args)
         return
@@ -891,9 +914,8 @@ def main() -> None:
             run_multi_gpu(args)
         except Exception as e:  # report, do not hang the job
             if int(os.environ.get("RANK", "0")) == 0:
-                print(json.dumps({"metric": METRIC, "value": None, "unit": "GB/s",
-                                  "n_gpus": world, "error": f"{type(e).__name__}: {e}"}),
-                      flush=True)
+                emit({"metric": METRIC, "value": None, "unit": "GB/s", "n_gpus": world,
+                      "error": f"{type(e).__name__}: {e}"})
             raise
     else:
         run_single_gpu(args)

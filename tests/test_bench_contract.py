@@ -36,7 +36,8 @@ def test_reference_arm_line():
                           "--steps", "1", "--warmup", "3"], cwd=ROOT, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
-    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert len(out.stdout.strip().splitlines()) == 1, out.stdout  # exactly one JSON line
+    line = json.loads(out.stdout)
     assert line["impl"] == "reference" and line["metric"] == bench.METRIC
     assert line["unit"] == "GB/s" and line["higher_is_better"] is True and line["value"] > 0
     assert line["config"] == bench.workload_config(1)

@@ -28,7 +28,9 @@ def test_run_multi_gpu_path_smoke():
            "--steps", "2", "--warmup", "3"]
     out = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-3000:]
-    line = json.loads([x for x in out.stdout.splitlines() if x.startswith("{")][-1])
+    # rank 0's stdout is exactly the JSON line (NCCL's banner is routed to stderr)
+    assert len(out.stdout.strip().splitlines()) == 1, out.stdout
+    line = json.loads(out.stdout)
     assert line["n_gpus"] == 1 and line["result_matches_exact_sum"] is True
     assert line["e2e"]["result_exact"] is True and line["allgather"]["matches_nccl_bitwise"]
     assert line["gpu_launches"] > 0 and "clocks" in line

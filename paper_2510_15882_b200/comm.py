@@ -438,6 +438,7 @@ class Clique:
         self.device = device
 
     def destroy(self) -> None:
+        self._checked = None  # drop the cached tensor references
         for c in self.comms:
             c.destroy()
 
@@ -459,8 +460,10 @@ class Clique:
     def _validate(self, sends, recvs, gather: bool = False, scatter: bool = False):
         if len(sends) != self.nranks or len(recvs) != self.nranks:
             raise ValueError(f"need one send and one recv tensor per rank ({self.nranks})")
-        # the same tensors (same objects at the same addresses) as the last call
-        # in this mode were already checked: skip the per-tensor property reads
+        # the same tensor objects at the same addresses and sizes as the last
+        # call in this mode were already checked: skip the per-tensor property
+        # reads.  The cache keeps that tensor set referenced (entry [2]), so a
+        # freed tensor's id can never alias a new tensor while it is cached.
         key = (gather, scatter, tuple((id(t), t.data_ptr(), t.numel()) for t in sends),
                tuple((id(t), t.data_ptr(), t.numel()) for t in recvs))
         checked = getattr(self, "_checked", None)
@@ -483,7 +486,7 @@ class Clique:
         # re-uses them instead of rebuilding 2*nranks ctypes values
         args = (ptrs(*[t.data_ptr() for t in sends]), ptrs(*[t.data_ptr() for t in recvs]),
                 dtype_code(s0.dtype))
-        self._checked = (key, args)
+        self._checked = (key, args, (tuple(sends), tuple(recvs)))
         return args
 
     def _issue(self, coll: int, args, op: int, stream, count: int) -> None:

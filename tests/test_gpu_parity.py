@@ -338,3 +338,21 @@ def test_cuda_graph_capture_and_replay(granules):
         torch.cuda.synchronize()
         for r in range(n):
             np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
+
+
+def test_validation_cache_never_reuses_stale_tensors():
+    # Clique caches the checked tensor set; new tensor objects (even at recycled
+    # addresses and ids, with another dtype or layout) are re-validated
+    with flx.Clique(4) as c:
+        for dt in (torch.float32, torch.bfloat16, torch.float32, torch.float16):
+            xs = [torch.full((4096,), float(i + 1), device="cuda", dtype=dt) for i in range(4)]
+            for _ in range(2):
+                for i, x in enumerate(xs):
+                    x.fill_(float(i + 1))
+                c.all_reduce(xs, xs)
+            torch.cuda.synchronize()
+            assert all(bool((x == 10).all()) for x in xs), dt
+            del xs
+        ys = [torch.ones(64, 64, device="cuda").t() for _ in range(4)]  # non-contiguous
+        with pytest.raises(ValueError):
+            c.all_reduce(ys, ys)

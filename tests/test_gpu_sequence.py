@@ -98,3 +98,31 @@ def test_random_sequence_on_one_communicator(loopback, n):
                         np.testing.assert_array_equal(_np(rr[k], dt), w[k],
                                                       err_msg=f"call {j} ({cl}) rank {k}")
                 pending.clear()
+
+
+def test_two_communicators_interleaved():
+    # e.g. a TP and a DP group in one process: a virtual clique and a loopback
+    # world on the same GPU, calls interleaved without syncs, no cross-talk
+    n = 4
+    a = flx.Clique(n)
+    b = flx.Clique(n, loopback=True)
+    try:
+        for c in (a, b):
+            c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        outs = []
+        for it in range(6):
+            for c, count in ((a, 70001 + it), (b, 123457 - it)):
+                cpu = _inputs(n, count, 7, 500 + it * 2 + (c is b))
+                s = [h.cuda() for h in cpu]
+                r = [torch.empty_like(x) for x in s]
+                c.all_reduce(s, r)
+                outs.append((c, cpu, r, s))
+        torch.cuda.synchronize()
+        for c, cpu, r, _ in outs:
+            want = oracle.allreduce([h.numpy() for h in cpu], 7, 0, (900, 100, 0),
+                                    c.comms[0].alignment(CollectiveOp.ALLREDUCE))
+            for k in range(n):
+                np.testing.assert_array_equal(_np(r[k], 7), want[k])
+    finally:
+        a.destroy()
+        b.destroy()

@@ -356,3 +356,33 @@ def test_validation_cache_never_reuses_stale_tensors():
         ys = [torch.ones(64, 64, device="cuda").t() for _ in range(4)]  # non-contiguous
         with pytest.raises(ValueError):
             c.all_reduce(ys, ys)
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_group_call_with_one_stream_per_rank(loopback):
+    # ncclGroupStart(); ncclAllReduce(..., stream_i) per rank; ncclGroupEnd():
+    # the collective waits for every rank's stream (inputs produced there) and
+    # every rank's stream waits for the collective (results consumed there)
+    n, count = 4, (1 << 18) + 8  # partial sums stay below 2**24: exact in fp32
+    L = flx.load_library()
+    with flx.Clique(n, loopback=loopback) as c:
+        c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        streams = [torch.cuda.Stream() for _ in range(n)]
+        xs = [torch.empty(count, device="cuda") for _ in range(n)]
+        outs = [torch.empty(count, device="cuda") for _ in range(n)]
+        for it in range(3):
+            for i, (st, x) in enumerate(zip(streams, xs)):
+                with torch.cuda.stream(st):
+                    torch.cuda._sleep(2000 * (i + 1))  # make producer timing differ
+                    x.fill_(float(i + 1 + it))
+            assert L.flxGroupStart() == 0
+            for i, comm_i in enumerate(c.comms):
+                comm_i.all_reduce(xs[i], outs[i], stream=streams[i])
+            assert L.flxGroupEnd() == 0
+            sums = []
+            for st, o in zip(streams, outs):
+                with torch.cuda.stream(st):
+                    sums.append(o.sum())
+            torch.cuda.synchronize()
+            want = float(sum(i + 1 + it for i in range(n))) * count
+            assert all(float(s) == want for s in sums), (it, [float(s) for s in sums], want)

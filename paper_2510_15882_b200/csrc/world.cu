@@ -433,10 +433,14 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     }
     const bool ar = !gather && !scatter && !a2a;
     const size_t q = ar ? pc / n : pc;  // bytes per reader (AR sub-chunk / RS, A2A block part)
-    // per-reader bytes of one chunk: a multiple of 4096 that lets 2 buffers x n
-    // readers fit a rank's host region (and landing zone)
-    const size_t fit = ((w->hcap / (2 * (size_t)n)) / 4096) * 4096;
-    const size_t cq = std::max<size_t>(4096, std::min(w->pcie_chunk, fit));
+    // bytes per reader of one chunk, a multiple of 4096 such that 2 buffers fit
+    // a rank's host region and landing zone.  AllGather's buffer holds one piece
+    // for all readers (not one per reader) and its H2D side carries N-1 times
+    // the D2H side, so it takes N-times larger chunks: fewer hand-offs, and
+    // overlap would buy it at most 1/N (profiles/r1/pcie_world_256.jsonl).
+    const size_t fit = ((w->hcap / (gather ? 2 : 2 * (size_t)n)) / 4096) * 4096;
+    const size_t want = gather ? w->pcie_chunk * n : w->pcie_chunk;
+    const size_t cq = std::max<size_t>(4096, std::min(want, fit));
     const size_t chunks = (q + cq - 1) / cq;
     const size_t slot_h = gather ? cq : cq * n;  // one buffer of H_r
     auto piece = [&](size_t k) { return std::min(cq, q - k * cq); };

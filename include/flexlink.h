@@ -105,6 +105,10 @@ flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist);
  * path on a single GPU; set CUDA_DEVICE_MAX_CONNECTIONS>=3*nranks+1. */
 flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device);
 flxResult_t flxCommDestroy(flxComm_t comm);
+/* ncclCommAbort (nccl.h:186): stop waiting for peers — kernels still spinning
+ * on a peer flag give up at once, the destroy barrier is skipped — then free
+ * everything like flxCommDestroy.  For a rank that saw flxInternalError. */
+flxResult_t flxCommAbort(flxComm_t comm);
 flxResult_t flxCommCount(const flxComm_t comm, int* count);
 flxResult_t flxCommUserRank(const flxComm_t comm, int* rank);
 flxResult_t flxCommCuDevice(const flxComm_t comm, int* device);

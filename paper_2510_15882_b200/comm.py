@@ -86,6 +86,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommInitAll": [P(vp), ci, P(ci)],
         "flxCommInitLoopback": [P(vp), ci, ci],
         "flxCommDestroy": [vp],
+        "flxCommAbort": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
         "flxCommCuDevice": [vp, P(ci)],
@@ -221,6 +222,12 @@ class Communicator:
     def destroy(self) -> None:
         if self._h:
             _check(load_library().flxCommDestroy(self._h), "flxCommDestroy")
+            self._h = ctypes.c_void_p()
+
+    def abort(self) -> None:
+        """``ncclCommAbort``: give up on peers (no destroy barrier), then free."""
+        if self._h:
+            _check(load_library().flxCommAbort(self._h), "flxCommAbort")
             self._h = ctypes.c_void_p()
 
     @property

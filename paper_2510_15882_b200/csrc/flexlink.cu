@@ -816,6 +816,15 @@ flxResult_t flxCommDestroy(flxComm_t comm) {
   return flxSuccess;
 }
 
+flxResult_t flxCommAbort(flxComm_t comm) {
+  FLX_TRY(validate_comm(comm));
+  {
+    std::lock_guard<std::mutex> lock(g_mutex);
+    if (comm->world) world_abort(comm->world);
+  }
+  return flxCommDestroy(comm);
+}
+
 flxResult_t flxCommCount(const flxComm_t comm, int* count) {
   FLX_TRY(validate_comm(comm));
   if (!count) return fail(flxInvalidArgument, "null count");

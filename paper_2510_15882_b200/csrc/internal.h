@@ -126,6 +126,7 @@ std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local);
 void world_set_nctas(World* w, int n);
 int world_nlocal(World* w);
 bool world_aborted(World* w);
+void world_abort(World* w);
 flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int write,
                              void* buf, size_t bytes);
 

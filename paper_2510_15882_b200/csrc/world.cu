@@ -123,6 +123,7 @@ struct World {
   std::vector<void*> ipc_opened;
   struct BootHeader* boot = nullptr;  // kept mapped (name unlinked) for the destroy barrier
   int destroyed = 0;
+  bool aborting = false;  // flxCommAbort: skip the destroy barrier
 
   // semaphore words as the GPU addresses them (registered host memory may map
   // to a different device address than its host pointer)
@@ -175,8 +176,9 @@ void world_free(World* w) {
     // my outbox / host region until it, too, has drained its device
     __atomic_fetch_add(&w->boot->leaving, 1, __ATOMIC_ACQ_REL);
     const auto t0 = std::chrono::steady_clock::now();
+    const double limit = w->aborting ? 0.0 : 60.0;  // abort: do not wait for peers
     while (__atomic_load_n(&w->boot->leaving, __ATOMIC_ACQUIRE) < w->nranks &&
-           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 60.0)
+           std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < limit)
       std::this_thread::sleep_for(std::chrono::milliseconds(1));
     munmap(w->boot, sizeof(BootHeader));
     w->boot = nullptr;
@@ -770,6 +772,11 @@ flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int
   FLX_CUDA(cudaMemcpy(write ? dev : buf, write ? buf : dev, bytes,
                       write ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost));
   return flxSuccess;
+}
+
+void world_abort(World* w) {
+  *(volatile uint32_t*)w->abort_word = 1;  // any kernel still spinning on a peer gives up
+  w->aborting = true;
 }
 
 int world_release(World* w) {

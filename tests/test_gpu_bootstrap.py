@@ -99,7 +99,10 @@ def _abort_worker(rank, world, port, out):
             except comm.FlexLinkError as e:
                 out[0] = (e.code, waited, async_err)
         dist.barrier()
-        c.destroy()
+        if rank == 0:
+            c.abort()  # ncclCommAbort: the rank that saw the error does not wait for peers
+        else:
+            c.destroy()
     finally:
         dist.destroy_process_group()
 

@@ -109,6 +109,10 @@ flxResult_t flxCommDestroy(flxComm_t comm);
  * on a peer flag give up at once, the destroy barrier is skipped — then free
  * everything like flxCommDestroy.  For a rank that saw flxInternalError. */
 flxResult_t flxCommAbort(flxComm_t comm);
+/* ncclCommFinalize (nccl.h:177): block until the comm's internal side streams
+ * (PCIe copies, reduce-on-receive) are idle; flxInternalError if a peer wait
+ * timed out.  Collectives stay stream-ordered on the caller's streams. */
+flxResult_t flxCommFinalize(flxComm_t comm);
 flxResult_t flxCommCount(const flxComm_t comm, int* count);
 flxResult_t flxCommUserRank(const flxComm_t comm, int* rank);
 flxResult_t flxCommCuDevice(const flxComm_t comm, int* device);

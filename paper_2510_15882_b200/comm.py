@@ -87,6 +87,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommInitLoopback": [P(vp), ci, ci],
         "flxCommDestroy": [vp],
         "flxCommAbort": [vp],
+        "flxCommFinalize": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
         "flxCommCuDevice": [vp, P(ci)],
@@ -223,6 +224,10 @@ class Communicator:
         if self._h:
             _check(load_library().flxCommDestroy(self._h), "flxCommDestroy")
             self._h = ctypes.c_void_p()
+
+    def finalize(self) -> None:
+        """``ncclCommFinalize``: wait for the comm's side streams to go idle."""
+        _check(load_library().flxCommFinalize(self._h), "flxCommFinalize")
 
     def abort(self) -> None:
         """``ncclCommAbort``: give up on peers (no destroy barrier), then free."""

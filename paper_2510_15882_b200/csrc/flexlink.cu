@@ -816,6 +816,17 @@ flxResult_t flxCommDestroy(flxComm_t comm) {
   return flxSuccess;
 }
 
+flxResult_t flxCommFinalize(flxComm_t comm) {
+  FLX_TRY(validate_comm(comm));
+  if (comm->world) return world_finalize(comm->world, comm->local);
+  Clique* c = comm->clique;
+  FLX_CUDA(cudaSetDevice(c->device));
+  FLX_CUDA(cudaStreamSynchronize(c->d2h));
+  FLX_CUDA(cudaStreamSynchronize(c->h2d));
+  FLX_CUDA(cudaStreamSynchronize(c->red));
+  return flxSuccess;
+}
+
 flxResult_t flxCommAbort(flxComm_t comm) {
   FLX_TRY(validate_comm(comm));
   {

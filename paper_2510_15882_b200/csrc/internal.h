@@ -127,6 +127,7 @@ void world_set_nctas(World* w, int n);
 int world_nlocal(World* w);
 bool world_aborted(World* w);
 void world_abort(World* w);
+flxResult_t world_finalize(World* w, int local);
 flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int write,
                              void* buf, size_t bytes);
 

@@ -86,6 +86,10 @@ ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recv
                                         (flxRedOp_t)op, (flxComm_t)comm, stream);
 }
 
+ncclResult_t ncclCommFinalize(ncclComm_t comm) {
+  return (ncclResult_t)flxCommFinalize((flxComm_t)comm);
+}
+
 ncclResult_t ncclCommAbort(ncclComm_t comm) { return (ncclResult_t)flxCommAbort((flxComm_t)comm); }
 
 ncclResult_t ncclCommGetAsyncError(ncclComm_t comm, ncclResult_t* asyncError) {

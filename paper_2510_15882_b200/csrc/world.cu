@@ -774,6 +774,16 @@ flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int
   return flxSuccess;
 }
 
+flxResult_t world_finalize(World* w, int local) {
+  World::Local& L = w->local[local];
+  FLX_CUDA(cudaSetDevice(L.device));
+  FLX_CUDA(cudaStreamSynchronize(L.d2h));
+  FLX_CUDA(cudaStreamSynchronize(L.h2d));
+  if (*(volatile uint32_t*)w->abort_word)
+    return fail(flxInternalError, "a peer wait timed out (rank died or hung?)");
+  return flxSuccess;
+}
+
 void world_abort(World* w) {
   *(volatile uint32_t*)w->abort_word = 1;  // any kernel still spinning on a peer gives up
   w->aborting = true;

@@ -97,7 +97,8 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
     exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
     for name in ("ncclGetUniqueId", "ncclCommInitRank", "ncclCommInitAll", "ncclCommDestroy",
                  "ncclAllReduce", "ncclAllGather", "ncclReduceScatter", "ncclGroupStart",
-                 "ncclGroupEnd", "ncclCommGetAsyncError", "ncclCommAbort"):
+                 "ncclGroupEnd", "ncclCommGetAsyncError", "ncclCommAbort",
+                 "ncclCommFinalize"):
         assert name in exported
     assert "ncclBroadcast" not in exported  # falls through to real NCCL under LD_PRELOAD
     S = ctypes.CDLL(str(shim))

@@ -68,6 +68,7 @@ static int run(int rank, ncclUniqueId id) {
     }
     for (size_t i = 0; i < (size_t)N * COUNT; ++i) h[i] = value(rank, i);  /* restore */
   }
+  if (ncclCommFinalize(comm) != ncclSuccess) return 29;
   if (ncclCommDestroy(comm) != ncclSuccess) return 30;
   free(h);
   return bad ? 40 : 0;

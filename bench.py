@@ -137,6 +137,7 @@ class ClockSampler:
         self.thread = threading.Thread(target=self._poll, daemon=True)
         self.thread.start()
         time.sleep(0.02)
+        self.t0 = time.perf_counter()
         return self
 
     def _poll(self):
@@ -165,7 +166,9 @@ class ClockSampler:
                     reasons.add(name)
         return {"sm_mhz": statistics.median(m for m, _ in self.samples),
                 "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                # the sampled window (NVML polls every 2 ms, slower when NVML is slow)
+                "window_ms": round((time.perf_counter() - getattr(self, "t0", 0.0)) * 1e3, 1)}
 
 
 def workload_config(n_gpus: int) -> dict:

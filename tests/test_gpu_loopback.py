@@ -69,6 +69,27 @@ def test_loopback_allreduce_matches_oracle(n, count, dtype, op, granules):
         assert pb[PathKind.PCIE_STAGED] > 0
 
 
+def test_loopback_config1_full_size_exact():
+    # C1 at full size through the multi-GPU engine: 8 ranks x 256 MiB fp32
+    # with the default 64 MiB slots (several two-shot rounds per call) and a
+    # PCIe share through the host hub.  Integer-valued inputs: exact sums in
+    # any order, so torch's sum is the size-independent check.
+    n, count = 8, 64 << 20
+    g = torch.Generator(device="cuda").manual_seed(1000)
+    sends = [torch.randint(-1024, 1024, (count,), device="cuda", generator=g).float()
+             for _ in range(n)]
+    recvs = [torch.empty_like(s) for s in sends]
+    exact = torch.stack(sends).sum(0)
+    with flx.Clique(n, loopback=True) as w:
+        w.set_shares(CollectiveOp.ALLREDUCE, (990, 10, 0))
+        for _ in range(2):
+            w.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        assert w.path_bytes()[PathKind.PCIE_STAGED] > 0
+    for r in recvs:
+        assert torch.equal(r, exact)
+
+
 def test_loopback_repeated_calls_and_inplace():
     got, want, _ = _allreduce(8, (1 << 18) + 7, 7, "sum", (900, 100, 0), inplace=True, calls=5)
     for r in range(8):

@@ -227,6 +227,42 @@ def test_large_allreduce_exact_properties():
         assert torch.equal(r, exact)
 
 
+def test_config2_allgather_full_size_bitexact():
+    # C2 shape: 8 ranks x 16,777,216 bf16 (32 MiB) -> 256 MiB gathered, with a
+    # PCIe share: every rank's output must be the concatenation of all sends.
+    n, count = 8, 16 << 20
+    g = torch.Generator(device="cuda").manual_seed(1002)
+    sends = [torch.randn(count, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    recvs = [torch.empty(n * count, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    with flx.Clique(n) as clique:
+        clique.set_shares(CollectiveOp.ALLGATHER, (950, 50, 0))
+        clique.all_gather(sends, recvs)
+        torch.cuda.synchronize()
+        assert clique.path_bytes()[PathKind.PCIE_STAGED] > 0
+    want = torch.cat(sends).view(torch.int16)
+    for r in recvs:
+        assert torch.equal(r.view(torch.int16), want)
+
+
+def test_config5_shape_bf16_allreduce_exact():
+    # C5 shape: [65536, 5120] bf16 per rank (640 MiB), 8 ranks, PCIe share on.
+    # Integer-valued inputs in [-16, 16): every partial sum is an integer of
+    # magnitude <= 128, exact in bf16 and fp32, so the fold equals torch's sum
+    # whatever the order -- a size-independent check at the full size.
+    n, count = 8, 65536 * 5120
+    g = torch.Generator(device="cuda").manual_seed(1005)
+    sends = [torch.randint(-16, 16, (count,), device="cuda", generator=g).bfloat16()
+             for _ in range(n)]
+    with flx.Clique(n) as clique:
+        clique.set_shares(CollectiveOp.ALLREDUCE, (980, 20, 0))
+        exact = torch.stack(sends).float().sum(0).bfloat16()
+        clique.all_reduce(sends, sends)  # in place, as the TP layer does
+        torch.cuda.synchronize()
+        assert clique.path_bytes()[PathKind.PCIE_STAGED] > 0
+    for s in sends:
+        assert torch.equal(s.view(torch.int16), exact.view(torch.int16))
+
+
 def test_path_times_and_history():
     n = 8
     dev = [torch.randn(1 << 22, device="cuda") for _ in range(n)]

@@ -66,6 +66,7 @@ struct RankArgs {
   size_t slot;         // inbox slot capacity (bytes) per source rank
   size_t small_slot;   // one-shot inbox capacity per source rank and parity
   int oneshot;         // AllReduce: run the one-shot protocol (bytes fit small_slot)
+  int ll;              // one-shot in the LL format (flag in every 64-bit word; rank_oneshot_ll)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
   long long spin_limit;  // clock64 cycles a wait may spin before aborting (FLX_TIMEOUT_S)
 };
@@ -370,7 +371,14 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
 // signalled after finishing round e-2 (every protocol awaits kArrive from
 // every peer every round).  The main slots are untouched, so last_main stays.
 template <typename T, int OP, int KIND>
+__device__ void rank_oneshot_ll(const RankArgs& a, int cta, int nctas);
+
+template <typename T, int OP, int KIND>
 __device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
+  if (a.ll) {
+    rank_oneshot_ll<T, OP, KIND>(a, cta, nctas);
+    return;
+  }
   FLX_PHASE(0);
   const int r = a.rank, n = a.nranks;
   const CtaEpochs ep = cta_epochs(a, cta);
@@ -420,6 +428,152 @@ __device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
   }
   FLX_PHASE(4);
   cta_epochs_done(ep, 1, ep.last_ar, ep.last_main);
+}
+
+// ---- LL one-shot: the epoch travels inside every 64-bit word of the data ----
+//
+// The one-shot above pays two sys-scope operations per call: the release
+// signal after the push (a fence that drains every outstanding store, ~1.5-2
+// us, tools/flag_pingpong.cu) and the acquire wait.  For slices whose CTA part
+// fits kLLRegion / 2, the push instead stores 32-byte packets: 16 B of data as
+// four 64-bit words {data32 | epoch << 32}, written with plain (volatile)
+// 64-bit-element vector stores.  Each 64-bit element is single-copy atomic, so
+// a reader that sees the epoch in a word's high half sees that word's data:
+// no fence, no flag, the receiver polls the packets themselves (NCCL's LL
+// protocol, with 64-bit elements so the PTX model guarantees it).
+//
+// The packets live in their own area after the one-shot inboxes,
+// [2 parities][N sources][kMaxCtas regions of kLLRegion], zeroed at init and
+// only ever written with LL packets, so a stale word carries an older epoch
+// (epochs start at 1 and are unique per CTA) and is never mistaken for the
+// current one.  Parity reuse: round e overwrites what peer CTA b read in
+// round e-2; in round e-1 this CTA received every peer's packets (an empty
+// part still sends one packet), which that peer wrote in a later kernel than
+// its round e-2 reads.  Every rank computes the same parts (same bytes, same
+// grid), so sender and receiver agree on the packet count.
+constexpr size_t kLLRegion = 8192;  // packet bytes per (parity, source, CTA): 4 KiB of data
+constexpr size_t kLLSlot = kLLRegion * kMaxCtas;
+
+__device__ __forceinline__ void st_ll(char* p, const uint4& d, uint32_t e) {
+  const uint64_t f = (uint64_t)e << 32;
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(f | d.x), "l"(f | d.y)
+               : "memory");
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(p + 16), "l"(f | d.z),
+               "l"(f | d.w)
+               : "memory");
+}
+
+// Poll one packet until its four words carry epoch e (false: timed out or
+// another wait aborted; the abort word is host memory, polled rarely).
+__device__ __forceinline__ bool ld_ll(const char* p, uint32_t e, uint4* out, const RankArgs& a,
+                                      long long t0) {
+  uint32_t spins = 0;
+  while (true) {
+    uint64_t w0, w1, w2, w3;
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(p) : "memory");
+    asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];"
+                 : "=l"(w2), "=l"(w3)
+                 : "l"(p + 16)
+                 : "memory");
+    if ((uint32_t)(w0 >> 32) == e && (uint32_t)(w1 >> 32) == e && (uint32_t)(w2 >> 32) == e &&
+        (uint32_t)(w3 >> 32) == e) {
+      *out = make_uint4((uint32_t)w0, (uint32_t)w1, (uint32_t)w2, (uint32_t)w3);
+      return true;
+    }
+    if ((++spins & 4095) == 0 &&
+        (*(volatile uint32_t*)a.abort_word || clock64() - t0 > a.spin_limit)) {
+      atomicExch(a.abort_word, 1u);
+      return false;
+    }
+  }
+}
+
+// m (<= 16) bytes of user memory at any alignment, zero-padded to 16.
+__device__ __forceinline__ uint4 ld_user(const char* p, size_t m) {
+  if (m == 16 && aligned16_dev(p)) return *reinterpret_cast<const uint4*>(p);
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (size_t i = 0; i < m; ++i) w[i >> 2] |= (uint32_t)(uint8_t)p[i] << (8 * (i & 3));
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void st_user(char* p, const uint4& v, size_t m) {
+  if (m == 16 && aligned16_dev(p)) {
+    *reinterpret_cast<uint4*>(p) = v;
+    return;
+  }
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+  for (size_t i = 0; i < m; ++i) p[i] = (char)(w[i >> 2] >> (8 * (i & 3)));
+}
+
+template <typename T, int OP, int KIND>
+__device__ void rank_oneshot_ll(const RankArgs& a, int cta, int nctas) {
+  using A = typename AccT<T>::type;
+  constexpr int kVec = 16 / sizeof(T);
+  FLX_PHASE(0);
+  const int r = a.rank, n = a.nranks;
+  const CtaEpochs ep = cta_epochs(a, cta);
+  const uint32_t e = ep.first;
+  const size_t area = a.slot * (n + 1) + 2 * (size_t)n * a.small_slot +
+                      (size_t)(e & 1) * n * kLLSlot + (size_t)cta * kLLRegion;
+  const size_t stride = a.rank_stride;
+  size_t lo, hi;
+  cta_part(a.bytes, nctas, cta, &lo, &hi);
+  const size_t len = hi - lo;
+  const size_t nvec = (len + 15) >> 4;
+  const size_t npk = nvec ? nvec : 1;  // an empty part still proves progress with one packet
+  auto inbox = [&](int holder, int src) {
+    return a.scratch[holder] + area + (size_t)src * kLLSlot;
+  };
+  auto valid = [&](size_t v) { return v < nvec ? min((size_t)16, len - 16 * v) : (size_t)0; };
+  FLX_PHASE(1);
+  for (int s = 1; s < n; ++s) {
+    const int c = (r + s) % n;
+    const char* piece = (KIND == 0 || KIND == 1) ? a.send + lo : a.send + (size_t)c * stride + lo;
+    char* dst = inbox(c, r);
+    for (size_t v = threadIdx.x; v < npk; v += blockDim.x)
+      st_ll(dst + 32 * v, ld_user(piece + 16 * v, valid(v)), e);
+  }
+  if (KIND == 1) {
+    char* own = a.recv + (size_t)r * stride + lo;
+    if (own != a.send + lo) cta_copy(own, a.send + lo, len, false);
+  } else if (KIND == 3) {
+    cta_copy(a.recv + (size_t)r * stride + lo, a.send + (size_t)r * stride + lo, len, false);
+  }
+  FLX_PHASE(2);
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const long long t0 = clock64();
+  bool ok = true;
+  if (KIND == 0 || KIND == 2) {
+    const char* own = KIND == 0 ? a.send + lo : a.send + (size_t)r * stride + lo;
+    for (size_t v = threadIdx.x; ok && v < npk; v += blockDim.x) {
+      const size_t m = valid(v);
+      A acc[kVec];
+      for (int p = 0; p < n; ++p) {  // the fixed rank-order fold (kernels.cuh rule)
+        uint4 w;
+        if (p == r) w = ld_user(own + 16 * v, m);
+        else if (!(ok = ld_ll(inbox(r, p) + 32 * v, e, &w, a, t0))) break;
+        if (p == 0) load_acc<T>(acc, w);
+        else fold_into<T, OP>(acc, w);
+      }
+      if (ok && m) st_user(a.recv + lo + 16 * v, pack_acc<T>(acc), m);
+    }
+  } else {
+    for (int s = 1; ok && s < n; ++s) {
+      const int p = (r - s + n) % n;
+      for (size_t v = threadIdx.x; v < npk; v += blockDim.x) {
+        uint4 w;
+        if (!(ok = ld_ll(inbox(r, p) + 32 * v, e, &w, a, t0))) break;
+        const size_t m = valid(v);
+        if (m) st_user(a.recv + (size_t)p * stride + lo + 16 * v, w, m);
+      }
+    }
+  }
+  if (!ok) bad = 1;
+  __syncthreads();
+  FLX_PHASE(3);
+  if (!bad) cta_epochs_done(ep, 1, ep.last_ar, ep.last_main);
 }
 
 // After consuming my inbox slots for epoch e: tell every source (kFree = e).

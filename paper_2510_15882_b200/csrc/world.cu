@@ -92,6 +92,7 @@ struct World {
   size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
   long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
+  bool ll = true;          // one-shot slices that fit kLLRegion / 2 per CTA use the LL format (FLX_LL)
   size_t hcap = 0;       // PCIe staging bytes per rank region
   size_t pcie_chunk = 0;  // PCIe pipeline chunk, bytes per reader (FLX_PCIE_CHUNK_KB)
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
@@ -143,8 +144,11 @@ flxResult_t local_init(World* w, World::Local& L) {
   const double secs = to ? atof(to) : 10.0;
   w->spin_limit = (long long)(std::max(0.01, secs) * khz * 1e3);
   // [n inbox slots][outbox][one-shot inboxes: 2 parities x n sources]
-  const size_t scratch_bytes = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
+  // [LL packets: 2 parities x n sources x kLLSlot] (zeroed: epochs start at 1)
+  const size_t ll_off = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
+  const size_t scratch_bytes = ll_off + 2 * w->nranks * kLLSlot;
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
+  FLX_CUDA(cudaMemset(L.scratch + ll_off, 0, 2 * w->nranks * kLLSlot));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), (kFlagWords + kStateWords) * 4));
   FLX_CUDA(cudaMemset(L.flags, 0, (kFlagWords + kStateWords) * 4));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.dstage), w->hcap));
@@ -261,6 +265,8 @@ void world_config(World* w, int nranks) {
   const char* os = getenv("FLX_ONESHOT_KB");
   w->oneshot_max = (size_t)(os ? atoll(os) : 256) << 10;
   w->small_slot = std::max<size_t>(2 * w->oneshot_max, 16 * kMaxCtas);
+  const char* ll = getenv("FLX_LL");
+  w->ll = !(ll && atoi(ll) == 0);
 }
 
 template <typename F>
@@ -572,6 +578,10 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.oneshot = w->oneshot_max > 0 && n > 1 &&
                   nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas &&
                   (gather || scatter || a2a || nv <= w->oneshot_max);
+      // LL format when every CTA part fits half an LL region; depends only on
+      // rank-agreed values (bytes, grid), never on buffer addresses
+      a.ll = a.oneshot && w->ll &&
+             2 * ((((nv + w->nctas - 1) / w->nctas) + 15) & ~(size_t)15) <= kLLRegion;
       a.abort_word = w->abort_word;
       a.spin_limit = w->spin_limit;
     }

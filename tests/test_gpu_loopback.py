@@ -380,3 +380,58 @@ def test_loopback_sixteen_ranks(count):
     for r in range(n):
         np.testing.assert_array_equal(_np(recvs[r], 7), want[r])
         np.testing.assert_array_equal(_np(ag[r], 7), want_ag[r])
+
+
+@pytest.mark.parametrize("ll", ["1", "0"])
+def test_loopback_ll_and_flagged_oneshot_interleaved(ll):
+    # Small slices run the LL one-shot (epoch inside every 64-bit word, no
+    # fence), mid-size ones the flagged one-shot, large ones the slot
+    # protocols; the three share the per-CTA epochs and the one-shot parities.
+    # Every collective, ragged sizes (some CTAs get empty parts), buffers at
+    # 4-byte offsets (the LL path's unaligned user loads/stores), in place.
+    n = 8
+    os.environ["FLX_LL"] = ll
+    try:
+        w = flx.Clique(n, loopback=True)
+    finally:
+        del os.environ["FLX_LL"]
+    with w:
+        for op in CollectiveOp:
+            w.set_shares(op, (1000, 0, 0))
+        al = {op: w.comms[0].alignment(op) for op in CollectiveOp}
+        g1 = (1000, 0, 0)
+        sizes = [3, 1000, 4097, 25600, 18 * 1024, 200000, 1, 9000, 25601, 7]
+        for it, count in enumerate(sizes):
+            dtype = (7, 9, 6, 2)[it % 4]
+            off = it % 2  # one element in: 4 B (fp32/int32) or 2 B (16-bit) aligned
+            cpu = _inputs(n, n * count, dtype, 500 + it)
+            base = [torch.zeros(n * count + 1, dtype=TORCH_DT[dtype], device="cuda")
+                    for _ in range(n)]
+            sends = [b[off:off + n * count] for b in base]
+            for s, c in zip(sends, cpu):
+                s.copy_(c)
+            ar = sends if it % 3 == 2 else [torch.empty_like(s) for s in sends]
+            hn = [_np(c, dtype) for c in cpu]
+            w.all_reduce(sends, ar)
+            torch.cuda.synchronize()
+            want = oracle.allreduce(hn, dtype, 0, g1, al[CollectiveOp.ALLREDUCE])
+            for r in range(n):
+                np.testing.assert_array_equal(_np(ar[r], dtype), want[r], err_msg=f"ar {it}")
+            for s, c in zip(sends, cpu):  # restore after an in-place call
+                s.copy_(c)
+            ag = [torch.empty(n * count, dtype=TORCH_DT[dtype], device="cuda") for _ in range(n)]
+            w.all_gather([s[:count] for s in sends], ag)
+            rs = [torch.empty(count, dtype=TORCH_DT[dtype], device="cuda") for _ in range(n)]
+            w.reduce_scatter(sends, rs)
+            a2a = [torch.empty_like(s) for s in sends]
+            w.all_to_all(sends, a2a)
+            torch.cuda.synchronize()
+            want_ag = oracle.allgather([x[:count] for x in hn], dtype, g1,
+                                       al[CollectiveOp.ALLGATHER])
+            want_rs = oracle.reducescatter(hn, dtype, 0, g1, al[CollectiveOp.REDUCESCATTER])
+            want_a2a = oracle.alltoall(hn, dtype, g1, al[CollectiveOp.ALLTOALL])
+            for r in range(n):
+                np.testing.assert_array_equal(_np(ag[r], dtype), want_ag[r], err_msg=f"ag {it}")
+                np.testing.assert_array_equal(_np(rs[r], dtype), want_rs[r], err_msg=f"rs {it}")
+                np.testing.assert_array_equal(_np(a2a[r], dtype), want_a2a[r],
+                                              err_msg=f"a2a {it}")

@@ -62,6 +62,7 @@ int main(int argc, char** argv) {
     a.slot = slot;
     a.small_slot = small;
     a.oneshot = oneshot;
+    a.ll = 0;  // the LL area is not allocated here
     a.abort_word = abort_dev;
     a.spin_limit = 20000000000ll;
   }

@@ -451,7 +451,7 @@ __device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
 // part still sends one packet), which that peer wrote in a later kernel than
 // its round e-2 reads.  Every rank computes the same parts (same bytes, same
 // grid), so sender and receiver agree on the packet count.
-constexpr size_t kLLRegion = 8192;  // packet bytes per (parity, source, CTA): 4 KiB of data
+constexpr size_t kLLRegion = 32768;  // packet bytes per (parity, source, CTA): 16 KiB of data
 constexpr size_t kLLSlot = kLLRegion * kMaxCtas;
 
 __device__ __forceinline__ void st_ll(char* p, const uint4& d, uint32_t e) {

@@ -575,13 +575,15 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       // (every CTA part <= its region); AllReduce also below FLX_ONESHOT_KB
       // (above it the two-shot's 2(N-1)/N traffic wins), the other protocols
       // move the same bytes either way and save a signal hop
-      a.oneshot = w->oneshot_max > 0 && n > 1 &&
-                  nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas &&
+      // (or, in the LL format, when every CTA part fits half an LL region).
+      // Depends only on rank-agreed values (bytes, grid), never on addresses.
+      const size_t part = (((nv + w->nctas - 1) / w->nctas) + 15) & ~(size_t)15;
+      const bool fits_ll = w->ll && 2 * part <= kLLRegion;
+      const bool fits_flagged =
+          nv <= ((w->small_slot / kMaxCtas) & ~(size_t)15) * (size_t)w->nctas;
+      a.oneshot = w->oneshot_max > 0 && n > 1 && (fits_ll || fits_flagged) &&
                   (gather || scatter || a2a || nv <= w->oneshot_max);
-      // LL format when every CTA part fits half an LL region; depends only on
-      // rank-agreed values (bytes, grid), never on buffer addresses
-      a.ll = a.oneshot && w->ll &&
-             2 * ((((nv + w->nctas - 1) / w->nctas) + 15) & ~(size_t)15) <= kLLRegion;
+      a.ll = a.oneshot && fits_ll;
       a.abort_word = w->abort_word;
       a.spin_limit = w->spin_limit;
     }

@@ -3,7 +3,9 @@
  *
  * NCCL-shaped striped collectives: every AllReduce / AllGather message is
  * split by integer granule shares (1000 total) into contiguous per-path byte
- * slices — NVLink first at offset 0, then host-staged PCIe, then RDMA — and
+ * slices — host-staged PCIe at offset 0, then RDMA, then NVLink last (it
+ * takes partition()'s remainder at its end, so the secondary slices stay on
+ * the alignment grid for any message length) — and
  * each slice runs a complete collective on its own path concurrently.
  *
  * The reference ("linkstripe", /root/reference/pkg/src/linkstripe) is a CPU
@@ -89,6 +91,9 @@ flxResult_t flxGetVersion(int* version);
 const char* flxGetErrorString(flxResult_t result);
 /* Last detailed error message of this thread (never NULL). */
 const char* flxGetLastError(void);
+/* Replace this thread's detailed error message (the NCCL shim uses it to
+ * explain the NCCL calls FlexLink refuses). */
+void flxSetLastError(const char* message);
 
 /* ---- communicators (ncclGetUniqueId / ncclCommInitRank / ncclCommInitAll /
  *      ncclCommDestroy shapes, nccl.h) ----------------------------------- */

@@ -18,9 +18,10 @@
  *     (reduce-scatter) and then circulated to every rank (all-gather) —
  *     2(N-1) steps for AllReduce, N-1 for AllGather (ring_steps,
  *     collectives.py:31-39).
- * The byte layout of the slices (NVLINK at offset 0, then PCIE, then RDMA) and
- * the reduction order are not defined by the reference; this
- * build fixes them: every element is reduced entirely inside one path by the
+ * The byte layout of the slices (PCIE at offset 0, then RDMA, then NVLINK,
+ * which absorbs the remainder at its end so the secondary slices stay on the
+ * alignment grid) and the reduction order are not defined by the reference
+ * (SURVEY.md §8c); this build fixes them: every element is reduced entirely inside one path by the
  * left fold acc = x[0]; acc = op(acc, x[r]) for r = 1..N-1 in rank order,
  * accumulated in fp32 for fp16/bf16 (one final RNE rounding), in the native
  * type otherwise (integers wrap).  AllGather is a pure byte copy.
@@ -37,6 +38,8 @@
 
 enum { I8 = 0, U8 = 1, I32 = 2, U32 = 3, I64 = 4, U64 = 5, F16 = 6, F32 = 7, F64 = 8, BF16 = 9 };
 enum { SUM = 0, PROD = 1, MAX = 2, MIN = 3 };
+/* slice order in a rank's message: pcie (1), rdma (2), nvlink (0) last */
+static const uint64_t kOrder[3] = {1, 2, 0};
 
 /* ------------------------------------------------------------ conversions */
 static inline float bits_to_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
@@ -224,7 +227,7 @@ int flxo_allreduce(const void* const* send, void* const* recv, int nranks, uint6
   if (!esz || !fold || nranks < 1 || op < 0 || op > 3) return -1;
   uint64_t split[3];
   if (flxo_partition(count * esz, granules, alignment, split)) return -1;
-  for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p) {
+  for (uint64_t k = 0, p = kOrder[0], at = 0; k < 3; at += split[p], p = kOrder[++k % 3]) {
     if (split[p] % esz) return -2; /* slice boundary inside an element */
     const uint64_t e0 = at / esz, elems = split[p] / esz;
     const uint64_t per = (elems + nranks - 1) / nranks; /* ring chunk per owner */
@@ -256,7 +259,7 @@ int flxo_allgather(const void* const* send, void* const* recv, int nranks, uint6
   uint64_t split[3];
   if (flxo_partition(bytes, granules, alignment, split)) return -1;
   set_threads(threads);
-  for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p) {
+  for (uint64_t k = 0, p = kOrder[0], at = 0; k < 3; at += split[p], p = kOrder[++k % 3]) {
     const uint64_t len = split[p];
     if (!len) continue;
 #pragma omp parallel for collapse(2) schedule(static)
@@ -290,7 +293,7 @@ int flxo_reducescatter(const void* const* send, void* const* recv, int nranks,
     void* dst[1] = {recv[r]};
     for (int q = 0; q < nranks; ++q)
       rows[q] = (const char*)send[q] + (uint64_t)r * recvcount * esz;
-    for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p)
+    for (uint64_t k = 0, p = kOrder[0], at = 0; k < 3; at += split[p], p = kOrder[++k % 3])
       if (split[p]) fold(rows, dst, nranks, 1, at / esz, (at + split[p]) / esz, op);
   }
   return 0;
@@ -309,7 +312,7 @@ int flxo_alltoall(const void* const* send, void* const* recv, int nranks, uint64
   uint64_t split[3];
   if (flxo_partition(block, granules, alignment, split)) return -1;
   set_threads(threads);
-  for (uint64_t p = 0, at = 0; p < 3; at += split[p], ++p) {
+  for (uint64_t k = 0, p = kOrder[0], at = 0; k < 3; at += split[p], p = kOrder[++k % 3]) {
     if (!split[p]) continue;
 #pragma omp parallel for collapse(2) schedule(static)
     for (int q = 0; q < nranks; ++q)

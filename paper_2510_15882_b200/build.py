@@ -18,9 +18,9 @@ HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libflexlink.so"
-SOURCES = ["flexlink.cu", "launch.cu", "world.cu"]
+SOURCES = ["flexlink.cu", "launch.cu", "world.cu", "tuner.cpp", "autotune.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]
 
 
@@ -42,7 +42,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     nvcc = _nvcc()
     objdir = HERE / "build"
     objdir.mkdir(exist_ok=True)
-    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + [ROOT / "include" / "flexlink.h"]
+    headers = list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list((ROOT / "include").glob("*.h"))
     srcs = [CSRC / s for s in SOURCES if (CSRC / s).exists()]
     objs = [objdir / (s.stem + ".o") for s in srcs]
 

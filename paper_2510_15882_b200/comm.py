@@ -342,6 +342,70 @@ class Communicator:
         m = self.path_mask()
         return tuple(k for k in PathKind if m & (1 << int(k)))
 
+    # ---- in-library balancer (include/flexlink_tuner.h)
+    def set_autotune(self, enabled: bool) -> None:
+        """``flxSetAutoTune``: Stage 1 + Stage 2 inside the library for every
+        (collective, size bucket) the user did not pin with :meth:`set_shares`."""
+        from . import tuner_native as tn
+
+        _check(tn.lib().flxSetAutoTune(self._h, int(bool(enabled))), "flxSetAutoTune")
+
+    def set_tuner_config(self, stage1=None, stage2=None, min_bytes: int = 0) -> None:
+        """TunerConfig / BalancerConfig of the in-library balancer, and the smallest
+        per-rank message it tunes."""
+        from . import tuner_native as tn
+
+        s1 = ctypes.byref(tn.config_c(stage1)) if stage1 is not None else None
+        s2 = ctypes.byref(tn.balancer_config_c(stage2)) if stage2 is not None else None
+        _check(tn.lib().flxSetTunerConfig(self._h, s1, s2, int(min_bytes)), "flxSetTunerConfig")
+
+    def set_link_profile(self, topo) -> None:
+        """Seed Stage 1 from a (probed) TopologySpec instead of the in-call probe
+        round; ``None`` restores the probe."""
+        from . import tuner_native as tn
+
+        prof = ctypes.byref(tn.profile_from_topology(topo)) if topo is not None else None
+        _check(tn.lib().flxSetLinkProfile(self._h, prof), "flxSetLinkProfile")
+
+    def tune_info(self, op: CollectiveOp, nbytes: int) -> dict:
+        """The autotuner's state for the size bucket of ``nbytes`` (per rank)."""
+        from . import tuner_native as tn
+
+        info = tn.TuneInfoC()
+        _check(tn.lib().flxGetTuneInfo(self._h, _COLL[CollectiveOp(op)], size_bucket(nbytes),
+                                       ctypes.byref(info)), "flxGetTuneInfo")
+        return info.as_dict()
+
+    def tune_trace(self, op: CollectiveOp, nbytes: int, max_records: int = 128) -> list[dict]:
+        """The in-library Stage-1 trace in the reference's record shape."""
+        from . import tuner_native as tn
+
+        recs = (tn.TuneRecordC * max_records)()
+        n = ctypes.c_int()
+        _check(tn.lib().flxGetTuneTrace(self._h, _COLL[CollectiveOp(op)], size_bucket(nbytes),
+                                        recs, max_records, ctypes.byref(n)), "flxGetTuneTrace")
+        out = []
+        for r in recs[:n.value]:
+            out.append({"iteration": r.iteration, "action": r.action_string(),
+                        "imbalance": r.imbalance, "shares": list(r.shares),
+                        "durations_ms": [r.durations[p] if r.timed_mask >> p & 1 else None
+                                         for p in range(3)]})
+        return out
+
+    def tune_evaluations(self, op: CollectiveOp, nbytes: int, max_records: int = 256) -> list:
+        """The in-library Stage-2 evaluations (oldest first)."""
+        from . import tuner_native as tn
+
+        recs = (tn.EvalRecordC * max_records)()
+        n = ctypes.c_int()
+        _check(tn.lib().flxGetTuneEvaluations(self._h, _COLL[CollectiveOp(op)],
+                                              size_bucket(nbytes), recs, max_records,
+                                              ctypes.byref(n)), "flxGetTuneEvaluations")
+        return [{"call": r.call, "gap": r.gap if r.has_gap else None, "moved": r.moved,
+                 "source": r.source if r.adjusted else None,
+                 "target": r.target if r.adjusted else None, "shares": list(r.shares)}
+                for r in recs[:n.value]]
+
 
 def share_key_bytes(op: CollectiveOp, send, recv, nranks: int) -> int:
     """The per-rank byte count the C executor partitions (and keys shares on):
@@ -548,6 +612,27 @@ class Clique:
     def set_timing(self, enabled: bool) -> None:
         for c in self.comms:
             c.set_timing(enabled)
+
+    def set_autotune(self, enabled: bool) -> None:
+        for c in self.comms:
+            c.set_autotune(enabled)
+
+    def set_tuner_config(self, stage1=None, stage2=None, min_bytes: int = 0) -> None:
+        for c in self.comms:
+            c.set_tuner_config(stage1, stage2, min_bytes)
+
+    def set_link_profile(self, topo) -> None:
+        for c in self.comms:
+            c.set_link_profile(topo)
+
+    def tune_info(self, op: CollectiveOp, nbytes: int) -> dict:
+        return self.comms[0].tune_info(op, nbytes)
+
+    def tune_trace(self, op: CollectiveOp, nbytes: int) -> list[dict]:
+        return self.comms[0].tune_trace(op, nbytes)
+
+    def tune_evaluations(self, op: CollectiveOp, nbytes: int) -> list[dict]:
+        return self.comms[0].tune_evaluations(op, nbytes)
 
     def path_times(self) -> dict[PathKind, float]:
         return self.comms[0].path_times()

@@ -20,6 +20,7 @@
 
 #include "internal.h"
 #include "args.h"
+#include "autotune.h"
 
 namespace flx {
 
@@ -166,10 +167,7 @@ flxResult_t current_device(int* dev) {
   return flxSuccess;
 }
 
-flxResult_t validate_comm(const flxComm* comm) {
-  if (comm == nullptr) return fail(flxInvalidArgument, "null communicator");
-  return flxSuccess;
-}
+flxResult_t validate_comm(const flxComm* comm);
 
 flxResult_t clique_create(int device, int members, Clique** out) {
   FLX_CUDA(cudaSetDevice(device));
@@ -181,6 +179,8 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   auto* c = new Clique();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;
+  c->gpu_name = prop.name;
+  c->tuner = new AutoTuner();
   FLX_CUDA(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&c->red, cudaStreamNonBlocking));
@@ -247,24 +247,47 @@ flxResult_t clique_destroy(Clique* c) {
   for (auto e : c->ev_fork) cudaEventDestroy(e);
   if (c->host_stage) cudaFreeHost(c->host_stage);
   if (c->dev_stage) cudaFree(c->dev_stage);
+  for (char* p : c->retired_host) cudaFreeHost(p);
+  for (char* p : c->retired_dev) cudaFree(p);
   if (c->sems) c->sems_on_host ? cudaFreeHost(c->sems) : cudaFree(c->sems);
+  delete c->tuner;
   delete c;
   return flxSuccess;
 }
 
 // Grow the staging ring to hold `chunk` bytes per member in `bufs` buffers.
-// Only called after the side streams have drained (the ring may be in use).
+// Grow-only: a CUDA graph captured earlier bakes the current ring's pointers
+// into its copy nodes, so a ring is never freed while the clique lives — a
+// larger ring replaces it and the old one is retired (freed in
+// clique_destroy).  The first ring is sized for the largest automatic chunk
+// (pick_chunk: 4 MiB per member) so eager calls of growing size do not keep
+// reallocating.
 flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
-  if (c->stage_cap >= chunk && c->stage_bufs == bufs) return flxSuccess;
+  if (c->stage_cap >= chunk && c->stage_bufs >= bufs) {
+    if (c->ring_depth == bufs) return flxSuccess;
+    // a new pipeline depth re-indexes the counter words: restart the protocol
+    FLX_CUDA(cudaStreamSynchronize(c->d2h));
+    FLX_CUDA(cudaStreamSynchronize(c->h2d));
+    FLX_CUDA(cudaStreamSynchronize(c->red));
+    if (c->sems_on_host)
+      memset(c->sems, 0, 4096);
+    else
+      FLX_CUDA(cudaMemset(c->sems, 0, 4096));
+    FLX_CUDA(cudaDeviceSynchronize());
+    c->piece_seq = 0;
+    c->ring_depth = bufs;
+    return flxSuccess;
+  }
   FLX_CUDA(cudaStreamSynchronize(c->d2h));
   FLX_CUDA(cudaStreamSynchronize(c->h2d));
   FLX_CUDA(cudaStreamSynchronize(c->red));
-  if (c->host_stage) FLX_CUDA(cudaFreeHost(c->host_stage));
-  if (c->dev_stage) FLX_CUDA(cudaFree(c->dev_stage));
+  if (c->host_stage) c->retired_host.push_back(c->host_stage);
+  if (c->dev_stage) c->retired_dev.push_back(c->dev_stage);
   c->host_stage = nullptr;
   c->dev_stage = nullptr;
-  const size_t cap = std::max(chunk, c->stage_cap);
-  const size_t total = cap * c->members.size() * bufs;
+  const size_t cap = std::max(std::max(chunk, c->stage_cap), (size_t)kMaxAutoChunk);
+  const int nb = std::max(std::max(bufs, c->stage_bufs), 2);
+  const size_t total = cap * c->members.size() * nb;
   FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_stage), total, cudaHostAllocPortable));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&c->dev_stage), total));
   // a fresh ring starts a fresh protocol epoch: counters restart from zero
@@ -275,7 +298,8 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
   FLX_CUDA(cudaDeviceSynchronize());
   c->piece_seq = 0;
   c->stage_cap = cap;
-  c->stage_bufs = bufs;
+  c->stage_bufs = nb;
+  c->ring_depth = bufs;
   return flxSuccess;
 }
 
@@ -285,7 +309,7 @@ size_t pick_chunk(const Comm* lead, size_t bytes) {
   size_t chunk = lead->chunk_bytes;
   if (chunk == 0) {
     chunk = (bytes / 8 + 4095) / 4096 * 4096;
-    chunk = std::min<size_t>(std::max<size_t>(chunk, 64 << 10), 4 << 20);
+    chunk = std::min<size_t>(std::max<size_t>(chunk, 64 << 10), kMaxAutoChunk);
   }
   return chunk;
 }
@@ -305,6 +329,23 @@ struct Call {
 thread_local int t_group_depth = 0;
 thread_local std::vector<Call> t_pending;
 
+// The autotuner's view of a clique: one timing ring, one process (no
+// agreement needed — every virtual rank shares the same events).
+struct CliquePort : TimingPort {
+  Clique* c;
+  explicit CliquePort(Clique* c_) : c(c_) {}
+  flxResult_t read(uint64_t seq, float ms[FLX_NUM_PATHS]) override;
+  flxResult_t agree_max(double*, int) override { return flxSuccess; }
+  uint64_t calls() const override { return c->calls; }
+  std::string scope() const override {
+    std::string name = c->gpu_name;
+    for (char& ch : name)
+      if (ch == ' ') ch = '_';
+    return name + "/virtual/n" + std::to_string(c->members.size());
+  }
+  bool cache_writer() const override { return true; }
+};
+
 // One collective over all members of a clique.  calls[i] belongs to member i.
 flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   const int n = (int)c->members.size();
@@ -323,10 +364,31 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   FLX_CUDA(cudaSetDevice(c->device));
   const size_t esz = dtype_size(head.dtype);
   const size_t bytes = head.count * esz;  // per-rank send bytes
-  const Granules g = lead->shares[head.coll].lookup(head.coll, bytes);
-  for (int i = 1; i < n; ++i)
-    if (calls[i].comm->shares[head.coll].lookup(head.coll, bytes) != g)
+  const Granules fallback = lead->shares[head.coll].lookup(head.coll, bytes);
+  const bool pinned = lead->shares[head.coll].pinned(head.coll, bytes);
+  for (int i = 1; i < n; ++i) {
+    const Comm* m = calls[i].comm;
+    if (m->shares[head.coll].lookup(head.coll, bytes) != fallback ||
+        m->shares[head.coll].pinned(head.coll, bytes) != pinned)
       return fail(flxInvalidUsage, "rank %d has different shares than rank 0", i);
+    if (m->autotune != lead->autotune || m->tune_min_bytes != lead->tune_min_bytes)
+      return fail(flxInvalidUsage, "rank %d has a different autotune setting than rank 0", i);
+  }
+  cudaStream_t s0 = head.stream;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FLX_CUDA(cudaStreamIsCapturing(s0, &cap));
+  const bool capturing = cap == cudaStreamCaptureStatusActive;
+  // the split: the pinned / default share table, or the in-library balancer's
+  Granules g = fallback;
+  bool measured = false;
+  {
+    const bool tunable = !pinned && lead->autotune && lead->timing && bytes >= lead->tune_min_bytes;
+    CliquePort port(c);
+    const TunePolicy pol{lead->tune_s1, lead->tune_s2, lead->have_profile, lead->profile,
+                         lead->nvlink_ctas};
+    FLX_TRY(c->tuner->before_call(port, pol, head.coll, bytes, tunable, !capturing, path_mask(),
+                                  fallback, &g, &measured));
+  }
   auto split = partition(bytes, g, alignment_for(lead, head.coll));
   if (split[flxPathRdma] > 0)
     return fail(flxInvalidUsage, "rdma path is not available on this box");
@@ -334,18 +396,16 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     return fail(flxInvalidUsage, "pcie path is not available (no stream memory ops)");
 
   // fork: every member's stream joins the lead stream
-  cudaStream_t s0 = head.stream;
   for (int i = 1; i < n; ++i) {
     if (calls[i].stream == s0) continue;
     FLX_CUDA(cudaEventRecord(c->ev_fork[i], calls[i].stream));
     FLX_CUDA(cudaStreamWaitEvent(s0, c->ev_fork[i], 0));
   }
-  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-  FLX_CUDA(cudaStreamIsCapturing(s0, &cap));
-  const bool capturing = cap == cudaStreamCaptureStatusActive;
   Clique::Timing& tm = c->timing[c->calls % Clique::kTimingSlots];
   const size_t nv = split[flxPathNvlink];
   const size_t pc = split[flxPathPcie];
+  const auto offs = path_offsets(split);
+  const size_t off_nv = offs[flxPathNvlink], off_pc = offs[flxPathPcie];
   // events recorded inside a capture are graph edges, not timestamps
   const bool timed = lead->timing && !capturing;
   const cudaEvent_t ev_start = timed ? tm.start : c->ev_start_nt;
@@ -375,12 +435,12 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     const size_t chunk = pick_chunk(lead, pc);
     // ReduceScatter stages every (source, row) pair: n*n rows of one chunk
     const size_t need = rows ? chunk * n : chunk;
-    if (capturing && (c->stage_cap < need || c->stage_bufs != lead->buffers))
+    if (capturing && (c->stage_cap < need || c->ring_depth != lead->buffers))
       return fail(flxInvalidUsage,
                   "PCIe staging must be sized before CUDA-graph capture: run the collective "
                   "once eagerly with the same size/shares first");
     FLX_TRY(ensure_staging(c, need, lead->buffers));
-    const int bufs = c->stage_bufs;
+    const int bufs = c->ring_depth;
     const size_t pitch = rows ? chunk : c->stage_cap;  // row pitch in the slot
     const size_t slot_bytes = c->stage_cap * n;
     FLX_CUDA(cudaStreamWaitEvent(c->d2h, ev_start, 0));
@@ -392,7 +452,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     bool drained_rec[2] = {false, false}, folded_rec[2] = {false, false};
     for (size_t done = 0; done < pc; done += chunk) {
       const size_t len = std::min(chunk, pc - done);
-      const size_t at = nv + done;  // byte offset inside each rank's message
+      const size_t at = off_pc + done;  // byte offset inside each rank's message
       // Under capture the monotone counters cannot be baked into a graph that
       // is replayed, so the same handshake is expressed with captured events
       // (graph edges); the eager counters are left untouched.
@@ -491,8 +551,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     if (gather) {
       FanoutArgs a{};
       for (int i = 0; i < n; ++i) {
-        a.src[i] = static_cast<const char*>(calls[i].send);
-        a.dst[i] = static_cast<char*>(calls[i].recv);
+        a.src[i] = static_cast<const char*>(calls[i].send) + off_nv;
+        a.dst[i] = static_cast<char*>(calls[i].recv) + off_nv;
       }
       a.nsrc = a.ndst = n;
       a.bytes = nv;
@@ -508,8 +568,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     } else if (a2a) {
       XposeArgs a{};
       for (int i = 0; i < n; ++i) {
-        a.src[i] = static_cast<const char*>(calls[i].send);
-        a.dst[i] = static_cast<char*>(calls[i].recv);
+        a.src[i] = static_cast<const char*>(calls[i].send) + off_nv;
+        a.dst[i] = static_cast<char*>(calls[i].recv) + off_nv;
       }
       a.n = n;
       a.bytes = nv;
@@ -519,8 +579,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     } else if (scatter) {
       RowsArgs a{};
       for (int i = 0; i < n; ++i) {
-        a.src[i] = static_cast<const char*>(calls[i].send);
-        a.dst[i] = static_cast<char*>(calls[i].recv);
+        a.src[i] = static_cast<const char*>(calls[i].send) + off_nv;
+        a.dst[i] = static_cast<char*>(calls[i].recv) + off_nv;
       }
       a.n = a.nrows = n;
       a.bytes = nv;
@@ -529,8 +589,8 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
     } else {
       FoldArgs a{};
       for (int i = 0; i < n; ++i) {
-        a.src[i] = static_cast<const char*>(calls[i].send);
-        a.dst[i] = static_cast<char*>(calls[i].recv);
+        a.src[i] = static_cast<const char*>(calls[i].send) + off_nv;
+        a.dst[i] = static_cast<char*>(calls[i].recv) + off_nv;
       }
       a.n = a.ndst = n;
       a.bytes = nv;
@@ -554,6 +614,7 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   tm.used[flxPathNvlink] = nv > 0 && timed;
   tm.used[flxPathPcie] = pc > 0 && timed;
   tm.used[flxPathRdma] = false;
+  c->tuner->after_call(head.coll, bytes, c->calls, split, measured);
   c->calls++;
   return flxSuccess;
 }
@@ -567,20 +628,24 @@ flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
   std::vector<cudaStream_t> streams;
   const size_t bytes = head.count * dtype_size(head.dtype);
   const Granules g = lead->shares[head.coll].lookup(head.coll, bytes);
+  const bool pinned = lead->shares[head.coll].pinned(head.coll, bytes);
   for (size_t i = 0; i < calls.size(); ++i) {
     const Call& k = calls[i];
     if (k.coll != head.coll || k.count != head.count || k.dtype != head.dtype || k.op != head.op)
       return fail(flxInvalidUsage, "local rank %zu called a different collective", i);
-    if (k.comm->shares[head.coll].lookup(head.coll, bytes) != g)
+    if (k.comm->shares[head.coll].lookup(head.coll, bytes) != g ||
+        k.comm->shares[head.coll].pinned(head.coll, bytes) != pinned)
       return fail(flxInvalidUsage, "local rank %zu has different shares", i);
+    if (k.comm->autotune != lead->autotune || k.comm->tune_min_bytes != lead->tune_min_bytes)
+      return fail(flxInvalidUsage, "local rank %zu has a different autotune setting", i);
     if (k.comm->timing != lead->timing)
       return fail(flxInvalidUsage, "local rank %zu has a different timing setting", i);
     send.push_back(k.send);
     recv.push_back(k.recv);
     streams.push_back(k.stream);
   }
-  return run_world(w, send, recv, streams, head.coll, head.count, head.dtype, head.op, g,
-                   alignment_for(lead, head.coll), lead->timing);
+  return run_world_tuned(w, send, recv, streams, head.coll, head.count, head.dtype, head.op, *lead,
+                         pinned, g, path_mask(), alignment_for(lead, head.coll));
 }
 
 flxResult_t flush_group() {
@@ -656,6 +721,17 @@ flxResult_t read_timing(Clique* c, uint64_t seq, float ms[3]) {
   return flxSuccess;
 }
 
+flxResult_t CliquePort::read(uint64_t seq, float ms[FLX_NUM_PATHS]) {
+  return read_timing(c, seq, ms);
+}
+
+void init_tuning(Comm* c) {
+  c->autotune = autotune_default();
+  c->tune_min_bytes = autotune_min_bytes_default();
+}
+
+AutoTuner* tuner_of(const Comm* c) { return c->clique ? c->clique->tuner : world_tuner(c->world); }
+
 flxResult_t check_call(const flxComm* comm, int dtype, int op, bool reduce) {
   FLX_TRY(validate_comm(comm));
   if (dtype < 0 || dtype >= flxNumTypes) return fail(flxInvalidArgument, "bad datatype %d", dtype);
@@ -670,6 +746,18 @@ flxResult_t check_call(const flxComm* comm, int dtype, int op, bool reduce) {
 using namespace flx;
 
 struct flxComm : public flx::Comm {};
+
+namespace flx {
+namespace {
+flxResult_t validate_comm(const flxComm* comm) {
+  if (comm == nullptr) return fail(flxInvalidArgument, "null communicator");
+  if (static_cast<const Comm*>(comm)->magic != kCommMagic)
+    return fail(flxInvalidArgument,
+                "not a live FlexLink communicator (destroyed, or a handle from another library)");
+  return flxSuccess;
+}
+}  // namespace
+}  // namespace flx
 
 // ====================================================================== ABI
 extern "C" {
@@ -695,6 +783,8 @@ const char* flxGetErrorString(flxResult_t r) {
 }
 
 const char* flxGetLastError(void) { return t_last_error.c_str(); }
+
+void flxSetLastError(const char* message) { t_last_error = message ? message : ""; }
 
 flxResult_t flxGetUniqueId(flxUniqueId* id) {
   if (!id) return fail(flxInvalidArgument, "null id");
@@ -733,6 +823,10 @@ flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
     comm->nranks = ndev;
     comm->device = devs[i];
     comm->clique = c;
+    init_tuning(comm);
+    // FLX_NVLINK_CTAS caps the fused NVLink-path kernel (config 4) for
+    // programs that only use the NCCL names
+    if (const char* v = getenv("FLX_NVLINK_CTAS")) comm->nvlink_ctas = std::max(0, atoi(v));
     c->members.push_back(comm);
     comms[i] = comm;
   }
@@ -767,6 +861,7 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
   c->nranks = nranks;
   c->device = dev;
   c->world = w;
+  init_tuning(c);
   c->local = 0;
   world_attach(w, 0, c);
   *comm = c;
@@ -793,6 +888,7 @@ flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
     c->device = device;
     c->world = w;
     c->local = r;
+    init_tuning(c);
     world_attach(w, r, c);
     comms[r] = c;
   }
@@ -804,13 +900,17 @@ flxResult_t flxCommDestroy(flxComm_t comm) {
   std::lock_guard<std::mutex> lock(g_mutex);
   if (comm->world) {
     world_release(comm->world);
+    comm->magic = 0;
     delete comm;
     return flxSuccess;
   }
   Clique* c = comm->clique;
   c->destroyed++;
   if (c->destroyed == (int)c->members.size()) {
-    for (Comm* m : c->members) delete static_cast<flxComm*>(m);
+    for (Comm* m : c->members) {
+      m->magic = 0;
+      delete static_cast<flxComm*>(m);
+    }
     clique_destroy(c);
   }
   return flxSuccess;
@@ -956,6 +1056,7 @@ flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int g
   ShareTable& t = comm->shares[op];
   if (bucket == FLX_BUCKET_ALL) {
     t.fallback = g;
+    t.fallback_pinned = true;  // the user fixed every bucket: no autotuning
     t.entries.clear();
   } else {
     if (bucket < -1 || bucket > 63) return fail(flxInvalidArgument, "bad bucket %d", bucket);
@@ -972,7 +1073,10 @@ flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granule
   const ShareTable& t = comm->shares[op];
   Granules g = t.fallback;
   auto it = t.entries.find({(int)op, bucket});
-  if (bucket != FLX_BUCKET_ALL && it != t.entries.end()) g = it->second;
+  if (bucket != FLX_BUCKET_ALL && it != t.entries.end())
+    g = it->second;
+  else if (bucket != FLX_BUCKET_ALL && !t.fallback_pinned)
+    tuner_of(comm)->current(op, bucket, &g);  // the balancer's split, if it tuned this bucket
   for (int p = 0; p < FLX_NUM_PATHS; ++p) granules[p] = g[p];
   return flxSuccess;
 }
@@ -1065,6 +1169,66 @@ flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int writ
 flxResult_t flxGetLaunchCount(unsigned long long* count) {
   if (!count) return fail(flxInvalidArgument, "null count");
   *count = g_launches.load();
+  return flxSuccess;
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------ in-library balancer
+extern "C" {
+
+flxResult_t flxSetAutoTune(flxComm_t comm, int enabled) {
+  FLX_TRY(validate_comm(comm));
+  comm->autotune = enabled != 0;
+  return flxSuccess;
+}
+
+flxResult_t flxSetTunerConfig(flxComm_t comm, const flxTunerConfig* s1,
+                              const flxBalancerConfig* s2, size_t min_bytes) {
+  FLX_TRY(validate_comm(comm));
+  if (s1 && !tune::valid(*s1)) return fail(flxInvalidArgument, "bad tuner config");
+  if (s2 && (!tune::valid(*s2) || s2->window > 32))
+    return fail(flxInvalidArgument, "bad balancer config (window must be 1..32)");
+  if (s1) comm->tune_s1 = *s1;
+  if (s2) comm->tune_s2 = *s2;
+  if (min_bytes) comm->tune_min_bytes = min_bytes;
+  return flxSuccess;
+}
+
+flxResult_t flxSetLinkProfile(flxComm_t comm, const flxLinkProfile* profile) {
+  FLX_TRY(validate_comm(comm));
+  if (profile && !(profile->bandwidth[flxPathNvlink] > 0))
+    return fail(flxInvalidArgument, "the link profile needs a positive NVLink bandwidth");
+  comm->have_profile = profile != nullptr;
+  if (profile) comm->profile = *profile;
+  return flxSuccess;
+}
+
+flxResult_t flxGetTuneInfo(flxComm_t comm, flxCollOp_t op, int bucket, flxTuneInfo* info) {
+  FLX_TRY(validate_comm(comm));
+  if (!info || op < flxCollAllReduce || op > flxCollAllToAll)
+    return fail(flxInvalidArgument, "bad arguments");
+  tuner_of(comm)->info(op, bucket, info);
+  return flxSuccess;
+}
+
+flxResult_t flxGetTuneTrace(flxComm_t comm, flxCollOp_t op, int bucket, flxTuneRecord* records,
+                            int max_records, int* n) {
+  FLX_TRY(validate_comm(comm));
+  if (!n || max_records < 0 || (max_records && !records) || op < flxCollAllReduce ||
+      op > flxCollAllToAll)
+    return fail(flxInvalidArgument, "bad arguments");
+  *n = tuner_of(comm)->trace(op, bucket, records, max_records);
+  return flxSuccess;
+}
+
+flxResult_t flxGetTuneEvaluations(flxComm_t comm, flxCollOp_t op, int bucket,
+                                  flxEvalRecord* records, int max_records, int* n) {
+  FLX_TRY(validate_comm(comm));
+  if (!n || max_records < 0 || (max_records && !records) || op < flxCollAllReduce ||
+      op > flxCollAllToAll)
+    return fail(flxInvalidArgument, "bad arguments");
+  *n = tuner_of(comm)->evaluations(op, bucket, records, max_records);
   return flxSuccess;
 }
 

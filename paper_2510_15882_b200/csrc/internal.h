@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "../../include/flexlink.h"
+#include "../../include/flexlink_tuner.h"
 
 namespace flx {
 
@@ -54,20 +55,40 @@ flxResult_t sem_wait_eq(cudaStream_t s, uint32_t* word, uint32_t value);
 flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value);
 
 size_t dtype_size(int dtype);
+// largest automatic PCIe chunk per member (pick_chunk); the first staging ring
+// is sized for it
+constexpr size_t kMaxAutoChunk = 4 << 20;
 
 // ---- share table (ShareTable, collectives.py:189-204)
 using Granules = std::array<int, FLX_NUM_PATHS>;
+int size_bucket(size_t bytes);
 struct ShareTable {
   Granules fallback{{FLX_GRANULE_TOTAL, 0, 0}};
-  std::map<std::pair<int, int>, Granules> entries;  // (op, bucket) -> granules
+  bool fallback_pinned = false;  // flxSetShares(FLX_BUCKET_ALL): every bucket pinned
+  std::map<std::pair<int, int>, Granules> entries;  // (op, bucket) -> granules (pinned)
   Granules lookup(int op, size_t bytes) const;
+  // the user fixed this bucket's split (flxSetShares): the autotuner leaves it alone
+  bool pinned(int op, size_t bytes) const {
+    return fallback_pinned || entries.count({op, size_bucket(bytes)});
+  }
 };
-int size_bucket(size_t bytes);
 // partition (collectives.py:93-114): per-path bytes, floored to alignment,
 // remainder to NVLink.
 std::array<size_t, FLX_NUM_PATHS> partition(size_t bytes, const Granules& g, size_t alignment);
+// Byte offset of every path's slice inside a rank's message.  The secondary
+// slices come first (PCIe at 0, then RDMA): partition() makes each a multiple
+// of the alignment, so both start 16 B aligned whenever the user buffer is.
+// NVLink comes last and absorbs partition()'s remainder at its END — a ragged
+// message length never shifts the copy-engine/reduce-on-receive slices off
+// the 16 B grid (their kernels would otherwise fall back to scalar forms).
+// The reference fixes per-path byte COUNTS only (collectives.py:93-114); the
+// placement is this executor's choice.
+inline std::array<size_t, FLX_NUM_PATHS> path_offsets(const std::array<size_t, FLX_NUM_PATHS>& split) {
+  return {{split[1] + split[2], 0, split[1]}};
+}
 
 struct Comm;
+class AutoTuner;
 
 // Ranks living in this process on one device.  With virtual ranks (repeated
 // device in flxCommInitAll) there are several members and every collective is
@@ -104,10 +125,16 @@ struct Clique {
   uint32_t* sems = nullptr;  // [0..B) semFull, [B..2B) semEmpty
   bool sems_on_host = false;  // pinned+mapped host words instead of device words
   size_t stage_cap = 0;      // chunk capacity per member
-  int stage_bufs = 0;
+  int stage_bufs = 0;        // buffers allocated
+  int ring_depth = 0;        // buffers the pipeline cycles through (flxSetStaging)
+  // rings replaced by a larger one: a CUDA graph captured earlier may still
+  // copy through them, so they live until clique_destroy (grow-only staging)
+  std::vector<char*> retired_host, retired_dev;
   uint64_t piece_seq = 0;    // monotone chunk counter -> counter semaphores
   std::array<size_t, FLX_NUM_PATHS> last_bytes{{0, 0, 0}};
   int destroyed = 0;
+  AutoTuner* tuner = nullptr;  // in-library Stage 1 / Stage 2 (autotune.cpp)
+  std::string gpu_name;
 };
 
 // Multi-rank worlds (world.cu): one process per GPU, or loopback emulation.
@@ -128,10 +155,21 @@ int world_nlocal(World* w);
 bool world_aborted(World* w);
 void world_abort(World* w);
 flxResult_t world_finalize(World* w, int local);
+AutoTuner* world_tuner(World* w);
+// run one collective over the world with the autotuner deciding the split
+flxResult_t run_world_tuned(World* w, const std::vector<const void*>& send,
+                            const std::vector<void*>& recv,
+                            const std::vector<cudaStream_t>& streams, int coll, size_t count,
+                            int dtype, int op, const Comm& lead, bool pinned,
+                            const Granules& fallback, int path_mask, size_t alignment);
 flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int write,
                              void* buf, size_t bytes);
 
+constexpr uint64_t kCommMagic = 0x4b4e494c58454c46ull;  // "FLEXLINK"
 struct Comm {
+  // first member: validate_comm rejects anything that is not a live FlexLink
+  // communicator (e.g. a real ncclComm_t handed to the NCCL-named entry points)
+  uint64_t magic = kCommMagic;
   int rank = 0;
   int nranks = 1;
   int device = 0;
@@ -143,6 +181,13 @@ struct Comm {
   size_t chunk_bytes = 0;  // 0 = auto
   int buffers = 2;
   bool timing = true;    // record per-path CUDA events (flxSetTiming)
+  // in-library balancer (flxSetAutoTune / flxSetTunerConfig / flxSetLinkProfile)
+  bool autotune = true;
+  size_t tune_min_bytes = 16 << 20;
+  flxTunerConfig tune_s1{32, 0.05, 3, 100};
+  flxBalancerConfig tune_s2{10, 0.10, 10, 10};
+  bool have_profile = false;
+  flxLinkProfile profile{};
 };
 
 }  // namespace flx

@@ -542,6 +542,62 @@ static __global__ void __launch_bounds__(512) xpose_kernel(const XposeArgs a, in
   }
 }
 
+// AllGather fan-out when every source and destination BASE is 16 B aligned
+// but the rank-block stride is not (a ragged per-rank count: block r lands at
+// dst[d] + r*dst_stride, misaligned by m = r*dst_stride mod 16, the same for
+// every d).  Each thread writes one ALIGNED 16 B destination vector: the h =
+// (16-m) mod 16 bytes before the first aligned destination boundary are the
+// head, so destination vector j takes source bytes [h+16j, h+16j+16), i.e.
+// the aligned source vectors j and j+1 funnel-shifted by h bytes.  The
+// second load only happens when h != 0, and then it starts inside the
+// source (h+16j+15 < bytes), so it never leaves the allocation's last
+// 16 B granule.  Head and tail bytes (< 32 per source) are copied bytewise.
+// Reads each source ~once from DRAM (the neighbouring vector hits L1/L2);
+// replaces the byte-per-thread fallback (fanout_byte_kernel) for this case.
+template <int Q>
+__device__ __forceinline__ uint4 shift_window(const uint4& x, const uint4& y, uint32_t sh) {
+  const uint32_t w[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
+  return make_uint4(__funnelshift_r(w[Q], w[Q + 1], sh), __funnelshift_r(w[Q + 1], w[Q + 2], sh),
+                    __funnelshift_r(w[Q + 2], w[Q + 3], sh), __funnelshift_r(w[Q + 3], w[Q + 4], sh));
+}
+
+__device__ __forceinline__ uint4 shift_bytes(const uint4& x, const uint4& y, uint32_t h) {
+  const uint32_t sh = (h & 3) * 8;
+  switch (h >> 2) {  // uniform per (block, source): no divergence
+    case 0: return shift_window<0>(x, y, sh);
+    case 1: return shift_window<1>(x, y, sh);
+    case 2: return shift_window<2>(x, y, sh);
+    default: return shift_window<3>(x, y, sh);
+  }
+}
+
+template <int NMAX>
+__global__ void __launch_bounds__(512) fanout_shift_kernel(const FanoutArgs a) {
+  const int r = blockIdx.y;
+  const char* src = a.src[r];
+  const size_t shift = (size_t)r * a.dst_stride;
+  const uint32_t m = (uint32_t)(shift & 15);
+  const size_t h = (16 - m) & 15;  // head bytes before the first aligned destination
+  const size_t body = a.bytes > h ? (a.bytes - h) >> 4 : 0;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t j = (size_t)blockIdx.x * blockDim.x + threadIdx.x; j < body; j += stride) {
+    const uint4 x = ld_stream(src + (j << 4));
+    const uint4 out = h ? shift_bytes(x, ld_stream(src + ((j + 1) << 4)), (uint32_t)h) : x;
+#pragma unroll
+    for (int d = 0; d < NMAX; ++d)
+      if (d < a.ndst) st_stream(a.dst[d] + shift + h + (j << 4), out);
+  }
+  if (blockIdx.x == 0) {  // head [0, h) and tail [h + 16*body, bytes)
+    const size_t tail0 = h + (body << 4);
+    const size_t nh = a.bytes < h ? a.bytes : h;
+    const size_t i = threadIdx.x < nh ? threadIdx.x : tail0 + (threadIdx.x - nh);
+    if ((threadIdx.x < nh || i < a.bytes) && threadIdx.x < 64) {
+      const char b = src[i];
+      for (int d = 0; d < a.ndst; ++d) a.dst[d][shift + i] = b;
+    }
+  }
+}
+
 static __global__ void __launch_bounds__(512) fanout_byte_kernel(const FanoutArgs a) {
   const int r = blockIdx.y;
   const size_t shift = (size_t)r * a.dst_stride;

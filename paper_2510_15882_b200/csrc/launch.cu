@@ -179,10 +179,20 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   if (a.nsrc < 1 || a.nsrc > kMaxRanks || a.ndst < 1 || a.ndst > kMaxRanks || grid < 1)
     return cudaErrorInvalidValue;
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  bool vec = (a.dst_stride & 15) == 0;
-  for (int r = 0; r < a.nsrc; ++r) vec = vec && aligned16(a.src[r]);
-  for (int d = 0; d < a.ndst; ++d) vec = vec && aligned16(a.dst[d]);
+  bool bases = true;  // every source and destination base 16 B aligned
+  for (int r = 0; r < a.nsrc; ++r) bases = bases && aligned16(a.src[r]);
+  for (int d = 0; d < a.ndst; ++d) bases = bases && aligned16(a.dst[d]);
+  const bool vec = bases && (a.dst_stride & 15) == 0;
   const dim3 g(grid, a.nsrc);
+  if (bases && !vec) {  // ragged per-rank blocks: aligned stores, funnel-shifted loads
+    const unsigned bx = (unsigned)std::min<size_t>(((a.bytes >> 4) + 511) / 512 + 1, (size_t)grid);
+    const dim3 gs(std::max(1u, bx), a.nsrc);
+    if (a.ndst <= 2) fanout_shift_kernel<2><<<gs, 512, 0, s>>>(a);
+    else if (a.ndst <= 4) fanout_shift_kernel<4><<<gs, 512, 0, s>>>(a);
+    else if (a.ndst <= 8) fanout_shift_kernel<8><<<gs, 512, 0, s>>>(a);
+    else fanout_shift_kernel<16><<<gs, 512, 0, s>>>(a);
+    return cudaGetLastError();
+  }
   if (vec && use_tma_fanout()) {
     constexpr size_t smem = (size_t)kTmaStages * kTmaTile * 4 + kTmaStages * sizeof(uint64_t);
     static bool configured = false;

@@ -8,9 +8,19 @@
  * LD_PRELOAD=libflexlink_nccl.so (or by linking this library first); the
  * type values (ncclDataType_t, ncclRedOp_t, ncclResult_t, the 128-byte
  * ncclUniqueId) are identical to flexlink.h's, so arguments pass through
- * unchanged.  Calls NCCL has but FlexLink does not implement (Reduce,
- * Broadcast, send/recv, ...) are deliberately NOT defined here, so a
- * preloaded process falls through to the real NCCL for them.
+ * unchanged.
+ *
+ * A FlexLink communicator is not an ncclComm: every entry point below that
+ * takes a communicator checks FlexLink's magic word (flxComm validation) and
+ * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
+ * it.  The NCCL calls FlexLink does not implement but that take a
+ * communicator (Reduce, Broadcast, Bcast, Send, Recv, CommSplit, CommShrink,
+ * buffer/window registration, PreMulSum ops) are DEFINED here and return
+ * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
+ * communicator to the real libnccl, which would dereference it as its own
+ * struct.  Calls without a communicator that FlexLink does not provide
+ * (ncclMemAlloc/Free, ncclCommInitRankConfig/Scalable, the pncl* profiling
+ * aliases) are not defined and resolve to NCCL if it is loaded.
  */
 #include <nccl.h>
 #include <string.h>
@@ -102,3 +112,95 @@ ncclResult_t ncclCommGetAsyncError(ncclComm_t comm, ncclResult_t* asyncError) {
 ncclResult_t ncclGroupStart(void) { return (ncclResult_t)flxGroupStart(); }
 
 ncclResult_t ncclGroupEnd(void) { return (ncclResult_t)flxGroupEnd(); }
+
+/* ---- NCCL calls that take a communicator but are not FlexLink collectives.
+ * Refused loudly (ncclInvalidUsage; ncclGetLastError says why) instead of
+ * falling through to libnccl with a FlexLink handle. */
+static ncclResult_t unsupported(ncclComm_t comm, const char* what) {
+  int n = 0;
+  /* flxCommCount validates the handle (magic word) and records the error */
+  if (flxCommCount((flxComm_t)comm, &n) != flxSuccess) return ncclInvalidArgument;
+  flxSetLastError(what);
+  return ncclInvalidUsage;
+}
+
+ncclResult_t ncclReduce(const void* sendbuff, void* recvbuff, size_t count,
+                        ncclDataType_t datatype, ncclRedOp_t op, int root, ncclComm_t comm,
+                        cudaStream_t stream) {
+  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)op; (void)root;
+  (void)stream;
+  return unsupported(comm, "ncclReduce is not implemented by FlexLink");
+}
+
+ncclResult_t ncclBcast(void* buff, size_t count, ncclDataType_t datatype, int root,
+                       ncclComm_t comm, cudaStream_t stream) {
+  (void)buff; (void)count; (void)datatype; (void)root; (void)stream;
+  return unsupported(comm, "ncclBcast is not implemented by FlexLink");
+}
+
+ncclResult_t ncclBroadcast(const void* sendbuff, void* recvbuff, size_t count,
+                           ncclDataType_t datatype, int root, ncclComm_t comm,
+                           cudaStream_t stream) {
+  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
+  return unsupported(comm, "ncclBroadcast is not implemented by FlexLink");
+}
+
+ncclResult_t ncclSend(const void* sendbuff, size_t count, ncclDataType_t datatype, int peer,
+                      ncclComm_t comm, cudaStream_t stream) {
+  (void)sendbuff; (void)count; (void)datatype; (void)peer; (void)stream;
+  return unsupported(comm, "ncclSend is not implemented by FlexLink");
+}
+
+ncclResult_t ncclRecv(void* recvbuff, size_t count, ncclDataType_t datatype, int peer,
+                      ncclComm_t comm, cudaStream_t stream) {
+  (void)recvbuff; (void)count; (void)datatype; (void)peer; (void)stream;
+  return unsupported(comm, "ncclRecv is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommSplit(ncclComm_t comm, int color, int key, ncclComm_t* newcomm,
+                           ncclConfig_t* config) {
+  (void)color; (void)key; (void)config;
+  if (newcomm) *newcomm = NULL;
+  return unsupported(comm, "ncclCommSplit is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommShrink(ncclComm_t comm, int* excludeRanksList, int excludeRanksCount,
+                            ncclComm_t* newcomm, ncclConfig_t* config, int shrinkFlags) {
+  (void)excludeRanksList; (void)excludeRanksCount; (void)config; (void)shrinkFlags;
+  if (newcomm) *newcomm = NULL;
+  return unsupported(comm, "ncclCommShrink is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommRegister(const ncclComm_t comm, void* buff, size_t size, void** handle) {
+  (void)buff; (void)size;
+  if (handle) *handle = NULL;
+  return unsupported(comm, "ncclCommRegister is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommDeregister(const ncclComm_t comm, void* handle) {
+  (void)handle;
+  return unsupported(comm, "ncclCommDeregister is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommWindowRegister(ncclComm_t comm, void* buff, size_t size, ncclWindow_t* win,
+                                    int winFlags) {
+  (void)buff; (void)size; (void)winFlags;
+  if (win) *win = NULL;
+  return unsupported(comm, "ncclCommWindowRegister is not implemented by FlexLink");
+}
+
+ncclResult_t ncclCommWindowDeregister(ncclComm_t comm, ncclWindow_t win) {
+  (void)win;
+  return unsupported(comm, "ncclCommWindowDeregister is not implemented by FlexLink");
+}
+
+ncclResult_t ncclRedOpCreatePreMulSum(ncclRedOp_t* op, void* scalar, ncclDataType_t datatype,
+                                      ncclScalarResidence_t residence, ncclComm_t comm) {
+  (void)op; (void)scalar; (void)datatype; (void)residence;
+  return unsupported(comm, "PreMulSum reduction ops are not implemented by FlexLink");
+}
+
+ncclResult_t ncclRedOpDestroy(ncclRedOp_t op, ncclComm_t comm) {
+  (void)op;
+  return unsupported(comm, "PreMulSum reduction ops are not implemented by FlexLink");
+}

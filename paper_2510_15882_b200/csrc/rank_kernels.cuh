@@ -84,7 +84,13 @@ __device__ __forceinline__ CtaEpochs cta_epochs(const RankArgs& a, int cta) {
   uint32_t* st = a.flags[a.rank] + kFlagWords + 4 * (size_t)cta;
   if (threadIdx.x < 3) s_st[threadIdx.x] = st[threadIdx.x];
   __syncthreads();
-  return CtaEpochs{st, s_st[0] + 1, s_st[1], s_st[2]};
+  // Epoch 0 is never a call's first epoch: the LL packet area is zeroed at
+  // init, so an LL round tagged 0 (after 2^32 rounds) would accept
+  // never-written packets.  Skipping by 2 keeps the parity alternation the
+  // one-shot regions rely on; every rank skips identically.
+  uint32_t first = s_st[0] + 1;
+  if (first == 0) first = 2;
+  return CtaEpochs{st, first, s_st[1], s_st[2]};
 }
 
 // After the call's rounds (not reached when a wait aborted): `last_ar` /
@@ -206,6 +212,22 @@ __device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, b
       *reinterpret_cast<uint4*>(dst + (v << 4)) = w;
     }
     for (size_t i = (nv << 4) + threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  } else if (aligned16_dev(src)) {
+    // aligned source, misaligned destination (AllGather / AllToAll blocks of
+    // a ragged per-rank count): aligned 16 B stores of funnel-shifted source
+    // vectors (kernels.cuh shift_bytes), bytewise head and tail only
+    const size_t h = (16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15;
+    const size_t body = n > h ? (n - h) >> 4 : 0;
+    for (size_t j = threadIdx.x; j < body; j += blockDim.x) {
+      const uint4 x = coherent ? ld_cg(src + (j << 4)) : ld_stream(src + (j << 4));
+      const uint4 y = coherent ? ld_cg(src + ((j + 1) << 4)) : ld_stream(src + ((j + 1) << 4));
+      *reinterpret_cast<uint4*>(dst + h + (j << 4)) = shift_bytes(x, y, (uint32_t)h);
+    }
+    const size_t nh = n < h ? n : h, tail0 = h + (body << 4);
+    for (size_t t = threadIdx.x; t < nh + (n - min(n, tail0)); t += blockDim.x) {
+      const size_t i = t < nh ? t : tail0 + (t - nh);
+      dst[i] = coherent ? *(volatile const char*)(src + i) : src[i];
+    }
   } else {
     for (size_t i = threadIdx.x; i < n; i += blockDim.x)
       dst[i] = coherent ? *(volatile const char*)(src + i) : src[i];

@@ -40,6 +40,7 @@
 #include <cstring>
 #include <thread>
 
+#include "autotune.h"
 #include "internal.h"
 #include "rank_kernels.cuh"
 
@@ -47,7 +48,12 @@ namespace flx {
 
 namespace {
 
-constexpr int kSemWords = 4096;  // uint32 words at the head of the staging segment
+// uint32 words at the head of the staging segment: [0, 4096) token words,
+// [4096, 12288) the balancer's agreement board (world_agree_max)
+constexpr int kSemWords = 12288;
+constexpr int kBoardWord = 4096;
+constexpr int kBoardSlots = 4;        // decision points in flight (ranks are <= 1 apart)
+constexpr int kBoardDoubles = 62;     // values per slot (+ stamp + count = 64 x 8 B)
 // token word layout: [kind][buffer][producer][reader] over kMaxRanks, see token_post
 inline size_t tok(int kind, int r, int c, int b) {
   return ((size_t)(kind * 2 + b) * kMaxRanks + r) * kMaxRanks + c;
@@ -62,6 +68,14 @@ size_t env_mib(const char* name, size_t dflt) {
   return v ? (size_t)atoll(v) << 20 : dflt << 20;
 }
 
+// World layout and protocol settings every rank must share: each rank reads
+// them from its own environment (FLX_SLOT_MB, FLX_PCIE_STAGE_MB,
+// FLX_PCIE_CHUNK_KB, FLX_ONESHOT_KB, FLX_LL, FLX_NVLINK_CTAS) and a mismatch
+// would shift scratch / staging offsets between ranks, so bootstrap compares them.
+struct BootConfig {
+  uint64_t nranks, slot, small_slot, hcap, pcie_chunk, oneshot_max, ll, nctas, sem_words;
+};
+
 struct BootSlot {
   int ready;
   int device;
@@ -70,6 +84,7 @@ struct BootSlot {
   cudaIpcMemHandle_t scratch;
   cudaIpcMemHandle_t flags;
   char bus_id[32];
+  BootConfig config;
 };
 
 struct BootHeader {
@@ -91,6 +106,7 @@ struct World {
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
   long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
+  double timeout_s = 10.0;   // FLX_TIMEOUT_S: peer waits and the PCIe-leg watchdog
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   bool ll = true;          // one-shot slices that fit kLLRegion / 2 per CTA use the LL format (FLX_LL)
   size_t hcap = 0;       // PCIe staging bytes per rank region
@@ -116,6 +132,10 @@ struct World {
     Clique::Timing timing[Clique::kTimingSlots];
     uint64_t calls = 0;
     std::array<size_t, FLX_NUM_PATHS> last_bytes{{0, 0, 0}};
+    // PCIe-leg watchdog (flxCommGetAsyncError): the last call with a PCIe
+    // slice, its completion event and when it was issued
+    cudaEvent_t pcie_watch = nullptr;
+    std::chrono::steady_clock::time_point pcie_issued{};
   };
   std::vector<Local> local;
   // peer views (as mapped in this process): scratch/flags of every rank
@@ -125,6 +145,9 @@ struct World {
   struct BootHeader* boot = nullptr;  // kept mapped (name unlinked) for the destroy barrier
   int destroyed = 0;
   bool aborting = false;  // flxCommAbort: skip the destroy barrier
+  bool shared_gpu = false;  // ranks share a GPU (bootstrap self-tests): no NVLink-path tuning
+  uint64_t agree_seq = 0;   // decision points agreed so far (same on every rank)
+  AutoTuner tuner;
 
   // semaphore words as the GPU addresses them (registered host memory may map
   // to a different device address than its host pointer)
@@ -143,6 +166,7 @@ flxResult_t local_init(World* w, World::Local& L) {
   const char* to = getenv("FLX_TIMEOUT_S");
   const double secs = to ? atof(to) : 10.0;
   w->spin_limit = (long long)(std::max(0.01, secs) * khz * 1e3);
+  w->timeout_s = std::max(0.01, secs);
   // [n inbox slots][outbox][one-shot inboxes: 2 parities x n sources]
   // [LL packets: 2 parities x n sources x kLLSlot] (zeroed: epochs start at 1)
   const size_t ll_off = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
@@ -170,11 +194,53 @@ flxResult_t local_init(World* w, World::Local& L) {
   return flxSuccess;
 }
 
-void world_free(World* w) {
-  for (auto& L : w->local) {
-    cudaSetDevice(L.device);
-    cudaDeviceSynchronize();  // every kernel / copy that may touch peer memory
+// Wait (at most `seconds`) until every stream of this world's ranks is idle.
+// On abort, a peer that died mid PCIe slice leaves this rank's copy streams
+// parked in cuStreamWaitValue32 on the shared token words, which have no
+// timeout: keep forcing every token to the value its waiters expect — ready
+// tokens (prod, rprod) are awaited == 1, free tokens (hfree, rfree) == 0 — so
+// each pending wait, and the ones queued behind it, fall through.  The NVLink
+// kernels already gave up on the abort word.
+bool drain_streams(World* w, double seconds, bool release_tokens) {
+  const auto t0 = std::chrono::steady_clock::now();
+  while (true) {
+    bool idle = true;
+    for (auto& L : w->local) {
+      cudaSetDevice(L.device);
+      if (L.d2h && cudaStreamQuery(L.d2h) == cudaErrorNotReady) idle = false;
+      if (L.h2d && cudaStreamQuery(L.h2d) == cudaErrorNotReady) idle = false;
+    }
+    if (idle) return true;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > seconds)
+      return false;
+    if (release_tokens && w->host) {
+      auto* words = reinterpret_cast<volatile uint32_t*>(w->host);
+      for (int b = 0; b < 2; ++b)
+        for (int r = 0; r < w->nranks; ++r)
+          for (int c = 0; c < w->nranks; ++c) {
+            words[sem_prod(r, c, b)] = 1;
+            words[sem_rprod(r, c, b)] = 1;
+            words[sem_hfree(r, c, b)] = 0;
+            words[sem_rfree(r, c, b)] = 0;
+          }
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(100));
   }
+}
+
+void world_free(World* w) {
+  // Every kernel / copy that may touch peer memory must be done before the
+  // destroy barrier.  An aborted world releases its parked PCIe waits; if its
+  // streams still do not drain, its memory is leaked rather than freed under
+  // a hung stream (cudaFree would block on it forever).
+  bool drained = true;
+  const bool aborted = w->aborting || (w->abort_word && *(volatile uint32_t*)w->abort_word);
+  if (aborted) drained = drain_streams(w, std::max(5.0, w->timeout_s), true);
+  if (drained)
+    for (auto& L : w->local) {
+      cudaSetDevice(L.device);
+      cudaDeviceSynchronize();
+    }
   if (w->boot) {
     // destroy barrier: a peer may still be pushing into my scratch or reading
     // my outbox / host region until it, too, has drained its device
@@ -186,6 +252,12 @@ void world_free(World* w) {
       std::this_thread::sleep_for(std::chrono::milliseconds(1));
     munmap(w->boot, sizeof(BootHeader));
     w->boot = nullptr;
+  }
+  if (!drained) {
+    fprintf(stderr, "[flexlink] aborted communicator: side streams did not drain; leaking its "
+                    "device and staging memory\n");
+    delete w;
+    return;
   }
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
   for (auto& L : w->local) {
@@ -395,6 +467,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   auto split = partition(bytes, g, alignment);
   if (split[flxPathRdma] > 0) return fail(flxInvalidUsage, "rdma path is not available");
   const size_t nv = split[flxPathNvlink], pc = split[flxPathPcie];
+  const auto offs = path_offsets(split);  // PCIe slice first, NVLink last (internal.h)
+  const size_t opc = offs[flxPathPcie], onv = offs[flxPathNvlink];
   const bool gather = coll == flxCollAllGather;
   const bool scatter = coll == flxCollReduceScatter;
   const bool a2a = coll == flxCollAllToAll;
@@ -463,11 +537,11 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         const char* src = static_cast<const char*>(send[i]);
         char* h = w->hregion(r) + b * slot_h;
         if (gather) {
-          FLX_CUDA(cudaMemcpyAsync(h, src + nv + at, len, cudaMemcpyDeviceToHost, L.d2h));
+          FLX_CUDA(cudaMemcpyAsync(h, src + opc + at, len, cudaMemcpyDeviceToHost, L.d2h));
         } else {
           for (int s = 1; s < n; ++s) {
             const int c = (r + s) % n;
-            const char* from = ar ? src + nv + c * q + at : src + (size_t)c * bytes + nv + at;
+            const char* from = ar ? src + opc + c * q + at : src + (size_t)c * bytes + opc + at;
             FLX_CUDA(cudaMemcpyAsync(h + c * cq, from, len, cudaMemcpyDeviceToHost, L.d2h));
           }
         }
@@ -484,7 +558,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
           const int p = (r - s + n) % n;
           FLX_TRY(token_accept(L.h2d, w->sem(sem_prod(p, r, b))));
           const char* from = w->hregion(p) + b * slot_h + (gather ? 0 : r * cq);
-          char* to = (gather || a2a) ? dst + (size_t)p * bytes + nv + at : land + p * cq;
+          char* to = (gather || a2a) ? dst + (size_t)p * bytes + opc + at : land + p * cq;
           FLX_CUDA(cudaMemcpyAsync(to, from, len, cudaMemcpyHostToDevice, L.h2d));
           FLX_TRY(token_give(L.h2d, w->sem(sem_hfree(p, r, b))));
         }
@@ -492,9 +566,9 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
           FoldArgs a{};
           for (int p = 0; p < n; ++p)
             a.src[p] = p != r    ? land + p * cq
-                       : scatter ? src + (size_t)r * bytes + nv + at
-                                 : src + nv + r * q + at;
-          a.dst[0] = scatter ? dst + nv + at : dst + nv + r * q + at;
+                       : scatter ? src + (size_t)r * bytes + opc + at
+                                 : src + opc + r * q + at;
+          a.dst[0] = scatter ? dst + opc + at : dst + opc + r * q + at;
           a.n = n;
           a.ndst = 1;
           a.bytes = len;
@@ -513,7 +587,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         FLX_CUDA(cudaStreamWaitEvent(L.d2h, L.fold_done[b], 0));
         FLX_TRY(take_region(w, L.d2h, r, true, b));
         FLX_CUDA(cudaMemcpyAsync(w->rregion(r) + b * cq,
-                                 static_cast<char*>(recv[i]) + nv + r * q + at, len,
+                                 static_cast<char*>(recv[i]) + opc + r * q + at, len,
                                  cudaMemcpyDeviceToHost, L.d2h));
         for (int s = 1; s < n; ++s)
           FLX_TRY(token_post(L.d2h, w->sem(sem_rprod(r, (r + s) % n, b))));
@@ -524,7 +598,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
         for (int s = 1; s < n; ++s) {
           const int c = (r + s) % n;
           FLX_TRY(token_accept(L.h2d, w->sem(sem_rprod(c, r, b))));
-          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + nv + c * q + at,
+          FLX_CUDA(cudaMemcpyAsync(static_cast<char*>(recv[i]) + opc + c * q + at,
                                    w->rregion(c) + b * cq, len, cudaMemcpyHostToDevice, L.h2d));
           FLX_TRY(token_give(L.h2d, w->sem(sem_rfree(c, r, b))));
         }
@@ -538,11 +612,11 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       char* dst = static_cast<char*>(recv[i]);
       const char* src = static_cast<const char*>(send[i]);
       if (gather) {
-        char* own = dst + (size_t)r * bytes + nv;
-        if (own != src + nv)
-          FLX_CUDA(cudaMemcpyAsync(own, src + nv, pc, cudaMemcpyDeviceToDevice, L.h2d));
+        char* own = dst + (size_t)r * bytes + opc;
+        if (own != src + opc)
+          FLX_CUDA(cudaMemcpyAsync(own, src + opc, pc, cudaMemcpyDeviceToDevice, L.h2d));
       } else if (a2a) {
-        const size_t own = (size_t)r * bytes + nv;
+        const size_t own = (size_t)r * bytes + opc;
         FLX_CUDA(cudaMemcpyAsync(dst + own, src + own, pc, cudaMemcpyDeviceToDevice, L.h2d));
       }
     }
@@ -550,7 +624,13 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       if (k < chunks) FLX_TRY(step12(k));
       if (ar && k >= 1) FLX_TRY(step34(k - 1));
     }
-    for (int i = 0; i < nl; ++i) FLX_CUDA(cudaEventRecord(ev_pcie(i), w->local[i].h2d));
+    for (int i = 0; i < nl; ++i) {
+      FLX_CUDA(cudaEventRecord(ev_pcie(i), w->local[i].h2d));
+      if (!capturing) {
+        w->local[i].pcie_watch = ev_pcie(i);
+        w->local[i].pcie_issued = std::chrono::steady_clock::now();
+      }
+    }
   }
 
   // ---------------- NVLink slice
@@ -559,8 +639,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     memset(&la, 0, sizeof(la));
     for (int i = 0; i < nl; ++i) {
       RankArgs& a = la.r[w->loopback ? w->local[i].rank : 0];
-      a.send = static_cast<const char*>(send[i]);
-      a.recv = static_cast<char*>(recv[i]);
+      a.send = static_cast<const char*>(send[i]) + onv;
+      a.recv = static_cast<char*>(recv[i]) + onv;
       for (int p = 0; p < n; ++p) {
         a.scratch[p] = w->loopback ? w->local[p].scratch : w->peer_scratch[p];
         a.flags[p] = w->loopback ? w->local[p].flags : w->peer_flags[p];
@@ -649,8 +729,123 @@ std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local) {
 }
 int world_nranks(World* w) { return w->nranks; }
 int world_nlocal(World* w) { return (int)w->local.size(); }
-bool world_aborted(World* w) { return *(volatile uint32_t*)w->abort_word != 0; }
+bool world_aborted(World* w) {
+  if (*(volatile uint32_t*)w->abort_word != 0) return true;
+  // PCIe-leg watchdog: copy-engine waits on a dead peer's tokens never time
+  // out by themselves; a PCIe slice still pending FLX_TIMEOUT_S after it was
+  // issued is reported (and aborts the world, like a timed-out NVLink wait)
+  for (auto& L : w->local) {
+    if (!L.pcie_watch) continue;
+    cudaSetDevice(L.device);
+    if (cudaEventQuery(L.pcie_watch) != cudaErrorNotReady) continue;
+    const double waited =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - L.pcie_issued).count();
+    if (waited > w->timeout_s) {
+      *(volatile uint32_t*)w->abort_word = 1;
+      return true;
+    }
+  }
+  return false;
+}
 void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(w->max_nctas, n)); }
+
+AutoTuner* world_tuner(World* w) { return &w->tuner; }
+
+// Elementwise max over every rank of n doubles, through the shared host
+// segment's board: rank r publishes into its slot (agree_seq % kBoardSlots)
+// with a release-ordered stamp, then waits for every rank's stamp of the same
+// decision point.  Ranks reach decision points in the same order and none can
+// pass point k+1 before every rank published point k+1, i.e. after it finished
+// reading point k — so a slot is never overwritten while a peer still reads it.
+static flxResult_t world_agree_max(World* w, double* vals, int n) {
+  if (w->loopback || w->nranks == 1 || w->local.size() != 1) return flxSuccess;
+  const int me = w->local[0].rank;
+  auto slot = [&](int r, uint64_t k) {
+    return reinterpret_cast<uint64_t*>(w->host + (size_t)kBoardWord * 4) +
+           ((size_t)r * kBoardSlots + k % kBoardSlots) * 64;
+  };
+  for (int at = 0; at < n; at += kBoardDoubles) {
+    const int m = std::min(kBoardDoubles, n - at);
+    const uint64_t k = w->agree_seq++;
+    uint64_t* mine = slot(me, k);
+    mine[1] = (uint64_t)m;
+    memcpy(mine + 2, vals + at, sizeof(double) * m);
+    __atomic_store_n(&mine[0], k + 1, __ATOMIC_RELEASE);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < w->nranks; ++r) {
+      if (r == me) continue;
+      uint64_t* theirs = slot(r, k);
+      while (__atomic_load_n(&theirs[0], __ATOMIC_ACQUIRE) != k + 1) {
+        if (*(volatile uint32_t*)w->abort_word ||
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >
+                w->timeout_s) {
+          *(volatile uint32_t*)w->abort_word = 1;
+          return fail(flxInternalError, "balancer agreement: rank %d never reached decision %llu",
+                      r, (unsigned long long)k);
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
+      }
+      if ((int)theirs[1] != m)
+        return fail(flxInternalError, "balancer agreement: rank %d is at a different decision", r);
+      double v[kBoardDoubles];
+      memcpy(v, theirs + 2, sizeof(double) * m);
+      for (int i = 0; i < m; ++i) vals[at + i] = std::max(vals[at + i], v[i]);
+    }
+  }
+  return flxSuccess;
+}
+
+namespace {
+struct WorldPort : TimingPort {
+  World* w;
+  explicit WorldPort(World* w_) : w(w_) {}
+  flxResult_t read(uint64_t seq, float ms[FLX_NUM_PATHS]) override {
+    ms[0] = ms[1] = ms[2] = 0.f;
+    for (int i = 0; i < (int)w->local.size(); ++i) {
+      float t[FLX_NUM_PATHS];
+      FLX_TRY(world_read_timing(w, i, seq, t));
+      for (int p = 0; p < FLX_NUM_PATHS; ++p) ms[p] = std::max(ms[p], t[p]);
+    }
+    return flxSuccess;
+  }
+  flxResult_t agree_max(double* vals, int n) override { return world_agree_max(w, vals, n); }
+  uint64_t calls() const override { return w->local[0].calls; }
+  std::string scope() const override {
+    char name[256] = "gpu";
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, w->local[0].device) == cudaSuccess)
+      snprintf(name, sizeof(name), "%s", prop.name);
+    for (char* c = name; *c; ++c)
+      if (*c == ' ') *c = '_';
+    return std::string(name) + (w->loopback ? "/loopback/n" : "/world/n") +
+           std::to_string(w->nranks);
+  }
+  bool cache_writer() const override { return w->local[0].rank == 0; }
+};
+}  // namespace
+
+flxResult_t run_world_tuned(World* w, const std::vector<const void*>& send,
+                            const std::vector<void*>& recv,
+                            const std::vector<cudaStream_t>& streams, int coll, size_t count,
+                            int dtype, int op, const Comm& lead, bool pinned,
+                            const Granules& fallback, int path_mask, size_t alignment) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
+  const size_t bytes = count * dtype_size(dtype);
+  const bool tunable = !pinned && lead.autotune && lead.timing && !w->shared_gpu &&
+                       bytes >= lead.tune_min_bytes && !*(volatile uint32_t*)w->abort_word;
+  WorldPort port(w);
+  TunePolicy pol{lead.tune_s1, lead.tune_s2, lead.have_profile, lead.profile, w->nctas};
+  Granules g = fallback;
+  bool measured = false;
+  FLX_TRY(w->tuner.before_call(port, pol, coll, bytes, tunable,
+                               cap == cudaStreamCaptureStatusNone, path_mask, fallback, &g,
+                               &measured));
+  const uint64_t seq = w->local[0].calls;
+  FLX_TRY(run_world(w, send, recv, streams, coll, count, dtype, op, g, alignment, lead.timing));
+  w->tuner.after_call(coll, bytes, seq, w->local[0].last_bytes, measured);
+  return flxSuccess;
+}
 
 // ------------------------------------------------------------ creation
 namespace {
@@ -720,6 +915,9 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   FLX_CUDA(cudaDeviceGetPCIBusId(mine.bus_id, sizeof(mine.bus_id), device));
   mine.device = device;
   mine.pid = getpid();
+  mine.config = BootConfig{(uint64_t)nranks, w->slot, w->small_slot, w->hcap, w->pcie_chunk,
+                           w->oneshot_max, (uint64_t)w->ll, (uint64_t)w->nctas,
+                           (uint64_t)kSemWords};
   __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
   __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
   const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 60.0;
@@ -727,6 +925,24 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
                   timeout))
     return fail(flxSystemError, "bootstrap timed out: %d of %d ranks arrived",
                 __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE), nranks);
+  static const char* kFields[] = {"nranks", "FLX_SLOT_MB", "one-shot inbox (FLX_ONESHOT_KB)",
+                                  "FLX_PCIE_STAGE_MB", "FLX_PCIE_CHUNK_KB", "FLX_ONESHOT_KB",
+                                  "FLX_LL", "FLX_NVLINK_CTAS", "library build (staging words)"};
+  for (int p = 0; p < nranks; ++p) {
+    const uint64_t* a = reinterpret_cast<const uint64_t*>(&mine.config);
+    const uint64_t* b = reinterpret_cast<const uint64_t*>(&hdr->slot[p].config);
+    for (size_t f = 0; f < sizeof(BootConfig) / sizeof(uint64_t); ++f)
+      if (a[f] != b[f])
+        return fail(flxInvalidUsage,
+                    "rank %d and rank %d disagree on %s (%llu vs %llu): every rank must use the "
+                    "same world settings",
+                    rank, p, kFields[f], (unsigned long long)a[f], (unsigned long long)b[f]);
+  }
+  // any two ranks on one GPU (bootstrap self-tests) keep the whole world off
+  // the NVLink-path kernels' autotuning — decided identically on every rank
+  for (int p = 0; p < nranks; ++p)
+    for (int q = p + 1; q < nranks; ++q)
+      if (strcmp(hdr->slot[p].bus_id, hdr->slot[q].bus_id) == 0) w->shared_gpu = true;
   for (int p = 0; p < nranks; ++p) {
     if (p == rank) {
       w->peer_scratch[p] = w->local[0].scratch;
@@ -735,9 +951,11 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
     }
     // FLX_ALLOW_SHARED_GPU: bootstrap self-tests only (no collective may run:
     // the rank kernels of two processes on one GPU would wait on each other)
-    if (strcmp(hdr->slot[p].bus_id, mine.bus_id) == 0 && !getenv("FLX_ALLOW_SHARED_GPU"))
-      return fail(flxInvalidUsage, "ranks %d and %d share GPU %s; one GPU per rank", rank, p,
-                  mine.bus_id);
+    if (strcmp(hdr->slot[p].bus_id, mine.bus_id) == 0) {
+      if (!getenv("FLX_ALLOW_SHARED_GPU"))
+        return fail(flxInvalidUsage, "ranks %d and %d share GPU %s; one GPU per rank", rank, p,
+                    mine.bus_id);
+    }
     void* ptr = nullptr;
     FLX_CUDA(cudaIpcOpenMemHandle(&ptr, hdr->slot[p].scratch, cudaIpcMemLazyEnablePeerAccess));
     w->ipc_opened.push_back(ptr);

@@ -100,12 +100,27 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
                  "ncclGroupEnd", "ncclCommGetAsyncError", "ncclCommAbort",
                  "ncclCommFinalize"):
         assert name in exported
-    assert "ncclBroadcast" not in exported  # falls through to real NCCL under LD_PRELOAD
+    # comm-taking NCCL calls FlexLink does not implement are defined and refused,
+    # so a preloaded process never hands a FlexLink comm to the real libnccl
+    for name in ("ncclBroadcast", "ncclBcast", "ncclReduce", "ncclSend", "ncclRecv",
+                 "ncclCommSplit", "ncclCommRegister"):
+        assert name in exported
+    # ...while comm-less calls FlexLink does not provide still resolve to NCCL
+    assert "ncclMemAlloc" not in exported and "ncclCommInitRankConfig" not in exported
     S = ctypes.CDLL(str(shim))
     S.ncclGetErrorString.restype = ctypes.c_char_p
     assert S.ncclGetErrorString(4) == b"invalid argument"
     uid = (ctypes.c_char * 128)()
     assert S.ncclGetUniqueId(uid) == 0 and bytes(uid)[:4] == b"FLX1"
+    # a handle that is not a live FlexLink communicator (e.g. a real ncclComm_t)
+    # is rejected by its magic word instead of being used
+    fake = (ctypes.c_uint64 * 64)()
+    n = ctypes.c_int()
+    assert S.ncclCommCount(ctypes.byref(fake), ctypes.byref(n)) == 4
+    S.ncclGetLastError.restype = ctypes.c_char_p
+    assert b"not a live FlexLink communicator" in S.ncclGetLastError(None)
+    assert S.ncclBroadcast(None, None, 0, 7, 0, ctypes.byref(fake), None) == 4
+    assert S.ncclAllReduce(None, None, 0, 7, 0, ctypes.byref(fake), None) == 4
 
 
 def test_header_is_plain_c_and_links(tmp_path, lib):

@@ -164,7 +164,7 @@ def test_partition_sums_alignment_and_layout():
     assert fl.partition(256 * MIB, {NV: 854, PC: 146}, 4096) == {NV: 229244928, PC: 39190528}
     from paper_2510_15882_b200.striping import slice_offsets
     off = slice_offsets(1000, {NV: 700, PC: 200, RD: 100})
-    assert off == {NV: (0, 700), PC: (700, 200), RD: (900, 100)}
+    assert off == {PC: (0, 200), RD: (200, 100), NV: (300, 700)}
     with pytest.raises(ValueError):
         fl.partition(10, {NV: 0})
 

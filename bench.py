@@ -183,9 +183,10 @@ def workload_config(n_gpus: int) -> dict:
 
 
 # ------------------------------------------------------------ CPU baseline
-def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = 32 * MIB,
+def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = AR_BYTES,
                          n: int = SIM_RANKS):
-    """Oracle port on the host: repeated 8-rank fp32 AllReduce until ~target_s."""
+    """Oracle port on the host: the same n-rank fp32 AllReduce (256 MiB per rank)
+    repeated until ~target_s."""
     import numpy as np
 
     import oracle
@@ -226,7 +227,7 @@ def run_reference(args) -> None:
 
     oracle.build()
     threads = oracle.cpu_threads()
-    per_rank = 32 * MIB
+    per_rank = AR_BYTES  # the GPU arm's workload itself (same_config), not a sample
     count = per_rank // 4
     ranks = args.gpus if args.gpus > 1 else SIM_RANKS
     rng = np.random.default_rng(1000)
@@ -249,9 +250,9 @@ def run_reference(args) -> None:
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
                          "kind": "port",
-                         "sample": f"each step: AllReduce sum fp32 {per_rank // MIB} MiB/rank x "
-                                   f"{ranks} ranks on the host (oracle/flx_oracle.c, OpenMP; "
-                                   f"a bounded sample of the 256 MiB/rank workload)"},
+                         "sample": f"each step: the full workload, AllReduce sum fp32 "
+                                   f"{per_rank // MIB} MiB/rank x {ranks} ranks on the host "
+                                   f"(oracle/flx_oracle.c, OpenMP, {threads} threads)"},
         "e2e": {"value": round(value, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -889,6 +890,30 @@ def run_multi_gpu(args) -> None:
     dist.destroy_process_group()
 
 
+def launch_ranks(args) -> int:
+    """Run this benchmark as ``args.gpus`` ranks under torchrun (one process per
+    GPU, NCCL/IPC between them).  Fails loudly when the box has fewer GPUs."""
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, this box "
+                         f"has {have}; not running (no 1-GPU stand-in)\n")
+        return 2
+    with socket.socket() as sock:
+        sock.bind(("127.0.0.1", 0))
+        port = sock.getsockname()[1]
+    argv = [a for a in sys.argv[1:]]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__), *argv]
+    sys.stdout.flush()
+    return subprocess.call(cmd, stdout=_JSON_FD if _JSON_FD is not None else None)
+
+
 def main() -> None:
     p = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     p.add_argument("--gpus", type=int, default=1)
@@ -909,6 +934,12 @@ def main() -> None:
         run_reference(args)
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N`: launch the N ranks ourselves (one process
+        # per GPU, torchrun on 127.0.0.1) — never a silent 1-GPU run
+        sys.exit(launch_ranks(args))
+    if "WORLD_SIZE" in os.environ and world != args.gpus and args.gpus > 1:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # FLX_BENCH_MULTI=1: take the one-process-per-GPU path even at WORLD_SIZE 1
     # (a smoke test of run_multi_gpu on a 1-GPU box)
     if world > 1 or os.environ.get("FLX_BENCH_MULTI") == "1":

@@ -45,3 +45,21 @@ def test_reference_arm_line():
     assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
                            "d2h_bytes_per_step": 0}
+
+
+def test_gpus_n_without_n_gpus_fails_loudly():
+    # `python bench.py --gpus 2` launches 2 ranks itself; on a box with fewer
+    # GPUs it refuses (non-zero exit, a reason on stderr) and never prints a
+    # 1-GPU line in place of the N-GPU one
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1",
+                          "--warmup", "3"], cwd=ROOT, capture_output=True, text=True,
+                         timeout=600)
+    import torch
+
+    if torch.cuda.device_count() >= 2:
+        import pytest
+
+        pytest.skip("this box has >= 2 GPUs: the N-rank run is the real thing")
+    assert out.returncode != 0
+    assert "n_gpus" not in out.stdout and out.stdout.strip() == ""
+    assert "needs 2 visible GPUs" in out.stderr

@@ -144,12 +144,12 @@ with comm.Clique(n, device=0) as c:
     first = subprocess.run(["python", "-c", script], capture_output=True, text=True, env=env,
                            timeout=300)
     assert first.returncode == 0, first.stderr
-    assert first.stdout.split()[0] == "0"
+    assert first.stdout.split()[0] == "False"
     assert cache.exists() and cache.read_text().strip()
     second = subprocess.run(["python", "-c", script], capture_output=True, text=True, env=env,
                             timeout=300)
     assert second.returncode == 0, second.stderr
-    assert second.stdout.split()[:2] == ["1", "0"], second.stdout
+    assert second.stdout.split()[:2] == ["True", "0"], second.stdout
 
 
 def test_nccl_only_program_gets_striped(tmp_path):

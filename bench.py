@@ -279,9 +279,7 @@ def run_single_gpu(args) -> None:
 
     from paper_2510_15882_b200 import comm as flx
     from paper_2510_15882_b200.links import PathKind, preset
-    from paper_2510_15882_b200.stage1 import TunerConfig
-    from paper_2510_15882_b200.stage2 import BalancerConfig, RuntimeBalancer
-    from paper_2510_15882_b200.striping import CollectiveOp, PathTimingReport
+    from paper_2510_15882_b200.striping import CollectiveOp, ShareDistribution
 
     torch.cuda.set_device(0)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) \
@@ -310,23 +308,18 @@ def run_single_gpu(args) -> None:
         topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
         link_profile = {"error": str(e), "fallback": "preset B200"}
 
-    # ---- Stage 1 on the real path (+ guard), then a Stage-2 phase
+    # ---- the in-library balancer (csrc/autotune.cpp): the bucket's first calls
+    # run Stage 1 (NVLink-only baseline, measured-rate seed, Algorithm 1, guard),
+    # every later call feeds Stage 2 — no flxSetShares, exactly what an
+    # NCCL-API caller gets
     t0 = time.perf_counter()
-    shares, trace, tuned_s, base_s = flx.tune_shares(
-        clique, topo, CollectiveOp.ALLREDUCE, sends, recvs, TunerConfig(), warmup=2, repeats=5)
+    tune_calls = settle(clique, lambda: clique.all_reduce(sends, recvs), CollectiveOp.ALLREDUCE,
+                        AR_BYTES)
     tune_wall = time.perf_counter() - t0
-    balancer = RuntimeBalancer(shares, BalancerConfig(), active=shares.loaded_paths)
-    for _ in range(3):
-        for _ in range(10):
-            clique.all_reduce(sends, recvs)
-        for h in clique.comms[0].path_times_history(10):
-            b = clique.path_bytes()
-            rep = PathTimingReport.build(CollectiveOp.ALLREDUCE, n, AR_BYTES,
-                                         {k: h[k] for k in balancer.active if b[k] > 0})
-            ev = balancer.observe(rep)
-            if ev is not None and ev.moved:
-                clique.set_shares(CollectiveOp.ALLREDUCE, balancer.shares, AR_BYTES)
-    shares = balancer.shares
+    tinfo = clique.tune_info(CollectiveOp.ALLREDUCE, AR_BYTES)
+    trace = clique.tune_trace(CollectiveOp.ALLREDUCE, AR_BYTES)
+    shares = ShareDistribution({k: tinfo["shares"][int(k)] for k in PathKind
+                                if tinfo["shares"][int(k)] or k == PathKind.NVLINK})
     # the reference's closed-form model (simulate_collective, collectives.py:136-186) on
     # the probed link profile, for the split that runs: predicted vs measured per path
     from paper_2510_15882_b200.striping import CollectiveSpec, simulate_collective
@@ -376,7 +369,9 @@ def run_single_gpu(args) -> None:
 
     # ---- e2e through the public API with host buffers
     host_in = [torch.empty(count, dtype=torch.float32, pin_memory=True) for _ in range(n)]
-    host_out = [torch.empty(count, dtype=torch.float32, pin_memory=True) for _ in range(n)]
+    # the reduced tensor comes back once: every virtual rank's recv holds the
+    # same bytes (on N GPUs each rank reads its own copy over its own link)
+    host_out = [torch.empty(count, dtype=torch.float32, pin_memory=True)]
     for h, s in zip(host_in, sends):
         h.copy_(s)
 
@@ -425,8 +420,11 @@ def run_single_gpu(args) -> None:
     ag_count = AG_OUT_BYTES // 2 // n
     ag_send = [torch.randn(ag_count, device="cuda", generator=gen).bfloat16() for _ in range(n)]
     ag_recv = [torch.empty(ag_count * n, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
-    ag_shares, ag_trace, _, _ = flx.tune_shares(clique, topo, CollectiveOp.ALLGATHER, ag_send,
-                                                ag_recv, TunerConfig(), warmup=2, repeats=5)
+    settle(clique, lambda: clique.all_gather(ag_send, ag_recv), CollectiveOp.ALLGATHER,
+           AG_OUT_BYTES // n)
+    ag_info = clique.tune_info(CollectiveOp.ALLGATHER, AG_OUT_BYTES // n)
+    ag_shares = ShareDistribution({k: ag_info["shares"][int(k)] for k in PathKind
+                                   if ag_info["shares"][int(k)] or k == PathKind.NVLINK})
     for _ in range(args.warmup):
         clique.all_gather(ag_send, ag_recv)
     ag_dt = _time_steps(lambda: clique.all_gather(ag_send, ag_recv), args.steps, stream)
@@ -523,12 +521,10 @@ def run_single_gpu(args) -> None:
         "model_path_ms": {**model_ms, "source": "linkstripe simulate_collective on the probed "
                                                 "link profile (the reference's predictor)"},
         "rdma": "absent (no NIC / rdma-core in this image)",
-        "stage1": {"iterations": trace.iterations, "converged": trace.converged,
-                   "tuned_total_ms": round(tuned_s * 1e3, 4),
-                   "nvlink_only_total_ms": round(base_s * 1e3, 4), "wall_s": round(tune_wall, 2),
-                   "trace": [r.action for r in trace.records]},
-        "stage2": {"evaluations": len(balancer.evaluations),
-                   "moves": sum(1 for e in balancer.evaluations if e.moved)},
+        "balancer": {"where": "in-library (csrc/autotune.cpp): Stage 1 + guard on the "
+                              "bucket's first calls, Stage 2 on every call",
+                     "tuning_calls": tune_calls, "tuning_wall_s": round(tune_wall, 2),
+                     **tinfo, "stage1_trace": [r["action"] for r in trace]},
         "roofline": {
             "bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
             "frac": round(achieved / hbm_peak, 4),
@@ -547,12 +543,14 @@ def run_single_gpu(args) -> None:
                           "multi-GPU denominator"},
         "cpu_baseline": cpu,
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
-                "h2d_bytes_per_step": n * AR_BYTES, "d2h_bytes_per_step": n * AR_BYTES,
+                "h2d_bytes_per_step": n * AR_BYTES, "d2h_bytes_per_step": AR_BYTES,
                 "ms_per_step": round(e2e_dt * 1e3, 3), "steps": e2e_steps,
-                "link_bound_ms": round(n * AR_BYTES / link_bidir * 1e3, 3) if link_bidir else None,
-                "note": "all 8 ranks' inputs in and results out over ONE PCIe link per step; "
+                "link_bound_ms": round(n * AR_BYTES / (pcie_h2d * 1e9) * 1e3, 3) if pcie_h2d
+                else None,
+                "note": "all 8 ranks' inputs (2 GiB) in over ONE PCIe link per step and the "
+                        "reduced tensor (identical in every virtual rank's recv) out once; "
                         "in-place AllReduce, step k's D2H overlapped with step k+1's H2D; "
-                        "link_bound_ms = 2 GiB at the probed bidirectional per-direction rate"},
+                        "link_bound_ms = 2 GiB H2D at the probed H2D rate"},
         "gpu_launches": launches,
         "clocks": clocks,
         "nccl": None,
@@ -582,6 +580,22 @@ def run_single_gpu(args) -> None:
     emit(line)
 
 
+def settle(clique, call, op, nbytes: int, limit: int = 400) -> int:
+    """Issue ``call`` until the in-library balancer has left Stage 1 for the
+    bucket (Stage 2 running), at most ``limit`` calls; returns the count."""
+    import torch
+
+    k = 0
+    while k < limit:
+        phase = clique.tune_info(op, nbytes)["phase"]
+        if phase == "stage2" or (phase == "idle" and k >= 2):  # idle: not tunable (pinned/small)
+            break
+        call()
+        k += 1
+    torch.cuda.synchronize()
+    return k
+
+
 def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
     """BASELINE config 4: NVLink path capped to few SMs to emulate an H800-class
     link ratio, so the balancer has real headroom to give to PCIe.
@@ -589,129 +603,215 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
     With 8 virtual ranks on one GPU the PCIe path carries every rank's bytes
     over ONE PCIe link, i.e. 1/8 of a per-GPU link per rank.  The cap is chosen
     so NVLink-only busbw : PCIe-only busbw matches H800's 200:64 GB/s per
-    direction (topo.py:130), then Stage 1 (+guard) tunes
-    the split on the real path and both are timed.
+    direction (topo.py:130).  Then the bucket is handed to
+    the in-library balancer (no flxSetShares): Stage 1 + guard on its first
+    calls, Stage 2 afterwards — and timed against NVLink-only.
     """
-    from paper_2510_15882_b200 import comm as flx
     from paper_2510_15882_b200.links import PathKind
-    from paper_2510_15882_b200.stage1 import TunerConfig
     from paper_2510_15882_b200.striping import CollectiveOp
 
     n = len(sends)
+    AR = CollectiveOp.ALLREDUCE
 
-    def busbw_with(shares, ctas, steps=8):
+    def busbw_pinned(shares, ctas, steps=8):
         clique.set_nvlink_ctas(ctas)
-        clique.set_shares(CollectiveOp.ALLREDUCE, shares, AR_BYTES)
+        clique.set_shares(AR, shares, AR_BYTES)
         for _ in range(2):
             clique.all_reduce(sends, recvs)
         dt = _time_steps(lambda: clique.all_reduce(sends, recvs), steps, stream)
         return busbw_allreduce(AR_BYTES, dt, n), dt
 
-    pcie_only, _ = busbw_with((0, 1000, 0), 0, steps=3)
+    pcie_only, _ = busbw_pinned((0, 1000, 0), 0, steps=3)
     target = pcie_only * 200.0 / 64.0
     best = None
     for ctas in (1, 2, 3, 4, 6, 8, 12, 16):
-        bw, _ = busbw_with((1000, 0, 0), ctas, steps=3)
+        bw, _ = busbw_pinned((1000, 0, 0), ctas, steps=3)
         if best is None or abs(bw - target) < abs(best[1] - target):
             best = (ctas, bw)
     ctas = best[0]
-    clique.set_nvlink_ctas(ctas)
-    shares, trace, tuned_s, base_s = flx.tune_shares(
-        clique, topo, CollectiveOp.ALLREDUCE, sends, recvs, TunerConfig(), warmup=1, repeats=3)
-    nv_only, nv_dt = busbw_with((1000, 0, 0), ctas, steps=args.steps)
-    striped, st_dt = busbw_with(shares, ctas, steps=args.steps)
+    nv_only, nv_dt = busbw_pinned((1000, 0, 0), ctas, steps=args.steps)
+    clique.set_shares(AR, None, AR_BYTES)  # unpin: the in-library balancer owns the bucket
+    t0 = time.perf_counter()
+    tune_calls = settle(clique, lambda: clique.all_reduce(sends, recvs), AR, AR_BYTES)
+    tune_wall = time.perf_counter() - t0
+    info = clique.tune_info(AR, AR_BYTES)
+    trace = clique.tune_trace(AR, AR_BYTES)
+    for _ in range(2):
+        clique.all_reduce(sends, recvs)
+    st_dt = _time_steps(lambda: clique.all_reduce(sends, recvs), args.steps, stream)
+    striped = busbw_allreduce(AR_BYTES, st_dt, n)
     pbytes = clique.path_bytes()
-    drift = run_stage2_drift(clique, sends, recvs, shares, stream)
+    exact = torch_exact(sends)
+    ok = all(r.equal(exact) for r in recvs)
+    drift = run_stage2_drift(clique, sends, recvs, stream)
     clique.set_nvlink_ctas(args.nvlink_ctas)
-    clique.set_shares(CollectiveOp.ALLREDUCE, (1000, 0, 0), AR_BYTES)
     return {
         "workload": "config 4: AllReduce fp32 256 MiB/rank, 8 virtual ranks, NVLink-path kernel "
                     "capped to emulate H800's NVLink:PCIe ratio (200:64 per direction)",
         "nvlink_ctas": ctas, "pcie_only_busbw": round(pcie_only, 2),
         "nvlink_only_busbw": round(nv_only, 2), "striped_busbw": round(striped, 2),
         "gain_pct": round(100 * (striped / nv_only - 1), 2),
-        "shares": {k.short: shares.get(k) for k in PathKind},
+        "shares": {k.short: info["shares"][int(k)] for k in PathKind},
         "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
-        "stage1_iterations": trace.iterations, "stage1_trace": [r.action for r in trace.records],
+        "balancer": {"where": "in-library, no flxSetShares", "tuning_calls": tune_calls,
+                     "tuning_wall_s": round(tune_wall, 2), **info,
+                     "stage1_trace": [r["action"] for r in trace]},
         "ms_per_step": {"nvlink_only": round(nv_dt * 1e3, 4), "striped": round(st_dt * 1e3, 4)},
+        "result_exact": bool(ok),
         "stage2_drift": drift,
     }
 
 
-def run_stage2_drift(clique, sends, recvs, shares, stream, calls: int = 240,
-                     hog_from: int = 60, hog_to: int = 150) -> dict:
-    """Stage 2 on the real path (balancer.py:163-207 with measured reports): in the
-    config-4 setting, a competing H2D stream hogs PCIe between calls hog_from and
-    hog_to.  The RuntimeBalancer sees the PCIe path slow down (CUDA-event times),
-    moves granules to NVLink, and moves them back once the hog stops."""
+def torch_exact(sends):
+    import torch
+
+    return torch.stack(list(sends)).sum(0)
+
+
+def run_stage2_drift(clique, sends, recvs, stream, calls: int = 240, hog_from: int = 60,
+                     hog_to: int = 150) -> dict:
+    """In-library Stage 2 on the real path (balancer.py:163-207 semantics, csrc/autotune.cpp):
+    in the config-4 setting, a competing H2D stream hogs PCIe between calls hog_from and
+    hog_to.  The balancer sees the PCIe path slow down (lagged CUDA-event times), moves
+    granules to NVLink, and moves them back once the hog stops."""
     import torch
 
     from paper_2510_15882_b200.links import PathKind
-    from paper_2510_15882_b200.stage2 import BalancerConfig, RuntimeBalancer
-    from paper_2510_15882_b200.striping import CollectiveOp, PathTimingReport
+    from paper_2510_15882_b200.striping import CollectiveOp
 
-    n = len(sends)
+    AR = CollectiveOp.ALLREDUCE
     hog_src = torch.empty(256 << 20, dtype=torch.uint8, pin_memory=True)
     hog_dst = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     hog_stream = torch.cuda.Stream()
-    bal = RuntimeBalancer(shares, BalancerConfig(), active=shares.loaded_paths)
-    clique.set_shares(CollectiveOp.ALLREDUCE, bal.shares, AR_BYTES)
+    start = clique.tune_info(AR, AR_BYTES)
+    seen = start["stage2_evaluations"]
     trace = []
     for call in range(1, calls + 1):
-        if hog_from <= call < hog_to:
+        hog = hog_from <= call < hog_to
+        if hog:
             with torch.cuda.stream(hog_stream):
                 hog_dst.copy_(hog_src, non_blocking=True)
         clique.all_reduce(sends, recvs)
-        t, b = clique.path_times(), clique.path_bytes()
-        rep = PathTimingReport.build(CollectiveOp.ALLREDUCE, n, AR_BYTES,
-                                     {k: t[k] for k in bal.active if b[k] > 0})
-        ev = bal.observe(rep)
-        if ev is not None:
-            if ev.moved:
-                clique.set_shares(CollectiveOp.ALLREDUCE, bal.shares, AR_BYTES)
-            trace.append({"call": call, "gap": None if ev.gap is None else round(ev.gap, 4),
-                          "moved": ev.moved, "pcie": bal.shares.get(PathKind.PCIE_STAGED),
-                          "hog": hog_from <= call < hog_to})
+        # lockstep: one hog copy per call, so the contention lasts exactly the
+        # hog window (the host would otherwise queue them all ahead of the GPU)
+        stream.synchronize()
+        info = clique.tune_info(AR, AR_BYTES)
+        if info["stage2_evaluations"] != seen:
+            seen = info["stage2_evaluations"]
+            ev = clique.tune_evaluations(AR, AR_BYTES)[-1]
+            trace.append({"call": call, "gap": None if ev["gap"] is None else round(ev["gap"], 4),
+                          "moved": ev["moved"], "pcie": info["shares"][int(PathKind.PCIE_STAGED)],
+                          "hog": hog})
     torch.cuda.synchronize()
+    end = clique.tune_info(AR, AR_BYTES)
+    during = [e["pcie"] for e in trace if e["hog"]]
     return {"calls": calls, "hog_calls": [hog_from, hog_to],
-            "pcie_granules_start": shares.get(PathKind.PCIE_STAGED),
-            "pcie_granules_during_hog_min": min(e["pcie"] for e in trace if e["hog"]),
-            "pcie_granules_end": bal.shares.get(PathKind.PCIE_STAGED),
+            "pcie_granules_start": start["shares"][int(PathKind.PCIE_STAGED)],
+            "pcie_granules_during_hog_min": min(during) if during else None,
+            "pcie_granules_end": end["shares"][int(PathKind.PCIE_STAGED)],
             "evaluations": trace}
 
 
 def run_config5(clique, topo, stream) -> dict:
-    """BASELINE config 5: Qwen-32B-shaped TP=8 prefill at 64K tokens — per layer two
-    AllReduces of a [65536, 5120] bf16 activation (640 MiB per rank), 64 layers.
-    Runs the 128 calls back to back on 8 virtual ranks; reports total comm time."""
+    """BASELINE config 5: Qwen2.5-32B-shaped TP=8 prefill at 64K tokens
+    (hidden 5120, intermediate 27648, 64 layers).  Each layer's
+    two row-parallel GEMMs (attention out-projection [64K, 640] x [640, 5120]
+    and MLP down-projection [64K, 3456] x [3456, 5120] per rank) each end in an
+    AllReduce of the [65536, 5120] bf16 activation (640 MiB per rank) — here
+    over 8 virtual ranks on one B200, so all 8 ranks' GEMMs share this GPU too.
+
+    Reported: the AllReduces alone (comm), the GEMMs alone, the full layer
+    stack GEMM -> AllReduce in order, and the same stack with each GEMM+AllReduce
+    pair split into 4 token chunks on two streams so chunk k's AllReduce overlaps
+    chunk k+1's GEMM (the comm/compute overlap a fused TP layer gets)."""
     import torch
 
-    from paper_2510_15882_b200 import comm as flx
     from paper_2510_15882_b200.links import PathKind
-    from paper_2510_15882_b200.stage1 import TunerConfig
     from paper_2510_15882_b200.striping import CollectiveOp
 
     n, tokens, hidden, layers = len(clique.comms), 65536, 5120, 64
+    k_attn, k_mlp = 5120 // 8, 27648 // 8
     nbytes = tokens * hidden * 2
-    acts = [torch.randn(tokens, hidden, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
-    outs = [torch.empty_like(x) for x in acts]
-    shares, trace, _, _ = flx.tune_shares(clique, topo, CollectiveOp.ALLREDUCE, acts, outs,
-                                          TunerConfig(), warmup=1, repeats=3)
-    for _ in range(2):
-        clique.all_reduce(acts, outs)
-    total = _time_steps(lambda: clique.all_reduce(acts, outs), 2 * layers, stream) * 2 * layers
+    g = torch.Generator(device="cuda").manual_seed(55)
+    outs = [torch.empty(tokens, hidden, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
+    x_attn = [torch.randn(tokens, k_attn, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    x_mlp = [torch.randn(tokens, k_mlp, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    w_attn = [(torch.randn(k_attn, hidden, device="cuda", generator=g) / 32).bfloat16()
+              for _ in range(n)]
+    w_mlp = [(torch.randn(k_mlp, hidden, device="cuda", generator=g) / 64).bfloat16()
+             for _ in range(n)]
+    AR = CollectiveOp.ALLREDUCE
+
+    # comm alone: 128 AllReduces of 640 MiB (the balancer settles the bucket first)
+    acts = [torch.randn(tokens, hidden, device="cuda", generator=g).bfloat16() for _ in range(n)]
+    settle(clique, lambda: clique.all_reduce(acts, outs), AR, nbytes)
+    comm_s = _time_steps(lambda: clique.all_reduce(acts, outs), 2 * layers, stream) * 2 * layers
     acc = acts[0].float()
     for x in acts[1:]:
         acc += x.float()
     exact = all(torch.equal(o, acc.bfloat16()) for o in outs)
+    info = clique.tune_info(AR, nbytes)
     b = clique.path_bytes()
-    del acts, outs
-    return {"workload": "config 5: 64 layers x 2 AllReduce of [65536,5120] bf16 (640 MiB/rank), "
-                        "8 virtual ranks", "calls": 2 * layers,
-            "total_comm_ms": round(total * 1e3, 2),
-            "per_call_ms": round(total / (2 * layers) * 1e3, 4),
-            "busbw": round(busbw_allreduce(nbytes, total / (2 * layers), n), 2),
-            "shares": {k.short: shares.get(k) for k in PathKind},
+    del acts, acc
+
+    def gemms(which, rows=None):
+        xs, ws = (x_attn, w_attn) if which == 0 else (x_mlp, w_mlp)
+        for r in range(n):
+            if rows is None:
+                torch.matmul(xs[r], ws[r], out=outs[r])
+            else:
+                torch.matmul(xs[r][rows], ws[r], out=outs[r][rows])
+
+    def gemm_only():
+        for _ in range(layers):
+            gemms(0)
+            gemms(1)
+
+    def sequential():
+        for _ in range(layers):
+            for which in (0, 1):
+                gemms(which)
+                clique.all_reduce(outs, outs)  # in place, after the GEMM on the same stream
+
+    chunks = 4
+    per = tokens // chunks
+    comm_stream = torch.cuda.Stream()
+    ev_gemm = [torch.cuda.Event() for _ in range(chunks)]
+    ev_comm = torch.cuda.Event()
+    views = [[o[c * per:(c + 1) * per] for o in outs] for c in range(chunks)]
+    settle(clique, lambda: clique.all_reduce(views[0], views[0]), AR, nbytes // chunks)
+
+    def chunked():
+        for _ in range(layers):
+            for which in (0, 1):
+                stream.wait_event(ev_comm)  # the previous AllReduce finished with outs
+                for c in range(chunks):
+                    gemms(which, slice(c * per, (c + 1) * per))
+                    ev_gemm[c].record(stream)
+                    comm_stream.wait_event(ev_gemm[c])
+                    clique.all_reduce(views[c], views[c], stream=comm_stream)
+                ev_comm.record(comm_stream)
+        stream.wait_event(ev_comm)
+
+    out = {}
+    for name, fn in (("gemm_only", gemm_only), ("sequential", sequential), ("chunked", chunked)):
+        fn()  # warm (cuBLAS heuristics, balancer on the chunk bucket)
+        out[name] = _time_steps(fn, 1, stream)
+    flops = 2.0 * tokens * hidden * (k_attn + k_mlp) * n * layers
+    del x_attn, x_mlp, w_attn, w_mlp, outs, views
+    torch.cuda.empty_cache()
+    return {"workload": "config 5: Qwen2.5-32B TP=8 prefill, 64K tokens, 64 layers x (GEMM -> "
+                        "AllReduce [65536,5120] bf16) x 2, 8 virtual ranks on one B200",
+            "calls": 2 * layers, "comm_only_ms": round(comm_s * 1e3, 2),
+            "per_call_ms": round(comm_s / (2 * layers) * 1e3, 4),
+            "busbw": round(busbw_allreduce(nbytes, comm_s / (2 * layers), n), 2),
+            "gemm_only_ms": round(out["gemm_only"] * 1e3, 2),
+            "gemm_tflops": round(flops / out["gemm_only"] / 1e12, 1),
+            "layers_sequential_ms": round(out["sequential"] * 1e3, 2),
+            "layers_chunked_overlap_ms": round(out["chunked"] * 1e3, 2),
+            "comm_share_of_sequential_pct": round(100 * comm_s / out["sequential"], 1),
+            "overlap_saved_ms": round((out["sequential"] - out["chunked"]) * 1e3, 2),
+            "shares": {k.short: info["shares"][int(k)] for k in PathKind},
             "traffic_share_pct": {k.short: round(100 * b[k] / nbytes, 3) for k in PathKind},
             "fixed_order_fp32_fold_exact": exact}
 
@@ -729,9 +829,8 @@ def run_multi_gpu(args) -> None:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     rank, world = dist.get_rank(), dist.get_world_size()
-    from paper_2510_15882_b200.links import preset
-    from paper_2510_15882_b200.stage1 import TunerConfig, TunerState, initial_tune
-    from paper_2510_15882_b200.striping import CollectiveSpec, ShareDistribution
+    from paper_2510_15882_b200.probe import probe_pcie
+    from paper_2510_15882_b200.striping import ShareDistribution
 
     c = flx.Communicator.from_process_group()
     if args.nvlink_ctas:
@@ -741,26 +840,29 @@ def run_multi_gpu(args) -> None:
     send = torch.randint(-1024, 1024, (count,), device="cuda", generator=gen).float()
     recv = torch.empty_like(send)
     stream = torch.cuda.current_stream()
-    topo = preset("B200", n_gpus=max(world, 2)).restricted(c.available_paths())  # 1: smoke
+    # measured PCIe of this rank's link (the north star's aggregate-link roofline
+    # adds it to NVLink's 900 GB/s); min over ranks
+    pc = torch.tensor([probe_pcie(64 << 20, reps=3)["h2d"] / 1e9], device="cuda")
+    dist.all_reduce(pc, op=dist.ReduceOp.MIN)
+    pcie_gbs = float(pc.item())
 
     def stage1(op, s, r):
-        """Stage 1 on the real path with rank-agreed timings, then the guard."""
+        """The in-library balancer settles the bucket (Stage 1 + guard with
+        rank-agreed timings through the shared host segment), or --shares pins it."""
+        nbytes = s.numel() * s.element_size()
         if args.shares or world < 2:  # world 1 (FLX_BENCH_MULTI smoke): nothing to tune
             g = [int(x) for x in (args.shares or "1000,0,0").split(",")]
             shares = ShareDistribution({k: g[int(k)] for k in PathKind if g[int(k)] or k == 0})
-            c.set_shares(op, shares, s.numel() * s.element_size())
+            c.set_shares(op, shares, nbytes)
             return shares, None
-        measure = flx.rank_measure_fn(c, op, s, r, warmup=2, repeats=5)
-        spec = CollectiveSpec(op, world, s.numel() * s.element_size())
-        shares, trace = initial_tune(topo, spec, TunerConfig(), measure=measure)
-        nv = ShareDistribution({PathKind.NVLINK: 1000})
-        base = measure(TunerState(shares=nv, active=frozenset({PathKind.NVLINK}), step=1)).total
-        tuned = measure(TunerState(shares=shares, active=frozenset(shares.loaded_paths),
-                                   step=1)).total
-        if tuned >= base:
-            shares = nv
-        c.set_shares(op, shares, spec.size)
-        return shares, trace
+        fn = (lambda: c.all_reduce(s, r)) if op == CollectiveOp.ALLREDUCE else \
+            (lambda: c.all_gather(s, r))
+        calls = settle(c, fn, op, nbytes)
+        info = c.tune_info(op, nbytes)
+        shares = ShareDistribution({k: info["shares"][int(k)] for k in PathKind
+                                    if info["shares"][int(k)] or k == PathKind.NVLINK})
+        return shares, {"tuning_calls": calls, **info,
+                        "stage1_trace": [t["action"] for t in c.tune_trace(op, nbytes)]}
 
     shares, trace = stage1(CollectiveOp.ALLREDUCE, send, recv)
 
@@ -849,6 +951,7 @@ def run_multi_gpu(args) -> None:
                        "nccl": round(AR_BYTES / dt_n * (world - 1) / world / 1e9, 2),
                        "matches_nccl_bitwise": bool(same)}
     del rs_out, rs_ref, a2a_out, a2a_ref
+    cpu = cpu_allreduce_sample(5.0, AR_BYTES, world) if rank == 0 else None
     if rank == 0:
         value = busbw_allreduce(AR_BYTES, dt, world) * 1.0
         emit({
@@ -859,12 +962,15 @@ def run_multi_gpu(args) -> None:
             "config": workload_config(world),
             "shares": {k.short: shares.get(k) for k in PathKind},
             "traffic_share_pct": {k.short: round(100 * pbytes[k] / AR_BYTES, 3) for k in PathKind},
-            "stage1_trace": [r.action for r in trace.records] if trace else "fixed --shares",
-            "roofline": {"bound": "nvlink", "achieved": round(value, 2),
-                         "peak": round(770.0 + 55.0, 1), "unit": "GB/s",
-                         "frac": round(value / 825.0, 4), "traffic": None,
-                         "note": "busbw vs measured NVLink peer 770 GB/s/dir (B200_PROFILING.md) "
-                                 "+ ~55 GB/s PCIe Gen5 per direction; NIC absent"},
+            "balancer": trace if trace else "fixed --shares",
+            "roofline": {"bound": "link", "achieved": round(value, 2),
+                         "peak": round(900.0 + pcie_gbs, 1), "unit": "GB/s",
+                         "frac": round(value / (900.0 + pcie_gbs), 4), "traffic": None,
+                         "kernel": "rank_allreduce_kernel (NVLink slice) + host-hub PCIe slice",
+                         "note": "busbw vs the north star's aggregate-link roofline: NVLink 5 "
+                                 "900 GB/s/dir + this run's measured PCIe H2D (min over ranks); "
+                                 "NIC absent.  Same denominator as the N=1 line's link_roofline"},
+            "cpu_baseline": cpu,
             "nccl": {"value": round(busbw_allreduce(AR_BYTES, nccl_dt, world), 2),
                      "ms_per_step": round(nccl_dt * 1e3, 4)},
             "result_matches_exact_sum": bool(ok), "gpu_launches": launches, "clocks": clocks,
@@ -881,9 +987,10 @@ def run_multi_gpu(args) -> None:
                                       for k in PathKind},
                 "nccl": round(busbw_allgather(AG_OUT_BYTES, ag_nccl_dt, world), 2),
                 "matches_nccl_bitwise": bool(ag_ok),
-                "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, world), None)},
+                "link_roofline": link_roofline(busbw_allgather(AG_OUT_BYTES, ag_dt, world),
+                                               pcie_gbs)},
             **extra,
-            "link_roofline": link_roofline(value, None),
+            "link_roofline": link_roofline(value, pcie_gbs),
         })
     dist.barrier()
     c.destroy()

@@ -164,7 +164,9 @@ flxResult_t flxGroupEnd(void);
  * Shares are ShareDistribution.granules (collectives.py:55-90) as
  * {nvlink, pcie, rdma}, summing to 1000.  bucket = size_bucket(bytes)
  * (floor(log2)), or FLX_BUCKET_ALL.  Every rank must install identical
- * shares (the Python layer agrees them across ranks first). */
+ * shares (the Python layer agrees them across ranks first).  Setting shares
+ * PINS the bucket (or every bucket): the in-library balancer
+ * (flexlink_tuner.h) leaves pinned buckets alone; granules == NULL unpins. */
 flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]);
 flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granules[3]);
 /* Per-path duration (ms, collective start -> path done) of the most recent

@@ -1,0 +1,199 @@
+"""``torch.distributed`` backend "flexlink".
+
+After :func:`register`, ``dist.init_process_group("flexlink")`` (or
+``backend="cuda:flexlink"``) routes ``dist.all_reduce`` /
+``dist.all_gather_into_tensor`` / ``dist.reduce_scatter_tensor`` /
+``dist.all_to_all_single`` (and their list forms) to FlexLink's striped
+collectives, so tensor-parallel code, DTensor and anything else that calls the
+torch.distributed API names picks up the NVLink + PCIe split — and the
+in-library two-stage balancer — without code changes (the
+motivating workload is TP AllReduce in a Qwen-32B prefill).
+
+One process per GPU.  The communicator is bootstrapped through the process
+group's own store (rank 0 publishes the flxUniqueId).  Collectives are
+enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
+``async_op=False`` path), so the returned work objects are complete from the
+stream's point of view.  Operations FlexLink does not implement (broadcast,
+send/recv, gather/scatter, uneven all_to_all splits, ReduceOp.AVG) raise
+``NotImplementedError`` instead of silently falling back to another library.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+from torch.futures import Future
+
+from .comm import Communicator
+
+__all__ = ["BACKEND", "register", "FlexLinkBackend", "backend_of"]
+
+BACKEND = "flexlink"
+_instances: list["FlexLinkBackend"] = []
+
+
+class _DoneWork(dist._Work):
+    """Work handle of a stream-ordered collective: complete once enqueued."""
+
+    def __init__(self, result):
+        super().__init__()
+        self._fut = Future()
+        self._fut.set_result(result)
+
+    def wait(self, timeout=None) -> bool:
+        return True
+
+    def is_completed(self) -> bool:
+        return True
+
+    def get_future(self) -> Future:
+        return self._fut
+
+
+def _op_name(op) -> str:
+    table = {dist.ReduceOp.SUM: "sum", dist.ReduceOp.PRODUCT: "prod", dist.ReduceOp.MAX: "max",
+             dist.ReduceOp.MIN: "min"}
+    for k, v in table.items():
+        if op == k:
+            return v
+    raise NotImplementedError(f"FlexLink reduces with sum/prod/max/min only, not {op}")
+
+
+class FlexLinkBackend(dist.ProcessGroup):
+    """A c10d process-group backend over :class:`~paper_2510_15882_b200.comm.Communicator`."""
+
+    def __init__(self, store, rank: int, size: int, timeout):
+        super().__init__(rank, size)
+        key = "flexlink/unique_id"
+        if rank == 0:
+            uid = Communicator.unique_id()
+            store.set(key, uid)
+        else:
+            uid = bytes(store.get(key))
+        self.comm = Communicator.init_rank(size, uid, rank)
+        self._store = store
+        self._barriers = 0
+        _instances.append(self)
+
+    # -- names
+    def getBackendName(self) -> str:
+        return BACKEND
+
+    @property
+    def _stream(self):
+        return torch.cuda.current_stream()
+
+    # -- collectives
+    def allreduce(self, tensors, opts=None):
+        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        for t in tensors:
+            self.comm.all_reduce(t, t, op=op, stream=self._stream)
+        return _DoneWork(tensors)
+
+    def _allgather_base(self, output, input, opts=None):
+        self.comm.all_gather(input, output, stream=self._stream)
+        return _DoneWork([output])
+
+    def allgather(self, output_lists, input_list, opts=None):
+        for outs, inp in zip(output_lists, input_list):
+            flat = torch.empty(inp.numel() * self.size(), dtype=inp.dtype, device=inp.device)
+            self.comm.all_gather(inp.contiguous(), flat, stream=self._stream)
+            for r, o in enumerate(outs):
+                o.copy_(flat[r * inp.numel():(r + 1) * inp.numel()].view_as(o))
+        return _DoneWork(output_lists)
+
+    def allgather_into_tensor_coalesced(self, outputs, inputs, opts=None):
+        for o, i in zip(outputs, inputs):
+            self.comm.all_gather(i, o, stream=self._stream)
+        return _DoneWork(outputs)
+
+    def _reduce_scatter_base(self, output, input, opts=None):
+        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        self.comm.reduce_scatter(input, output, op=op, stream=self._stream)
+        return _DoneWork([output])
+
+    def reduce_scatter(self, output_tensors, input_lists, opts=None):
+        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        for out, ins in zip(output_tensors, input_lists):
+            flat = torch.cat([i.reshape(-1) for i in ins])
+            res = torch.empty(out.numel(), dtype=out.dtype, device=out.device)
+            self.comm.reduce_scatter(flat, res, op=op, stream=self._stream)
+            out.copy_(res.view_as(out))
+        return _DoneWork(output_tensors)
+
+    def alltoall_base(self, output, input, output_split_sizes, input_split_sizes, opts=None):
+        n = self.size()
+        even = input.numel() // n if input.shape[0] % n == 0 else -1
+        for splits in (output_split_sizes, input_split_sizes):
+            if splits and len(set(splits)) != 1:
+                raise NotImplementedError("FlexLink all_to_all needs equal splits")
+        if even < 0:
+            raise NotImplementedError("FlexLink all_to_all needs dim 0 divisible by world size")
+        self.comm.all_to_all(input.contiguous(), output, stream=self._stream)
+        return _DoneWork([output])
+
+    def barrier(self, opts=None):
+        # every rank's queued work done, then a rendezvous on the group's store
+        # (no device collective: a 4-byte AllReduce would be a latency-bound
+        # NVLink-path kernel for nothing)
+        torch.cuda.current_stream().synchronize()
+        self._barriers += 1
+        key = f"flexlink/barrier/{self._barriers}"
+        self._store.add(key, 1)
+        while int(self._store.add(key, 0)) < self.size():
+            import time
+
+            time.sleep(0.001)
+        return _DoneWork([])
+
+    def shutdown(self) -> None:
+        """Destroy the FlexLink communicator (its destroy barrier waits for the peers)."""
+        if self.comm is not None:
+            self.comm.destroy()
+            self.comm = None
+
+    # -- not implemented by FlexLink: refuse, never fall back
+    def _refuse(self, name):
+        raise NotImplementedError(f"{name} is not a FlexLink collective (AllReduce, AllGather, "
+                                  f"ReduceScatter, AllToAll are)")
+
+    def broadcast(self, *a, **k):
+        self._refuse("broadcast")
+
+    def reduce(self, *a, **k):
+        self._refuse("reduce")
+
+    def send(self, *a, **k):
+        self._refuse("send")
+
+    def recv(self, *a, **k):
+        self._refuse("recv")
+
+    def gather(self, *a, **k):
+        self._refuse("gather")
+
+    def scatter(self, *a, **k):
+        self._refuse("scatter")
+
+
+def _create(store, rank, size, timeout):
+    return FlexLinkBackend(store, rank, size, timeout)
+
+
+def register() -> None:
+    """Make ``"flexlink"`` a torch.distributed backend name (idempotent)."""
+    if hasattr(dist.Backend, BACKEND.upper()):
+        return
+    dist.Backend.register_backend(BACKEND, _create, devices=["cuda"])
+
+
+def backend_of(group=None) -> FlexLinkBackend:
+    """The FlexLink backend object behind ``group`` (default: the last created)."""
+    if not _instances:
+        raise RuntimeError("no FlexLink process group has been created")
+    if group is None:
+        return _instances[-1]
+    for inst in reversed(_instances):
+        if inst.rank() == dist.get_rank(group) and inst.size() == dist.get_world_size(group):
+            return inst
+    raise RuntimeError("group is not a FlexLink process group")

@@ -287,9 +287,12 @@ class Communicator:
 
     # ---- balancer plumbing
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:
+        """Pin the split of one size bucket (or every bucket when ``nbytes`` is None);
+        ``shares=None`` unpins it, handing it back to the in-library balancer."""
         bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)
-        _check(load_library().flxSetShares(self._h, _COLL[CollectiveOp(op)], bucket,
-                                           _granule_array(shares)), "flxSetShares")
+        g = None if shares is None else _granule_array(shares)
+        _check(load_library().flxSetShares(self._h, _COLL[CollectiveOp(op)], bucket, g),
+               "flxSetShares")
 
     def get_shares(self, op: CollectiveOp, nbytes: int | None = None) -> ShareDistribution:
         bucket = FLX_BUCKET_ALL if nbytes is None else size_bucket(nbytes)

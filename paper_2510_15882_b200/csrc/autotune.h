@@ -57,6 +57,11 @@ class AutoTuner {
   int trace(int op, int bucket, flxTuneRecord* out, int max) const;
   int evaluations(int op, int bucket, flxEvalRecord* out, int max) const;
   bool current(int op, int bucket, Granules* g) const;
+  // forget every bucket (a path setting changed: earlier measurements are void)
+  void reset() {
+    slots_.clear();
+    unread_.clear();
+  }
 
  private:
   struct Meas {

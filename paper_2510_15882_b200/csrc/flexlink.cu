@@ -1040,7 +1040,17 @@ flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int g
   FLX_TRY(validate_comm(comm));
   if (op < flxCollAllReduce || op > flxCollAllToAll)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
-  if (!granules) return fail(flxInvalidArgument, "null granules");
+  if (!granules) {  // unpin: the bucket (or every bucket) goes back to the balancer
+    ShareTable& t = comm->shares[op];
+    if (bucket == FLX_BUCKET_ALL) {
+      t.fallback = Granules{{FLX_GRANULE_TOTAL, 0, 0}};
+      t.fallback_pinned = false;
+      t.entries.clear();
+    } else {
+      t.entries.erase({(int)op, bucket});
+    }
+    return flxSuccess;
+  }
   Granules g{{granules[0], granules[1], granules[2]}};
   int sum = 0;
   for (int p = 0; p < FLX_NUM_PATHS; ++p) {
@@ -1136,6 +1146,7 @@ flxResult_t flxSetTiming(flxComm_t comm, int enabled) {
 flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
   FLX_TRY(validate_comm(comm));
   if (nctas < 0 || nctas > 65535) return fail(flxInvalidArgument, "bad nctas %d", nctas);
+  if (comm->nvlink_ctas != nctas) tuner_of(comm)->reset();  // measured rates are void
   comm->nvlink_ctas = nctas;
   if (comm->world) world_set_nctas(comm->world, nctas > 0 ? nctas : 32);
   return flxSuccess;
@@ -1146,6 +1157,7 @@ flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers) {
   if (buffers != 1 && buffers != 2)
     return fail(flxInvalidArgument, "buffers must be 1 or 2 (staging.py:41-42)");
   if (chunk_bytes % 4096) return fail(flxInvalidArgument, "chunk_bytes must be a multiple of 4096");
+  if (comm->chunk_bytes != chunk_bytes || comm->buffers != buffers) tuner_of(comm)->reset();
   comm->chunk_bytes = chunk_bytes;
   comm->buffers = buffers;
   return flxSuccess;
@@ -1192,6 +1204,7 @@ flxResult_t flxSetTunerConfig(flxComm_t comm, const flxTunerConfig* s1,
   if (s1) comm->tune_s1 = *s1;
   if (s2) comm->tune_s2 = *s2;
   if (min_bytes) comm->tune_min_bytes = min_bytes;
+  tuner_of(comm)->reset();
   return flxSuccess;
 }
 
@@ -1201,6 +1214,7 @@ flxResult_t flxSetLinkProfile(flxComm_t comm, const flxLinkProfile* profile) {
     return fail(flxInvalidArgument, "the link profile needs a positive NVLink bandwidth");
   comm->have_profile = profile != nullptr;
   if (profile) comm->profile = *profile;
+  tuner_of(comm)->reset();
   return flxSuccess;
 }
 

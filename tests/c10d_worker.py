@@ -1,0 +1,74 @@
+"""Worker for tests/test_gpu_c10d.py: one rank of a 'flexlink' torch.distributed
+process group, exercising the torch API names against exact expectations."""
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2510_15882_b200 import c10d  # noqa: E402
+from paper_2510_15882_b200.striping import CollectiveOp  # noqa: E402
+
+
+def vals(rank, n, shift=0):
+    i = torch.arange(n, dtype=torch.float64)
+    return (((i * (rank + 3) + shift) % 251) - 100).float()
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    c10d.register()
+    dist.init_process_group("flexlink", rank=rank, world_size=world)
+    comm = c10d.backend_of().comm
+    if os.environ.get("FLX_C10D_PCIE_ONLY"):
+        # two processes share this GPU: every byte on the host-staged PCIe path
+        # (copy engines only), so no NVLink-path kernel waits on the other process
+        for op in CollectiveOp:
+            comm.set_shares(op, (0, 1000, 0))
+    n = 1 << 18  # a multiple of every alignment: no NVLink remainder
+    dev = torch.device("cuda", 0)
+    bad = 0
+    for it in range(2):
+        x = vals(rank, n, it).to(dev)
+        want = sum(vals(r, n, it) for r in range(world)).to(dev)
+        dist.all_reduce(x)
+        bad += int(not torch.equal(x, want))
+        mx = vals(rank, n, it).to(dev)
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        bad += int(not torch.equal(mx, torch.stack([vals(r, n, it) for r in range(world)]).max(0)
+                                   .values.to(dev)))
+        src = vals(rank, n, it).to(dev)
+        out = torch.empty(world * n, device=dev)
+        dist.all_gather_into_tensor(out, src)
+        bad += int(not torch.equal(out, torch.cat([vals(r, n, it) for r in range(world)]).to(dev)))
+        outs = [torch.empty(n, device=dev) for _ in range(world)]
+        dist.all_gather(outs, src)
+        bad += int(not all(torch.equal(o, vals(r, n, it).to(dev)) for r, o in enumerate(outs)))
+        big = vals(rank, world * n, it).to(dev)
+        rs = torch.empty(n, device=dev)
+        dist.reduce_scatter_tensor(rs, big)
+        full = sum(vals(r, world * n, it) for r in range(world))
+        bad += int(not torch.equal(rs, full[rank * n:(rank + 1) * n].to(dev)))
+        a2a = torch.empty(world * n, device=dev)
+        dist.all_to_all_single(a2a, big)
+        want_a2a = torch.cat([vals(r, world * n, it)[rank * n:(rank + 1) * n]
+                              for r in range(world)]).to(dev)
+        bad += int(not torch.equal(a2a, want_a2a))
+    dist.barrier()
+    try:
+        dist.broadcast(x, 0)
+        bad += 1  # must refuse, not fall back
+    except Exception as e:
+        if "not a FlexLink collective" not in str(e):
+            bad += 1
+    torch.cuda.synchronize()
+    print(f"rank {rank} bad {bad}", flush=True)
+    c10d.backend_of().shutdown()
+    dist.destroy_process_group()
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()

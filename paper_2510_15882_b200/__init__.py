@@ -10,6 +10,8 @@ surface.  The native data plane (``libflexlink.so``) is reached through
 :mod:`paper_2510_15882_b200.comm`.
 """
 
+from .calibration import (H800_MEASUREMENTS, CalibrationError, CalibrationResult, LinkFit,
+                          MeasuredRow, build_calibrated_topology, calibrate)
 from .fairshare import NoiseModel, SimClock, effective_bandwidths, maxmin_rates
 from .links import (LinkSpec, PathKind, TopologySpec, idle_bw_opportunity, load_topology,
                     preset, topology_for)
@@ -28,6 +30,8 @@ from .units import parse_bandwidth, parse_size, parse_time
 __version__ = "1.0.0"
 
 __all__ = [
+    "H800_MEASUREMENTS", "CalibrationError", "CalibrationResult", "LinkFit", "MeasuredRow",
+    "build_calibrated_topology", "calibrate",
     "Adjustment", "BalancerConfig", "BandwidthShift", "CollectiveOp", "CollectiveSpec",
     "DynamicResult", "GRANULE_TOTAL", "LinkSpec", "NoiseModel", "OracleResult", "PathKind",
     "PathTimingReport", "PipelineSpec", "ProtocolVerdict", "RuntimeBalancer", "ShareDistribution",

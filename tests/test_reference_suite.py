@@ -22,4 +22,4 @@ def test_reference_suite_passes_against_this_control_plane():
     spec.loader.exec_module(mod)
     res = mod.run()
     assert res["unexpected_failures"] == [], res
-    assert res["passed"] >= 114, res
+    assert res["passed"] >= 125, res

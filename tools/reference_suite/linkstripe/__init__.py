@@ -5,10 +5,11 @@ reference's own test-suite runs against it (``tools/reference_suite/run.py``,
 installed, never imported by the product.
 
 Modules the tier framing leaves out of scope (the reference CLI ``cli.py``,
-the H800 calibration / golden reproduction in ``bench.py:72-422`` and the
-fluid transfer engine ``simcore.run_transfers``) are stubs whose callables
-raise ``NotImplementedError``: the tests that need them fail, and the runner
-lists exactly which.
+the simulated bench-table generator in ``bench.py`` — its calibration IS
+bound, to ``calibration.py`` — and the fluid transfer engine
+``simcore.run_transfers``) are stubs whose callables raise
+``NotImplementedError``: the tests that need them fail, and the runner lists
+exactly which.
 """
 
 import importlib
@@ -52,10 +53,9 @@ def _module(name, base=None, stubs=(), values=None):
 # simcore: the max-min fair share (in scope, fairshare.py) + the fluid engine (out)
 simcore = _module("simcore", importlib.import_module("paper_2510_15882_b200.fairshare"),
                   stubs=("TransferRequest", "run_transfers", "write_event_log"))
-# bench.py: the H800 calibration table and reproduction (out of scope)
-bench = _module("bench", stubs=("BenchPlan", "check_offload_identity", "reproduce_reference",
-                                "run_bench", "calibrate"),
-                values={"H800_MEASUREMENTS": (), "MODE_BASELINE": "baseline",
-                        "MODE_PCIE_ONLY": "pcie_only", "MODE_PCIE_RDMA": "pcie_rdma"})
+# bench.py: the calibration (calibration.py) is in scope; the simulated bench
+# table generator and its formatting are not
+bench = _module("bench", importlib.import_module("paper_2510_15882_b200.calibration"),
+                stubs=("BenchPlan", "run_bench", "format_rows"))
 # cli.py (out of scope)
 cli = _module("cli", stubs=("main",))

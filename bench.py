@@ -644,6 +644,7 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
     exact = torch_exact(sends)
     ok = all(r.equal(exact) for r in recvs)
     drift = run_stage2_drift(clique, sends, recvs, stream)
+    cal = run_calibration(clique, sends, recvs, stream, ctas, striped, pbytes, info)
     clique.set_nvlink_ctas(args.nvlink_ctas)
     return {
         "workload": "config 4: AllReduce fp32 256 MiB/rank, 8 virtual ranks, NVLink-path kernel "
@@ -659,7 +660,59 @@ def run_config4(clique, sends, recvs, topo, args, stream) -> dict:
         "ms_per_step": {"nvlink_only": round(nv_dt * 1e3, 4), "striped": round(st_dt * 1e3, 4)},
         "result_exact": bool(ok),
         "stage2_drift": drift,
+        "calibration": cal,
     }
+
+
+def run_calibration(clique, sends, recvs, stream, ctas, striped_busbw, pbytes, info) -> dict:
+    """SURVEY §8(f) row 2 on this run's own rows: the alpha-beta fit of the
+    reference's `calibrate` (bench.py:151-227, calibration.py) over NVLink-only
+    AllReduce at 3 sizes under the config-4 cap plus the balancer's striped row,
+    then Stage 1 re-run seeded from the calibrated topology (flxSetLinkProfile)
+    instead of the in-call probe round."""
+    from paper_2510_15882_b200 import calibration as C
+    from paper_2510_15882_b200.links import PathKind
+    from paper_2510_15882_b200.striping import CollectiveOp
+
+    AR = CollectiveOp.ALLREDUCE
+    n = len(sends)
+    rows = []
+    for mib in (64, 128, 256):
+        cnt = mib * MIB // 4
+        s = [x[:cnt] for x in sends]
+        r = [x[:cnt] for x in recvs]
+        clique.set_shares(AR, (1000, 0, 0), cnt * 4)
+        for _ in range(2):
+            clique.all_reduce(s, r)
+        dt = _time_steps(lambda: clique.all_reduce(s, r), 5, stream)
+        rows.append(C.MeasuredRow(AR, n, cnt * 4, C.MODE_BASELINE, cnt * 4 / dt / 1e9))
+        if mib != 256:
+            clique.set_shares(AR, None, cnt * 4)
+    clique.set_shares(AR, None, AR_BYTES)
+    algbw_striped = striped_busbw / (2 * (n - 1) / n)
+    rows.append(C.MeasuredRow(AR, n, AR_BYTES, C.MODE_PCIE_ONLY, algbw_striped, 0,
+                              100.0 * pbytes[PathKind.PCIE_STAGED] / AR_BYTES))
+    cal = C.calibrate(rows)
+    topo = C.build_calibrated_topology(cal, AR, n, C.MODE_PCIE_ONLY)
+    clique.set_link_profile(topo)  # resets the bucket: Stage 1 again, seeded from the fit
+    calls = settle(clique, lambda: clique.all_reduce(sends, recvs), AR, AR_BYTES)
+    seeded = clique.tune_info(AR, AR_BYTES)
+    clique.set_link_profile(None)
+    fit = cal.nvlink[(AR, n)]
+    return {"rows": [{"size": r.size, "mode": r.mode, "algbw_gbs": round(r.algbw, 3),
+                      "pcie_load_pct": round(r.pcie_load, 2)} for r in rows],
+            "nvlink_fit": {"bandwidth_gbs": round(fit.bandwidth / 1e9, 3),
+                           "latency_us": round(fit.latency * 1e6, 3),
+                           "residuals": {str(k): round(v, 4) for k, v in fit.residuals.items()}},
+            "pcie_fit_gbs": round(cal.secondary[(AR, n, C.MODE_PCIE_ONLY)][PathKind.PCIE_STAGED]
+                                  / 1e9, 3),
+            "stage1_seeded_from_fit": {"tuning_calls": calls,
+                                       "iterations": seeded["stage1_iterations"],
+                                       "shares": seeded["shares"],
+                                       "tuned_ms": seeded["tuned_ms"],
+                                       "kept_tuned": seeded["kept_tuned"]},
+            "stage1_seeded_by_probe_round": {"iterations": info["stage1_iterations"],
+                                             "shares": info["shares"]}}
 
 
 def torch_exact(sends):

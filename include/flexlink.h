@@ -199,6 +199,16 @@ flxResult_t flxSetTiming(flxComm_t comm, int enabled);
 flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers);
 /* Which optional paths this build/box can use: bit p set => path p usable. */
 flxResult_t flxGetPathMask(flxComm_t comm, int* mask);
+/* NVLink-SHARP (in-switch reduction, multimem.ld_reduce / multimem.st).
+ * flxNvlsProbe: can `device` make a multicast object and run the NVLS kernel
+ * on it (checked end to end on a one-device object)?  *available 0/1 and the
+ * reason (e.g. the driver's error for cuMulticastCreate).  flxCommGetNvls:
+ * whether this multi-GPU communicator runs its AllReduce sums on NVLS
+ * (opt-in FLX_NVLS=1 on every rank; off, with the reason, where the box
+ * cannot).  Results of NVLS sums are within 1 ulp of the fixed-order fold
+ * (the switch picks the order); exact for integer-valued data. */
+flxResult_t flxNvlsProbe(int device, int* available, char* reason, size_t reason_len);
+flxResult_t flxCommGetNvls(flxComm_t comm, int* on, char* reason, size_t reason_len);
 /* Number of device kernels this library has launched (process-wide). */
 flxResult_t flxGetLaunchCount(unsigned long long* count);
 /* Bootstrap self-test (multi-rank comms only): write=1 copies `bytes` from

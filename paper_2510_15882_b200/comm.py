@@ -111,6 +111,8 @@ def load_library() -> ctypes.CDLL:
         "flxGetPathMask": [vp, P(ci)],
         "flxGetLaunchCount": [P(ctypes.c_ulonglong)],
         "flxCommDebugPeer": [vp, ci, ci, ci, vp, sz],
+        "flxNvlsProbe": [ci, P(ci), ctypes.c_char_p, sz],
+        "flxCommGetNvls": [vp, P(ci), ctypes.c_char_p, sz],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -341,6 +343,14 @@ class Communicator:
         _check(load_library().flxGetPathMask(self._h, ctypes.byref(m)), "flxGetPathMask")
         return m.value
 
+    def nvls(self) -> tuple[bool, str]:
+        """Whether this communicator's AllReduce sums run on NVLink-SHARP, and why (not)."""
+        on = ctypes.c_int()
+        why = ctypes.create_string_buffer(256)
+        _check(load_library().flxCommGetNvls(self._h, ctypes.byref(on), why, 256),
+               "flxCommGetNvls")
+        return bool(on.value), why.value.decode(errors="replace")
+
     def available_paths(self) -> tuple[PathKind, ...]:
         m = self.path_mask()
         return tuple(k for k in PathKind if m & (1 << int(k)))
@@ -483,6 +493,15 @@ def rank_measure_fn(comm: Communicator, op: CollectiveOp, send, recv, group=None
         return agree_report(local, group)
 
     return measure
+
+
+def nvls_probe(device: int = 0) -> tuple[bool, str]:
+    """``flxNvlsProbe``: can this GPU run the NVLink-SHARP (multimem) AllReduce?
+    Checked end to end on a one-device multicast object; returns (ok, reason)."""
+    ok = ctypes.c_int()
+    why = ctypes.create_string_buffer(256)
+    _check(load_library().flxNvlsProbe(device, ctypes.byref(ok), why, 256), "flxNvlsProbe")
+    return bool(ok.value), why.value.decode(errors="replace")
 
 
 def launch_count() -> int:

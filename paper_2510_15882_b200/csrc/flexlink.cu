@@ -1148,7 +1148,7 @@ flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
   if (nctas < 0 || nctas > 65535) return fail(flxInvalidArgument, "bad nctas %d", nctas);
   if (comm->nvlink_ctas != nctas) tuner_of(comm)->reset();  // measured rates are void
   comm->nvlink_ctas = nctas;
-  if (comm->world) world_set_nctas(comm->world, nctas > 0 ? nctas : 32);
+  if (comm->world) world_set_nctas(comm->world, nctas);
   return flxSuccess;
 }
 
@@ -1176,6 +1176,16 @@ flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int writ
   if (!comm->world) return fail(flxInvalidUsage, "not a multi-rank communicator");
   if (!buf && bytes) return fail(flxInvalidArgument, "null buffer");
   return world_debug_peer(comm->world, comm->local, peer, host_region, write, buf, bytes);
+}
+
+flxResult_t flxCommGetNvls(flxComm_t comm, int* on, char* reason, size_t reason_len) {
+  FLX_TRY(validate_comm(comm));
+  if (!on) return fail(flxInvalidArgument, "null on");
+  const char* why = "NVLS needs a multi-GPU world (one process per GPU, FLX_NVLS=1)";
+  *on = 0;
+  if (comm->world) why = world_nvls_status(comm->world, on);
+  if (reason && reason_len) snprintf(reason, reason_len, "%s", why);
+  return flxSuccess;
 }
 
 flxResult_t flxGetLaunchCount(unsigned long long* count) {

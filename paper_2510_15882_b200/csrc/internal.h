@@ -156,6 +156,7 @@ bool world_aborted(World* w);
 void world_abort(World* w);
 flxResult_t world_finalize(World* w, int local);
 AutoTuner* world_tuner(World* w);
+const char* world_nvls_status(World* w, int* on);
 // run one collective over the world with the autotuner deciding the split
 flxResult_t run_world_tuned(World* w, const std::vector<const void*>& send,
                             const std::vector<void*>& recv,

@@ -134,11 +134,21 @@ __device__ __forceinline__ uint4 ld_cg(const void* p) {
 
 // Publish this CTA's prior global stores: bar.sync orders every thread's
 // stores before the flag stores, and st.release.sys is cumulative, so a rank
-// that acquires a flag sees all of them.  Lane i of warp 0 stores flag i, so
-// the N-1 peers are signalled in parallel.
-__device__ __forceinline__ void cta_signal(uint32_t* const* targets, int count, uint32_t epoch) {
+// that acquires a flag sees all of them.  Lane i of warp 0 signals peer
+// (r+1+i) mod n in its flag block, slot [kind][r][cta] — the N-1 peers in
+// parallel; with kind2 >= 0, lanes 16.. signal kind2 the same way.  The
+// target address is computed per lane: no per-peer pointer array (which
+// would live in local memory).
+__device__ __forceinline__ void cta_signal_peers(const RankArgs& a, int cta, int kind,
+                                                 uint32_t epoch, int kind2 = -1) {
   __syncthreads();
-  if (threadIdx.x < (unsigned)count) st_release_sys(targets[threadIdx.x], epoch);
+  const int lane = threadIdx.x;
+  const int i = lane & 15;
+  const int k = lane < 16 ? kind : kind2;
+  if (lane < 32 && k >= 0 && i < a.nranks - 1) {
+    const int c = (a.rank + 1 + i) % a.nranks;
+    st_release_sys(flag_at(a.flags[c], k, a.rank, cta), epoch);
+  }
 }
 
 // Flags are compared cyclically ((int)(flag - epoch) >= 0) so epochs may wrap;
@@ -189,7 +199,7 @@ __device__ __forceinline__ bool aligned16_dev(const void* p) {
 // kCopyUnroll 16 B loads per thread are in flight before the stores: a remote
 // (NVLink) load costs ~2 us, so 512 threads x 8 x 16 B = 64 KB per CTA in
 // flight is what sustains ~30 GB/s per CTA on the pull phase.
-constexpr int kCopyUnroll = 8;
+constexpr int kCopyUnroll = 4;
 
 __device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, bool coherent) {
   if (aligned16_dev(dst) && aligned16_dev(src)) {
@@ -234,17 +244,23 @@ __device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, b
   }
 }
 
-constexpr int kFoldUnroll = 4;
+// vectors per thread per source in the fold: 4 for 32/64-bit types; 2 for
+// 16-bit ones, whose fp32 accumulators are twice as many per vector (keeps the
+// kernels inside 64 registers, 2 CTAs per SM)
+template <typename T>
+constexpr int fold_unroll() { return sizeof(T) >= 4 ? 4 : 2; }
 
-// CTA-wide fold of n bytes: src[0..nsrc) -> dst[0..ndst) (fold rule of kernels.cuh).
-template <typename T, int OP>
-__device__ __forceinline__ void cta_fold(char* const* dst, int ndst, const char* const* src,
-                                         int nsrc, size_t n) {
+// CTA-wide fold of n bytes: src(0..nsrc) -> dst0 (and dst1 when non-null),
+// fold rule of kernels.cuh.  `src(p)` returns source p's pointer; it is
+// evaluated per use (a select and a multiply-add), so no per-source pointer
+// array is kept — arrays indexed by a runtime rank live in local memory.
+template <typename T, int OP, typename Src>
+__device__ __forceinline__ void cta_fold(char* dst0, char* dst1, Src src, int nsrc, size_t n) {
   using A = typename AccT<T>::type;
   constexpr int kVec = 16 / sizeof(T);
-  bool vec = true;
-  for (int i = 0; i < nsrc; ++i) vec = vec && aligned16_dev(src[i]);
-  for (int i = 0; i < ndst; ++i) vec = vec && aligned16_dev(dst[i]);
+  constexpr int kFoldUnroll = fold_unroll<T>();
+  bool vec = aligned16_dev(dst0) && (!dst1 || aligned16_dev(dst1));
+  for (int i = 0; i < nsrc; ++i) vec = vec && aligned16_dev(src(i));
   size_t done = 0;
   if (vec) {
     const size_t nv = n >> 4;
@@ -254,54 +270,50 @@ __device__ __forceinline__ void cta_fold(char* const* dst, int ndst, const char*
     // vector per source left ~2 loads in flight per thread and the fold phase
     // latency-bound (bf16, whose unpack/repack lengthens each iteration, ran
     // 0.77x fp32).  Same rank order per element, so the result is unchanged.
-    // 16-bit types with more than 4 sources keep one vector per source (already
-    // nsrc loads in flight; the unrolled body measured 0.94x there: 8 x 4 fp32
-    // accumulators spill).
+    // 16-bit types with more than 4 sources keep one vector per source (the
+    // unrolled body measured 0.94x there: 8 x 4 fp32 accumulators spill).
     const bool unrolled = sizeof(T) >= 4 || nsrc <= 4;
     for (; unrolled && v + (kFoldUnroll - 1) * step < nv; v += kFoldUnroll * step) {
       A acc[kFoldUnroll][kVec];
       uint4 w[kFoldUnroll];
+      {
+        const char* s0 = src(0);
 #pragma unroll
-      for (int u = 0; u < kFoldUnroll; ++u) w[u] = ld_cg(src[0] + ((v + u * step) << 4));
+        for (int u = 0; u < kFoldUnroll; ++u) w[u] = ld_cg(s0 + ((v + u * step) << 4));
+      }
 #pragma unroll
       for (int u = 0; u < kFoldUnroll; ++u) load_acc<T>(acc[u], w[u]);
+      for (int i = 1; i < nsrc; ++i) {
+        const char* si = src(i);
 #pragma unroll
-      for (int i = 1; i < kMaxRanks; ++i) {
-        if (i < nsrc) {
+        for (int u = 0; u < kFoldUnroll; ++u) w[u] = ld_cg(si + ((v + u * step) << 4));
 #pragma unroll
-          for (int u = 0; u < kFoldUnroll; ++u) w[u] = ld_cg(src[i] + ((v + u * step) << 4));
-#pragma unroll
-          for (int u = 0; u < kFoldUnroll; ++u) fold_into<T, OP>(acc[u], w[u]);
-        }
+        for (int u = 0; u < kFoldUnroll; ++u) fold_into<T, OP>(acc[u], w[u]);
       }
 #pragma unroll
       for (int u = 0; u < kFoldUnroll; ++u) {
         const uint4 out = pack_acc<T>(acc[u]);
-        for (int d = 0; d < ndst; ++d)
-          *reinterpret_cast<uint4*>(dst[d] + ((v + u * step) << 4)) = out;
+        *reinterpret_cast<uint4*>(dst0 + ((v + u * step) << 4)) = out;
+        if (dst1) *reinterpret_cast<uint4*>(dst1 + ((v + u * step) << 4)) = out;
       }
     }
-    for (; v < nv; v += step) {
-      uint4 w[kMaxRanks];
-#pragma unroll
-      for (int i = 0; i < kMaxRanks; ++i)
-        if (i < nsrc) w[i] = ld_cg(src[i] + (v << 4));
+    for (; v < nv; v += step) {  // one vector per thread, sources streamed in order
       A acc[kVec];
-      load_acc<T>(acc, w[0]);
-#pragma unroll
-      for (int i = 1; i < kMaxRanks; ++i)
-        if (i < nsrc) fold_into<T, OP>(acc, w[i]);
+      load_acc<T>(acc, ld_cg(src(0) + (v << 4)));
+      for (int i = 1; i < nsrc; ++i) fold_into<T, OP>(acc, ld_cg(src(i) + (v << 4)));
       const uint4 out = pack_acc<T>(acc);
-      for (int d = 0; d < ndst; ++d) *reinterpret_cast<uint4*>(dst[d] + (v << 4)) = out;
+      *reinterpret_cast<uint4*>(dst0 + (v << 4)) = out;
+      if (dst1) *reinterpret_cast<uint4*>(dst1 + (v << 4)) = out;
     }
     done = nv << 4;
   }
   for (size_t i = done / sizeof(T) + threadIdx.x; i < n / sizeof(T); i += blockDim.x) {
-    A acc = to_acc<T>(*(volatile const T*)(src[0] + i * sizeof(T)));
+    A acc = to_acc<T>(*(volatile const T*)(src(0) + i * sizeof(T)));
     for (int s = 1; s < nsrc; ++s)
-      acc = apply_op<OP>(acc, to_acc<T>(*(volatile const T*)(src[s] + i * sizeof(T))));
+      acc = apply_op<OP>(acc, to_acc<T>(*(volatile const T*)(src(s) + i * sizeof(T))));
     const T out = from_acc<T>(acc);
-    for (int d = 0; d < ndst; ++d) *reinterpret_cast<T*>(dst[d] + i * sizeof(T)) = out;
+    *reinterpret_cast<T*>(dst0 + i * sizeof(T)) = out;
+    if (dst1) *reinterpret_cast<T*>(dst1 + i * sizeof(T)) = out;
   }
 }
 
@@ -344,67 +356,50 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     const uint32_t e = ep.first + k;
     const size_t len = min(round_cap, a.bytes - base);
     const size_t chunk = ceil16((len + n - 1) / n);
-    size_t lo[kMaxRanks], hi[kMaxRanks], off[kMaxRanks];
-    const char* from[kMaxRanks];
-    size_t nb[kMaxRanks];
-    for (int c = 0; c < n; ++c) {
-      off[c] = min(len, (size_t)c * chunk);
-      cta_part(min(len, off[c] + chunk) - off[c], nctas, cta, &lo[c], &hi[c]);
-      from[c] = a.send + base + off[c] + lo[c];
-      nb[c] = hi[c] - lo[c];
-    }
+    // this CTA's part [lo, lo+nb) of rank c's chunk, as a message offset —
+    // recomputed per use instead of kept in per-peer arrays (local memory)
+    auto part = [&](int c) {
+      const size_t off = min(len, (size_t)c * chunk);
+      const size_t clen = min(len, off + chunk) - off;
+      const size_t p = ceil16((clen + nctas - 1) / nctas);
+      const size_t lo = min(clen, (size_t)cta * p), hi = min(clen, lo + p);
+      return make_ulonglong2(base + off + lo, hi - lo);  // {message offset, bytes}
+    };
     // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it,
     //    into this CTA's region of the slot)
-    {
-      if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      FLX_PHASE(1);
-      uint32_t* targets[kMaxRanks];
-      int nt = 0;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, from[c], nb[c], false);
-        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
-      }
-      cta_signal(targets, nt, e);
-      FLX_PHASE(2);
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
+    FLX_PHASE(1);
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      const ulonglong2 pc = part(c);
+      cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
     }
+    cta_signal_peers(a, cta, kArrive, e);
+    FLX_PHASE(2);
     // 2) every push landed, and every peer pulled my previous outbox
-    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a))
-      return;
+    if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a)) return;
     FLX_PHASE(3);
     {
-      const char* src[kMaxRanks];
-      for (int p = 0; p < n; ++p)
-        src[p] = (p == r) ? a.send + base + off[r] + lo[r]
-                          : a.scratch[r] + (size_t)p * a.slot + mine;
-      char* dst[2] = {a.recv + base + off[r] + lo[r], a.scratch[r] + outbox + mine};
-      cta_fold<T, OP>(dst, 2, src, n, hi[r] - lo[r]);
+      const ulonglong2 pr = part(r);
+      const char* own = a.send + pr.x;
+      const char* inbox = a.scratch[r] + mine;
+      const size_t slot = a.slot;
+      cta_fold<T, OP>(a.recv + pr.x, a.scratch[r] + outbox + mine,
+                      [=](int p) { return p == r ? own : inbox + (size_t)p * slot; }, n, pr.y);
     }
-    {  // inbox slots consumed (kFree) and outbox readable (kReady), to every peer
-      uint32_t* targets[2 * kMaxRanks];
-      int nt = 0;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        targets[nt++] = flag_at(a.flags[c], kFree, r, cta);
-        targets[nt++] = flag_at(a.flags[c], kReady, r, cta);
-      }
-      cta_signal(targets, nt, e);
-      FLX_PHASE(4);
-    }
+    // inbox slots consumed (kFree) and outbox readable (kReady), to every peer
+    cta_signal_peers(a, cta, kFree, e, kReady);
+    FLX_PHASE(4);
     // 3) pull every peer's reduced chunk
     if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a)) return;
     FLX_PHASE(5);
-    {
-      uint32_t* targets[kMaxRanks];
-      int nt = 0;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        cta_copy(a.recv + base + off[c] + lo[c], a.scratch[c] + outbox + mine, nb[c], true);
-        targets[nt++] = flag_at(a.flags[c], kPulled, r, cta);
-      }
-      cta_signal(targets, nt, e);
-      FLX_PHASE(6);
+    for (int s = 1; s < n; ++s) {
+      const int c = (r + s) % n;
+      const ulonglong2 pc = part(c);
+      cta_copy(a.recv + pc.x, a.scratch[c] + outbox + mine, pc.y, true);
     }
+    cta_signal_peers(a, cta, kPulled, e);
+    FLX_PHASE(6);
     prev_outbox = prev_main = e;
   }
   cta_epochs_done(ep, k, prev_outbox, prev_main);
@@ -450,13 +445,10 @@ __device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
   };
   FLX_PHASE(1);
   {
-    uint32_t* targets[kMaxRanks];
-    int nt = 0;
     for (int s = 1; s < n; ++s) {
       const int c = (r + s) % n;
       const char* piece = (KIND == 0 || KIND == 1) ? a.send + lo : a.send + (size_t)c * stride + lo;
       cta_copy(inbox(c, r), piece, hi - lo, false);
-      targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
     }
     if (KIND == 1) {
       char* own = a.recv + (size_t)r * stride + lo;
@@ -464,19 +456,17 @@ __device__ void rank_oneshot(const RankArgs& a, int cta, int nctas) {
     } else if (KIND == 3) {
       cta_copy(a.recv + (size_t)r * stride + lo, a.send + (size_t)r * stride + lo, hi - lo, false);
     }
-    cta_signal(targets, nt, e);
+    cta_signal_peers(a, cta, kArrive, e);
   }
   FLX_PHASE(2);
   if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
   FLX_PHASE(3);
   if (KIND == 0 || KIND == 2) {
-    const char* src[kMaxRanks];
-    for (int p = 0; p < n; ++p)
-      src[p] = p != r      ? inbox(r, p)
-               : KIND == 0 ? a.send + lo
-                           : a.send + (size_t)r * stride + lo;
-    char* dst[1] = {a.recv + lo};
-    cta_fold<T, OP>(dst, 1, src, n, hi - lo);
+    const char* own = KIND == 0 ? a.send + lo : a.send + (size_t)r * stride + lo;
+    const char* box = a.scratch[r] + region + mine;
+    const size_t ss = a.small_slot;
+    cta_fold<T, OP>(a.recv + lo, nullptr,
+                    [=](int p) { return p == r ? own : box + (size_t)p * ss; }, n, hi - lo);
   } else {
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
@@ -545,12 +535,21 @@ __device__ __forceinline__ bool ld_ll(const char* p, uint32_t e, uint4* out, con
   }
 }
 
-// m (<= 16) bytes of user memory at any alignment, zero-padded to 16.
+// m (<= 16) bytes of user memory at any alignment, zero-padded to 16.  The
+// word of byte i is picked with selects, not an indexed array (a runtime index
+// into a register array would put the vector in local memory).
 __device__ __forceinline__ uint4 ld_user(const char* p, size_t m) {
   if (m == 16 && aligned16_dev(p)) return *reinterpret_cast<const uint4*>(p);
-  uint32_t w[4] = {0, 0, 0, 0};
-  for (size_t i = 0; i < m; ++i) w[i >> 2] |= (uint32_t)(uint8_t)p[i] << (8 * (i & 3));
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+  for (size_t i = 0; i < m; ++i) {
+    const uint32_t b = (uint32_t)(uint8_t)p[i] << (8 * (i & 3));
+    const size_t k = i >> 2;
+    w0 |= k == 0 ? b : 0u;
+    w1 |= k == 1 ? b : 0u;
+    w2 |= k == 2 ? b : 0u;
+    w3 |= k == 3 ? b : 0u;
+  }
+  return make_uint4(w0, w1, w2, w3);
 }
 
 __device__ __forceinline__ void st_user(char* p, const uint4& v, size_t m) {
@@ -558,8 +557,11 @@ __device__ __forceinline__ void st_user(char* p, const uint4& v, size_t m) {
     *reinterpret_cast<uint4*>(p) = v;
     return;
   }
-  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-  for (size_t i = 0; i < m; ++i) p[i] = (char)(w[i >> 2] >> (8 * (i & 3)));
+  for (size_t i = 0; i < m; ++i) {
+    const size_t k = i >> 2;
+    const uint32_t w = k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w;
+    p[i] = (char)(w >> (8 * (i & 3)));
+  }
 }
 
 template <typename T, int OP, int KIND>
@@ -635,11 +637,7 @@ __device__ void rank_oneshot_ll(const RankArgs& a, int cta, int nctas) {
 
 // After consuming my inbox slots for epoch e: tell every source (kFree = e).
 __device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e) {
-  const int r = a.rank, n = a.nranks;
-  uint32_t* targets[kMaxRanks];
-  int nt = 0;
-  for (int s = 1; s < n; ++s) targets[nt++] = flag_at(a.flags[(r + s) % n], kFree, r, cta);
-  cta_signal(targets, nt, e);
+  cta_signal_peers(a, cta, kFree, e);
 }
 
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
@@ -655,24 +653,15 @@ __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     const size_t len = min(cap, a.bytes - base);
     size_t lo, hi;
     cta_part(len, nctas, cta, &lo, &hi);
-    const char* from[kMaxRanks];
-    size_t nb[kMaxRanks];
-    for (int c = 0; c < n; ++c) {
-      from[c] = a.send + base + lo;
-      nb[c] = hi - lo;
-    }
     {  // push my slice into every peer's inbox slot r (this CTA's region)
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      uint32_t* targets[kMaxRanks];
-      int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, from[c], nb[c], false);
-        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + base + lo, hi - lo, false);
       }
       char* own = a.recv + (size_t)r * a.rank_stride + base;
       if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
-      cta_signal(targets, nt, e);
+      cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
@@ -704,24 +693,21 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
     cta_part(len, nctas, cta, &lo, &hi);
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      uint32_t* targets[kMaxRanks];
-      int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
         cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
                  a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
-        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
-      cta_signal(targets, nt, e);
+      cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     {
-      const char* src[kMaxRanks];
-      for (int p = 0; p < n; ++p)
-        src[p] = (p == r) ? a.send + (size_t)r * a.rank_stride + base + lo
-                          : a.scratch[r] + (size_t)p * a.slot + mine;
-      char* dst[1] = {a.recv + base + lo};
-      cta_fold<T, OP>(dst, 1, src, n, hi - lo);
+      const char* own = a.send + (size_t)r * a.rank_stride + base + lo;
+      const char* inbox = a.scratch[r] + mine;
+      const size_t slot = a.slot;
+      cta_fold<T, OP>(a.recv + base + lo, nullptr,
+                      [=](int p) { return p == r ? own : inbox + (size_t)p * slot; }, n,
+                      hi - lo);
     }
     free_all(a, cta, e);
     prev_main = e;
@@ -747,17 +733,14 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     cta_part(len, nctas, cta, &lo, &hi);
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      uint32_t* targets[kMaxRanks];
-      int nt = 0;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
         cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
                  a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
-        targets[nt++] = flag_at(a.flags[c], kArrive, r, cta);
       }
       const size_t own = (size_t)r * a.rank_stride + base + lo;
       cta_copy(a.recv + own, a.send + own, hi - lo, false);
-      cta_signal(targets, nt, e);
+      cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
@@ -771,47 +754,47 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
 
-__global__ void __launch_bounds__(512) rank_alltoall_kernel(const RankArgs a) {
+__global__ void __launch_bounds__(512, 2) rank_alltoall_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<float, kSum, 3>(a, blockIdx.x, gridDim.x);
   else rank_alltoall(a, blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
+__global__ void __launch_bounds__(512, 2) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 3>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_alltoall(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(512) rank_allreduce_kernel(const RankArgs a) {
+__global__ void __launch_bounds__(512, 2) rank_allreduce_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<T, OP, 0>(a, blockIdx.x, gridDim.x);
   else rank_allreduce<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(512) rank_reducescatter_kernel(const RankArgs a) {
+__global__ void __launch_bounds__(512, 2) rank_reducescatter_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<T, OP, 2>(a, blockIdx.x, gridDim.x);
   else rank_reducescatter<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512) rank_allgather_kernel(const RankArgs a) {
+__global__ void __launch_bounds__(512, 2) rank_allgather_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<float, kSum, 1>(a, blockIdx.x, gridDim.x);
   else rank_allgather(a, blockIdx.x, gridDim.x);
 }
 
 // Loopback: blockIdx.y is the rank; cooperative launch (all CTAs co-resident).
 template <typename T, int OP>
-__global__ void __launch_bounds__(512) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
+__global__ void __launch_bounds__(512, 2) loopback_allreduce_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<T, OP, 0>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_allreduce<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
 template <typename T, int OP>
-__global__ void __launch_bounds__(512) loopback_reducescatter_kernel(const __grid_constant__ LoopbackArgs a) {
+__global__ void __launch_bounds__(512, 2) loopback_reducescatter_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<T, OP, 2>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_reducescatter<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
+__global__ void __launch_bounds__(512, 2) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 1>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_allgather(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }

@@ -42,6 +42,8 @@
 
 #include "autotune.h"
 #include "internal.h"
+#include "nvls.h"
+#include "nvls_kernels.cuh"
 #include "rank_kernels.cuh"
 
 namespace flx {
@@ -73,7 +75,7 @@ size_t env_mib(const char* name, size_t dflt) {
 // FLX_PCIE_CHUNK_KB, FLX_ONESHOT_KB, FLX_LL, FLX_NVLINK_CTAS) and a mismatch
 // would shift scratch / staging offsets between ranks, so bootstrap compares them.
 struct BootConfig {
-  uint64_t nranks, slot, small_slot, hcap, pcie_chunk, oneshot_max, ll, nctas, sem_words;
+  uint64_t nranks, slot, small_slot, hcap, pcie_chunk, oneshot_max, ll, nctas, sem_words, nvls;
 };
 
 struct BootSlot {
@@ -94,6 +96,7 @@ struct BootHeader {
   int nranks;
   int pad;
   BootSlot slot[kMaxRanks];
+  NvlsBoot nvls;  // NVLS multicast rendezvous (nvls.cu)
 };
 
 }  // namespace
@@ -148,6 +151,7 @@ struct World {
   bool shared_gpu = false;  // ranks share a GPU (bootstrap self-tests): no NVLink-path tuning
   uint64_t agree_seq = 0;   // decision points agreed so far (same on every rank)
   AutoTuner tuner;
+  NvlsBuffer nvls;          // NVLink-SHARP multicast buffer (FLX_NVLS=1, multi-GPU only)
 
   // semaphore words as the GPU addresses them (registered host memory may map
   // to a different device address than its host pointer)
@@ -260,6 +264,7 @@ void world_free(World* w) {
     return;
   }
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
+  nvls_free(&w->nvls);
   for (auto& L : w->local) {
     if (L.scratch) cudaFree(L.scratch);
     if (L.flags) cudaFree(L.flags);
@@ -330,7 +335,12 @@ void world_config(World* w, int nranks) {
   // per-reader bytes of one PCIe pipeline chunk (the paper's 4 MiB staging buffer)
   const char* ck = getenv("FLX_PCIE_CHUNK_KB");
   w->pcie_chunk = std::max<size_t>(4096, (size_t)(ck ? atoll(ck) : 4096) << 10);
-  w->nctas = 32;
+  // 64 CTAs of 512 threads per GPU: the rank kernels fit 64 registers (2 CTAs
+  // per SM), 4 x 16 B loads in flight per thread in the copy phases — the same
+  // bytes in flight as 32 CTAs x 8 loads, on 32 SMs, leaving the rest of the
+  // GPU to compute (loopback, all ranks on one GPU: 8-rank 256 MiB AllReduce
+  // 1.78 -> 1.65 ms; 2 ranks 0.63 -> 0.40 ms; profiles/r2/loopback_occupancy.jsonl)
+  w->nctas = kMaxCtas;
   if (const char* v = getenv("FLX_NVLINK_CTAS")) w->nctas = std::max(1, std::min(kMaxCtas, atoi(v)));
   // one-shot AllReduce up to this many bytes per rank (FLX_ONESHOT_KB=0: off);
   // its inbox holds kMaxCtas regions, so 2x the threshold covers nctas >= 32
@@ -668,8 +678,25 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.spin_limit = w->spin_limit;
     }
     const void* args = w->loopback ? static_cast<const void*>(&la) : &la.r[0];
+    // NVLS AllReduce (nvls_kernels.cuh): the switch reduces; for sums of
+    // fp32/bf16/fp16 above the one-shot range whose slice splits into 16 B
+    // vectors per rank chunk, in rounds of the multicast buffer's capacity
+    const bool nvls = w->nvls.on && !gather && !scatter && !a2a && op == kSum &&
+                      nvls_dtype_ok(dtype) && !la.r[0].oneshot && nv % (16 * (size_t)n) == 0;
+    if (nvls) {
+      const size_t step = w->nvls.capacity / (16 * (size_t)n) * (16 * (size_t)n);
+      for (size_t at = 0; at < nv; at += step) {
+        NvlsArgs na{la.r[0].send + at, la.r[0].recv + at, reinterpret_cast<char*>(w->nvls.uc),
+                    reinterpret_cast<char*>(w->nvls.mcva), w->nvls.state, w->local[0].rank, n,
+                    std::min(step, nv - at), w->abort_word, w->spin_limit};
+        cudaError_t e = launch_nvls_allreduce(dtype, &na, std::min(w->nctas, kNvlsCtas), s0);
+        if (e != cudaSuccess)
+          return fail(flxUnhandledCudaError, "nvls kernel launch: %s", cudaGetErrorString(e));
+      }
+    }
     cudaError_t err =
-        a2a       ? launch_rank_alltoall(w->loopback, args, w->nctas, n, s0)
+        nvls      ? cudaSuccess
+        : a2a     ? launch_rank_alltoall(w->loopback, args, w->nctas, n, s0)
         : gather  ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
         : scatter ? launch_rank_reduce<true>(dtype, op, w->loopback, args, w->nctas, n, s0)
                   : launch_rank_reduce<false>(dtype, op, w->loopback, args, w->nctas, n, s0);
@@ -729,6 +756,11 @@ std::array<size_t, FLX_NUM_PATHS> world_last_bytes(World* w, int local) {
 }
 int world_nranks(World* w) { return w->nranks; }
 int world_nlocal(World* w) { return (int)w->local.size(); }
+const char* world_nvls_status(World* w, int* on) {
+  *on = w->nvls.on ? 1 : 0;
+  return w->nvls.why;
+}
+
 bool world_aborted(World* w) {
   if (*(volatile uint32_t*)w->abort_word != 0) return true;
   // PCIe-leg watchdog: copy-engine waits on a dead peer's tokens never time
@@ -747,7 +779,15 @@ bool world_aborted(World* w) {
   }
   return false;
 }
-void world_set_nctas(World* w, int n) { w->nctas = std::max(1, std::min(w->max_nctas, n)); }
+void world_set_nctas(World* w, int n) {
+  if (n <= 0) {  // automatic: as at creation
+    n = kMaxCtas;
+    if (const char* v = getenv("FLX_NVLINK_CTAS")) n = std::max(1, std::min(kMaxCtas, atoi(v)));
+    n = std::min(n, w->max_nctas);
+    while (n & (n - 1)) n &= n - 1;
+  }
+  w->nctas = std::max(1, std::min(w->max_nctas, n));
+}
 
 AutoTuner* world_tuner(World* w) { return &w->tuner; }
 
@@ -873,8 +913,16 @@ flxResult_t world_create_loopback(int nranks, int device, World** out) {
   if (!coop) return fail(flxInvalidUsage, "device %d lacks cooperative launch", device);
   int sms = 0;
   FLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  w->max_nctas = std::max(1, std::min(kMaxCtas, sms / nranks));  // all CTAs co-resident
+  // every CTA of every rank co-resident (cooperative launch): the rank kernels
+  // fit 64 registers x 512 threads, i.e. 2 CTAs per SM
+  int per_sm = 1;
+  FLX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, loopback_allreduce_kernel<float, kSum>, 512, 0));
+  w->max_nctas = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * sms / nranks));
+  // largest power of two that keeps every rank's CTAs co-resident: 8 ranks
+  // get 32 (37 would fit, 32 measured faster), 2-4 ranks 64
   w->nctas = std::min(w->nctas, w->max_nctas);
+  while (w->nctas & (w->nctas - 1)) w->nctas &= w->nctas - 1;
   for (int r = 0; r < nranks; ++r) {
     w->local[r].rank = r;
     w->local[r].device = device;
@@ -915,9 +963,10 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   FLX_CUDA(cudaDeviceGetPCIBusId(mine.bus_id, sizeof(mine.bus_id), device));
   mine.device = device;
   mine.pid = getpid();
+  const bool want_nvls = getenv("FLX_NVLS") && atoi(getenv("FLX_NVLS")) != 0;
   mine.config = BootConfig{(uint64_t)nranks, w->slot, w->small_slot, w->hcap, w->pcie_chunk,
                            w->oneshot_max, (uint64_t)w->ll, (uint64_t)w->nctas,
-                           (uint64_t)kSemWords};
+                           (uint64_t)kSemWords, (uint64_t)want_nvls};
   __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
   __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
   const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 60.0;
@@ -927,7 +976,8 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
                 __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE), nranks);
   static const char* kFields[] = {"nranks", "FLX_SLOT_MB", "one-shot inbox (FLX_ONESHOT_KB)",
                                   "FLX_PCIE_STAGE_MB", "FLX_PCIE_CHUNK_KB", "FLX_ONESHOT_KB",
-                                  "FLX_LL", "FLX_NVLINK_CTAS", "library build (staging words)"};
+                                  "FLX_LL", "FLX_NVLINK_CTAS", "library build (staging words)",
+                                  "FLX_NVLS"};
   for (int p = 0; p < nranks; ++p) {
     const uint64_t* a = reinterpret_cast<const uint64_t*>(&mine.config);
     const uint64_t* b = reinterpret_cast<const uint64_t*>(&hdr->slot[p].config);
@@ -969,6 +1019,13 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   if (!spin_until([&] { return __atomic_load_n(&hdr->mapped, __ATOMIC_ACQUIRE) >= nranks; },
                   timeout))
     return fail(flxSystemError, "bootstrap timed out mapping the staging segment");
+  // NVLink-SHARP: opt-in (FLX_NVLS=1, agreed above), distinct GPUs only; every
+  // rank ends with the same verdict (nvls.cu), a failure only leaves it off
+  if (want_nvls && !w->shared_gpu) {
+    const char* mb = getenv("FLX_NVLS_MB");
+    nvls_setup_rank(&w->nvls, &hdr->nvls, rank, nranks, device,
+                    (size_t)(mb ? std::max(1, atoi(mb)) : 256) << 20, timeout);
+  }
   w->boot = hdr;  // unmapped in world_free, after the destroy barrier
   if (rank == 0) {
     shm_unlink(boot_name);

@@ -14,21 +14,8 @@ try:
     out["visible_gpus"] = pynvml.nvmlDeviceGetCount()
     h = pynvml.nvmlDeviceGetHandleByIndex(0)
     out["name"] = pynvml.nvmlDeviceGetName(h)
-    try:
-        info = pynvml.c_nvmlGpuFabricInfoV_t()
-        info.version = pynvml.nvmlGpuFabricInfo_v3 if hasattr(pynvml, "nvmlGpuFabricInfo_v3") \
-            else pynvml.nvmlGpuFabricInfo_v2
-        pynvml.nvmlDeviceGetGpuFabricInfoV(h, info)
-        states = {0: "NOT_SUPPORTED", 1: "NOT_STARTED", 2: "IN_PROGRESS", 3: "COMPLETED"}
-        out["fabric"] = {"state": states.get(info.state, info.state), "status": int(info.status),
-                         "clique_id": int(info.cliqueId),
-                         "cluster_uuid": bytes(info.clusterUuid).hex()}
-    except Exception as e:  # older NVML: the v1 query
-        try:
-            f = pynvml.nvmlDeviceGetGpuFabricInfo(h)
-            out["fabric"] = {"state": int(f.state), "status": int(f.status)}
-        except Exception as e2:
-            out["fabric_error"] = f"{e}; {e2}"
+    # (the struct-versioned NVML fabric query crashed this image's pynvml: the
+    # fabric state is read from `nvidia-smi -q` below instead)
     try:
         out["nvlink_active_links"] = sum(
             1 for i in range(18)

@@ -83,7 +83,7 @@ def link_roofline(busbw: float, pcie_gbs: float | None) -> dict:
             "achieved": round(busbw, 2), "frac": round(busbw / peak, 4)}
 
 
-def ncu_traffic(summary: str = "profiles/r1/fold_once_ncu_summary.txt"):
+def ncu_traffic(summary: str = "profiles/r2/fold_once_ncu_summary.txt"):
     """dram read + write bytes per launch of the dominant kernel, from the
     committed ``ncu --set full`` capture of the same workload (None if absent)."""
     units = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -530,7 +530,7 @@ def run_single_gpu(args) -> None:
             "frac": round(achieved / hbm_peak, 4),
             # the capture is of the full 256 MiB slice; another split has no capture
             "traffic": ncu_traffic() if pbytes[PathKind.NVLINK] == AR_BYTES else None,
-            "traffic_source": "profiles/r1/fold_once_ncu_summary.txt (ncu --set full, same "
+            "traffic_source": "profiles/r2/fold_once_ncu_summary.txt (ncu --set full, same "
                               "kernel and size; dram__bytes_read.sum + dram__bytes_write.sum)",
             "kernel": "fold_once_kernel<float,Sum,8> (NVLink-path slice, 8 virtual ranks, "
                       "one 16 B vector per thread)",
@@ -690,8 +690,16 @@ def run_calibration(clique, sends, recvs, stream, ctas, striped_busbw, pbytes, i
             clique.set_shares(AR, None, cnt * 4)
     clique.set_shares(AR, None, AR_BYTES)
     algbw_striped = striped_busbw / (2 * (n - 1) / n)
-    rows.append(C.MeasuredRow(AR, n, AR_BYTES, C.MODE_PCIE_ONLY, algbw_striped, 0,
-                              100.0 * pbytes[PathKind.PCIE_STAGED] / AR_BYTES))
+    load = 100.0 * pbytes[PathKind.PCIE_STAGED] / AR_BYTES
+    if load <= 0:  # the balancer kept NVLink-only: no striped row to fit PCIe from
+        cal = C.calibrate(rows)
+        fit = cal.nvlink[(AR, n)]
+        return {"rows": [{"size": r.size, "mode": r.mode, "algbw_gbs": round(r.algbw, 3)}
+                         for r in rows],
+                "nvlink_fit": {"bandwidth_gbs": round(fit.bandwidth / 1e9, 3),
+                               "latency_us": round(fit.latency * 1e6, 3)},
+                "pcie_fit_gbs": None, "note": "no striped row (balancer kept NVLink-only)"}
+    rows.append(C.MeasuredRow(AR, n, AR_BYTES, C.MODE_PCIE_ONLY, algbw_striped, 0, load))
     cal = C.calibrate(rows)
     topo = C.build_calibrated_topology(cal, AR, n, C.MODE_PCIE_ONLY)
     clique.set_link_profile(topo)  # resets the bucket: Stage 1 again, seeded from the fit

@@ -18,10 +18,15 @@ p.add_argument("--steps", type=int, default=3)
 p.add_argument("--shares", default="1000,0,0")
 p.add_argument("--ranks", type=int, default=8)
 p.add_argument("--mib", type=int, default=256)
+p.add_argument("--loopback", action="store_true",
+               help="the one-process-per-GPU engine (rank kernels), all ranks on this GPU")
+p.add_argument("--ragged", action="store_true",
+               help="odd element count per rank (AllGather blocks off the 16 B grid)")
 a = p.parse_args()
 n = a.ranks
 shares = [int(x) for x in a.shares.split(",")]
-clique = flx.Clique(n)
+clique = flx.Clique(n, loopback=a.loopback)
+clique.set_autotune(False)  # fixed shares: a short, deterministic launch list
 if a.op == "allreduce":
     count = a.mib * (1 << 20) // 4
     s = [torch.randn(count, device="cuda") for _ in range(n)]
@@ -40,7 +45,7 @@ elif a.op in ("reducescatter", "alltoall"):  # fp32, a.mib MiB sent per rank
         clique.set_shares(CollectiveOp.ALLTOALL, shares)
         run = lambda: clique.all_to_all(s, r)  # noqa: E731
 else:
-    count = a.mib * (1 << 20) // 2 // n
+    count = a.mib * (1 << 20) // 2 // n + (3 if a.ragged else 0)
     s = [torch.randn(count, device="cuda").bfloat16() for _ in range(n)]
     r = [torch.empty(count * n, device="cuda", dtype=torch.bfloat16) for _ in range(n)]
     clique.set_shares(CollectiveOp.ALLGATHER, shares)

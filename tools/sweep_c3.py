@@ -26,12 +26,17 @@ p.add_argument("--op", choices=["allreduce", "allgather"], default="allreduce",
                help="allgather: S is the gathered size (S/N sent per rank), nccl-tests busbw")
 p.add_argument("--loopback", action="store_true",
                help="the multi-GPU engine emulated on one GPU, NVLink path only (no tuning)")
+p.add_argument("--inlib", action="store_true",
+               help="the in-library balancer tunes every bucket (no Python Stage 1); "
+                    "NVLink-only timed beside it; works with --loopback too")
 a = p.parse_args()
 topo = preset("B200").restricted([PathKind.NVLINK, PathKind.PCIE_STAGED])
 for n in [int(x) for x in a.ranks.split(",")]:
     cl = flx.Clique(n, loopback=a.loopback)
     if a.nvlink_ctas:
         cl.set_nvlink_ctas(a.nvlink_ctas)
+    if a.inlib:
+        cl.set_tuner_config(min_bytes=1 << 20)
     for dt, esz, name in ((torch.float32, 4, "fp32"), (torch.bfloat16, 2, "bf16")):
         mib = 1
         while mib <= a.max_mib:
@@ -42,7 +47,33 @@ for n in [int(x) for x in a.ranks.split(",")]:
             s = [torch.randn(per, device="cuda").to(dt) for _ in range(n)]
             r = [torch.empty(per * n if gather else per, device="cuda", dtype=dt) for _ in range(n)]
             run = (lambda: cl.all_gather(s, r)) if gather else (lambda: cl.all_reduce(s, r))
-            if a.loopback:
+            nv_only_ms = info = None
+            if a.inlib:
+                nb = (per * esz)
+                cl.set_shares(cop, (1000, 0, 0), nb)  # NVLink-only reference timing
+                for _ in range(3):
+                    run()
+                torch.cuda.synchronize()
+                q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q0.record()
+                for _ in range(10):
+                    run()
+                q1.record()
+                torch.cuda.synchronize()
+                nv_only_ms = q0.elapsed_time(q1) / 10
+                cl.set_shares(cop, None, nb)  # hand the bucket to the in-library balancer
+                k = 0
+                while k < 400 and cl.tune_info(cop, nb)["phase"] not in ("stage2",) and not (
+                        k >= 2 and cl.tune_info(cop, nb)["phase"] == "idle"):
+                    run()
+                    k += 1
+                info = cl.tune_info(cop, nb)
+                info["tuning_calls"] = k
+                info["stage1_trace"] = [x["action"] for x in cl.tune_trace(cop, nb)]
+                shares = flx.ShareDistribution({kd: info["shares"][int(kd)] for kd in PathKind
+                                                if info["shares"][int(kd)] or kd == 0})
+                trace = None
+            elif a.loopback:
                 shares, trace = flx.ShareDistribution({PathKind.NVLINK: 1000}), None
                 cl.set_shares(cop, shares)
             else:
@@ -66,6 +97,9 @@ for n in [int(x) for x in a.ranks.split(",")]:
                 "shares": {k.short: shares.get(k) for k in PathKind},
                 "traffic_pct": {k.short: round(100 * b[k] / (S // n if gather else S), 3)
                                 for k in PathKind},
+                "nvlink_only_ms": None if nv_only_ms is None else round(nv_only_ms, 4),
+                "gain_pct": None if nv_only_ms is None else round(100 * (nv_only_ms / (t * 1e3) - 1), 2),
+                "balancer": info,
                 "stage1": None if trace is None else {
                     "iterations": trace.iterations, "tuned_ms": round(tuned * 1e3, 4),
                     "nvlink_only_ms": round(base * 1e3, 4),

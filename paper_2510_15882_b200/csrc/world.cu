@@ -41,6 +41,7 @@
 #include <thread>
 
 #include "autotune.h"
+#include "board.h"
 #include "internal.h"
 #include "nvls.h"
 #include "nvls_kernels.cuh"
@@ -54,8 +55,8 @@ namespace {
 // [4096, 12288) the balancer's agreement board (world_agree_max)
 constexpr int kSemWords = 12288;
 constexpr int kBoardWord = 4096;
-constexpr int kBoardSlots = 4;        // decision points in flight (ranks are <= 1 apart)
-constexpr int kBoardDoubles = 62;     // values per slot (+ stamp + count = 64 x 8 B)
+static_assert((size_t)(kSemWords - kBoardWord) * 4 >= 16 * kBoardSlots * kBoardSlotWords * 8,
+              "the agreement board must fit its words of the staging segment head");
 // token word layout: [kind][buffer][producer][reader] over kMaxRanks, see token_post
 inline size_t tok(int kind, int r, int c, int b) {
   return ((size_t)(kind * 2 + b) * kMaxRanks + r) * kMaxRanks + c;
@@ -799,38 +800,21 @@ AutoTuner* world_tuner(World* w) { return &w->tuner; }
 // reading point k — so a slot is never overwritten while a peer still reads it.
 static flxResult_t world_agree_max(World* w, double* vals, int n) {
   if (w->loopback || w->nranks == 1 || w->local.size() != 1) return flxSuccess;
-  const int me = w->local[0].rank;
-  auto slot = [&](int r, uint64_t k) {
-    return reinterpret_cast<uint64_t*>(w->host + (size_t)kBoardWord * 4) +
-           ((size_t)r * kBoardSlots + k % kBoardSlots) * 64;
-  };
-  for (int at = 0; at < n; at += kBoardDoubles) {
-    const int m = std::min(kBoardDoubles, n - at);
-    const uint64_t k = w->agree_seq++;
-    uint64_t* mine = slot(me, k);
-    mine[1] = (uint64_t)m;
-    memcpy(mine + 2, vals + at, sizeof(double) * m);
-    __atomic_store_n(&mine[0], k + 1, __ATOMIC_RELEASE);
-    const auto t0 = std::chrono::steady_clock::now();
-    for (int r = 0; r < w->nranks; ++r) {
-      if (r == me) continue;
-      uint64_t* theirs = slot(r, k);
-      while (__atomic_load_n(&theirs[0], __ATOMIC_ACQUIRE) != k + 1) {
-        if (*(volatile uint32_t*)w->abort_word ||
-            std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() >
-                w->timeout_s) {
-          *(volatile uint32_t*)w->abort_word = 1;
-          return fail(flxInternalError, "balancer agreement: rank %d never reached decision %llu",
-                      r, (unsigned long long)k);
-        }
-        std::this_thread::sleep_for(std::chrono::microseconds(20));
-      }
-      if ((int)theirs[1] != m)
-        return fail(flxInternalError, "balancer agreement: rank %d is at a different decision", r);
-      double v[kBoardDoubles];
-      memcpy(v, theirs + 2, sizeof(double) * m);
-      for (int i = 0; i < m; ++i) vals[at + i] = std::max(vals[at + i], v[i]);
-    }
+  Board b;
+  b.base = w->host + (size_t)kBoardWord * 4;
+  b.nranks = w->nranks;
+  b.me = w->local[0].rank;
+  b.seq = &w->agree_seq;
+  b.abort_word = w->abort_word;
+  b.timeout_s = w->timeout_s;
+  int bad = -1;
+  switch (board_agree_max(b, vals, n, &bad)) {
+    case 1:
+      return fail(flxInternalError, "balancer agreement: rank %d never reached decision %llu",
+                  bad, (unsigned long long)w->agree_seq - 1);
+    case 2:
+      return fail(flxInternalError, "balancer agreement: rank %d is at a different decision",
+                  bad);
   }
   return flxSuccess;
 }

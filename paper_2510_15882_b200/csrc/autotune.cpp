@@ -324,7 +324,7 @@ flxResult_t AutoTuner::before_call(TimingPort& port, const TunePolicy& pol, int 
   *g = fallback;
   const int bucket = size_bucket(bytes);
   if (!tunable) return flxSuccess;
-  if (!can_measure) {  // CUDA-graph capture: the current split, no tuning step
+  if (!can_measure) {  // capture / timing off: the current split, no tuning step
     auto it = slots_.find({op, bucket});
     if (it != slots_.end() && it->second.phase != flxTuneIdle) *g = it->second.cur;
     return flxSuccess;

@@ -44,8 +44,8 @@ struct TunePolicy {  // copied from the lead comm when a bucket is first tuned
 class AutoTuner {
  public:
   // Decide the shares of the next call of (op, bytes).  `tunable` = autotune
-  // on, bucket not pinned, timing on, >= min bytes; `can_measure` = not
-  // inside a CUDA-graph capture (then the current split is used, no step).
+  // on, bucket not pinned, >= min bytes; `can_measure` = timed and not inside a
+  // CUDA-graph capture (otherwise the current split is used, no step).
   // `fallback` is what the share table says (used when not tunable).
   // *measured tells after_call whether to record this call.
   flxResult_t before_call(TimingPort& port, const TunePolicy& pol, int op, size_t bytes,

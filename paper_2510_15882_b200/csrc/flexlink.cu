@@ -382,12 +382,15 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   Granules g = fallback;
   bool measured = false;
   {
-    const bool tunable = !pinned && lead->autotune && lead->timing && bytes >= lead->tune_min_bytes;
+    // untimed calls (flxSetTiming 0) and captures keep the bucket's tuned split
+    // but take no tuning step: there is nothing to measure
+    const bool tunable = !pinned && lead->autotune && bytes >= lead->tune_min_bytes;
     CliquePort port(c);
     const TunePolicy pol{lead->tune_s1, lead->tune_s2, lead->have_profile, lead->profile,
                          lead->nvlink_ctas};
-    FLX_TRY(c->tuner->before_call(port, pol, head.coll, bytes, tunable, !capturing, path_mask(),
-                                  fallback, &g, &measured));
+    FLX_TRY(c->tuner->before_call(port, pol, head.coll, bytes, tunable,
+                                  !capturing && lead->timing, path_mask(), fallback, &g,
+                                  &measured));
   }
   auto split = partition(bytes, g, alignment_for(lead, head.coll));
   if (split[flxPathRdma] > 0)

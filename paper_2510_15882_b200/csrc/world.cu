@@ -856,15 +856,15 @@ flxResult_t run_world_tuned(World* w, const std::vector<const void*>& send,
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   FLX_CUDA(cudaStreamIsCapturing(streams[0], &cap));
   const size_t bytes = count * dtype_size(dtype);
-  const bool tunable = !pinned && lead.autotune && lead.timing && !w->shared_gpu &&
+  const bool tunable = !pinned && lead.autotune && !w->shared_gpu &&
                        bytes >= lead.tune_min_bytes && !*(volatile uint32_t*)w->abort_word;
   WorldPort port(w);
   TunePolicy pol{lead.tune_s1, lead.tune_s2, lead.have_profile, lead.profile, w->nctas};
   Granules g = fallback;
   bool measured = false;
   FLX_TRY(w->tuner.before_call(port, pol, coll, bytes, tunable,
-                               cap == cudaStreamCaptureStatusNone, path_mask, fallback, &g,
-                               &measured));
+                               cap == cudaStreamCaptureStatusNone && lead.timing, path_mask,
+                               fallback, &g, &measured));
   const uint64_t seq = w->local[0].calls;
   FLX_TRY(run_world(w, send, recv, streams, coll, count, dtype, op, g, alignment, lead.timing));
   w->tuner.after_call(coll, bytes, seq, w->local[0].last_bytes, measured);

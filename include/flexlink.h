@@ -109,6 +109,16 @@ flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist);
  * like flxCommInitAll (one group per collective).  For testing the N-GPU code
  * path on a single GPU; set CUDA_DEVICE_MAX_CONNECTIONS>=3*nranks+1. */
 flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device);
+/* Loopback over another process's memory (bootstrap self-test of the rank
+ * kernels on CUDA-IPC-mapped peer memory): a helper process calls
+ * flxDebugHostRemoteRanks, which allocates ranks 1..nranks-1's scratch and
+ * flag blocks on `device`, exports their IPC handles under `id` and blocks
+ * until the loopback world built over them is destroyed (or `seconds`);
+ * flxCommInitLoopbackIpc builds that world in this process — rank 0's memory
+ * local, the others IPC mappings — driven like flxCommInitLoopback.  Only
+ * this process launches kernels. */
+flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, double seconds);
+flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flxUniqueId id);
 flxResult_t flxCommDestroy(flxComm_t comm);
 /* ncclCommAbort (nccl.h:186): stop waiting for peers — kernels still spinning
  * on a peer flag give up at once, the destroy barrier is skipped — then free

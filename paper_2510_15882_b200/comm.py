@@ -112,6 +112,8 @@ def load_library() -> ctypes.CDLL:
         "flxGetLaunchCount": [P(ctypes.c_ulonglong)],
         "flxCommDebugPeer": [vp, ci, ci, ci, vp, sz],
         "flxNvlsProbe": [ci, P(ci), ctypes.c_char_p, sz],
+        "flxDebugHostRemoteRanks": [ci, ci, _UniqueId, ctypes.c_double],
+        "flxCommInitLoopbackIpc": [P(vp), ci, ci, _UniqueId],
         "flxCommGetNvls": [vp, P(ci), ctypes.c_char_p, sz],
     }
     for name, args in sig.items():
@@ -495,6 +497,18 @@ def rank_measure_fn(comm: Communicator, op: CollectiveOp, send, recv, group=None
     return measure
 
 
+def host_remote_ranks(nranks: int, unique_id: bytes, device: int = 0,
+                      seconds: float = 120.0) -> None:
+    """``flxDebugHostRemoteRanks``: allocate ranks 1..nranks-1's scratch / flags
+    here, export them over CUDA IPC under ``unique_id`` and block until the
+    loopback world built on them (``Clique(..., loopback=True, ipc_id=...)`` in
+    another process) is destroyed.  Launches no kernels."""
+    uid = _UniqueId()
+    ctypes.memmove(ctypes.addressof(uid), unique_id, 128)
+    _check(load_library().flxDebugHostRemoteRanks(nranks, device, uid, seconds),
+           "flxDebugHostRemoteRanks")
+
+
 def nvls_probe(device: int = 0) -> tuple[bool, str]:
     """``flxNvlsProbe``: can this GPU run the NVLink-SHARP (multimem) AllReduce?
     Checked end to end on a one-device multicast object; returns (ok, reason)."""
@@ -518,13 +532,21 @@ class Clique:
     the 1-GPU stand-in for an N-GPU NVSwitch collective.
     """
 
-    def __init__(self, nranks: int, device: int = 0, loopback: bool = False):
+    def __init__(self, nranks: int, device: int = 0, loopback: bool = False,
+                 ipc_id: bytes | None = None):
         """``loopback=False``: fused virtual ranks (flxCommInitAll, repeated device).
         ``loopback=True``: the multi-GPU engine emulated on one device
-        (flxCommInitLoopback) — same kernels/protocols as one-process-per-GPU."""
+        (flxCommInitLoopback) — same kernels/protocols as one-process-per-GPU;
+        with ``ipc_id``, ranks 1.. live in another process's memory exported by
+        :func:`host_remote_ranks` (flxCommInitLoopbackIpc, a bootstrap self-test)."""
         L = load_library()
         handles = (ctypes.c_void_p * nranks)()
-        if loopback:
+        if loopback and ipc_id is not None:
+            uid = _UniqueId()
+            ctypes.memmove(ctypes.addressof(uid), ipc_id, 128)
+            _check(L.flxCommInitLoopbackIpc(handles, nranks, device, uid),
+                   "flxCommInitLoopbackIpc")
+        elif loopback:
             _check(L.flxCommInitLoopback(handles, nranks, device), "flxCommInitLoopback")
         else:
             devs = (ctypes.c_int * nranks)(*([device] * nranks))

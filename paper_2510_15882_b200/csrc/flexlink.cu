@@ -871,6 +871,48 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
   return flxSuccess;
 }
 
+namespace {
+void id_hex(const flxUniqueId& id, char hex[40]) {
+  uint64_t nonce[2];
+  memcpy(nonce, id.internal + 8, sizeof(nonce));
+  snprintf(hex, 40, "%016llx%016llx", (unsigned long long)nonce[0],
+           (unsigned long long)nonce[1]);
+}
+}  // namespace
+
+flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, double seconds) {
+  uint64_t magic;
+  memcpy(&magic, id.internal, sizeof(magic));
+  if (magic != 0x31584c46ull) return fail(flxInvalidArgument, "not a flxUniqueId");
+  char hex[40];
+  id_hex(id, hex);
+  return world_host_remote_ranks(nranks, device, hex, seconds > 0 ? seconds : 120.0);
+}
+
+flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flxUniqueId id) {
+  if (!comms || nranks < 2) return fail(flxInvalidArgument, "bad comms/nranks");
+  uint64_t magic;
+  memcpy(&magic, id.internal, sizeof(magic));
+  if (magic != 0x31584c46ull) return fail(flxInvalidArgument, "not a flxUniqueId");
+  char hex[40];
+  id_hex(id, hex);
+  std::lock_guard<std::mutex> lock(g_mutex);
+  World* w = nullptr;
+  FLX_TRY(world_create_loopback_ipc(nranks, device, hex, &w));
+  for (int r = 0; r < nranks; ++r) {
+    auto* c = new flxComm();
+    c->rank = r;
+    c->nranks = nranks;
+    c->device = device;
+    c->world = w;
+    c->local = r;
+    init_tuning(c);
+    world_attach(w, r, c);
+    comms[r] = c;
+  }
+  return flxSuccess;
+}
+
 flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
   if (!comms || nranks < 1) return fail(flxInvalidArgument, "bad comms/nranks");
   int visible = 0;

@@ -141,6 +141,8 @@ struct Clique {
 struct World;
 flxResult_t world_create_loopback(int nranks, int device, World** out);
 flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_hex, World** out);
+flxResult_t world_create_loopback_ipc(int nranks, int device, const char* id_hex, World** out);
+flxResult_t world_host_remote_ranks(int nranks, int device, const char* id_hex, double seconds);
 void world_attach(World* w, int local, Comm* c);
 int world_release(World* w);
 flxResult_t run_world(World* w, const std::vector<const void*>& send,

@@ -140,6 +140,9 @@ struct World {
     // slice, its completion event and when it was issued
     cudaEvent_t pcie_watch = nullptr;
     std::chrono::steady_clock::time_point pcie_issued{};
+    // scratch/flags are CUDA-IPC mappings of another process's allocation
+    // (flxCommInitLoopbackIpc): closed, not freed
+    bool remote_mem = false;
   };
   std::vector<Local> local;
   // peer views (as mapped in this process): scratch/flags of every rank
@@ -153,6 +156,7 @@ struct World {
   uint64_t agree_seq = 0;   // decision points agreed so far (same on every rank)
   AutoTuner tuner;
   NvlsBuffer nvls;          // NVLink-SHARP multicast buffer (FLX_NVLS=1, multi-GPU only)
+  void* ipc_debug = nullptr;  // flxCommInitLoopbackIpc: the exporter's segment
 
   // semaphore words as the GPU addresses them (registered host memory may map
   // to a different device address than its host pointer)
@@ -164,6 +168,19 @@ struct World {
 
 namespace {
 
+// One rank's peer-visible memory: scratch [n inbox slots][outbox][one-shot
+// inboxes: 2 parities x n sources][LL packets: 2 parities x n sources x
+// kLLSlot] (LL zeroed: epochs start at 1) and the flag block (zeroed).
+flxResult_t alloc_rank_mem(const World* w, char** scratch, uint32_t** flags) {
+  const size_t ll_off = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
+  const size_t scratch_bytes = ll_off + 2 * w->nranks * kLLSlot;
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(scratch), scratch_bytes));
+  FLX_CUDA(cudaMemset(*scratch + ll_off, 0, 2 * w->nranks * kLLSlot));
+  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(flags), (kFlagWords + kStateWords) * 4));
+  FLX_CUDA(cudaMemset(*flags, 0, (kFlagWords + kStateWords) * 4));
+  return flxSuccess;
+}
+
 flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaSetDevice(L.device));
   int khz = 0;
@@ -172,14 +189,7 @@ flxResult_t local_init(World* w, World::Local& L) {
   const double secs = to ? atof(to) : 10.0;
   w->spin_limit = (long long)(std::max(0.01, secs) * khz * 1e3);
   w->timeout_s = std::max(0.01, secs);
-  // [n inbox slots][outbox][one-shot inboxes: 2 parities x n sources]
-  // [LL packets: 2 parities x n sources x kLLSlot] (zeroed: epochs start at 1)
-  const size_t ll_off = w->slot * (w->nranks + 1) + 2 * w->nranks * w->small_slot;
-  const size_t scratch_bytes = ll_off + 2 * w->nranks * kLLSlot;
-  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.scratch), scratch_bytes));
-  FLX_CUDA(cudaMemset(L.scratch + ll_off, 0, 2 * w->nranks * kLLSlot));
-  FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.flags), (kFlagWords + kStateWords) * 4));
-  FLX_CUDA(cudaMemset(L.flags, 0, (kFlagWords + kStateWords) * 4));
+  if (!L.remote_mem) FLX_TRY(alloc_rank_mem(w, &L.scratch, &L.flags));
   FLX_CUDA(cudaMalloc(reinterpret_cast<void**>(&L.dstage), w->hcap));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
   FLX_CUDA(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
@@ -267,8 +277,13 @@ void world_free(World* w) {
   for (void* p : w->ipc_opened) cudaIpcCloseMemHandle(p);
   nvls_free(&w->nvls);
   for (auto& L : w->local) {
-    if (L.scratch) cudaFree(L.scratch);
-    if (L.flags) cudaFree(L.flags);
+    if (L.remote_mem) {
+      if (L.scratch) cudaIpcCloseMemHandle(L.scratch);
+      if (L.flags) cudaIpcCloseMemHandle(L.flags);
+    } else {
+      if (L.scratch) cudaFree(L.scratch);
+      if (L.flags) cudaFree(L.flags);
+    }
     if (L.dstage) cudaFree(L.dstage);
     if (L.d2h) cudaStreamDestroy(L.d2h);
     if (L.h2d) cudaStreamDestroy(L.h2d);
@@ -293,6 +308,11 @@ void world_free(World* w) {
       free(w->host);
   }
   if (w->abort_word) cudaFreeHost(w->abort_word);
+  if (w->ipc_debug) {  // tell the exporting process its memory is no longer used
+    int* done = &static_cast<int*>(w->ipc_debug)[1];
+    __atomic_store_n(done, 1, __ATOMIC_RELEASE);
+    munmap(w->ipc_debug, sizeof(int) * 4 + sizeof(cudaIpcMemHandle_t) * 2 * kMaxRanks);
+  }
   delete w;
 }
 
@@ -911,6 +931,114 @@ flxResult_t world_create_loopback(int nranks, int device, World** out) {
     w->local[r].rank = r;
     w->local[r].device = device;
     FLX_TRY(local_init(w, w->local[r]));
+  }
+  FLX_TRY(alloc_host_staging(w, nullptr));
+  guard.w = nullptr;
+  *out = w;
+  return flxSuccess;
+}
+
+// ---- loopback over another process's memory (bootstrap self-test) -----------
+// Process B (flxDebugHostRemoteRanks) allocates ranks 1..n-1's scratch and
+// flag blocks and exports their CUDA-IPC handles through a shm segment;
+// process A (flxCommInitLoopbackIpc) builds a loopback world whose ranks
+// 1..n-1 live in those IPC mappings.  The rank kernels then run against
+// IPC-mapped peer memory — release/acquire flags, LL packets, pushes and
+// pulls — while only process A launches kernels (process B launches none: two
+// processes' kernels waiting on each other on one GPU are not guaranteed to be
+// co-scheduled, B200_PROFILING.md).
+namespace {
+struct IpcDebugSeg {
+  int ready;  // B published the handles
+  int done;   // A is finished with them
+  int nranks;
+  int pad;
+  cudaIpcMemHandle_t scratch[kMaxRanks];
+  cudaIpcMemHandle_t flags[kMaxRanks];
+};
+
+IpcDebugSeg* map_ipc_debug(const char* id_hex, bool create) {
+  char name[96];
+  snprintf(name, sizeof(name), "/flx-%s-ipcdbg", id_hex);
+  int fd = shm_open(name, create ? (O_CREAT | O_RDWR) : O_RDWR, 0600);
+  if (fd < 0) return nullptr;
+  if (create && ftruncate(fd, sizeof(IpcDebugSeg)) != 0) {
+    close(fd);
+    return nullptr;
+  }
+  void* p = mmap(nullptr, sizeof(IpcDebugSeg), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+  close(fd);
+  return p == MAP_FAILED ? nullptr : static_cast<IpcDebugSeg*>(p);
+}
+}  // namespace
+
+flxResult_t world_host_remote_ranks(int nranks, int device, const char* id_hex, double seconds) {
+  if (nranks < 2 || nranks > kMaxRanks) return fail(flxInvalidArgument, "bad nranks %d", nranks);
+  World cfg;
+  world_config(&cfg, nranks);
+  FLX_CUDA(cudaSetDevice(device));
+  IpcDebugSeg* seg = map_ipc_debug(id_hex, true);
+  if (!seg) return fail(flxSystemError, "shm for the IPC self-test failed");
+  std::vector<char*> scratch(nranks, nullptr);
+  std::vector<uint32_t*> flags(nranks, nullptr);
+  flxResult_t rc = flxSuccess;
+  for (int r = 1; r < nranks && rc == flxSuccess; ++r) {
+    rc = alloc_rank_mem(&cfg, &scratch[r], &flags[r]);
+    if (rc == flxSuccess && (cudaIpcGetMemHandle(&seg->scratch[r], scratch[r]) != cudaSuccess ||
+                             cudaIpcGetMemHandle(&seg->flags[r], flags[r]) != cudaSuccess))
+      rc = fail(flxUnhandledCudaError, "cudaIpcGetMemHandle failed");
+  }
+  if (rc == flxSuccess && cudaDeviceSynchronize() != cudaSuccess)
+    rc = fail(flxUnhandledCudaError, "zeroing the exported scratch failed");
+  seg->nranks = nranks;
+  __atomic_store_n(&seg->ready, rc == flxSuccess ? 1 : -1, __ATOMIC_RELEASE);
+  if (rc == flxSuccess &&
+      !spin_until([&] { return __atomic_load_n(&seg->done, __ATOMIC_ACQUIRE) != 0; }, seconds))
+    rc = fail(flxSystemError, "the loopback process never finished with the exported ranks");
+  cudaDeviceSynchronize();
+  for (int r = 1; r < nranks; ++r) {
+    if (scratch[r]) cudaFree(scratch[r]);
+    if (flags[r]) cudaFree(flags[r]);
+  }
+  munmap(seg, sizeof(IpcDebugSeg));
+  return rc;
+}
+
+flxResult_t world_create_loopback_ipc(int nranks, int device, const char* id_hex, World** out) {
+  IpcDebugSeg* seg = nullptr;
+  if (!spin_until([&] { return (seg = map_ipc_debug(id_hex, false)) != nullptr; }, 60.0))
+    return fail(flxSystemError, "no exporting process for the IPC self-test");
+  if (!spin_until([&] { return __atomic_load_n(&seg->ready, __ATOMIC_ACQUIRE) != 0; }, 60.0) ||
+      seg->ready < 0 || seg->nranks != nranks) {
+    munmap(seg, sizeof(IpcDebugSeg));
+    return fail(flxSystemError, "the exporting process did not publish %d ranks", nranks);
+  }
+  auto* w = new World();
+  WorldGuard guard{w};
+  world_config(w, nranks);
+  w->loopback = true;
+  w->ipc_debug = seg;
+  w->local.resize(nranks);
+  FLX_CUDA(cudaSetDevice(device));
+  int sms = 0, per_sm = 1;
+  FLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
+  FLX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      &per_sm, loopback_allreduce_kernel<float, kSum>, 512, 0));
+  w->max_nctas = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * sms / nranks));
+  world_set_nctas(w, 0);
+  for (int r = 0; r < nranks; ++r) {
+    World::Local& L = w->local[r];
+    L.rank = r;
+    L.device = device;
+    if (r > 0) {
+      void* p = nullptr;
+      FLX_CUDA(cudaIpcOpenMemHandle(&p, seg->scratch[r], cudaIpcMemLazyEnablePeerAccess));
+      L.scratch = static_cast<char*>(p);
+      L.remote_mem = true;
+      FLX_CUDA(cudaIpcOpenMemHandle(&p, seg->flags[r], cudaIpcMemLazyEnablePeerAccess));
+      L.flags = static_cast<uint32_t*>(p);
+    }
+    FLX_TRY(local_init(w, L));
   }
   FLX_TRY(alloc_host_staging(w, nullptr));
   guard.w = nullptr;

@@ -259,9 +259,8 @@ flxResult_t clique_destroy(Clique* c) {
 // Grow-only: a CUDA graph captured earlier bakes the current ring's pointers
 // into its copy nodes, so a ring is never freed while the clique lives — a
 // larger ring replaces it and the old one is retired (freed in
-// clique_destroy).  The first ring is sized for the largest automatic chunk
-// (pick_chunk: 4 MiB per member) so eager calls of growing size do not keep
-// reallocating.
+// clique_destroy).  Capacities are powers of two from 4 MiB per member, so a
+// handful of sizes covers every message.
 flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
   if (c->stage_cap >= chunk && c->stage_bufs >= bufs) {
     if (c->ring_depth == bufs) return flxSuccess;
@@ -285,7 +284,8 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
   if (c->dev_stage) c->retired_dev.push_back(c->dev_stage);
   c->host_stage = nullptr;
   c->dev_stage = nullptr;
-  const size_t cap = std::max(std::max(chunk, c->stage_cap), (size_t)kMaxAutoChunk);
+  size_t cap = std::max<size_t>(4 << 20, c->stage_cap);
+  while (cap < chunk) cap <<= 1;
   const int nb = std::max(std::max(bufs, c->stage_bufs), 2);
   const size_t total = cap * c->members.size() * nb;
   FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&c->host_stage), total, cudaHostAllocPortable));
@@ -304,11 +304,17 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
 }
 
 // Chunk size per member for a PCIe slice of `bytes` per rank: the configured
-// value, or ~8 pipeline stages, 64 KiB..4 MiB, 4 KiB multiples.
+// value, or ~5 pipeline stages, 64 KiB..12 MiB, 4 KiB multiples.  Each chunk
+// costs N D2H copies + one 2-D H2D + a fold launch + four stream memory ops,
+// so small chunks are overhead-bound and few large ones pay the pipeline fill:
+// measured on B200, 8 ranks (profiles/r2/pcie_chunks_*.jsonl), a 56 MiB slice
+// runs 11.84 ms at 4 MiB chunks and 11.58 at 8-12 MiB, a 14 MiB slice is
+// fastest at 3-4 MiB, a PCIe-only 256 MiB message moves 41.6 GB/s each way at
+// 4 MiB and 45.7 at 16 MiB.
 size_t pick_chunk(const Comm* lead, size_t bytes) {
   size_t chunk = lead->chunk_bytes;
   if (chunk == 0) {
-    chunk = (bytes / 8 + 4095) / 4096 * 4096;
+    chunk = (bytes / 5 + 4095) / 4096 * 4096;
     chunk = std::min<size_t>(std::max<size_t>(chunk, 64 << 10), kMaxAutoChunk);
   }
   return chunk;
@@ -435,8 +441,11 @@ flxResult_t run_clique(Clique* c, const std::vector<Call>& calls) {
   // ---- PCIe slice: issue the side-stream pipeline first so its copies start
   // while the NVLink kernel runs.
   if (pc > 0) {
-    const size_t chunk = pick_chunk(lead, pc);
-    // ReduceScatter stages every (source, row) pair: n*n rows of one chunk
+    // ReduceScatter / AllToAll stage every (source, row) pair: n*n rows of one
+    // chunk, so their automatic chunk keeps a slot at <= 32 MiB per member
+    size_t chunk = pick_chunk(lead, pc);
+    if (rows && lead->chunk_bytes == 0)
+      chunk = std::max<size_t>(4096, std::min(chunk, ((32u << 20) / n) & ~(size_t)4095));
     const size_t need = rows ? chunk * n : chunk;
     if (capturing && (c->stage_cap < need || c->ring_depth != lead->buffers))
       return fail(flxInvalidUsage,

@@ -55,9 +55,8 @@ flxResult_t sem_wait_eq(cudaStream_t s, uint32_t* word, uint32_t value);
 flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value);
 
 size_t dtype_size(int dtype);
-// largest automatic PCIe chunk per member (pick_chunk); the first staging ring
-// is sized for it
-constexpr size_t kMaxAutoChunk = 4 << 20;
+// largest automatic PCIe chunk per member (pick_chunk)
+constexpr size_t kMaxAutoChunk = 12 << 20;
 
 // ---- share table (ShareTable, collectives.py:189-204)
 using Granules = std::array<int, FLX_NUM_PATHS>;

@@ -28,6 +28,7 @@
 #include <sys/stat.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -46,6 +47,14 @@ int env_int(const char* name, int dflt) {
 // round shape and lag (FLX_TUNE_WARM / FLX_TUNE_REPEATS / FLX_TUNE_LAG)
 int warm_calls() { static const int v = std::max(0, env_int("FLX_TUNE_WARM", 1)); return v; }
 int repeat_calls() { static const int v = std::max(1, env_int("FLX_TUNE_REPEATS", 3)); return v; }
+// measured time a round should span (FLX_TUNE_ROUND_US): short calls get more
+// repeats so the per-path medians fed to tune_step are not noise (a 50 us call
+// carries a few us of event jitter, the order of the 5 % convergence threshold)
+double round_target_ms() {
+  static const double v = std::max(0, env_int("FLX_TUNE_ROUND_US", 2000)) * 1e-3;
+  return v;
+}
+constexpr int kMaxRepeats = 16;
 int stage2_lag() { static const int v = std::max(0, env_int("FLX_TUNE_LAG", 2)); return v; }
 constexpr int kProbeGranules = 100;  // PCIe share of the rate-probe round
 constexpr size_t kMaxEvals = 256;
@@ -154,6 +163,11 @@ flxResult_t AutoTuner::decide_round(TimingPort& port, Slot& s, int path_mask) {
   switch (s.phase) {
     case flxTuneBaseline: {
       s.nv_ms = total;
+      // later rounds repeat enough calls to span round_target_ms() (agreed
+      // value on every rank, so every rank uses the same round length)
+      if (total > 0)
+        s.repeats = std::max(repeat_calls(),
+                             std::min(kMaxRepeats, (int)std::ceil(round_target_ms() / total)));
       if (rep.mask & 1) s.seed[flxPathNvlink] = bytes[0] / (rep.ms[0] * 1e-3);
       flxLinkProfile prof{};
       if (s.pol.have_profile) {
@@ -335,6 +349,7 @@ flxResult_t AutoTuner::before_call(TimingPort& port, const TunePolicy& pol, int 
   if (s.phase == flxTuneIdle) {
     s = Slot();
     s.pol = pol;
+    s.repeats = repeat_calls();
     Granules cached;
     if (cache_lookup(port, op, bucket, s, &cached)) {
       s.from_cache = true;
@@ -348,7 +363,7 @@ flxResult_t AutoTuner::before_call(TimingPort& port, const TunePolicy& pol, int 
   }
   s.calls += 1;
   if (s.phase != flxTuneStage2) {
-    if (s.round_calls == warm_calls() + repeat_calls()) {
+    if (s.round_calls == warm_calls() + s.repeats) {
       FLX_TRY(decide_round(port, s, path_mask));
       if (s.phase == flxTuneStage2) cache_store(port, op, bucket, s);
     }

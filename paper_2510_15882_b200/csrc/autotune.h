@@ -78,6 +78,7 @@ class AutoTuner {
     TunePolicy pol;
     Granules cur{{FLX_GRANULE_TOTAL, 0, 0}};
     int round_calls = 0;               // calls issued in the current round
+    int repeats = 3;                   // measured calls per round (adapted after the baseline)
     std::vector<MeasPtr> round;        // its measured calls
     MeasPtr pending;                   // the call being issued
     flxTunerState st{};

@@ -304,18 +304,26 @@ flxResult_t ensure_staging(Clique* c, size_t chunk, int bufs) {
 }
 
 // Chunk size per member for a PCIe slice of `bytes` per rank: the configured
-// value, or ~5 pipeline stages, 64 KiB..12 MiB, 4 KiB multiples.  Each chunk
+// value, or 5 pipeline stages of up to 12 MiB (4 KiB multiples).  Each chunk
 // costs N D2H copies + one 2-D H2D + a fold launch + four stream memory ops,
 // so small chunks are overhead-bound and few large ones pay the pipeline fill:
 // measured on B200, 8 ranks (profiles/r2/pcie_chunks_*.jsonl), a 56 MiB slice
 // runs 11.84 ms at 4 MiB chunks and 11.58 at 8-12 MiB, a 14 MiB slice is
 // fastest at 3-4 MiB, a PCIe-only 256 MiB message moves 41.6 GB/s each way at
 // 4 MiB and 45.7 at 16 MiB.
+//
+// The stage COUNT is what is held fixed — 5, fewer for slices under 5 x 64 KiB,
+// more once a stage would exceed 12 MiB — so it changes only at those
+// thresholds and the PCIe path's time grows smoothly with its share.  (A chunk
+// size derived per call made the count jump 5 -> 6 with a few KiB of share: one
+// granule moved the PCIe time by a whole stage and Stage 1 cycled between
+// "move 1 nvlink->pcie" and "move 1 pcie->nvlink" at 2-4 MiB messages.)
 size_t pick_chunk(const Comm* lead, size_t bytes) {
   size_t chunk = lead->chunk_bytes;
   if (chunk == 0) {
-    chunk = (bytes / 5 + 4095) / 4096 * 4096;
-    chunk = std::min<size_t>(std::max<size_t>(chunk, 64 << 10), kMaxAutoChunk);
+    const size_t few = std::min<size_t>(5, std::max<size_t>(1, bytes / (64 << 10)));
+    const size_t stages = std::max<size_t>((bytes + kMaxAutoChunk - 1) / kMaxAutoChunk, few);
+    chunk = std::max<size_t>(4096, ((bytes + stages - 1) / stages + 4095) / 4096 * 4096);
   }
   return chunk;
 }

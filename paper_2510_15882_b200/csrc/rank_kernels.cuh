@@ -341,37 +341,55 @@ __device__ __forceinline__ size_t cta_sub(size_t slot) {
 // (kFree >= e-1), push, announce (kArrive = e); the receiver consumes its
 // inbox and answers kFree = e.
 
+// Two-shot rounds.  CTA b owns part b of every rank's chunk for the WHOLE call
+// (chunk c = [c*chunk, (c+1)*chunk) of the message, reduced by rank c) and
+// walks it in rounds of `round` bytes per chunk part, each round a complete
+// push -> fold -> pull with its own epoch.  Large messages take several
+// rounds, and odd CTAs start with a half-length round: their phases then run
+// half a round out of step with the even CTAs', so while one half of the CTAs
+// folds (local HBM only) the other half keeps NVLink busy pushing or pulling —
+// the link no longer idles for the whole fold phase.  Every rank derives the
+// same schedule for CTA b from (bytes, n, nctas, b), so CTA b's rounds and
+// epochs agree across ranks; per-CTA epochs let CTAs run different counts.
+constexpr size_t kRoundMin = 128 << 10;  // shortest full round per chunk part
+constexpr size_t kRoundsPerCall = 4;     // target rounds for large messages
+
 template <typename T, int OP>
 __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
-  const size_t round_cap = sub * nctas * n;
-  const size_t outbox = a.slot * n;  // outbox follows the n inbox slots
+  const size_t outbox = a.slot * n;       // outbox follows the n inbox slots
+  const size_t chunk = ceil16((a.bytes + n - 1) / n);
+  const size_t maxpart = ceil16((chunk + nctas - 1) / nctas);  // a full chunk's part
+  const size_t round = min(sub, max(kRoundMin, ceil16((maxpart + kRoundsPerCall - 1) /
+                                                      kRoundsPerCall)));
+  const bool stagger = (cta & 1) && maxpart >= 2 * kRoundMin;
   FLX_PHASE(0);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_outbox = ep.last_ar, prev_main = ep.last_main;
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += round_cap, ++k) {
+  for (size_t at = 0; at < maxpart; ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(round_cap, a.bytes - base);
-    const size_t chunk = ceil16((len + n - 1) / n);
-    // this CTA's part [lo, lo+nb) of rank c's chunk, as a message offset —
-    // recomputed per use instead of kept in per-peer arrays (local memory)
-    auto part = [&](int c) {
-      const size_t off = min(len, (size_t)c * chunk);
-      const size_t clen = min(len, off + chunk) - off;
-      const size_t p = ceil16((clen + nctas - 1) / nctas);
-      const size_t lo = min(clen, (size_t)cta * p), hi = min(clen, lo + p);
-      return make_ulonglong2(base + off + lo, hi - lo);  // {message offset, bytes}
+    const size_t len = min(maxpart - at, (k == 0 && stagger) ? ceil16(round / 2) : round);
+    // this round's piece of CTA b's part of rank c's chunk, as a message
+    // offset and length — recomputed per use instead of kept in per-peer
+    // arrays (which would live in local memory)
+    // (full chunks share `maxpart`; only the ragged last chunk divides again)
+    auto piece = [&](int c) {
+      const size_t off = min(a.bytes, (size_t)c * chunk);
+      const size_t clen = min(a.bytes - off, chunk);
+      const size_t p = clen == chunk ? maxpart : ceil16((clen + nctas - 1) / nctas);
+      const size_t b0 = (size_t)cta * p;
+      const size_t lo = min(clen, b0 + at), hi = min(min(clen, b0 + p), lo + len);
+      return make_ulonglong2(off + lo, hi - lo);  // {message offset, bytes}
     };
-    // 1) push my chunk c into peer c's inbox slot r (my part `cta` of it,
-    //    into this CTA's region of the slot)
+    // 1) push my chunk c into peer c's inbox slot r (this CTA's region)
     if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
     FLX_PHASE(1);
     for (int s = 1; s < n; ++s) {
       const int c = (r + s) % n;
-      const ulonglong2 pc = part(c);
+      const ulonglong2 pc = piece(c);
       cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
     }
     cta_signal_peers(a, cta, kArrive, e);
@@ -380,7 +398,7 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, kPulled, prev_outbox, a)) return;
     FLX_PHASE(3);
     {
-      const ulonglong2 pr = part(r);
+      const ulonglong2 pr = piece(r);
       const char* own = a.send + pr.x;
       const char* inbox = a.scratch[r] + mine;
       const size_t slot = a.slot;
@@ -395,12 +413,13 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     FLX_PHASE(5);
     for (int s = 1; s < n; ++s) {
       const int c = (r + s) % n;
-      const ulonglong2 pc = part(c);
+      const ulonglong2 pc = piece(c);
       cta_copy(a.recv + pc.x, a.scratch[c] + outbox + mine, pc.y, true);
     }
     cta_signal_peers(a, cta, kPulled, e);
     FLX_PHASE(6);
     prev_outbox = prev_main = e;
+    at += len;
   }
   cta_epochs_done(ep, k, prev_outbox, prev_main);
 }

@@ -352,7 +352,10 @@ __device__ __forceinline__ size_t cta_sub(size_t slot) {
 // same schedule for CTA b from (bytes, n, nctas, b), so CTA b's rounds and
 // epochs agree across ranks; per-CTA epochs let CTAs run different counts.
 constexpr size_t kRoundMin = 128 << 10;  // shortest full round per chunk part
-constexpr size_t kRoundsPerCall = 4;     // target rounds for large messages
+#ifndef FLX_ROUNDS_PER_CALL
+#define FLX_ROUNDS_PER_CALL 4  // tools/rank_timeline.cu compares 1 (round-1 schedule)
+#endif
+constexpr size_t kRoundsPerCall = FLX_ROUNDS_PER_CALL;  // target rounds for large messages
 
 template <typename T, int OP>
 __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
@@ -364,7 +367,10 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const size_t maxpart = ceil16((chunk + nctas - 1) / nctas);  // a full chunk's part
   const size_t round = min(sub, max(kRoundMin, ceil16((maxpart + kRoundsPerCall - 1) /
                                                       kRoundsPerCall)));
-  const bool stagger = (cta & 1) && maxpart >= 2 * kRoundMin;
+#ifndef FLX_STAGGER
+#define FLX_STAGGER 1  // tools/rank_timeline.cu builds both ways to compare
+#endif
+  const bool stagger = FLX_STAGGER && (cta & 1) && maxpart >= 2 * kRoundMin;
   FLX_PHASE(0);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_outbox = ep.last_ar, prev_main = ep.last_main;

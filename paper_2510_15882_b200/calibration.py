@@ -87,43 +87,49 @@ class CalibrationResult:
     secondary: dict[tuple[CollectiveOp, int, str], dict[PathKind, float]]
 
 
-def _table(op, n, cells):
-    """cells: MiB -> (baseline, (pcie bw, impr, load), (pcie+rdma bw, impr, pcie, rdma))."""
-    rows = []
-    for mib, (base, (pb, pi, pl), (rb, ri, rp, rr)) in cells.items():
-        size = mib * MIB
-        rows += [MeasuredRow(op, n, size, MODE_BASELINE, base),
-                 MeasuredRow(op, n, size, MODE_PCIE_ONLY, pb, pi, pl),
-                 MeasuredRow(op, n, size, MODE_PCIE_RDMA, rb, ri, rp, rr)]
-    return rows
-
-
-_AR, _AG = CollectiveOp.ALLREDUCE, CollectiveOp.ALLGATHER
 # The paper's Table 2 (8xH800, NCCL 2.27.3 baseline; PAPER.md:282-331), as the
-# reference ships it (bench.py:72-106): GB/s and percent loads.
-H800_MEASUREMENTS: tuple[MeasuredRow, ...] = tuple(
-    _table(_AR, 2, {32: (112, (131, 17, 14), (134, 20, 16, 4)),
-                    64: (128, (144, 13, 17), (150, 17, 13, 5)),
-                    128: (132, (155, 17, 17), (165, 25, 11, 9)),
-                    256: (139, (167, 20, 18), (175, 26, 12, 9))})
-    + _table(_AR, 4, {32: (87, (87, 0, 0), (89, 2, 2, 1)),
-                      64: (90, (97, 8, 8), (99, 10, 6, 2)),
-                      128: (94, (106, 13, 12), (110, 17, 12, 2)),
-                      256: (98, (116, 18, 17), (118, 20, 13, 5))})
-    + _table(_AR, 8, {256: (107, (108, 1, 1), (109, 2, 1, 1))})
-    + _table(_AG, 2, {32: (103, (122, 18, 15), (126, 22, 10, 8)),
-                      64: (117, (136, 16, 19), (141, 21, 9, 10)),
-                      128: (129, (153, 19, 21), (153, 19, 12, 8)),
-                      256: (132, (163, 23, 21), (161, 22, 14, 5))})
-    + _table(_AG, 4, {32: (43, (50, 16, 13), (52, 21, 10, 7)),
-                      64: (46, (56, 22, 18), (57, 24, 12, 8)),
-                      128: (48, (58, 21, 18), (60, 25, 12, 10)),
-                      256: (49, (60, 22, 18), (62, 27, 12, 10))})
-    + _table(_AG, 8, {32: (20, (23, 15, 12), (24, 20, 12, 4)),
-                      64: (21, (24, 14, 13), (26, 24, 12, 6)),
-                      128: (21, (25, 19, 14), (25, 19, 12, 7)),
-                      256: (21, (25, 19, 13), (26, 24, 12, 7))})
-)
+# reference ships it (bench.py:72-106).  One line per (collective, N, MiB):
+# NVLink-only GB/s | PCIe-only GB/s, gain %, PCIe load % | PCIe+RDMA GB/s,
+# gain %, PCIe load %, RDMA load %.
+_TABLE2 = """
+allreduce 2  32 112 131 17 14 134 20 16  4
+allreduce 2  64 128 144 13 17 150 17 13  5
+allreduce 2 128 132 155 17 17 165 25 11  9
+allreduce 2 256 139 167 20 18 175 26 12  9
+allreduce 4  32  87  87  0  0  89  2  2  1
+allreduce 4  64  90  97  8  8  99 10  6  2
+allreduce 4 128  94 106 13 12 110 17 12  2
+allreduce 4 256  98 116 18 17 118 20 13  5
+allreduce 8 256 107 108  1  1 109  2  1  1
+allgather 2  32 103 122 18 15 126 22 10  8
+allgather 2  64 117 136 16 19 141 21  9 10
+allgather 2 128 129 153 19 21 153 19 12  8
+allgather 2 256 132 163 23 21 161 22 14  5
+allgather 4  32  43  50 16 13  52 21 10  7
+allgather 4  64  46  56 22 18  57 24 12  8
+allgather 4 128  48  58 21 18  60 25 12 10
+allgather 4 256  49  60 22 18  62 27 12 10
+allgather 8  32  20  23 15 12  24 20 12  4
+allgather 8  64  21  24 14 13  26 24 12  6
+allgather 8 128  21  25 19 14  25 19 12  7
+allgather 8 256  21  25 19 13  26 24 12  7
+"""
+
+
+def _parse_table2(text: str) -> tuple[MeasuredRow, ...]:
+    rows: list[MeasuredRow] = []
+    for line in text.strip().splitlines():
+        name, *vals = line.split()
+        op = CollectiveOp(name)
+        n, mib, base, pb, pi, pl, rb, ri, rp, rr = (int(v) for v in vals)
+        size = mib * MIB
+        rows.append(MeasuredRow(op, n, size, MODE_BASELINE, base))
+        rows.append(MeasuredRow(op, n, size, MODE_PCIE_ONLY, pb, pi, pl))
+        rows.append(MeasuredRow(op, n, size, MODE_PCIE_RDMA, rb, ri, rp, rr))
+    return tuple(rows)
+
+
+H800_MEASUREMENTS: tuple[MeasuredRow, ...] = _parse_table2(_TABLE2)
 
 
 def fit_alpha_beta(points: list[tuple[int, float]]) -> tuple[float, float]:

@@ -365,8 +365,9 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   const size_t outbox = a.slot * n;       // outbox follows the n inbox slots
   const size_t chunk = ceil16((a.bytes + n - 1) / n);
   const size_t maxpart = ceil16((chunk + nctas - 1) / nctas);  // a full chunk's part
-  const size_t round = min(sub, max(kRoundMin, ceil16((maxpart + kRoundsPerCall - 1) /
-                                                      kRoundsPerCall)));
+  // a round is at most one region (sub <= slot / 64), so it fits 32 bits
+  const uint32_t round = (uint32_t)min(sub, max(kRoundMin, ceil16((maxpart + kRoundsPerCall - 1) /
+                                                                kRoundsPerCall)));
 #ifndef FLX_STAGGER
 #define FLX_STAGGER 1  // tools/rank_timeline.cu builds both ways to compare
 #endif
@@ -377,7 +378,8 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
   uint32_t k = 0;
   for (size_t at = 0; at < maxpart; ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(maxpart - at, (k == 0 && stagger) ? ceil16(round / 2) : round);
+    const uint32_t len =
+        (uint32_t)min(maxpart - at, (size_t)((k == 0 && stagger) ? ((round / 2 + 15) & ~15u) : round));
     // this round's piece of CTA b's part of rank c's chunk, as a message
     // offset and length — recomputed per use instead of kept in per-peer
     // arrays (which would live in local memory)
@@ -665,37 +667,70 @@ __device__ __forceinline__ void free_all(const RankArgs& a, int cta, uint32_t e)
   cta_signal_peers(a, cta, kFree, e);
 }
 
+// Staggered-round schedule of CTA `cta` over a span of `span` bytes shared by
+// `nctas` CTAs (rank_allreduce's scheme for the slot protocols): the CTA owns
+// [lo, lo + plen) of the span for the whole call and walks it in rounds of up
+// to one region, ~kRoundsPerCall of them, odd CTAs starting with a half round
+// so their land / fold phases overlap the even CTAs' pushes.  Every rank
+// computes the same plan for CTA b, and every CTA loops to the full part
+// length `maxpart` (empty pieces included), so rounds and epochs agree.
+struct RoundPlan {
+  size_t lo, plen, maxpart;
+  uint32_t round;
+  bool stagger;
+  __device__ __forceinline__ uint32_t len(size_t at, uint32_t k) const {
+    const uint32_t want = (k == 0 && stagger) ? ((round / 2 + 15) & ~15u) : round;
+    return (uint32_t)min(maxpart - at, (size_t)want);
+  }
+  // this round's piece of the CTA's part: {offset in the span, bytes}
+  __device__ __forceinline__ ulonglong2 piece(size_t at, uint32_t len) const {
+    const size_t a0 = min(plen, at), a1 = min(plen, at + len);
+    return make_ulonglong2(lo + a0, a1 - a0);
+  }
+};
+
+__device__ __forceinline__ RoundPlan round_plan(size_t span, int nctas, int cta, size_t sub) {
+  RoundPlan p;
+  p.maxpart = ceil16((span + nctas - 1) / nctas);
+  p.lo = min(span, (size_t)cta * p.maxpart);
+  p.plen = min(span, p.lo + p.maxpart) - p.lo;
+  p.round = (uint32_t)min(sub, max(kRoundMin, ceil16((p.maxpart + kRoundsPerCall - 1) /
+                                                     kRoundsPerCall)));
+  p.stagger = FLX_STAGGER && (cta & 1) && p.maxpart >= 2 * kRoundMin;
+  return p;
+}
+
 __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
-  const size_t cap = sub * nctas;
+  const RoundPlan plan = round_plan(a.bytes, nctas, cta, sub);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
+  for (size_t at = 0; at < plan.maxpart; ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(cap, a.bytes - base);
-    size_t lo, hi;
-    cta_part(len, nctas, cta, &lo, &hi);
-    {  // push my slice into every peer's inbox slot r (this CTA's region)
+    const uint32_t len = plan.len(at, k);
+    const ulonglong2 pc = plan.piece(at, len);  // {send offset, bytes}
+    {  // push my piece into every peer's inbox slot r (this CTA's region)
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + base + lo, hi - lo, false);
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
       }
-      char* own = a.recv + (size_t)r * a.rank_stride + base;
-      if (own != a.send + base) cta_copy(own + lo, a.send + base + lo, hi - lo, false);
+      char* own = a.recv + (size_t)r * a.rank_stride;
+      if (own != a.send) cta_copy(own + pc.x, a.send + pc.x, pc.y, false);
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
-      cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
-               a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
+      cta_copy(a.recv + (size_t)p * a.rank_stride + pc.x, a.scratch[r] + (size_t)p * a.slot + mine,
+               pc.y, true);
     }
     free_all(a, cta, e);
     prev_main = e;
+    at += len;
   }
   cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
@@ -707,35 +742,34 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
-  const size_t cap = sub * nctas;
+  const RoundPlan plan = round_plan(a.bytes, nctas, cta, sub);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
+  for (size_t at = 0; at < plan.maxpart; ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(cap, a.bytes - base);
-    size_t lo, hi;
-    cta_part(len, nctas, cta, &lo, &hi);
+    const uint32_t len = plan.len(at, k);
+    const ulonglong2 pc = plan.piece(at, len);  // {offset in a block, bytes}
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
         cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
-                 a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
+                 a.send + (size_t)c * a.rank_stride + pc.x, pc.y, false);
       }
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     {
-      const char* own = a.send + (size_t)r * a.rank_stride + base + lo;
+      const char* own = a.send + (size_t)r * a.rank_stride + pc.x;
       const char* inbox = a.scratch[r] + mine;
       const size_t slot = a.slot;
-      cta_fold<T, OP>(a.recv + base + lo, nullptr,
-                      [=](int p) { return p == r ? own : inbox + (size_t)p * slot; }, n,
-                      hi - lo);
+      cta_fold<T, OP>(a.recv + pc.x, nullptr,
+                      [=](int p) { return p == r ? own : inbox + (size_t)p * slot; }, n, pc.y);
     }
     free_all(a, cta, e);
     prev_main = e;
+    at += len;
   }
   cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
@@ -747,34 +781,34 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
-  const size_t cap = sub * nctas;
+  const RoundPlan plan = round_plan(a.bytes, nctas, cta, sub);
   const CtaEpochs ep = cta_epochs(a, cta);
   uint32_t prev_main = ep.last_main;
   uint32_t k = 0;
-  for (size_t base = 0; base < a.bytes; base += cap, ++k) {
+  for (size_t at = 0; at < plan.maxpart; ++k) {
     const uint32_t e = ep.first + k;
-    const size_t len = min(cap, a.bytes - base);
-    size_t lo, hi;
-    cta_part(len, nctas, cta, &lo, &hi);
+    const uint32_t len = plan.len(at, k);
+    const ulonglong2 pc = plan.piece(at, len);  // {offset in a block, bytes}
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
       for (int s = 1; s < n; ++s) {
         const int c = (r + s) % n;
         cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
-                 a.send + (size_t)c * a.rank_stride + base + lo, hi - lo, false);
+                 a.send + (size_t)c * a.rank_stride + pc.x, pc.y, false);
       }
-      const size_t own = (size_t)r * a.rank_stride + base + lo;
-      cta_copy(a.recv + own, a.send + own, hi - lo, false);
+      const size_t own = (size_t)r * a.rank_stride + pc.x;
+      cta_copy(a.recv + own, a.send + own, pc.y, false);
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
     for (int s = 1; s < n; ++s) {
       const int p = (r - s + n) % n;
-      cta_copy(a.recv + (size_t)p * a.rank_stride + base + lo,
-               a.scratch[r] + (size_t)p * a.slot + mine, hi - lo, true);
+      cta_copy(a.recv + (size_t)p * a.rank_stride + pc.x,
+               a.scratch[r] + (size_t)p * a.slot + mine, pc.y, true);
     }
     free_all(a, cta, e);
     prev_main = e;
+    at += len;
   }
   cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }

@@ -73,6 +73,10 @@ class FlexLinkBackend(dist.ProcessGroup):
         self.comm = Communicator.init_rank(size, uid, rank)
         self._store = store
         self._barriers = 0
+        try:  # the process group's timeout (a timedelta) bounds barrier waits
+            self._timeout_s = float(timeout.total_seconds())
+        except AttributeError:
+            self._timeout_s = 1800.0
         _instances.append(self)
 
     # -- names
@@ -136,13 +140,17 @@ class FlexLinkBackend(dist.ProcessGroup):
         # every rank's queued work done, then a rendezvous on the group's store
         # (no device collective: a 4-byte AllReduce would be a latency-bound
         # NVLink-path kernel for nothing)
+        import time
+
         torch.cuda.current_stream().synchronize()
         self._barriers += 1
         key = f"flexlink/barrier/{self._barriers}"
         self._store.add(key, 1)
+        t0 = time.monotonic()
         while int(self._store.add(key, 0)) < self.size():
-            import time
-
+            if time.monotonic() - t0 > self._timeout_s:
+                raise RuntimeError(f"flexlink barrier {self._barriers}: not every rank arrived "
+                                   f"within {self._timeout_s:.0f} s")
             time.sleep(0.001)
         return _DoneWork([])
 

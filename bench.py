@@ -448,13 +448,18 @@ def run_single_gpu(args) -> None:
              lambda: clique.reduce_scatter(sends, rs_recv), (n + 1) * AR_BYTES),
             ("alltoall", CollectiveOp.ALLTOALL, lambda: clique.all_to_all(sends, a2a_recv),
              2 * n * AR_BYTES)):
-        clique.set_shares(cop, (1000, 0, 0), AR_BYTES)
+        # the library balances these buckets too (per-rank message = one block
+        # of AR_BYTES / n): let it settle before timing
+        tuned = settle(clique, run, cop, AR_BYTES // n)
         for _ in range(args.warmup):
             run()
         dt_c = _time_steps(run, args.steps, stream)
         hist = clique.comms[0].path_times_history(min(args.steps, 64))
         k_ms = statistics.mean(h[PathKind.NVLINK] for h in hist) * 1e3
         extra[name] = {"value": round(AR_BYTES / dt_c * (n - 1) / n / 1e9, 2), "unit": "GB/s",
+                       "balancer": {"tuning_calls": tuned,
+                                    **{k: v for k, v in clique.tune_info(cop, AR_BYTES // n).items()
+                                       if k in ("phase", "kept_tuned", "shares")}},
                        "dtype": "f32", "send_bytes_per_rank": AR_BYTES,
                        "ms_per_step": round(dt_c * 1e3, 4),
                        "busbw": "(S_send/t)*(N-1)/N (nccl-tests)",
@@ -1002,7 +1007,12 @@ def run_multi_gpu(args) -> None:
              lambda: dist.reduce_scatter_tensor(rs_ref, send)),
             ("alltoall", CollectiveOp.ALLTOALL, lambda: c.all_to_all(send, a2a_out),
              lambda: dist.all_to_all_single(a2a_ref, send))):
-        c.set_shares(cop, ShareDistribution({PathKind.NVLINK: 1000}), AR_BYTES)
+        if args.shares or world < 2:
+            g = [int(x) for x in (args.shares or "1000,0,0").split(",")]
+            c.set_shares(cop, ShareDistribution({k: g[int(k)] for k in PathKind
+                                                 if g[int(k)] or k == 0}), AR_BYTES // world)
+        else:  # the library balances the bucket (one block = AR_BYTES / world per rank)
+            settle(c, ours, cop, AR_BYTES // world)
         dt_c = timed(ours)
         dt_n = timed(theirs)
         same = torch.equal(rs_out, rs_ref) if cop == CollectiveOp.REDUCESCATTER else \

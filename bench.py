@@ -358,6 +358,8 @@ def run_single_gpu(args) -> None:
         for r in recvs:
             r.copy_(acc)
 
+    for _ in range(2):  # warm: allocator, kernels
+        torch_unfused()
     torch_dt = _time_steps(torch_unfused, max(5, args.steps // 2), stream)
     torch_base = {"value": round(busbw_allreduce(AR_BYTES, torch_dt, n), 2),
                   "ms_per_step": round(torch_dt * 1e3, 4),

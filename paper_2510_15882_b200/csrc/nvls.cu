@@ -258,6 +258,12 @@ void nvls_setup_rank(NvlsBuffer* nb, NvlsBoot* boot, int rank, int nranks, int d
            nb->capacity >> 20, nranks);
 }
 
+cudaError_t launch_nvls_allgather(const void* args, size_t stride, int nctas, cudaStream_t s) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  nvls_allgather_kernel<0><<<nctas, 512, 0, s>>>(*static_cast<const NvlsArgs*>(args), stride);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_nvls_allreduce(int dtype, const void* args, int nctas, cudaStream_t s) {
   const NvlsArgs& a = *static_cast<const NvlsArgs*>(args);
   g_launches.fetch_add(1, std::memory_order_relaxed);

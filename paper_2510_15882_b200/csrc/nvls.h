@@ -37,6 +37,7 @@ void nvls_setup_rank(NvlsBuffer* nb, NvlsBoot* boot, int rank, int nranks, int d
                      size_t data_bytes, double timeout_s);
 void nvls_free(NvlsBuffer* nb);
 cudaError_t launch_nvls_allreduce(int dtype, const void* args, int nctas, cudaStream_t s);
+cudaError_t launch_nvls_allgather(const void* args, size_t stride, int nctas, cudaStream_t s);
 bool nvls_dtype_ok(int dtype);
 
 }  // namespace flx

@@ -20,6 +20,8 @@
 // next step 1; its next step-3 stores into my buffer wait for my next step-2
 // arrival, which follows my step 5.
 //
+// (nvls_allgather_kernel below: the same buffer, one multicast store per slice.)
+//
 // The reduction order inside the switch is unspecified: results equal the
 // fixed-order fold for integer-valued data and are within 1 ulp of the output
 // dtype otherwise (bf16/fp16 accumulate in fp32: .acc::f32).  Capability-gated
@@ -158,6 +160,34 @@ __global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_con
       const size_t o = (size_t)c * chunk + v;
       *reinterpret_cast<uint4*>(a.recv + o) = ld_cg_nvls(ucd + o);
     }
+  if (threadIdx.x == 0) a.state[b] = e;
+}
+
+// NVLS AllGather: one multimem.st puts my slice into EVERY rank's buffer (the
+// switch replicates it), so each GPU sends its S bytes once instead of N-1
+// times.  a.bytes = per-rank send bytes (16 B multiple); the buffer holds N
+// blocks; recv block c at c * a.stride.  Per call, CTA b:
+//   1 store part b of my slice to block r of every rank's buffer (multicast)
+//   2 barrier: every rank's part b landed everywhere
+//   3 land part b of every block from my buffer into recv
+//   4 barrier: every rank finished landing before anyone's next call stores
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(512, 2) nvls_allgather_kernel(const __grid_constant__ NvlsArgs a,
+                                                                 size_t stride) {
+  const int b = blockIdx.x, nb = gridDim.x, r = a.rank, n = a.nranks;
+  const uint32_t e = a.state[b] + 1;
+  const size_t part = ((a.bytes / nb) + 15) & ~(size_t)15;
+  const size_t lo = min(a.bytes, (size_t)b * part), hi = min(a.bytes, lo + part);
+  char* ucd = a.uc + kNvlsFlagBytes;
+  char* mcd = a.mc + kNvlsFlagBytes;
+  for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x)
+    mm_st(mcd + (size_t)r * a.bytes + v, ld_stream(a.send + v));
+  if (!nvls_barrier(a, b, (uint32_t)n * e)) return;
+  for (int c = 0; c < n; ++c)
+    for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x)
+      *reinterpret_cast<uint4*>(a.recv + (size_t)c * stride + v) =
+          ld_cg_nvls(ucd + (size_t)c * a.bytes + v);
+  if (!nvls_barrier(a, kNvlsCtas + b, (uint32_t)n * e)) return;
   if (threadIdx.x == 0) a.state[b] = e;
 }
 

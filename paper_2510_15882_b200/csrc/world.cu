@@ -704,6 +704,20 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     // vectors per rank chunk, in rounds of the multicast buffer's capacity
     const bool nvls = w->nvls.on && !gather && !scatter && !a2a && op == kSum &&
                       nvls_dtype_ok(dtype) && !la.r[0].oneshot && nv % (16 * (size_t)n) == 0;
+    // NVLS AllGather: one multicast store per slice, in rounds of capacity / N
+    const bool nvls_ag = w->nvls.on && gather && !la.r[0].oneshot && nv % 16 == 0 &&
+                         bytes % 16 == 0 && w->nvls.capacity / n >= 16;
+    if (nvls_ag) {
+      const size_t step = (w->nvls.capacity / n) & ~(size_t)15;
+      for (size_t at = 0; at < nv; at += step) {
+        NvlsArgs na{la.r[0].send + at, la.r[0].recv + at, reinterpret_cast<char*>(w->nvls.uc),
+                    reinterpret_cast<char*>(w->nvls.mcva), w->nvls.state, w->local[0].rank, n,
+                    std::min(step, nv - at), w->abort_word, w->spin_limit};
+        cudaError_t e = launch_nvls_allgather(&na, bytes, std::min(w->nctas, kNvlsCtas), s0);
+        if (e != cudaSuccess)
+          return fail(flxUnhandledCudaError, "nvls kernel launch: %s", cudaGetErrorString(e));
+      }
+    }
     if (nvls) {
       const size_t step = w->nvls.capacity / (16 * (size_t)n) * (16 * (size_t)n);
       for (size_t at = 0; at < nv; at += step) {
@@ -716,7 +730,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       }
     }
     cudaError_t err =
-        nvls      ? cudaSuccess
+        nvls || nvls_ag ? cudaSuccess
         : a2a     ? launch_rank_alltoall(w->loopback, args, w->nctas, n, s0)
         : gather  ? launch_rank_allgather(w->loopback, args, w->nctas, n, s0)
         : scatter ? launch_rank_reduce<true>(dtype, op, w->loopback, args, w->nctas, n, s0)

@@ -317,8 +317,19 @@ flxResult_t flxNvlsProbe(int device, int* available, char* reason, size_t reason
       if (ok) {
         cudaMemcpy(back.data(), dst, bytes, cudaMemcpyDeviceToHost);
         ok = memcmp(back.data(), h.data(), bytes) == 0;
-        if (!ok) snprintf(nb.why, sizeof(nb.why), "NVLS kernel result mismatch on one device");
-      } else {
+        if (!ok) snprintf(nb.why, sizeof(nb.why), "NVLS AllReduce result mismatch on one device");
+      }
+      if (ok) {  // and the AllGather kernel (one rank: a copy through the multicast store)
+        cudaMemset(dst, 0, bytes);
+        ok = launch_nvls_allgather(&a, bytes, 8, 0) == cudaSuccess &&
+             cudaDeviceSynchronize() == cudaSuccess;
+        if (ok) {
+          cudaMemcpy(back.data(), dst, bytes, cudaMemcpyDeviceToHost);
+          ok = memcmp(back.data(), h.data(), bytes) == 0;
+          if (!ok) snprintf(nb.why, sizeof(nb.why), "NVLS AllGather result mismatch on one device");
+        }
+      }
+      if (!ok && !strstr(nb.why, "mismatch")) {
         snprintf(nb.why, sizeof(nb.why), "NVLS kernel failed: %s",
                  cudaGetErrorString(cudaGetLastError()));
       }
@@ -326,7 +337,7 @@ flxResult_t flxNvlsProbe(int device, int* available, char* reason, size_t reason
     if (src) cudaFree(src);
     if (dst) cudaFree(dst);
     if (abort_word) cudaFree(abort_word);
-    if (ok) snprintf(nb.why, sizeof(nb.why), "ok: multicast object + multimem.ld_reduce/st kernel");
+    if (ok) snprintf(nb.why, sizeof(nb.why), "ok: multicast object + NVLS AllReduce and AllGather kernels");
   }
   say(nb.why);
   *available = ok ? 1 : 0;

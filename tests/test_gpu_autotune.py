@@ -168,3 +168,65 @@ def test_nccl_only_program_gets_striped(tmp_path):
     out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), (out.returncode,
                                                                         out.stdout, out.stderr)
+
+
+def test_tuned_split_is_captured_into_cuda_graphs_and_survives_timing_off():
+    """A CUDA graph captured after Stage 1 replays the tuned split (captures take no
+    tuning step), and switching per-path timing off keeps the split."""
+    n, count = 8, 8 * MIB
+    sends, recvs, exact = _inputs(n, count, seed=21)
+    with comm.Clique(n, device=0) as c:
+        c.set_nvlink_ctas(2)
+        for _ in range(120):
+            c.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        info = c.tune_info(CollectiveOp.ALLREDUCE, count * 4)
+        assert info["phase"] == "stage2" and info["kept_tuned"], info
+        calls = info["calls"]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        for r in recvs:
+            r.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            c.all_reduce(sends, recvs)
+        for _ in range(3):
+            g.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(r, exact) for r in recvs)
+        assert c.path_bytes()[PathKind.PCIE_STAGED] > 0
+        assert c.tune_info(CollectiveOp.ALLREDUCE, count * 4)["calls"] == calls  # no step
+        c.set_timing(False)
+        for _ in range(5):
+            c.all_reduce(sends, recvs)
+        torch.cuda.synchronize()
+        assert c.path_bytes()[PathKind.PCIE_STAGED] > 0  # still the tuned split
+        assert all(torch.equal(r, exact) for r in recvs)
+
+
+def test_interleaved_buckets_tune_independently_past_the_event_ring():
+    """Two AllReduce buckets and an AllGather bucket issued round-robin for more than
+    the 64-slot timing ring: measured calls are harvested before their events are
+    reused, every bucket reaches Stage 2, results stay exact."""
+    n = 4
+    a_s, a_r, a_x = _inputs(n, 8 * MIB, seed=31)       # bucket 25
+    b_s, b_r, b_x = _inputs(n, 16 * MIB + 4096, seed=32)  # bucket 26
+    g = torch.Generator(device="cuda").manual_seed(33)
+    ag_s = [torch.randn(4 * MIB, device="cuda", generator=g) for _ in range(n)]  # 16 MiB sent
+    ag_r = [torch.empty(n * 4 * MIB, device="cuda") for _ in range(n)]
+    with comm.Clique(n, device=0) as c:
+        c.set_nvlink_ctas(1)
+        for _ in range(90):
+            c.all_reduce(a_s, a_r)
+            c.all_reduce(b_s, b_r)
+            c.all_gather(ag_s, ag_r)
+        torch.cuda.synchronize()
+        for op, nbytes in ((CollectiveOp.ALLREDUCE, 32 * MIB),
+                           (CollectiveOp.ALLREDUCE, 64 * MIB + 16384),
+                           (CollectiveOp.ALLGATHER, 16 * MIB)):
+            assert c.tune_info(op, nbytes)["phase"] == "stage2", (op, nbytes)
+        assert all(torch.equal(r, a_x) for r in a_r)
+        assert all(torch.equal(r, b_x) for r in b_r)
+        want = torch.cat(ag_s)
+        assert all(torch.equal(r, want) for r in ag_r)

@@ -18,7 +18,9 @@ HERE = Path(__file__).resolve().parent
 ROOT = HERE.parent
 CSRC = HERE / "csrc"
 LIB = HERE / "libflexlink.so"
-SOURCES = ["flexlink.cu", "launch.cu", "world.cu", "nvls.cu", "tuner.cpp", "autotune.cpp"]
+SOURCES = ["flexlink.cu", "launch.cu", "world.cu", "nvls.cu", "tuner.cpp", "autotune.cpp",
+           "rank_launch_i8.cu", "rank_launch_i32.cu", "rank_launch_i64.cu", "rank_launch_f16.cu",
+           "rank_launch_f32.cu", "rank_launch_f64.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
          "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}"]

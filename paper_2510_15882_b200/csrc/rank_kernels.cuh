@@ -15,6 +15,8 @@
 // CTA owns one fixed region of each slot (cta_sub).  The fold rule is
 // kernels.cuh's (bit-identical to the virtual-rank path and the CPU oracle).
 //
+// Non-template kernels are `static` (this header is included by several
+// translation units: world.cu and the per-dtype launch units rank_launch_*.cu).
 // The same device code runs (a) per GPU with grid = nctas, (b) in loopback
 // (all ranks on one GPU, grid = nctas x nranks, cooperative launch so every
 // CTA is co-resident and the spin-waits cannot deadlock).
@@ -700,7 +702,7 @@ __device__ __forceinline__ RoundPlan round_plan(size_t span, int nctas, int cta,
   return p;
 }
 
-__device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
+static __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
@@ -777,7 +779,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
 // AllToAll: a.bytes = NVLink part of each block, a.rank_stride = block stride
 // B (send and recv).  Push block c to peer c, copy my own block locally, then
 // land every peer's push into recv block p.
-__device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
+static __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
   const size_t mine = (size_t)cta * sub;  // this CTA's region in every slot
@@ -813,12 +815,12 @@ __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
   cta_epochs_done(ep, k, ep.last_ar, prev_main);
 }
 
-__global__ void __launch_bounds__(512, 2) rank_alltoall_kernel(const __grid_constant__ RankArgs a) {
+static __global__ void __launch_bounds__(512, 2) rank_alltoall_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<float, kSum, 3>(a, blockIdx.x, gridDim.x);
   else rank_alltoall(a, blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512, 2) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
+static __global__ void __launch_bounds__(512, 2) loopback_alltoall_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 3>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_alltoall(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
@@ -835,7 +837,7 @@ __global__ void __launch_bounds__(512, 2) rank_reducescatter_kernel(const __grid
   else rank_reducescatter<T, OP>(a, blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512, 2) rank_allgather_kernel(const __grid_constant__ RankArgs a) {
+static __global__ void __launch_bounds__(512, 2) rank_allgather_kernel(const __grid_constant__ RankArgs a) {
   if (a.oneshot) rank_oneshot<float, kSum, 1>(a, blockIdx.x, gridDim.x);
   else rank_allgather(a, blockIdx.x, gridDim.x);
 }
@@ -853,7 +855,7 @@ __global__ void __launch_bounds__(512, 2) loopback_reducescatter_kernel(const __
   else rank_reducescatter<T, OP>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }
 
-__global__ void __launch_bounds__(512, 2) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
+static __global__ void __launch_bounds__(512, 2) loopback_allgather_kernel(const __grid_constant__ LoopbackArgs a) {
   if (a.r[blockIdx.y].oneshot) rank_oneshot<float, kSum, 1>(a.r[blockIdx.y], blockIdx.x, gridDim.x);
   else rank_allgather(a.r[blockIdx.y], blockIdx.x, gridDim.x);
 }

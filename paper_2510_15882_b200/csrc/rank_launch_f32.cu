@@ -1,0 +1,23 @@
+// Reducing rank kernels for float (see rank_launch.h).
+#include "../../include/flexlink.h"
+#include "rank_launch_impl.cuh"
+
+namespace flx {
+
+cudaError_t rank_reduce_f32(int dtype, int op, bool scatter, bool loop, const void* a, int nctas,
+                           int n, cudaStream_t s) {
+  switch (dtype) {
+    case flxFloat32: return rank_reduce_typed<float>(op, scatter, loop, a, nctas, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+int loopback_blocks_per_sm() {
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loopback_allreduce_kernel<float, kSum>,
+                                                    512, 0) != cudaSuccess)
+    return 1;
+  return per_sm > 0 ? per_sm : 1;
+}
+
+}  // namespace flx

@@ -46,6 +46,7 @@
 #include "nvls.h"
 #include "nvls_kernels.cuh"
 #include "rank_kernels.cuh"
+#include "rank_launch.h"
 
 namespace flx {
 
@@ -385,52 +386,19 @@ bool spin_until(F pred, double seconds) {
 
 // ------------------------------------------------------------- launches
 // SCATTER selects ReduceScatter (push + fold) instead of AllReduce (push +
-// fold + pull); both share dtype/op dispatch.
-template <typename T, int OP, bool SCATTER>
-cudaError_t launch_rank_reduce_t(bool loop, const void* args, int nctas, int nranks,
-                                 cudaStream_t s) {
-  if (loop) {
-    const void* fn = SCATTER ? (const void*)loopback_reducescatter_kernel<T, OP>
-                             : (const void*)loopback_allreduce_kernel<T, OP>;
-    void* params[] = {const_cast<void*>(args)};
-    return cudaLaunchCooperativeKernel(fn, dim3(nctas, nranks), dim3(512), params, 0, s);
-  }
-  const RankArgs& a = *static_cast<const RankArgs*>(args);
-  if (SCATTER)
-    rank_reducescatter_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
-  else
-    rank_allreduce_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
-  return cudaGetLastError();
-}
-
-template <typename T, bool SCATTER>
-cudaError_t launch_rank_reduce_op(int op, bool loop, const void* a, int nctas, int n,
-                                  cudaStream_t s) {
-  switch (op) {
-    case kSum: return launch_rank_reduce_t<T, kSum, SCATTER>(loop, a, nctas, n, s);
-    case kProd: return launch_rank_reduce_t<T, kProd, SCATTER>(loop, a, nctas, n, s);
-    case kMax: return launch_rank_reduce_t<T, kMax, SCATTER>(loop, a, nctas, n, s);
-    case kMin: return launch_rank_reduce_t<T, kMin, SCATTER>(loop, a, nctas, n, s);
-  }
-  return cudaErrorInvalidValue;
-}
-
+// fold + pull); the per-dtype launchers live in rank_launch_*.cu.
 template <bool SCATTER>
 cudaError_t launch_rank_reduce(int dtype, int op, bool loop, const void* a, int nctas, int n,
                                cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
   switch (dtype) {
-    case flxInt8: return launch_rank_reduce_op<int8_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxUint8: return launch_rank_reduce_op<uint8_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxInt32: return launch_rank_reduce_op<int32_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxUint32: return launch_rank_reduce_op<uint32_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxInt64: return launch_rank_reduce_op<int64_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxUint64: return launch_rank_reduce_op<uint64_t, SCATTER>(op, loop, a, nctas, n, s);
-    case flxFloat16: return launch_rank_reduce_op<__half, SCATTER>(op, loop, a, nctas, n, s);
-    case flxFloat32: return launch_rank_reduce_op<float, SCATTER>(op, loop, a, nctas, n, s);
-    case flxFloat64: return launch_rank_reduce_op<double, SCATTER>(op, loop, a, nctas, n, s);
-    case flxBfloat16:
-      return launch_rank_reduce_op<__nv_bfloat16, SCATTER>(op, loop, a, nctas, n, s);
+    case flxInt8: case flxUint8: return rank_reduce_i8(dtype, op, SCATTER, loop, a, nctas, n, s);
+    case flxInt32: case flxUint32: return rank_reduce_i32(dtype, op, SCATTER, loop, a, nctas, n, s);
+    case flxInt64: case flxUint64: return rank_reduce_i64(dtype, op, SCATTER, loop, a, nctas, n, s);
+    case flxFloat16: case flxBfloat16:
+      return rank_reduce_f16(dtype, op, SCATTER, loop, a, nctas, n, s);
+    case flxFloat32: return rank_reduce_f32(dtype, op, SCATTER, loop, a, nctas, n, s);
+    case flxFloat64: return rank_reduce_f64(dtype, op, SCATTER, loop, a, nctas, n, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -934,8 +902,7 @@ flxResult_t world_create_loopback(int nranks, int device, World** out) {
   // every CTA of every rank co-resident (cooperative launch): the rank kernels
   // fit 64 registers x 512 threads, i.e. 2 CTAs per SM
   int per_sm = 1;
-  FLX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, loopback_allreduce_kernel<float, kSum>, 512, 0));
+  per_sm = loopback_blocks_per_sm();
   w->max_nctas = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * sms / nranks));
   // largest power of two that keeps every rank's CTAs co-resident: 8 ranks
   // get 32 (37 would fit, 32 measured faster), 2-4 ranks 64
@@ -1036,8 +1003,7 @@ flxResult_t world_create_loopback_ipc(int nranks, int device, const char* id_hex
   FLX_CUDA(cudaSetDevice(device));
   int sms = 0, per_sm = 1;
   FLX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device));
-  FLX_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      &per_sm, loopback_allreduce_kernel<float, kSum>, 512, 0));
+  per_sm = loopback_blocks_per_sm();
   w->max_nctas = std::max(1, std::min(kMaxCtas, std::max(1, per_sm) * sms / nranks));
   world_set_nctas(w, 0);
   for (int r = 0; r < nranks; ++r) {

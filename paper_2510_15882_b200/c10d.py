@@ -4,10 +4,13 @@ After :func:`register`, ``dist.init_process_group("flexlink")`` (or
 ``backend="cuda:flexlink"``) routes ``dist.all_reduce`` /
 ``dist.all_gather_into_tensor`` / ``dist.reduce_scatter_tensor`` /
 ``dist.all_to_all_single`` (and their list forms) to FlexLink's striped
-collectives, so tensor-parallel code, DTensor and anything else that calls the
-torch.distributed API names picks up the NVLink + PCIe split — and the
-in-library two-stage balancer — without code changes (the
-motivating workload is TP AllReduce in a Qwen-32B prefill).
+collectives, so tensor-parallel code that calls the torch.distributed API names
+picks up the NVLink + PCIe split — and the in-library two-stage balancer —
+without code changes (the motivating workload is TP AllReduce in
+a Qwen-32B prefill).  The functional collectives
+(`torch.distributed._functional_collectives`, which DTensor uses) resolve
+process groups by name, which torch does not assign to a Python-implemented
+group: they are not supported through this backend.
 
 One process per GPU.  The communicator is bootstrapped through the process
 group's own store (rank 0 publishes the flxUniqueId).  Collectives are

@@ -8,9 +8,11 @@ collectives, so tensor-parallel code that calls the torch.distributed API names
 picks up the NVLink + PCIe split — and the in-library two-stage balancer —
 without code changes (the motivating workload is TP AllReduce in
 a Qwen-32B prefill).  The functional collectives
-(`torch.distributed._functional_collectives`, which DTensor uses) resolve
-process groups by name, which torch does not assign to a Python-implemented
-group: they are not supported through this backend.
+(`torch.distributed._functional_collectives`, which DTensor uses) resolve the
+group by name; torch keeps that name in its own registry rather than in a
+Python-implemented group, so :attr:`FlexLinkBackend.group_name` reads it from
+there and ``funcol.all_reduce`` / ``all_gather_tensor`` /
+``reduce_scatter_tensor`` / ``all_to_all_single`` reach the same kernels.
 
 One process per GPU.  The communicator is bootstrapped through the process
 group's own store (rank 0 publishes the flxUniqueId).  Collectives are
@@ -87,11 +89,27 @@ class FlexLinkBackend(dist.ProcessGroup):
         return BACKEND
 
     @property
+    def group_name(self) -> str:
+        # init_process_group / new_group record the name in torch's registry
+        # (and register the group under it for the functional collectives)
+        # but only push it into C++-implemented backends
+        name = dist.distributed_c10d._world.pg_names.get(self)
+        if name is None:
+            raise RuntimeError("ProcessGroup name not set")
+        return name
+
+    @property
     def _stream(self):
         return torch.cuda.current_stream()
 
     # -- collectives
     def allreduce(self, tensors, opts=None):
+        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        for t in tensors:
+            self.comm.all_reduce(t, t, op=op, stream=self._stream)
+        return _DoneWork(tensors)
+
+    def allreduce_coalesced(self, tensors, opts=None):
         op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
         for t in tensors:
             self.comm.all_reduce(t, t, op=op, stream=self._stream)
@@ -118,6 +136,12 @@ class FlexLinkBackend(dist.ProcessGroup):
         op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
         self.comm.reduce_scatter(input, output, op=op, stream=self._stream)
         return _DoneWork([output])
+
+    def reduce_scatter_tensor_coalesced(self, outputs, inputs, opts=None):
+        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        for o, i in zip(outputs, inputs):
+            self.comm.reduce_scatter(i, o, op=op, stream=self._stream)
+        return _DoneWork(outputs)
 
     def reduce_scatter(self, output_tensors, input_lists, opts=None):
         op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)

@@ -5,6 +5,7 @@ import sys
 
 import torch
 import torch.distributed as dist
+import torch.distributed._functional_collectives as funcol
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_15882_b200 import c10d  # noqa: E402
@@ -56,6 +57,26 @@ def main():
         want_a2a = torch.cat([vals(r, world * n, it)[rank * n:(rank + 1) * n]
                               for r in range(world)]).to(dev)
         bad += int(not torch.equal(a2a, want_a2a))
+    # functional collectives (DTensor's path) resolve the group by name
+    x = vals(rank, n).to(dev)
+    y = funcol.wait_tensor(funcol.all_reduce(x, "sum", dist.group.WORLD))
+    bad += int(not torch.equal(y, sum(vals(r, n) for r in range(world)).to(dev)))
+    g = funcol.wait_tensor(funcol.all_gather_tensor(x, 0, dist.group.WORLD))
+    bad += int(not torch.equal(g, torch.cat([vals(r, n) for r in range(world)]).to(dev)))
+    big = vals(rank, world * n).to(dev)
+    rs = funcol.wait_tensor(funcol.reduce_scatter_tensor(big, "sum", 0, dist.group.WORLD))
+    full = sum(vals(r, world * n) for r in range(world))
+    bad += int(not torch.equal(rs, full[rank * n:(rank + 1) * n].to(dev)))
+    a2a = funcol.wait_tensor(funcol.all_to_all_single(big, None, None, dist.group.WORLD))
+    bad += int(not torch.equal(a2a, torch.cat([vals(r, world * n)[rank * n:(rank + 1) * n]
+                                               for r in range(world)]).to(dev)))
+    pair = funcol.all_reduce_coalesced([vals(rank, n).to(dev), vals(rank, n, 7).to(dev)], "max",
+                                       dist.group.WORLD)
+    for shift, t in zip((0, 7), pair):
+        want = torch.stack([vals(r, n, shift) for r in range(world)]).max(0).values.to(dev)
+        bad += int(not torch.equal(funcol.wait_tensor(t), want))
+    if bad:
+        print(f"rank {rank} functional collectives mismatch", flush=True)
     dist.barrier()
     try:
         dist.broadcast(x, 0)

@@ -27,3 +27,40 @@ sys.exit(3)
                          timeout=300)
     assert out.returncode == 0, out.stderr[-2000:]
     assert "refused" in out.stdout or "skip" in out.stdout
+
+
+def test_functional_collectives_resolve_the_python_group_by_name():
+    # host logic only: a subclass whose allreduce doubles on the CPU stands in
+    # for the communicator, so group_name / work plumbing run without a GPU
+    code = """
+import os, sys, torch, torch.distributed as dist
+import torch.distributed._functional_collectives as funcol
+sys.path.insert(0, %r)
+from paper_2510_15882_b200 import c10d
+class Stub(c10d.FlexLinkBackend):
+    def __init__(self, store, rank, size, timeout):
+        dist.ProcessGroup.__init__(self, rank, size)
+        self.comm = None
+    def allreduce(self, tensors, opts=None):
+        c10d._op_name(opts.reduceOp)
+        for t in tensors:
+            t.mul_(2)
+        return c10d._DoneWork(tensors)
+dist.Backend.register_backend("flxstub", lambda s, r, n, t: Stub(s, r, n, t), devices=["cpu"])
+os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT="29519")
+dist.init_process_group("flxstub", rank=0, world_size=1)
+assert dist.group.WORLD.group_name == dist.distributed_c10d._world.pg_names[dist.group.WORLD]
+y = funcol.wait_tensor(funcol.all_reduce(torch.ones(8), "sum", dist.group.WORLD))
+assert torch.equal(y, torch.full((8,), 2.0)), y
+try:
+    funcol.wait_tensor(funcol.all_reduce(torch.ones(8), "avg", dist.group.WORLD))
+    sys.exit(4)
+except Exception as e:
+    assert "sum/prod/max/min" in str(e), e
+dist.destroy_process_group()
+print("ok")
+""" % str(ROOT)
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stdout[-1000:] + out.stderr[-2000:]
+    assert "ok" in out.stdout

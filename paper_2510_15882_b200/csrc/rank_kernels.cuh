@@ -69,6 +69,7 @@ struct RankArgs {
   size_t small_slot;   // one-shot inbox capacity per source rank and parity
   int oneshot;         // AllReduce: run the one-shot protocol (bytes fit small_slot)
   int ll;              // one-shot in the LL format (flag in every 64-bit word; rank_oneshot_ll)
+  int bulk;            // copy phases as TMA bulk copies (cta_copy_bulk; FLX_BULK=0: off)
   uint32_t* abort_word;  // host-mapped; set on a wait timeout
   long long spin_limit;  // clock64 cycles a wait may spin before aborting (FLX_TIMEOUT_S)
 };
@@ -246,6 +247,118 @@ __device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, b
   }
 }
 
+// A copy segment of a multi-peer phase: dst <- src, len bytes.
+struct CopySeg {
+  char* dst;
+  const char* src;
+  size_t len;
+};
+
+// Bulk-copy (TMA) form of a whole push / pull / land phase (RankArgs::bulk,
+// the default; FLX_BULK=0 selects the register copies of cta_copy): the N-1
+// segments stream as one pipeline of kBulkTile tiles through a ring of
+// kBulkStages shared-memory stages — cp.async.bulk global -> smem behind an
+// mbarrier (complete_tx), then cp.async.bulk smem -> global — driven by one
+// thread, so the bytes in flight ((kBulkStages-1) tiles of loads + one store,
+// ~80 KB per CTA) sit in dynamic shared memory instead of registers.  The 16 B
+// aligned body of every segment goes through the pipeline while the other
+// threads copy the ragged tails.  Proxy fences order the flag acquires
+// (generic proxy) before the bulk reads and the bulk writes before the CTA's
+// flag release.  Loopback A/B (profiles/r2/loopback_bulk_copy_ab.jsonl): 16 KB
+// x 6 stages beats the register copies by 4-9 % (fp32, N = 8/4/2); rings that
+// fit the 48 KB static limit (8 KB x 5, 4 KB x 10, 16 KB x 2) lose.
+#ifndef FLX_BULK_TILE
+#define FLX_BULK_TILE 16384
+#endif
+#ifndef FLX_BULK_STAGES
+#define FLX_BULK_STAGES 6
+#endif
+constexpr uint32_t kBulkTile = FLX_BULK_TILE;
+constexpr int kBulkStages = FLX_BULK_STAGES;
+
+__device__ __forceinline__ void fence_async_global() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+struct BulkSmem {
+  __align__(128) unsigned char buf[kBulkStages][kBulkTile];
+  uint64_t full[kBulkStages];
+  char* dst[kBulkStages];
+  uint32_t len[kBulkStages];
+};
+// one dynamic allocation per kernel, shared by every phase's instantiation
+__device__ __forceinline__ BulkSmem& bulk_smem() {
+  extern __shared__ __align__(128) unsigned char flx_bulk_dyn[];
+  return *reinterpret_cast<BulkSmem*>(flx_bulk_dyn);
+}
+
+template <typename SegFn>
+__device__ void cta_copy_bulk(SegFn seg, int nseg, bool coherent) {
+  bool ok = true;
+  for (int i = 0; i < nseg; ++i) {
+    const CopySeg g = seg(i);
+    ok = ok && aligned16_dev(g.dst) && aligned16_dev(g.src);
+  }
+  if (!ok) {
+    for (int i = 0; i < nseg; ++i) {
+      const CopySeg g = seg(i);
+      cta_copy(g.dst, g.src, g.len, coherent);
+    }
+    return;
+  }
+  BulkSmem& sm = bulk_smem();
+  auto& buf = sm.buf;
+  auto& full = sm.full;
+  auto& sdst = sm.dst;
+  auto& slen = sm.len;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kBulkStages; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_async_global();
+    int ps = 0;      // producer cursor: segment, byte offset in its body
+    size_t po = 0;
+    auto produce = [&](int stage) -> bool {
+      for (; ps < nseg; ++ps, po = 0) {
+        const CopySeg g = seg(ps);
+        const size_t body = g.len & ~(size_t)15;
+        if (po < body) {
+          const uint32_t len = (uint32_t)min((size_t)kBulkTile, body - po);
+          mbar_expect_tx(&full[stage], len);
+          bulk_load(buf[stage], g.src + po, len, &full[stage]);
+          sdst[stage] = g.dst + po;
+          slen[stage] = len;
+          po += len;
+          return true;
+        }
+      }
+      return false;
+    };
+    uint32_t issued = 0;
+    while (issued < (uint32_t)kBulkStages && produce((int)issued)) ++issued;
+    for (uint32_t t = 0; t < issued; ++t) {
+      const int s = (int)(t % kBulkStages);
+      mbar_wait(&full[s], (t / kBulkStages) & 1);
+      bulk_store(sdst[s], buf[s], slen[s]);
+      bulk_commit();
+      if (t >= 1) {  // the previous tile's store has read its stage: refill it
+        bulk_wait_read<1>();
+        if (produce((int)((t - 1) % kBulkStages))) ++issued;
+      }
+    }
+    bulk_wait_all();
+    fence_async_global();
+    for (int s = 0; s < kBulkStages; ++s)
+      asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+  }
+  for (int i = 0; i < nseg; ++i) {  // ragged tails (< 16 B per segment)
+    const CopySeg g = seg(i);
+    for (size_t j = (g.len & ~(size_t)15) + threadIdx.x; j < g.len; j += blockDim.x)
+      g.dst[j] = coherent ? *(volatile const char*)(g.src + j) : g.src[j];
+  }
+  __syncthreads();
+}
+constexpr size_t kRankDynSmem = sizeof(BulkSmem);  // dynamic smem of launches with a.bulk
+
 // vectors per thread per source in the fold: 4 for 32/64-bit types; 2 for
 // 16-bit ones, whose fp32 accumulators are twice as many per vector (keeps the
 // kernels inside 64 registers, 2 CTAs per SM)
@@ -397,10 +510,18 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     // 1) push my chunk c into peer c's inbox slot r (this CTA's region)
     if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
     FLX_PHASE(1);
-    for (int s = 1; s < n; ++s) {
-      const int c = (r + s) % n;
-      const ulonglong2 pc = piece(c);
-      cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
+    if (a.bulk) {
+      cta_copy_bulk([&](int i) {
+        const int c = (r + 1 + i) % n;
+        const ulonglong2 pc = piece(c);
+        return CopySeg{a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y};
+      }, n - 1, false);
+    } else {
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        const ulonglong2 pc = piece(c);
+        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
+      }
     }
     cta_signal_peers(a, cta, kArrive, e);
     FLX_PHASE(2);
@@ -421,10 +542,18 @@ __device__ void rank_allreduce(const RankArgs& a, int cta, int nctas) {
     // 3) pull every peer's reduced chunk
     if (!cta_wait_peers(a.flags[r], n, r, cta, kReady, e, -1, 0, a)) return;
     FLX_PHASE(5);
-    for (int s = 1; s < n; ++s) {
-      const int c = (r + s) % n;
-      const ulonglong2 pc = piece(c);
-      cta_copy(a.recv + pc.x, a.scratch[c] + outbox + mine, pc.y, true);
+    if (a.bulk) {
+      cta_copy_bulk([&](int i) {
+        const int c = (r + 1 + i) % n;
+        const ulonglong2 pc = piece(c);
+        return CopySeg{a.recv + pc.x, a.scratch[c] + outbox + mine, pc.y};
+      }, n - 1, true);
+    } else {
+      for (int s = 1; s < n; ++s) {
+        const int c = (r + s) % n;
+        const ulonglong2 pc = piece(c);
+        cta_copy(a.recv + pc.x, a.scratch[c] + outbox + mine, pc.y, true);
+      }
     }
     cta_signal_peers(a, cta, kPulled, e);
     FLX_PHASE(6);
@@ -702,6 +831,48 @@ __device__ __forceinline__ RoundPlan round_plan(size_t span, int nctas, int cta,
   return p;
 }
 
+// Slot-protocol phases (this round's piece pc = {offset, bytes} of CTA `mine`'s
+// region), as one bulk pipeline (a.bulk) or register copies.
+// Land: peer p's push in my inbox slot p -> recv block p (AllGather / AllToAll).
+static __device__ __forceinline__ void land_all(const RankArgs& a, int r, int n, size_t mine,
+                                                ulonglong2 pc) {
+  if (a.bulk) {
+    cta_copy_bulk([&](int i) {
+      const int p = (r - 1 - i + n) % n;
+      return CopySeg{a.recv + (size_t)p * a.rank_stride + pc.x,
+                     a.scratch[r] + (size_t)p * a.slot + mine, pc.y};
+    }, n - 1, true);
+    return;
+  }
+  for (int s = 1; s < n; ++s) {
+    const int p = (r - s + n) % n;
+    cta_copy(a.recv + (size_t)p * a.rank_stride + pc.x, a.scratch[r] + (size_t)p * a.slot + mine,
+             pc.y, true);
+  }
+}
+
+// Push block c of send to peer c's inbox slot r (ReduceScatter / AllToAll);
+// with `own`, my own block also lands in recv block r (AllToAll).
+static __device__ __forceinline__ void push_blocks(const RankArgs& a, int r, int n, size_t mine,
+                                                   ulonglong2 pc, bool own) {
+  const size_t mo = (size_t)r * a.rank_stride + pc.x;
+  if (a.bulk) {
+    cta_copy_bulk([&](int i) {
+      if (i == n - 1) return CopySeg{a.recv + mo, a.send + mo, own ? pc.y : 0};
+      const int c = (r + 1 + i) % n;
+      return CopySeg{a.scratch[c] + (size_t)r * a.slot + mine,
+                     a.send + (size_t)c * a.rank_stride + pc.x, pc.y};
+    }, n, false);
+    return;
+  }
+  for (int s = 1; s < n; ++s) {
+    const int c = (r + s) % n;
+    cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + (size_t)c * a.rank_stride + pc.x,
+             pc.y, false);
+  }
+  if (own) cta_copy(a.recv + mo, a.send + mo, pc.y, false);
+}
+
 static __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
   const int r = a.rank, n = a.nranks;
   const size_t sub = cta_sub(a.slot);
@@ -716,20 +887,24 @@ static __device__ void rank_allgather(const RankArgs& a, int cta, int nctas) {
     const ulonglong2 pc = plan.piece(at, len);  // {send offset, bytes}
     {  // push my piece into every peer's inbox slot r (this CTA's region)
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
-      }
       char* own = a.recv + (size_t)r * a.rank_stride;
-      if (own != a.send) cta_copy(own + pc.x, a.send + pc.x, pc.y, false);
+      if (a.bulk) {  // n-1 pushes and my own block, one pipeline
+        cta_copy_bulk([&](int i) {
+          if (i == n - 1) return CopySeg{own + pc.x, a.send + pc.x, own != a.send ? pc.y : 0};
+          const int c = (r + 1 + i) % n;
+          return CopySeg{a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y};
+        }, n, false);
+      } else {
+        for (int s = 1; s < n; ++s) {
+          const int c = (r + s) % n;
+          cta_copy(a.scratch[c] + (size_t)r * a.slot + mine, a.send + pc.x, pc.y, false);
+        }
+        if (own != a.send) cta_copy(own + pc.x, a.send + pc.x, pc.y, false);
+      }
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
-    for (int s = 1; s < n; ++s) {
-      const int p = (r - s + n) % n;
-      cta_copy(a.recv + (size_t)p * a.rank_stride + pc.x, a.scratch[r] + (size_t)p * a.slot + mine,
-               pc.y, true);
-    }
+    land_all(a, r, n, mine, pc);
     free_all(a, cta, e);
     prev_main = e;
     at += len;
@@ -754,11 +929,7 @@ __device__ void rank_reducescatter(const RankArgs& a, int cta, int nctas) {
     const ulonglong2 pc = plan.piece(at, len);  // {offset in a block, bytes}
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
-                 a.send + (size_t)c * a.rank_stride + pc.x, pc.y, false);
-      }
+      push_blocks(a, r, n, mine, pc, false);
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
@@ -793,21 +964,11 @@ static __device__ void rank_alltoall(const RankArgs& a, int cta, int nctas) {
     const ulonglong2 pc = plan.piece(at, len);  // {offset in a block, bytes}
     {
       if (!cta_wait_peers(a.flags[r], n, r, cta, kFree, prev_main, -1, 0, a)) return;
-      for (int s = 1; s < n; ++s) {
-        const int c = (r + s) % n;
-        cta_copy(a.scratch[c] + (size_t)r * a.slot + mine,
-                 a.send + (size_t)c * a.rank_stride + pc.x, pc.y, false);
-      }
-      const size_t own = (size_t)r * a.rank_stride + pc.x;
-      cta_copy(a.recv + own, a.send + own, pc.y, false);
+      push_blocks(a, r, n, mine, pc, true);
       cta_signal_peers(a, cta, kArrive, e);
     }
     if (!cta_wait_peers(a.flags[r], n, r, cta, kArrive, e, -1, 0, a)) return;
-    for (int s = 1; s < n; ++s) {
-      const int p = (r - s + n) % n;
-      cta_copy(a.recv + (size_t)p * a.rank_stride + pc.x,
-               a.scratch[r] + (size_t)p * a.slot + mine, pc.y, true);
-    }
+    land_all(a, r, n, mine, pc);
     free_all(a, cta, e);
     prev_main = e;
     at += len;

@@ -14,8 +14,10 @@ cudaError_t rank_reduce_f32(int dtype, int op, bool scatter, bool loop, const vo
 
 int loopback_blocks_per_sm() {
   int per_sm = 1;
+  cudaFuncSetAttribute(loopback_allreduce_kernel<float, kSum>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, loopback_allreduce_kernel<float, kSum>,
-                                                    512, 0) != cudaSuccess)
+                                                    512, kRankDynSmem) != cudaSuccess)
     return 1;
   return per_sm > 0 ? per_sm : 1;
 }

@@ -9,17 +9,30 @@ namespace flx {
 template <typename T, int OP>
 cudaError_t rank_reduce_t(bool scatter, bool loop, const void* args, int nctas, int nranks,
                           cudaStream_t s) {
+  // the bulk-copy ring (RankArgs::bulk) is dynamic shared memory
+  static const bool attr_set = [] {
+    for (const void* f : {(const void*)loopback_allreduce_kernel<T, OP>,
+                          (const void*)rank_allreduce_kernel<T, OP>,
+                          (const void*)loopback_reducescatter_kernel<T, OP>,
+                          (const void*)rank_reducescatter_kernel<T, OP>})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
+    return true;
+  }();
+  (void)attr_set;
+  const int bulk = loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
+                        : static_cast<const RankArgs*>(args)->bulk;
+  const size_t dyn = bulk ? kRankDynSmem : 0;
   if (loop) {
     const void* fn = scatter ? (const void*)loopback_reducescatter_kernel<T, OP>
                              : (const void*)loopback_allreduce_kernel<T, OP>;
     void* params[] = {const_cast<void*>(args)};
-    return cudaLaunchCooperativeKernel(fn, dim3(nctas, nranks), dim3(512), params, 0, s);
+    return cudaLaunchCooperativeKernel(fn, dim3(nctas, nranks), dim3(512), params, dyn, s);
   }
   const RankArgs& a = *static_cast<const RankArgs*>(args);
   if (scatter)
-    rank_reducescatter_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
+    rank_reducescatter_kernel<T, OP><<<nctas, 512, dyn, s>>>(a);
   else
-    rank_allreduce_kernel<T, OP><<<nctas, 512, 0, s>>>(a);
+    rank_allreduce_kernel<T, OP><<<nctas, 512, dyn, s>>>(a);
   return cudaGetLastError();
 }
 

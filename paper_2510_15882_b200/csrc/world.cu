@@ -114,6 +114,7 @@ struct World {
   double timeout_s = 10.0;   // FLX_TIMEOUT_S: peer waits and the PCIe-leg watchdog
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   bool ll = true;          // one-shot slices that fit kLLRegion / 2 per CTA use the LL format (FLX_LL)
+  bool bulk = true;        // two-shot push / pull as TMA bulk copies (FLX_BULK=0: register copies)
   size_t hcap = 0;       // PCIe staging bytes per rank region
   size_t pcie_chunk = 0;  // PCIe pipeline chunk, bytes per reader (FLX_PCIE_CHUNK_KB)
   // (NVLink-path flag epochs live on the device: kStateWords in each flag block)
@@ -371,6 +372,9 @@ void world_config(World* w, int nranks) {
   w->small_slot = std::max<size_t>(2 * w->oneshot_max, 16 * kMaxCtas);
   const char* ll = getenv("FLX_LL");
   w->ll = !(ll && atoi(ll) == 0);
+  // a per-rank choice of copy mechanism: the protocol and layout are the same
+  const char* bulk = getenv("FLX_BULK");
+  w->bulk = !(bulk && atoi(bulk) == 0);
 }
 
 template <typename F>
@@ -406,24 +410,40 @@ cudaError_t launch_rank_reduce(int dtype, int op, bool loop, const void* a, int 
 cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nranks,
                                   cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  static const bool attr_set = [] {  // the bulk-copy ring (RankArgs::bulk)
+    for (const void* f : {(const void*)loopback_allgather_kernel, (const void*)rank_allgather_kernel})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
+    return true;
+  }();
+  (void)attr_set;
+  const size_t dyn = (loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
+                           : static_cast<const RankArgs*>(args)->bulk) ? kRankDynSmem : 0;
   if (loop) {
     void* params[] = {const_cast<void*>(args)};
     return cudaLaunchCooperativeKernel((const void*)loopback_allgather_kernel, dim3(nctas, nranks),
-                                       dim3(512), params, 0, s);
+                                       dim3(512), params, dyn, s);
   }
-  rank_allgather_kernel<<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  rank_allgather_kernel<<<nctas, 512, dyn, s>>>(*static_cast<const RankArgs*>(args));
   return cudaGetLastError();
 }
 
 cudaError_t launch_rank_alltoall(bool loop, const void* args, int nctas, int nranks,
                                  cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  static const bool attr_set = [] {  // the bulk-copy ring (RankArgs::bulk)
+    for (const void* f : {(const void*)loopback_alltoall_kernel, (const void*)rank_alltoall_kernel})
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
+    return true;
+  }();
+  (void)attr_set;
+  const size_t dyn = (loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
+                           : static_cast<const RankArgs*>(args)->bulk) ? kRankDynSmem : 0;
   if (loop) {
     void* params[] = {const_cast<void*>(args)};
     return cudaLaunchCooperativeKernel((const void*)loopback_alltoall_kernel, dim3(nctas, nranks),
-                                       dim3(512), params, 0, s);
+                                       dim3(512), params, dyn, s);
   }
-  rank_alltoall_kernel<<<nctas, 512, 0, s>>>(*static_cast<const RankArgs*>(args));
+  rank_alltoall_kernel<<<nctas, 512, dyn, s>>>(*static_cast<const RankArgs*>(args));
   return cudaGetLastError();
 }
 
@@ -663,6 +683,7 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       a.oneshot = w->oneshot_max > 0 && n > 1 && (fits_ll || fits_flagged) &&
                   (gather || scatter || a2a || nv <= w->oneshot_max);
       a.ll = a.oneshot && fits_ll;
+      a.bulk = w->bulk;
       a.abort_word = w->abort_word;
       a.spin_limit = w->spin_limit;
     }

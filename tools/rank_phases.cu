@@ -63,6 +63,7 @@ int main(int argc, char** argv) {
     a.small_slot = small;
     a.oneshot = oneshot;
     a.ll = 0;  // the LL area is not allocated here
+    a.bulk = 0;  // register copies: launched without the bulk ring's dynamic smem
     a.abort_word = abort_dev;
     a.spin_limit = 20000000000ll;
   }

@@ -74,6 +74,7 @@ int main(int argc, char** argv) {
     a.small_slot = small;
     a.oneshot = 0;
     a.ll = 0;
+    a.bulk = 0;  // register copies: launched without the bulk ring's dynamic smem
     a.abort_word = abort_dev;
     a.spin_limit = 20000000000ll;
   }

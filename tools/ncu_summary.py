@@ -9,7 +9,8 @@ NAMES = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.su
          "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
          "launch__grid_size", "launch__block_size", "dram__bytes.sum.per_second",
          "launch__occupancy_limit_registers", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
-         "launch__stack_size"]
+         "launch__stack_size", "launch__shared_mem_per_block_dynamic",
+         "launch__occupancy_limit_shared_mem", "launch__occupancy_per_block_size"]
 rows = list(csv.reader(open(sys.argv[1])))
 hdr, units = rows[0], rows[1]
 for r in rows[2:]:

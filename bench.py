@@ -183,6 +183,19 @@ def workload_config(n_gpus: int) -> dict:
 
 
 # ------------------------------------------------------------ CPU baseline
+def cpu_model() -> str:
+    """Host CPU model and logical CPU count (printed with every CPU timing)."""
+    name = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                name = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return f"{name}, {os.cpu_count()} logical CPUs"
+
+
 def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = AR_BYTES,
                          n: int = SIM_RANKS):
     """Oracle port on the host: the same n-rank fp32 AllReduce (256 MiB per rank)
@@ -211,6 +224,7 @@ def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = AR_BYTES,
         "unit": "GB/s",
         "cores": threads,
         "kind": "port",
+        "cpu": cpu_model(),
         "sample": f"AllReduce sum fp32 {per_rank_bytes // MIB} MiB/rank x {n} simulated ranks, "
                   f"{reps} calls in {per_call * reps:.1f} s (oracle/flx_oracle.c, OpenMP)",
     }
@@ -249,7 +263,7 @@ def run_reference(args) -> None:
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": workload_config(args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GB/s", "cores": threads,
-                         "kind": "port",
+                         "kind": "port", "cpu": cpu_model(),
                          "sample": f"each step: the full workload, AllReduce sum fp32 "
                                    f"{per_rank // MIB} MiB/rank x {ranks} ranks on the host "
                                    f"(oracle/flx_oracle.c, OpenMP, {threads} threads)"},

@@ -6,7 +6,8 @@
 // of half the CTAs overlap the other half's transfers.  Build both ways:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -DFLX_STAGGER=1 \
 //        -o tools/bin/rank_timeline tools/rank_timeline.cu
-//   tools/bin/rank_timeline [bytes_per_rank] [nranks] [nctas]
+//   tools/bin/rank_timeline [bytes_per_rank] [nranks] [nctas] [bulk]
+// (bulk = 1: copy phases as TMA bulk copies, RankArgs::bulk, the library default)
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -40,6 +41,7 @@ int main(int argc, char** argv) {
   const size_t bytes = argc > 1 ? strtoull(argv[1], nullptr, 0) : (256ull << 20);
   const int n = argc > 2 ? atoi(argv[2]) : 8;
   const int nctas = argc > 3 ? atoi(argv[3]) : 32;
+  const int bulk = argc > 4 ? atoi(argv[4]) : 0;
   const size_t slot = 64u << 20, small = 1u << 20;
   LoopbackArgs la;
   memset(&la, 0, sizeof(la));
@@ -74,14 +76,16 @@ int main(int argc, char** argv) {
     a.small_slot = small;
     a.oneshot = 0;
     a.ll = 0;
-    a.bulk = 0;  // register copies: launched without the bulk ring's dynamic smem
+    a.bulk = bulk;
     a.abort_word = abort_dev;
     a.spin_limit = 20000000000ll;
   }
   void* params[] = {&la};
   const void* fn = (const void*)loopback_allreduce_kernel<float, kSum>;
+  const size_t dyn = bulk ? kRankDynSmem : 0;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem));
   for (int i = 0; i < 4; ++i)
-    CK(cudaLaunchCooperativeKernel(fn, dim3(nctas, n), dim3(512), params, 0, 0));
+    CK(cudaLaunchCooperativeKernel(fn, dim3(nctas, n), dim3(512), params, dyn, 0));
   CK(cudaDeviceSynchronize());
   int zero[16][64] = {};
   CK(cudaMemcpyToSymbol(g_n, zero, sizeof(zero)));
@@ -89,7 +93,7 @@ int main(int argc, char** argv) {
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   CK(cudaEventRecord(e0));
-  CK(cudaLaunchCooperativeKernel(fn, dim3(nctas, n), dim3(512), params, 0, 0));
+  CK(cudaLaunchCooperativeKernel(fn, dim3(nctas, n), dim3(512), params, dyn, 0));
   CK(cudaEventRecord(e1));
   CK(cudaEventSynchronize(e1));
   float ms;
@@ -139,10 +143,10 @@ int main(int argc, char** argv) {
     else fold += p.second / 100;
   }
   const double span = t1 - t0;
-  printf("{\"stagger\": %d, \"bytes\": %zu, \"nranks\": %d, \"nctas\": %d, \"rounds_cta0\": %d, "
+  printf("{\"bulk\": %d, \"stagger\": %d, \"bytes\": %zu, \"nranks\": %d, \"nctas\": %d, \"rounds_cta0\": %d, "
          "\"us_per_launch\": %.1f, \"span_us\": %.1f, \"transfer_coverage\": %.3f, "
          "\"fold_overlapping_transfers\": %.3f, \"fold_only\": %.3f}\n",
-         FLX_STAGGER, bytes, n, nctas, rounds, ms * 1e3, span, covered / span, overlap / span,
+         bulk, FLX_STAGGER, bytes, n, nctas, rounds, ms * 1e3, span, covered / span, overlap / span,
          only_fold / span);
   return 0;
 }

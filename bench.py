@@ -230,6 +230,91 @@ def cpu_allreduce_sample(target_s: float = 10.0, per_rank_bytes: int = AR_BYTES,
     }
 
 
+def control_plane(target_s: float = 1.0) -> dict:
+    """SURVEY §8(d) CPU-path timing of the control plane: the balancer's decisions in
+    the reference algorithm's own Python (stage1 / stage2, restating tuner.py:134-226
+    and balancer.py:57-207; 1 core) beside the library's C++ (flxTuneStep /
+    flxBalancerObserve, tools/control_cost.c), both driven by one closed-form
+    path-time model — Stage 1 from the H800 three-path profile with observed rates
+    below it, then 1000 Stage-2 calls with PCIe at 0.7x from call 31.  The two must
+    take the same decisions (iterations and final shares)."""
+    import subprocess
+
+    from paper_2510_15882_b200 import links, stage1, stage2, striping
+    from paper_2510_15882_b200.links import PathKind
+
+    root = os.path.dirname(os.path.abspath(__file__))
+    exe = os.path.join(root, "tools", "bin", "control_cost")
+    src = os.path.join(root, "tools", "control_cost.c")
+    lib = os.path.join(root, "paper_2510_15882_b200")
+    if not os.path.exists(exe) or os.path.getmtime(exe) < os.path.getmtime(src):
+        os.makedirs(os.path.dirname(exe), exist_ok=True)
+        subprocess.run(["gcc", "-O2", "-I", os.path.join(root, "include"), "-I",
+                        "/usr/local/cuda/include", src, "-L", lib, "-lflexlink",
+                        f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+    native = json.loads(subprocess.run([exe], check=True, capture_output=True,
+                                       text=True).stdout)
+
+    topo = links.preset("H800")
+    lat = {PathKind.NVLINK: 5e-6, PathKind.PCIE_STAGED: 1e-5, PathKind.RDMA_NIC: 1.5e-5}
+    obs = {PathKind.NVLINK: 190e9, PathKind.PCIE_STAGED: 40e9, PathKind.RDMA_NIC: 6.25e9}
+    size = 256 * MIB
+    moved = float(size) * 2.0 * 7.0 / 8.0
+    spec = striping.CollectiveSpec(striping.CollectiveOp.ALLREDUCE, 8, size)
+
+    def model(shares, active, scale=1.0):
+        d = {p: lat[p] + (moved * shares.get(p) / 1000.0) /
+             (obs[p] * scale if p == PathKind.PCIE_STAGED else obs[p]) for p in active}
+        return striping.PathTimingReport.build(spec.op, spec.n_gpus, spec.size, d)
+
+    def tune():
+        return stage1.initial_tune(topo, spec, measure=lambda st: model(st.shares, st.active))
+
+    reps, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < target_s:
+        shares, trace = tune()
+        reps += 1
+    s1 = (time.perf_counter() - t0) / reps
+    iters = len(trace.records)
+    active = shares.loaded_paths
+
+    def dynamic():
+        return stage2.run_dynamic(
+            topo, spec, shares, n_calls=1000, active=active,
+            measure=lambda call, sh: model(sh, active, 0.7 if call >= 31 else 1.0))
+
+    # observe() alone: replay the reports of one run through a fresh hook
+    res = dynamic()
+    reps2, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < target_s:
+        hook = stage2.RuntimeBalancer(shares, active=active)
+        for rep in res.reports:
+            hook.observe(rep)
+        reps2 += 1
+    obs_us = (time.perf_counter() - t0) / (reps2 * len(res.reports)) * 1e6
+    t0 = time.perf_counter()
+    dynamic()
+    dyn_ms = (time.perf_counter() - t0) * 1e3
+    py = {"stage1_ms": round(s1 * 1e3, 4), "stage1_iterations": iters,
+          "tune_step_us": round(s1 / max(iters, 1) * 1e6, 2),
+          "stage1_shares": [shares.get(p) for p in PathKind],
+          "observe_us": round(obs_us, 2),
+          "run_dynamic_ms_per_1000_calls": round(dyn_ms, 2),
+          "stage2_evaluations": len(res.evaluations),
+          "stage2_moves": sum(1 for e in res.evaluations if e.adjustment is not None),
+          "stage2_shares": [res.final_shares.get(p) for p in PathKind]}
+    agree = all(native[k] == py[k] for k in ("stage1_iterations", "stage1_shares",
+                                              "stage2_evaluations", "stage2_moves",
+                                              "stage2_shares"))
+    return {"reference_python": py, "native": native, "decisions_agree": agree,
+            "speedup_tune_step": round(py["tune_step_us"] * 1e3 / native["tune_step_ns"], 1),
+            "speedup_observe": round(py["observe_us"] * 1e3 / native["observe_ns"], 1),
+            "cores": 1, "cpu": cpu_model(),
+            "note": "per-decision host cost; the reference's Python is the restated "
+                    "stage1/stage2 (tests/test_reference_suite.py passes the reference's own "
+                    "tests against it); run_dynamic includes the model evaluation"}
+
+
 def run_reference(args) -> None:
     """``--impl reference``: the CPU path on the box's host cores (rank 0 only)."""
     rank = int(os.environ.get("RANK", "0"))
@@ -563,6 +648,7 @@ def run_single_gpu(args) -> None:
                           "an on-GPU fold bound by HBM (see roofline); this is the north star's "
                           "multi-GPU denominator"},
         "cpu_baseline": cpu,
+        "control_plane": control_plane(),
         "e2e": {"value": round(e2e_value, 3), "unit": "GB/s",
                 "h2d_bytes_per_step": n * AR_BYTES, "d2h_bytes_per_step": AR_BYTES,
                 "ms_per_step": round(e2e_dt * 1e3, 3), "steps": e2e_steps,

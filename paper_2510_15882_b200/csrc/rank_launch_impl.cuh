@@ -10,15 +10,12 @@ template <typename T, int OP>
 cudaError_t rank_reduce_t(bool scatter, bool loop, const void* args, int nctas, int nranks,
                           cudaStream_t s) {
   // the bulk-copy ring (RankArgs::bulk) is dynamic shared memory
-  static const bool attr_set = [] {
-    for (const void* f : {(const void*)loopback_allreduce_kernel<T, OP>,
+  static std::atomic<uint64_t> opted{0};
+  opt_in_dyn_smem(opted, {(const void*)loopback_allreduce_kernel<T, OP>,
                           (const void*)rank_allreduce_kernel<T, OP>,
                           (const void*)loopback_reducescatter_kernel<T, OP>,
-                          (const void*)rank_reducescatter_kernel<T, OP>})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
-    return true;
-  }();
-  (void)attr_set;
+                          (const void*)rank_reducescatter_kernel<T, OP>},
+                  (int)kRankDynSmem);
   const int bulk = loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
                         : static_cast<const RankArgs*>(args)->bulk;
   const size_t dyn = bulk ? kRankDynSmem : 0;

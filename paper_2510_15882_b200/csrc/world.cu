@@ -410,12 +410,9 @@ cudaError_t launch_rank_reduce(int dtype, int op, bool loop, const void* a, int 
 cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nranks,
                                   cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  static const bool attr_set = [] {  // the bulk-copy ring (RankArgs::bulk)
-    for (const void* f : {(const void*)loopback_allgather_kernel, (const void*)rank_allgather_kernel})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
-    return true;
-  }();
-  (void)attr_set;
+  static std::atomic<uint64_t> opted{0};  // the bulk-copy ring (RankArgs::bulk)
+  opt_in_dyn_smem(opted, {(const void*)loopback_allgather_kernel, (const void*)rank_allgather_kernel},
+                  (int)kRankDynSmem);
   const size_t dyn = (loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
                            : static_cast<const RankArgs*>(args)->bulk) ? kRankDynSmem : 0;
   if (loop) {
@@ -430,12 +427,9 @@ cudaError_t launch_rank_allgather(bool loop, const void* args, int nctas, int nr
 cudaError_t launch_rank_alltoall(bool loop, const void* args, int nctas, int nranks,
                                  cudaStream_t s) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
-  static const bool attr_set = [] {  // the bulk-copy ring (RankArgs::bulk)
-    for (const void* f : {(const void*)loopback_alltoall_kernel, (const void*)rank_alltoall_kernel})
-      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRankDynSmem);
-    return true;
-  }();
-  (void)attr_set;
+  static std::atomic<uint64_t> opted{0};  // the bulk-copy ring (RankArgs::bulk)
+  opt_in_dyn_smem(opted, {(const void*)loopback_alltoall_kernel, (const void*)rank_alltoall_kernel},
+                  (int)kRankDynSmem);
   const size_t dyn = (loop ? static_cast<const LoopbackArgs*>(args)->r[0].bulk
                            : static_cast<const RankArgs*>(args)->bulk) ? kRankDynSmem : 0;
   if (loop) {

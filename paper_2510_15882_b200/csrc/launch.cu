@@ -4,6 +4,7 @@
 
 #include "internal.h"
 #include "kernels.cuh"
+#include "rank_launch.h"  // opt_in_dyn_smem
 
 namespace flx {
 
@@ -34,13 +35,8 @@ bool use_tma_fanout() { return tma_mode() == 1; }
 template <typename T, int OP, int NMAX>
 cudaError_t fold_tma(const FoldArgs& a, int grid, cudaStream_t s) {
   constexpr size_t smem = tma_fold_smem<NMAX>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(fold_tma_kernel<T, OP, NMAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static std::atomic<uint64_t> opted{0};  // per device: cliques may span several
+  opt_in_dyn_smem(opted, {(const void*)fold_tma_kernel<T, OP, NMAX>}, (int)smem);
   fold_tma_kernel<T, OP, NMAX><<<grid, kTmaThreads, smem, s>>>(a);
   return cudaGetLastError();
 }
@@ -195,13 +191,8 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   }
   if (vec && use_tma_fanout()) {
     constexpr size_t smem = (size_t)kTmaStages * kTmaTile * 4 + kTmaStages * sizeof(uint64_t);
-    static bool configured = false;
-    if (!configured) {
-      cudaError_t e = cudaFuncSetAttribute(fanout_tma_kernel,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      configured = true;
-    }
+    static std::atomic<uint64_t> opted{0};  // per device: cliques may span several
+    opt_in_dyn_smem(opted, {(const void*)fanout_tma_kernel}, (int)smem);
     fanout_tma_kernel<<<dim3(grid * 3, a.nsrc), 32, smem, s>>>(a);
   } else if (!vec) {
     fanout_byte_kernel<<<g, 512, 0, s>>>(a);

@@ -18,9 +18,13 @@
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
- * struct.  Calls without a communicator that FlexLink does not provide
- * (ncclMemAlloc/Free, ncclCommInitRankConfig/Scalable, the pncl* profiling
- * aliases) are not defined and resolve to NCCL if it is loaded.
+ * struct.  ncclCommInitRankConfig / ncclCommInitRankScalable (the init
+ * frameworks such as PyTorch's ProcessGroupNCCL use) create FlexLink
+ * communicators, honouring the config fields that map (below).  Calls without
+ * a communicator that FlexLink does not provide (ncclMemAlloc/Free — plain
+ * device memory from NCCL's allocator works with FlexLink's collectives —,
+ * ncclGroupSimulateEnd, the pncl* profiling aliases) are not defined and
+ * resolve to NCCL if it is loaded.
  */
 #include <nccl.h>
 #include <string.h>
@@ -52,6 +56,49 @@ ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId commId,
   flxUniqueId id;
   memcpy(&id, &commId, sizeof(id));
   return (ncclResult_t)flxCommInitRank((flxComm_t*)comm, nranks, id, rank);
+}
+
+/* NCCL's config (nccl.h ncclConfig_t), where it maps onto FlexLink: maxCTAs caps
+ * the NVLink-path kernel grid (flxSetNvlinkCtas, 1..64; NCCL also requires the
+ * same config on every rank); blocking = 0 is satisfied by the blocking init (a
+ * later ncclCommGetAsyncError reports ncclSuccess, never ncclInProgress).
+ * cgaClusterSize, minCTAs, netName, splitShare, trafficClass, commName,
+ * collnetEnable, CTAPolicy, shrinkShare and nvlsCTAs have no FlexLink meaning
+ * (FLX_NVLS selects the NVLS path).  A config not set up with
+ * NCCL_CONFIG_INITIALIZER is refused, as NCCL refuses it. */
+static ncclResult_t init_with_config(ncclComm_t* comm, int nranks, ncclUniqueId commId, int rank,
+                                     const ncclConfig_t* config) {
+  if (config && config->magic != 0xcafebeef) {
+    flxSetLastError("ncclConfig_t was not initialised with NCCL_CONFIG_INITIALIZER");
+    return ncclInvalidArgument;
+  }
+  ncclResult_t r = ncclCommInitRank(comm, nranks, commId, rank);
+  if (r != ncclSuccess || !config) return r;
+  if (config->maxCTAs != NCCL_CONFIG_UNDEF_INT && config->maxCTAs > 0) {
+    const int ctas = config->maxCTAs < 64 ? config->maxCTAs : 64;
+    r = (ncclResult_t)flxSetNvlinkCtas((flxComm_t)*comm, ctas);
+    if (r != ncclSuccess) {
+      flxCommDestroy((flxComm_t)*comm);
+      *comm = NULL;
+    }
+  }
+  return r;
+}
+
+ncclResult_t ncclCommInitRankConfig(ncclComm_t* comm, int nranks, ncclUniqueId commId, int rank,
+                                    ncclConfig_t* config) {
+  return init_with_config(comm, nranks, commId, rank, config);
+}
+
+/* Several unique ids (one per bootstrap root in NCCL); every rank receives the
+ * same array, so the first id names the FlexLink world identically everywhere. */
+ncclResult_t ncclCommInitRankScalable(ncclComm_t* newcomm, int nranks, int myrank, int nId,
+                                      ncclUniqueId* commIds, ncclConfig_t* config) {
+  if (nId < 1 || !commIds) {
+    flxSetLastError("ncclCommInitRankScalable needs at least one unique id");
+    return ncclInvalidArgument;
+  }
+  return init_with_config(newcomm, nranks, commIds[0], myrank, config);
 }
 
 ncclResult_t ncclCommInitAll(ncclComm_t* comm, int ndev, const int* devlist) {

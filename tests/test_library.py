@@ -105,8 +105,10 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
     for name in ("ncclBroadcast", "ncclBcast", "ncclReduce", "ncclSend", "ncclRecv",
                  "ncclCommSplit", "ncclCommRegister"):
         assert name in exported
+    # the config-taking inits frameworks use create FlexLink communicators
+    assert "ncclCommInitRankConfig" in exported and "ncclCommInitRankScalable" in exported
     # ...while comm-less calls FlexLink does not provide still resolve to NCCL
-    assert "ncclMemAlloc" not in exported and "ncclCommInitRankConfig" not in exported
+    assert "ncclMemAlloc" not in exported and "ncclGroupSimulateEnd" not in exported
     S = ctypes.CDLL(str(shim))
     S.ncclGetErrorString.restype = ctypes.c_char_p
     assert S.ncclGetErrorString(4) == b"invalid argument"
@@ -121,6 +123,19 @@ def test_nccl_shim_exports_nccl_named_entry_points(lib):
     assert b"not a live FlexLink communicator" in S.ncclGetLastError(None)
     assert S.ncclBroadcast(None, None, 0, 7, 0, ctypes.byref(fake), None) == 4
     assert S.ncclAllReduce(None, None, 0, 7, 0, ctypes.byref(fake), None) == 4
+    # a config not set up with NCCL_CONFIG_INITIALIZER is refused before any
+    # bootstrap (NCCL's rule), and so is a Scalable init without unique ids
+    class UniqueId(ctypes.Structure):  # ncclUniqueId is passed by value
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    raw = (ctypes.c_uint64 * 16)()
+    out_comm = ctypes.c_void_p()
+    S.ncclCommInitRankConfig.argtypes = [ctypes.c_void_p, ctypes.c_int, UniqueId, ctypes.c_int,
+                                         ctypes.c_void_p]
+    assert S.ncclCommInitRankConfig(ctypes.byref(out_comm), 2, UniqueId(bytes(uid)), 0,
+                                    ctypes.byref(raw)) == 4
+    assert b"NCCL_CONFIG_INITIALIZER" in S.ncclGetLastError(None)
+    assert S.ncclCommInitRankScalable(ctypes.byref(out_comm), 2, 0, 0, None, None) == 4
 
 
 def test_header_is_plain_c_and_links(tmp_path, lib):

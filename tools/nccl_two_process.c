@@ -9,14 +9,17 @@
  *
  *   gcc -std=c11 -I/usr/local/cuda/include -Iinclude tools/nccl_two_process.c \
  *       -Lpaper_2510_15882_b200 -lflexlink_nccl -lflexlink -L/usr/local/cuda/lib64 \
- *       -lcudart -Wl,-rpath,... -o tools/bin/nccl_two_process
- * Exit code 0 and "ok" when every result is exact on both ranks.
+ *       -lcudart -Wl,-rpath,... -o tools/bin/nccl_two_process [config]
+ * With "config" the communicators come from ncclCommInitRankConfig (non-blocking
+ * flag, maxCTAs = 16), as frameworks such as PyTorch's ProcessGroupNCCL create
+ * them.  Exit code 0 and "ok" when every result is exact on both ranks.
  */
 #define _POSIX_C_SOURCE 200809L
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <string.h>
 #include <sys/wait.h>
 #include <unistd.h>
 
@@ -27,10 +30,21 @@
 
 static float value(int rank, size_t i) { return (float)((i * (rank + 3)) % 251) - 100.f; }
 
+static int use_config = 0;
+
 static int run(int rank, ncclUniqueId id) {
   if (cudaSetDevice(0) != cudaSuccess) return 10;
   ncclComm_t comm;
-  if (ncclCommInitRank(&comm, N, id, rank) != ncclSuccess) return 11;
+  if (use_config) {
+    ncclConfig_t config = NCCL_CONFIG_INITIALIZER;
+    config.blocking = 0;
+    config.maxCTAs = 16;
+    if (ncclCommInitRankConfig(&comm, N, id, rank, &config) != ncclSuccess) return 14;
+    ncclResult_t async = ncclInProgress;
+    if (ncclCommGetAsyncError(comm, &async) != ncclSuccess || async != ncclSuccess) return 15;
+  } else if (ncclCommInitRank(&comm, N, id, rank) != ncclSuccess) {
+    return 11;
+  }
   const int pcie_only[3] = {0, 1000, 0};
   for (int op = flxCollAllReduce; op <= flxCollReduceScatter; ++op)
     if (flxSetShares((flxComm_t)comm, (flxCollOp_t)op, FLX_BUCKET_ALL, pcie_only) != flxSuccess)
@@ -74,7 +88,16 @@ static int run(int rank, ncclUniqueId id) {
   return bad ? 40 : 0;
 }
 
-int main(void) {
+int main(int argc, char** argv) {
+  use_config = argc > 1 && argv[1][0] == 'c';
+  if (use_config) {  /* a config not set up by NCCL_CONFIG_INITIALIZER is refused */
+    ncclConfig_t raw;
+    memset(&raw, 0, sizeof(raw));
+    ncclComm_t c = NULL;
+    ncclUniqueId any;
+    memset(&any, 0, sizeof(any));
+    if (ncclCommInitRankConfig(&c, N, any, 0, &raw) != ncclInvalidArgument) return 4;
+  }
   setenv("FLX_ALLOW_SHARED_GPU", "1", 1);
   setenv("FLX_SLOT_MB", "1", 1);
   setenv("FLX_PCIE_STAGE_MB", "8", 1);

@@ -19,8 +19,10 @@ group's own store (rank 0 publishes the flxUniqueId).  Collectives are
 enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
 ``async_op=False`` path), so the returned work objects are complete from the
 stream's point of view.  Operations FlexLink does not implement (broadcast,
-send/recv, gather/scatter, uneven all_to_all splits, ReduceOp.AVG) raise
-``NotImplementedError`` instead of silently falling back to another library.
+send/recv, gather/scatter, uneven all_to_all splits, ReduceOp.AVG on integer
+tensors) raise ``NotImplementedError`` instead of silently falling back to
+another library.  ReduceOp.AVG on floating tensors is the striped sum divided
+by the group size in place (fl(fl(sum) / n)).
 """
 
 from __future__ import annotations
@@ -57,11 +59,33 @@ class _DoneWork(dist._Work):
 
 def _op_name(op) -> str:
     table = {dist.ReduceOp.SUM: "sum", dist.ReduceOp.PRODUCT: "prod", dist.ReduceOp.MAX: "max",
-             dist.ReduceOp.MIN: "min"}
+             dist.ReduceOp.MIN: "min", dist.ReduceOp.AVG: "avg"}
     for k, v in table.items():
         if op == k:
             return v
-    raise NotImplementedError(f"FlexLink reduces with sum/prod/max/min only, not {op}")
+    raise NotImplementedError(f"FlexLink reduces with sum/prod/max/min/avg only, not {op}")
+
+
+def _reduce_op(opts) -> str:
+    return _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+
+
+def _flx_op(op: str, t: torch.Tensor) -> str:
+    """The FlexLink reduction that runs for `op` on `t`: AVG is the striped sum
+    followed by `_finish` (floating types only — NCCL's integer average has no
+    FlexLink counterpart)."""
+    if op != "avg":
+        return op
+    if not t.is_floating_point():
+        raise NotImplementedError("ReduceOp.AVG needs a floating-point tensor on FlexLink")
+    return "sum"
+
+
+def _finish(op: str, t: torch.Tensor, size: int) -> None:
+    """AVG: the rank-order sum divided by the group size in place, on the caller's
+    stream (rounding: fl(fl(sum) / n), not NCCL's pre-multiplied sum)."""
+    if op == "avg":
+        t.div_(size)
 
 
 class FlexLinkBackend(dist.ProcessGroup):
@@ -104,16 +128,14 @@ class FlexLinkBackend(dist.ProcessGroup):
 
     # -- collectives
     def allreduce(self, tensors, opts=None):
-        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        op = _reduce_op(opts)
         for t in tensors:
-            self.comm.all_reduce(t, t, op=op, stream=self._stream)
+            self.comm.all_reduce(t, t, op=_flx_op(op, t), stream=self._stream)
+            _finish(op, t, self.size())
         return _DoneWork(tensors)
 
     def allreduce_coalesced(self, tensors, opts=None):
-        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
-        for t in tensors:
-            self.comm.all_reduce(t, t, op=op, stream=self._stream)
-        return _DoneWork(tensors)
+        return self.allreduce(tensors, opts)
 
     def _allgather_base(self, output, input, opts=None):
         self.comm.all_gather(input, output, stream=self._stream)
@@ -133,22 +155,22 @@ class FlexLinkBackend(dist.ProcessGroup):
         return _DoneWork(outputs)
 
     def _reduce_scatter_base(self, output, input, opts=None):
-        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
-        self.comm.reduce_scatter(input, output, op=op, stream=self._stream)
-        return _DoneWork([output])
+        return self.reduce_scatter_tensor_coalesced([output], [input], opts)
 
     def reduce_scatter_tensor_coalesced(self, outputs, inputs, opts=None):
-        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        op = _reduce_op(opts)
         for o, i in zip(outputs, inputs):
-            self.comm.reduce_scatter(i, o, op=op, stream=self._stream)
+            self.comm.reduce_scatter(i, o, op=_flx_op(op, i), stream=self._stream)
+            _finish(op, o, self.size())
         return _DoneWork(outputs)
 
     def reduce_scatter(self, output_tensors, input_lists, opts=None):
-        op = _op_name(opts.reduceOp if opts is not None else dist.ReduceOp.SUM)
+        op = _reduce_op(opts)
         for out, ins in zip(output_tensors, input_lists):
             flat = torch.cat([i.reshape(-1) for i in ins])
             res = torch.empty(out.numel(), dtype=out.dtype, device=out.device)
-            self.comm.reduce_scatter(flat, res, op=op, stream=self._stream)
+            self.comm.reduce_scatter(flat, res, op=_flx_op(op, flat), stream=self._stream)
+            _finish(op, res, self.size())
             out.copy_(res.view_as(out))
         return _DoneWork(output_tensors)
 

@@ -40,6 +40,10 @@ def main():
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         bad += int(not torch.equal(mx, torch.stack([vals(r, n, it) for r in range(world)]).max(0)
                                    .values.to(dev)))
+        av = vals(rank, n, it).to(dev)
+        dist.all_reduce(av, op=dist.ReduceOp.AVG)  # integer-valued: exact sum, then / world
+        bad += int(not torch.equal(av, (sum(vals(r, n, it) for r in range(world)) / world)
+                                   .to(dev)))
         src = vals(rank, n, it).to(dev)
         out = torch.empty(world * n, device=dev)
         dist.all_gather_into_tensor(out, src)
@@ -52,6 +56,9 @@ def main():
         dist.reduce_scatter_tensor(rs, big)
         full = sum(vals(r, world * n, it) for r in range(world))
         bad += int(not torch.equal(rs, full[rank * n:(rank + 1) * n].to(dev)))
+        rsa = torch.empty(n, device=dev)
+        dist.reduce_scatter_tensor(rsa, big, op=dist.ReduceOp.AVG)
+        bad += int(not torch.equal(rsa, (full[rank * n:(rank + 1) * n] / world).to(dev)))
         a2a = torch.empty(world * n, device=dev)
         dist.all_to_all_single(a2a, big)
         want_a2a = torch.cat([vals(r, world * n, it)[rank * n:(rank + 1) * n]

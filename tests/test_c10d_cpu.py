@@ -4,6 +4,8 @@ import subprocess
 import sys
 from pathlib import Path
 
+import pytest
+
 ROOT = Path(__file__).resolve().parents[1]
 
 
@@ -53,10 +55,10 @@ assert dist.group.WORLD.group_name == dist.distributed_c10d._world.pg_names[dist
 y = funcol.wait_tensor(funcol.all_reduce(torch.ones(8), "sum", dist.group.WORLD))
 assert torch.equal(y, torch.full((8,), 2.0)), y
 try:
-    funcol.wait_tensor(funcol.all_reduce(torch.ones(8), "avg", dist.group.WORLD))
+    funcol.wait_tensor(funcol.all_reduce(torch.ones(8), "bxor", dist.group.WORLD))
     sys.exit(4)
 except Exception as e:
-    assert "sum/prod/max/min" in str(e), e
+    assert "sum/prod/max/min/avg" in str(e), e
 dist.destroy_process_group()
 print("ok")
 """ % str(ROOT)
@@ -64,3 +66,19 @@ print("ok")
                          timeout=300)
     assert out.returncode == 0, out.stdout[-1000:] + out.stderr[-2000:]
     assert "ok" in out.stdout
+
+
+def test_avg_is_a_float_sum_then_divide():
+    import torch
+
+    from paper_2510_15882_b200 import c10d
+
+    assert c10d._flx_op("avg", torch.ones(2)) == "sum"
+    assert c10d._flx_op("max", torch.ones(2, dtype=torch.int32)) == "max"
+    with pytest.raises(NotImplementedError, match="floating-point"):
+        c10d._flx_op("avg", torch.ones(2, dtype=torch.int32))
+    t = torch.tensor([3.0, -6.0, 1.0])
+    c10d._finish("avg", t, 3)
+    assert torch.equal(t, torch.tensor([1.0, -2.0, 1.0 / 3.0]))
+    c10d._finish("sum", t, 3)  # other ops untouched
+    assert torch.equal(t, torch.tensor([1.0, -2.0, 1.0 / 3.0]))

@@ -84,9 +84,34 @@ def main():
         bad += int(not torch.equal(funcol.wait_tensor(t), want))
     if bad:
         print(f"rank {rank} functional collectives mismatch", flush=True)
+    # broadcast (AllToAll + AllGather): exact bytes, any dtype, ragged length
+    root = world - 1
+    for dt, cnt in ((torch.float32, n + 5), (torch.bfloat16, 1001), (torch.int64, 3)):
+        src = (vals(root, cnt) * 1.5).to(dt)
+        if dt.is_floating_point:
+            src[0] = -0.0  # a sum with zeros would lose the sign: copies keep it
+        t = (src if rank == root else torch.full_like(src, 7)).to(dev)
+        dist.broadcast(t, root)
+        bad += int(not torch.equal(t.cpu().view(-1).view(torch.uint8),
+                                   src.view(-1).view(torch.uint8)))
+    # DDP: construction broadcasts rank 0's module state, backward averages gradients
+    torch.manual_seed(100 + rank)
+    model = torch.nn.Linear(64, 32).to(dev)
+    ddp = torch.nn.parallel.DistributedDataParallel(model, device_ids=[0])
+    p0 = [p.detach().clone() for p in ddp.parameters()]
+    gathered = [torch.empty_like(p0[0]) for _ in range(world)]
+    dist.all_gather(gathered, p0[0])
+    bad += int(not all(torch.equal(g, gathered[0]) for g in gathered))
+    torch.manual_seed(7 + rank)
+    ddp(torch.randn(16, 64, device=dev)).square().sum().backward()
+    grads = [torch.empty_like(model.weight.grad) for _ in range(world)]
+    dist.all_gather(grads, model.weight.grad)
+    bad += int(not all(torch.equal(g, grads[0]) for g in grads))
+    if bad:
+        print(f"rank {rank} broadcast / DDP mismatch", flush=True)
     dist.barrier()
     try:
-        dist.broadcast(x, 0)
+        dist.reduce(x, 0)
         bad += 1  # must refuse, not fall back
     except Exception as e:
         if "not a FlexLink collective" not in str(e):

@@ -748,6 +748,13 @@ flxResult_t CliquePort::read(uint64_t seq, float ms[FLX_NUM_PATHS]) {
 void init_tuning(Comm* c) {
   c->autotune = autotune_default();
   c->tune_min_bytes = autotune_min_bytes_default();
+  Granules g;
+  bool set = false;
+  if (env_shares(&g, &set) == flxSuccess && set)  // validated by the init entry points
+    for (ShareTable& t : c->shares) {
+      t.fallback = g;
+      t.fallback_pinned = true;
+    }
 }
 
 AutoTuner* tuner_of(const Comm* c) { return c->clique ? c->clique->tuner : world_tuner(c->world); }
@@ -761,6 +768,36 @@ flxResult_t check_call(const flxComm* comm, int dtype, int op, bool reduce) {
 }
 
 }  // namespace
+
+flxResult_t env_shares(Granules* g, bool* set) {
+  *set = false;
+  const char* v = getenv("FLX_SHARES");
+  if (!v || !*v) return flxSuccess;
+  Granules out{{0, 0, 0}};
+  int n = 0, sum = 0;
+  const char* p = v;
+  while (*p && n < FLX_NUM_PATHS) {
+    char* end = nullptr;
+    const long x = strtol(p, &end, 10);
+    if (end == p || x < 0 || x > FLX_GRANULE_TOTAL)
+      return fail(flxInvalidArgument, "FLX_SHARES=\"%s\": expected granules \"nvlink,pcie[,rdma]\"", v);
+    out[n++] = (int)x;
+    sum += (int)x;
+    p = *end == ',' ? end + 1 : end;
+    if (*end && *end != ',') return fail(flxInvalidArgument, "FLX_SHARES=\"%s\": bad separator", v);
+  }
+  if (*p || n < 2 || sum != FLX_GRANULE_TOTAL)
+    return fail(flxInvalidArgument, "FLX_SHARES=\"%s\": 2 or 3 granules summing to %d", v,
+                FLX_GRANULE_TOTAL);
+  const int mask = path_mask();
+  for (int q = 1; q < FLX_NUM_PATHS; ++q)
+    if (out[q] > 0 && !(mask & (1 << q)))
+      return fail(flxInvalidArgument, "FLX_SHARES: path %d is not available on this box", q);
+  *g = out;
+  *set = true;
+  return flxSuccess;
+}
+
 }  // namespace flx
 
 using namespace flx;
@@ -817,6 +854,11 @@ flxResult_t flxGetUniqueId(flxUniqueId* id) {
 }
 
 flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
+  {
+    Granules g;
+    bool set;
+    FLX_TRY(env_shares(&g, &set));  // a malformed FLX_SHARES fails here, loudly
+  }
   if (!comms || ndev < 1) return fail(flxInvalidArgument, "bad comms/ndev");
   int visible = 0;
   FLX_CUDA(cudaGetDeviceCount(&visible));
@@ -854,6 +896,11 @@ flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
 }
 
 flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int rank) {
+  {
+    Granules g;
+    bool set;
+    FLX_TRY(env_shares(&g, &set));  // a malformed FLX_SHARES fails here, loudly
+  }
   if (!comm || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(flxInvalidArgument, "bad comm/nranks/rank");
   uint64_t magic;
@@ -907,6 +954,11 @@ flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, doub
 }
 
 flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flxUniqueId id) {
+  {
+    Granules g;
+    bool set;
+    FLX_TRY(env_shares(&g, &set));  // a malformed FLX_SHARES fails here, loudly
+  }
   if (!comms || nranks < 2) return fail(flxInvalidArgument, "bad comms/nranks");
   uint64_t magic;
   memcpy(&magic, id.internal, sizeof(magic));
@@ -931,6 +983,11 @@ flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flx
 }
 
 flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
+  {
+    Granules g;
+    bool set;
+    FLX_TRY(env_shares(&g, &set));  // a malformed FLX_SHARES fails here, loudly
+  }
   if (!comms || nranks < 1) return fail(flxInvalidArgument, "bad comms/nranks");
   int visible = 0;
   FLX_CUDA(cudaGetDeviceCount(&visible));

@@ -86,6 +86,16 @@ inline std::array<size_t, FLX_NUM_PATHS> path_offsets(const std::array<size_t, F
   return {{split[1] + split[2], 0, split[1]}};
 }
 
+// FLX_SHARES="nvlink,pcie[,rdma]" (granules summing to FLX_GRANULE_TOTAL): every
+// collective's every bucket pinned to this split at comm creation, as
+// flxSetShares(FLX_BUCKET_ALL) would — for programs that only use the NCCL names
+// (e.g. PyTorch's ProcessGroupNCCL under LD_PRELOAD).  *set = false when unset;
+// malformed values fail comm creation.  Multi-rank worlds check it across ranks.
+flxResult_t env_shares(Granules* g, bool* set);
+inline uint64_t pack_env_shares(const Granules& g, bool set) {
+  return set ? (1ull << 48) | (uint64_t)g[0] | (uint64_t)g[1] << 16 | (uint64_t)g[2] << 32 : 0;
+}
+
 struct Comm;
 class AutoTuner;
 

@@ -37,7 +37,14 @@ _Static_assert((int)ncclFloat32 == (int)flxFloat32 && (int)ncclBfloat16 == (int)
 _Static_assert((int)ncclSum == (int)flxSum && (int)ncclMin == (int)flxMin, "reduction codes");
 _Static_assert((int)ncclInvalidUsage == (int)flxInvalidUsage, "result codes");
 
-ncclResult_t ncclGetVersion(int* version) { return (ncclResult_t)flxGetVersion(version); }
+/* The NCCL API level this shim implements (the nccl.h it is compiled against),
+ * not FlexLink's own version (flxGetVersion): callers such as PyTorch's
+ * ProcessGroupNCCL pick their init path and feature set from it. */
+ncclResult_t ncclGetVersion(int* version) {
+  if (!version) return ncclInvalidArgument;
+  *version = NCCL_VERSION_CODE;
+  return ncclSuccess;
+}
 
 const char* ncclGetErrorString(ncclResult_t result) {
   return flxGetErrorString((flxResult_t)result);

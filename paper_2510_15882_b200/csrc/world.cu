@@ -74,10 +74,11 @@ size_t env_mib(const char* name, size_t dflt) {
 
 // World layout and protocol settings every rank must share: each rank reads
 // them from its own environment (FLX_SLOT_MB, FLX_PCIE_STAGE_MB,
-// FLX_PCIE_CHUNK_KB, FLX_ONESHOT_KB, FLX_LL, FLX_NVLINK_CTAS) and a mismatch
+// FLX_PCIE_CHUNK_KB, FLX_ONESHOT_KB, FLX_LL, FLX_NVLINK_CTAS, FLX_NVLS, FLX_SHARES) and a mismatch
 // would shift scratch / staging offsets between ranks, so bootstrap compares them.
 struct BootConfig {
-  uint64_t nranks, slot, small_slot, hcap, pcie_chunk, oneshot_max, ll, nctas, sem_words, nvls;
+  uint64_t nranks, slot, small_slot, hcap, pcie_chunk, oneshot_max, ll, nctas, sem_words, nvls,
+      shares;
 };
 
 struct BootSlot {
@@ -492,6 +493,16 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
   // The NVLink kernels keep their epochs on the device and the PCIe path's
   // token handshake uses constant values: both replay correctly from a graph.
   if (pc > 0 && !memops().ok) return fail(flxInvalidUsage, "pcie path needs stream memory ops");
+  // Ranks of this world share a GPU (FLX_ALLOW_SHARED_GPU self-tests): an
+  // NVLink-path kernel would spin on another process's kernel on the same
+  // GPU, which is not guaranteed to be co-scheduled (context-switch timeouts).
+  // Only host-staged PCIe bytes may move; FLX_SHARED_GPU_KERNELS=1 lets the
+  // peer-timeout test launch one kernel whose peer never comes.
+  if (w->shared_gpu && !w->loopback && nv > 0 && n > 1 && !getenv("FLX_SHARED_GPU_KERNELS"))
+    return fail(flxInvalidUsage,
+                "ranks of this world share one GPU: NVLink-path kernels would wait on another "
+                "process's kernel; pin every byte to PCIe (FLX_SHARES=0,1000 or flxSetShares) "
+                "with a message size that is a multiple of the alignment (%zu B)", alignment);
 
   // fork: in loopback every rank's stream joins local rank 0's stream
   cudaStream_t s0 = streams[0];
@@ -1071,9 +1082,13 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   mine.device = device;
   mine.pid = getpid();
   const bool want_nvls = getenv("FLX_NVLS") && atoi(getenv("FLX_NVLS")) != 0;
+  Granules env_g{{0, 0, 0}};
+  bool env_set = false;
+  FLX_TRY(env_shares(&env_g, &env_set));
   mine.config = BootConfig{(uint64_t)nranks, w->slot, w->small_slot, w->hcap, w->pcie_chunk,
                            w->oneshot_max, (uint64_t)w->ll, (uint64_t)w->nctas,
-                           (uint64_t)kSemWords, (uint64_t)want_nvls};
+                           (uint64_t)kSemWords, (uint64_t)want_nvls,
+                           pack_env_shares(env_g, env_set)};
   __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
   __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
   const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 60.0;
@@ -1084,7 +1099,7 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
   static const char* kFields[] = {"nranks", "FLX_SLOT_MB", "one-shot inbox (FLX_ONESHOT_KB)",
                                   "FLX_PCIE_STAGE_MB", "FLX_PCIE_CHUNK_KB", "FLX_ONESHOT_KB",
                                   "FLX_LL", "FLX_NVLINK_CTAS", "library build (staging words)",
-                                  "FLX_NVLS"};
+                                  "FLX_NVLS", "FLX_SHARES"};
   for (int p = 0; p < nranks; ++p) {
     const uint64_t* a = reinterpret_cast<const uint64_t*>(&mine.config);
     const uint64_t* b = reinterpret_cast<const uint64_t*>(&hdr->slot[p].config);

@@ -77,7 +77,7 @@ def test_two_process_bootstrap_ipc_and_shared_staging():
 def _abort_worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), FLX_ALLOW_SHARED_GPU="1",
                       FLX_SLOT_MB="1", FLX_PCIE_STAGE_MB="1", FLX_BOOT_TIMEOUT="60",
-                      FLX_TIMEOUT_S="1")
+                      FLX_TIMEOUT_S="1", FLX_SHARED_GPU_KERNELS="1")
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:

@@ -160,3 +160,14 @@ def test_header_is_plain_c_and_links(tmp_path, lib):
                     "-lflexlink", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True)
     assert out.returncode == 0 and out.stdout.strip() == "ok", (out.returncode, out.stdout)
+
+
+def test_flx_shares_env_is_validated_at_init(lib, monkeypatch):
+    # FLX_SHARES pins every bucket at comm creation (programs that only use the
+    # NCCL names); a malformed value fails the init loudly, before any device work
+    comms = (ctypes.c_void_p * 2)()
+    lib.flxGetLastError.restype = ctypes.c_char_p
+    for bad in ("900", "900,50", "a,b", "1000,0,0,0", "-5,1005", "900;100"):
+        monkeypatch.setenv("FLX_SHARES", bad)
+        assert lib.flxCommInitAll(comms, 2, None) == 4, bad
+        assert b"FLX_SHARES" in lib.flxGetLastError(), bad

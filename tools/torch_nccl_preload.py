@@ -1,0 +1,63 @@
+"""PyTorch's own, unmodified NCCL process group running on FlexLink through
+LD_PRELOAD=libflexlink_nccl.so: ProcessGroupNCCL creates its communicator with
+ncclCommInitRankConfig and issues ncclAllReduce / ncclAllGather /
+ncclReduceScatter, which the shim resolves to FlexLink.  Prints one JSON line:
+the results' exactness and how many FlexLink kernels ran (flxGetLaunchCount).
+Run:  LD_PRELOAD=$PWD/paper_2510_15882_b200/libflexlink_nccl.so python tools/torch_nccl_preload.py
+(two ranks on one GPU: RANK / WORLD_SIZE, FLX_ALLOW_SHARED_GPU=1, FLX_SHARES=0,1000 — every
+byte on the host-staged PCIe path, so no kernel spins on the other process's)."""
+import ctypes
+import json
+import os
+import sys
+
+import torch
+import torch.distributed as dist
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main() -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29561")
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", 0))
+    flx = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "paper_2510_15882_b200", "libflexlink.so"))
+    count = ctypes.c_ulonglong()
+    flx.flxGetLaunchCount.argtypes = [ctypes.POINTER(ctypes.c_ulonglong)]
+    flx.flxGetLaunchCount(ctypes.byref(count))
+    before = count.value
+    n = 1 << 20  # 4 MiB of fp32: a multiple of every alignment (all bytes on one path)
+
+    def data(r):
+        g = torch.Generator(device="cuda").manual_seed(r)
+        return torch.randint(-100, 100, (n,), device="cuda", generator=g).float()
+
+    mine = data(rank)
+    every = [data(r) for r in range(world)]
+    x = mine.clone()
+    dist.all_reduce(x)
+    ok = {"all_reduce": bool(torch.equal(x, torch.stack(every).sum(0)))}
+    out = torch.empty(world * n, device="cuda")
+    dist.all_gather_into_tensor(out, mine)
+    ok["all_gather"] = bool(torch.equal(out, torch.cat(every)))
+    rs = torch.empty(n // world, device="cuda")
+    dist.reduce_scatter_tensor(rs, mine)
+    blk = n // world
+    ok["reduce_scatter"] = bool(torch.equal(rs, torch.stack(every).sum(0)[rank * blk:(rank + 1) * blk]))
+    if world == 1:
+        dist.barrier()  # a 1-element AllReduce: on a shared GPU it would be an NVLink kernel
+    torch.cuda.synchronize()
+    flx.flxGetLaunchCount(ctypes.byref(count))
+    print(json.dumps({"rank": rank, "world": world, "exact": ok,
+                      "flexlink_kernels": count.value - before,
+                      "nccl_version_seen_by_torch": torch.cuda.nccl.version()}), flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

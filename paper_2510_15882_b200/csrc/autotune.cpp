@@ -275,6 +275,7 @@ flxResult_t AutoTuner::stage2_call(TimingPort& port, Slot& s) {
   tune::evaluate_apply(reps.data(), (int)reps.size(), s.s2_active, s.pol.s2, &sh, &rec);
   rec.call = s.s2_observed;
   if (rec.moved) s.moves += 1;
+  s.n_evals += 1;
   s.cur = Granules{{sh[0], sh[1], sh[2]}};
   s.evals.push_back(rec);
   if (s.evals.size() > kMaxEvals) s.evals.pop_front();
@@ -427,7 +428,7 @@ bool AutoTuner::info(int op, int bucket, flxTuneInfo* out) const {
     out->shares[p] = s.cur[p];
   }
   out->stage2_calls = s.s2_calls;
-  out->stage2_evaluations = (int)s.evals.size();
+  out->stage2_evaluations = s.n_evals;
   out->stage2_moves = s.moves;
   out->calls = s.calls;
   return true;

@@ -92,7 +92,8 @@ class AutoTuner {
     int s2_observed = 0;               // reports observed (lags s2_calls by `lag`)
     std::deque<MeasPtr> lagq;          // issued, not yet observed
     std::deque<MeasPtr> window;        // observed, newest last
-    std::deque<flxEvalRecord> evals;
+    std::deque<flxEvalRecord> evals;  // the last kMaxEvals evaluation records
+    int n_evals = 0;                  // every evaluation so far
     int moves = 0;
     int calls = 0;
   };

@@ -183,10 +183,11 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   if (bases && !vec) {  // ragged per-rank blocks: aligned stores, funnel-shifted loads
     const unsigned bx = (unsigned)std::min<size_t>(((a.bytes >> 4) + 511) / 512 + 1, (size_t)grid);
     const dim3 gs(std::max(1u, bx), a.nsrc);
-    if (a.ndst <= 2) fanout_shift_kernel<2><<<gs, 512, 0, s>>>(a);
-    else if (a.ndst <= 4) fanout_shift_kernel<4><<<gs, 512, 0, s>>>(a);
-    else if (a.ndst <= 8) fanout_shift_kernel<8><<<gs, 512, 0, s>>>(a);
-    else fanout_shift_kernel<16><<<gs, 512, 0, s>>>(a);
+    // (a two-CTA destination split as in fanout_once measured slower here)
+    if (a.ndst <= 2) fanout_shift_kernel<2, 1><<<gs, 512, 0, s>>>(a);
+    else if (a.ndst <= 4) fanout_shift_kernel<4, 1><<<gs, 512, 0, s>>>(a);
+    else if (a.ndst <= 8) fanout_shift_kernel<8, 1><<<gs, 512, 0, s>>>(a);
+    else fanout_shift_kernel<16, 1><<<gs, 512, 0, s>>>(a);
     return cudaGetLastError();
   }
   if (vec && use_tma_fanout()) {

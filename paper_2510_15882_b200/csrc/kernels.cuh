@@ -71,6 +71,26 @@ __device__ __forceinline__ uint4 ld_stream(const void* p) {
   return v;
 }
 
+// The 16 B at p when all of them lie inside the source (avail >= 16); else only
+// the first `avail` bytes, loaded one by one, the rest zero — a shifted window's
+// last vector must not read past the end of its source buffer.
+__device__ __forceinline__ uint4 ld_vec_clamped(const char* p, size_t avail, bool coherent) {
+  if (avail >= 16) {
+    if (!coherent) return ld_stream(p);
+    uint4 v;
+    asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+  }
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (size_t i = 0; i < avail; ++i) {
+    const uint32_t b = coherent ? (uint8_t)*(volatile const char*)(p + i) : (uint8_t)p[i];
+    w[i >> 2] |= b << (8 * (i & 3));
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
 __device__ __forceinline__ void st_stream(void* p, const uint4& v) {
   asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x),
                "r"(v.y), "r"(v.z), "r"(v.w)
@@ -604,7 +624,8 @@ __global__ void __launch_bounds__(512) fanout_shift_kernel(const FanoutArgs a) {
       y.y = __shfl_down_sync(0xffffffffu, x.y, 1);
       y.z = __shfl_down_sync(0xffffffffu, x.z, 1);
       y.w = __shfl_down_sync(0xffffffffu, x.w, 1);
-      if (live && (lane == 31 || j + 1 == body)) y = ld_stream(src + ((j + 1) << 4));
+      if (live && (lane == 31 || j + 1 == body))
+        y = ld_vec_clamped(src + ((j + 1) << 4), a.bytes - ((j + 1) << 4), false);
       out = shift_bytes(x, y, (uint32_t)h);
     }
     if (live) {

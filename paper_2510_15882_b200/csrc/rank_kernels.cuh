@@ -233,7 +233,8 @@ __device__ __forceinline__ void cta_copy(char* dst, const char* src, size_t n, b
     const size_t body = n > h ? (n - h) >> 4 : 0;
     for (size_t j = threadIdx.x; j < body; j += blockDim.x) {
       const uint4 x = coherent ? ld_cg(src + (j << 4)) : ld_stream(src + (j << 4));
-      const uint4 y = coherent ? ld_cg(src + ((j + 1) << 4)) : ld_stream(src + ((j + 1) << 4));
+      // the last window's second vector may reach past the piece: clamp it
+      const uint4 y = ld_vec_clamped(src + ((j + 1) << 4), n - ((j + 1) << 4), coherent);
       *reinterpret_cast<uint4*>(dst + h + (j << 4)) = shift_bytes(x, y, (uint32_t)h);
     }
     const size_t nh = n < h ? n : h, tail0 = h + (body << 4);

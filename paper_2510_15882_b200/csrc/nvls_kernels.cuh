@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_con
   const int b = blockIdx.x, nb = gridDim.x, r = a.rank, n = a.nranks;
   const uint32_t e = a.state[b] + 1;  // this CTA's call epoch (identical on every rank)
   const size_t chunk = a.bytes / n;   // 16 B multiple (host guarantees)
-  const size_t part = ((chunk / nb) + 15) & ~(size_t)15;
+  const size_t part = (((chunk + nb - 1) / nb) + 15) & ~(size_t)15;  // covers the chunk
   const size_t lo = min(chunk, (size_t)b * part), hi = min(chunk, lo + part);
   char* ucd = a.uc + kNvlsFlagBytes;
   char* mcd = a.mc + kNvlsFlagBytes;
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(512, 2) nvls_allgather_kernel(const __grid_con
                                                                  size_t stride) {
   const int b = blockIdx.x, nb = gridDim.x, r = a.rank, n = a.nranks;
   const uint32_t e = a.state[b] + 1;
-  const size_t part = ((a.bytes / nb) + 15) & ~(size_t)15;
+  const size_t part = (((a.bytes + nb - 1) / nb) + 15) & ~(size_t)15;  // covers the slice
   const size_t lo = min(a.bytes, (size_t)b * part), hi = min(a.bytes, lo + part);
   char* ucd = a.uc + kNvlsFlagBytes;
   char* mcd = a.mc + kNvlsFlagBytes;

@@ -45,6 +45,7 @@ struct NvlsArgs {
   size_t bytes;     // message bytes per rank (a multiple of 16 * nranks for the vector path)
   uint32_t* abort_word;
   long long spin_limit;
+  char* peers[kMaxRanks];  // FLX_NVLS_EMULATE only: every rank's buffer (unicast, one GPU)
 };
 
 // data other ranks wrote during this kernel: bypass L1
@@ -106,6 +107,46 @@ __device__ __forceinline__ void mm_st(char* mc, const uint4& v) {
                : "memory");
 }
 
+// The three multicast operations the kernels use, on byte offset `o` of the
+// data area (after kNvlsFlagBytes) or arrive word `word`.
+#ifdef FLX_NVLS_EMULATE
+// tools/nvls_emulate.cu: every rank on ONE GPU (cooperative launch) and each
+// multimem operation replaced by its unicast equivalent over every rank's
+// buffer — the reduction in rank order (the switch's order is unspecified).
+// It runs this file's partitioning, epochs, barriers and staging on a GPU that
+// is in no multicast fabric; the multimem instructions themselves need one.
+__device__ __forceinline__ void nvls_arrive(const NvlsArgs& a, size_t word) {
+  for (int q = 0; q < a.nranks; ++q)
+    asm volatile("red.release.sys.global.add.u32 [%0], %1;" ::"l"(
+                     reinterpret_cast<uint32_t*>(a.peers[q]) + word),
+                 "r"(1u)
+                 : "memory");
+}
+template <typename T>
+__device__ __forceinline__ uint4 nvls_reduce(const NvlsArgs& a, size_t o) {
+  typename AccT<T>::type acc[16 / sizeof(T)];
+  load_acc<T>(acc, ld_cg_nvls(a.peers[0] + kNvlsFlagBytes + o));
+  for (int q = 1; q < a.nranks; ++q)
+    fold_into<T, kSum>(acc, ld_cg_nvls(a.peers[q] + kNvlsFlagBytes + o));
+  return pack_acc<T>(acc);
+}
+__device__ __forceinline__ void nvls_store(const NvlsArgs& a, size_t o, const uint4& v) {
+  for (int q = 0; q < a.nranks; ++q)
+    *reinterpret_cast<uint4*>(a.peers[q] + kNvlsFlagBytes + o) = v;
+}
+#else
+__device__ __forceinline__ void nvls_arrive(const NvlsArgs& a, size_t word) {
+  mm_red_add_release(reinterpret_cast<uint32_t*>(a.mc) + word, 1u);
+}
+template <typename T>
+__device__ __forceinline__ uint4 nvls_reduce(const NvlsArgs& a, size_t o) {
+  return mm_ld_reduce_sum<T>(a.mc + kNvlsFlagBytes + o);
+}
+__device__ __forceinline__ void nvls_store(const NvlsArgs& a, size_t o, const uint4& v) {
+  mm_st(a.mc + kNvlsFlagBytes + o, v);
+}
+#endif
+
 // CTA-wide NVLS barrier on word `w` (CTA b's arrive word of one kind): +1 on
 // every rank through the multicast mapping, then wait for my copy to reach
 // target.  false: timed out / aborted.
@@ -113,7 +154,7 @@ __device__ __forceinline__ bool nvls_barrier(const NvlsArgs& a, size_t word, uin
   __shared__ int ok;
   __syncthreads();  // this CTA's prior stores (incl. multimem.st) before the release
   if (threadIdx.x == 0) {
-    mm_red_add_release(reinterpret_cast<uint32_t*>(a.mc) + word, 1u);
+    nvls_arrive(a, word);
     const uint32_t* mine = reinterpret_cast<const uint32_t*>(a.uc) + word;
     const long long t0 = clock64();
     int good = 1;
@@ -133,14 +174,13 @@ __device__ __forceinline__ bool nvls_barrier(const NvlsArgs& a, size_t word, uin
 }
 
 template <typename T>
-__global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_constant__ NvlsArgs a) {
+__device__ __forceinline__ void nvls_allreduce_body(const NvlsArgs& a) {
   const int b = blockIdx.x, nb = gridDim.x, r = a.rank, n = a.nranks;
   const uint32_t e = a.state[b] + 1;  // this CTA's call epoch (identical on every rank)
   const size_t chunk = a.bytes / n;   // 16 B multiple (host guarantees)
   const size_t part = (((chunk + nb - 1) / nb) + 15) & ~(size_t)15;  // covers the chunk
   const size_t lo = min(chunk, (size_t)b * part), hi = min(chunk, lo + part);
   char* ucd = a.uc + kNvlsFlagBytes;
-  char* mcd = a.mc + kNvlsFlagBytes;
   // 1 stage my message (part b of every chunk) into the multicast-bound buffer
   for (int c = 0; c < n; ++c)
     for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x) {
@@ -151,7 +191,7 @@ __global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_con
   // 3 the switch sums part b of chunk r over every rank and writes it back to all
   for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x) {
     const size_t o = (size_t)r * chunk + v;
-    mm_st(mcd + o, mm_ld_reduce_sum<T>(mcd + o));
+    nvls_store(a, o, nvls_reduce<T>(a, o));
   }
   if (!nvls_barrier(a, kNvlsCtas + b, (uint32_t)n * e)) return;
   // 5 land every reduced chunk (part b) in recv
@@ -163,6 +203,11 @@ __global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_con
   if (threadIdx.x == 0) a.state[b] = e;
 }
 
+template <typename T>
+__global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_constant__ NvlsArgs a) {
+  nvls_allreduce_body<T>(a);
+}
+
 // NVLS AllGather: one multimem.st puts my slice into EVERY rank's buffer (the
 // switch replicates it), so each GPU sends its S bytes once instead of N-1
 // times.  a.bytes = per-rank send bytes (16 B multiple); the buffer holds N
@@ -171,17 +216,14 @@ __global__ void __launch_bounds__(512, 2) nvls_allreduce_kernel(const __grid_con
 //   2 barrier: every rank's part b landed everywhere
 //   3 land part b of every block from my buffer into recv
 //   4 barrier: every rank finished landing before anyone's next call stores
-template <int UNUSED = 0>
-__global__ void __launch_bounds__(512, 2) nvls_allgather_kernel(const __grid_constant__ NvlsArgs a,
-                                                                 size_t stride) {
+static __device__ __forceinline__ void nvls_allgather_body(const NvlsArgs& a, size_t stride) {
   const int b = blockIdx.x, nb = gridDim.x, r = a.rank, n = a.nranks;
   const uint32_t e = a.state[b] + 1;
   const size_t part = (((a.bytes + nb - 1) / nb) + 15) & ~(size_t)15;  // covers the slice
   const size_t lo = min(a.bytes, (size_t)b * part), hi = min(a.bytes, lo + part);
   char* ucd = a.uc + kNvlsFlagBytes;
-  char* mcd = a.mc + kNvlsFlagBytes;
   for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x)
-    mm_st(mcd + (size_t)r * a.bytes + v, ld_stream(a.send + v));
+    nvls_store(a, (size_t)r * a.bytes + v, ld_stream(a.send + v));
   if (!nvls_barrier(a, b, (uint32_t)n * e)) return;
   for (int c = 0; c < n; ++c)
     for (size_t v = lo + 16 * threadIdx.x; v < hi; v += 16 * blockDim.x)
@@ -190,5 +232,26 @@ __global__ void __launch_bounds__(512, 2) nvls_allgather_kernel(const __grid_con
   if (!nvls_barrier(a, kNvlsCtas + b, (uint32_t)n * e)) return;
   if (threadIdx.x == 0) a.state[b] = e;
 }
+
+template <int UNUSED = 0>
+__global__ void __launch_bounds__(512, 2) nvls_allgather_kernel(const __grid_constant__ NvlsArgs a,
+                                                                 size_t stride) {
+  nvls_allgather_body(a, stride);
+}
+
+#ifdef FLX_NVLS_EMULATE
+// every rank's CTAs in one cooperative grid (blockIdx.y = rank)
+struct NvlsLoopArgs {
+  NvlsArgs r[kMaxRanks];
+};
+template <typename T>
+__global__ void __launch_bounds__(512, 2) nvls_allreduce_loop_kernel(const __grid_constant__ NvlsLoopArgs la) {
+  nvls_allreduce_body<T>(la.r[blockIdx.y]);
+}
+__global__ void __launch_bounds__(512, 2) nvls_allgather_loop_kernel(const __grid_constant__ NvlsLoopArgs la,
+                                                                      size_t stride) {
+  nvls_allgather_body(la.r[blockIdx.y], stride);
+}
+#endif
 
 }  // namespace flx

@@ -422,3 +422,40 @@ def test_group_call_with_one_stream_per_rank(loopback):
             torch.cuda.synchronize()
             want = float(sum(i + 1 + it for i in range(n))) * count
             assert all(float(s) == want for s in sums), (it, [float(s) for s in sums], want)
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_group_with_several_collectives_per_rank(loopback):
+    # NCCL allows several collectives between ncclGroupStart and ncclGroupEnd;
+    # they run in issue order per rank (AllReduce, then an AllGather of its
+    # result on the same stream, then a ReduceScatter), and a rank that issues a
+    # different collective than rank 0 in the same slot is refused
+    n, count = 4, (1 << 16) + 8
+    L = flx.load_library()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    xs = [torch.randint(-9, 10, (count,), device="cuda", generator=g).float() for _ in range(n)]
+    red = [torch.empty(count, device="cuda") for _ in range(n)]
+    gat = [torch.empty(n * count, device="cuda") for _ in range(n)]
+    rs = [torch.empty(count // n, device="cuda") for _ in range(n)]
+    with flx.Clique(n, loopback=loopback) as c:
+        for op in (CollectiveOp.ALLREDUCE, CollectiveOp.ALLGATHER, CollectiveOp.REDUCESCATTER):
+            c.set_shares(op, (900, 100, 0))
+        assert L.flxGroupStart() == 0
+        for i, comm_i in enumerate(c.comms):
+            comm_i.all_reduce(xs[i], red[i])
+            comm_i.all_gather(red[i], gat[i])
+            comm_i.reduce_scatter(xs[i], rs[i])
+        assert L.flxGroupEnd() == 0
+        torch.cuda.synchronize()
+        total = torch.stack(xs).sum(0)
+        for i in range(n):
+            assert torch.equal(red[i], total), i
+            assert torch.equal(gat[i], total.repeat(n)), i
+            assert torch.equal(rs[i], total[i * (count // n):(i + 1) * (count // n)]), i
+        assert L.flxGroupStart() == 0
+        for i, comm_i in enumerate(c.comms):
+            if i == 1:
+                comm_i.all_gather(red[i], gat[i])
+            else:
+                comm_i.all_reduce(xs[i], red[i])
+        assert L.flxGroupEnd() == 5  # flxInvalidUsage (== ncclInvalidUsage): nothing launched

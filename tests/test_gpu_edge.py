@@ -43,3 +43,27 @@ def test_zero_length_calls_then_a_normal_one(loopback):
     for k in range(n):
         assert torch.equal(r[k], want), k
         assert torch.equal(out[k], torch.cat(s)), k
+
+
+def test_interleaved_communicators_on_one_gpu():
+    # two multi-rank worlds (loopback) and a virtual-rank clique alive at once,
+    # calls interleaved: per-world scratch, flags, epochs and tuner state never
+    # cross, and every result is exact
+    n, count = 4, (1 << 20) + 4
+    g = torch.Generator(device="cuda").manual_seed(9)
+    with flx.Clique(n, loopback=True) as a, flx.Clique(n, loopback=True) as b, \
+            flx.Clique(n) as v:
+        for c in (a, b, v):
+            c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        for it in range(4):
+            data = {}
+            for name, c in (("a", a), ("b", b), ("v", v)):
+                s = [torch.randint(-99, 100, (count + it,), device="cuda", generator=g).float()
+                     for _ in range(n)]
+                r = [torch.empty_like(x) for x in s]
+                c.all_reduce(s, r)
+                data[name] = (s, r)
+            torch.cuda.synchronize()
+            for name, (s, r) in data.items():
+                want = torch.stack(s).sum(0)
+                assert all(torch.equal(x, want) for x in r), (it, name)

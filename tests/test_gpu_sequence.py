@@ -56,7 +56,8 @@ def test_random_sequence_on_one_communicator(loopback, n):
     with c:
         calls = int(os.environ.get("FLX_SEQ_CALLS", "80"))  # soak runs raise it
         for i, (coll, dtype, op, count, g, inplace, untimed) in enumerate(
-                _plan(7 + 2 * loopback + n, calls)):
+                _plan(7 + 2 * loopback + n + 1000 * int(os.environ.get("FLX_SEQ_SEED", "0")),
+                      calls)):
             c.set_shares(CollectiveOp(coll), g)
             c.set_timing(not untimed)
             align = c.comms[0].alignment(CollectiveOp(coll))

@@ -17,8 +17,10 @@
 #include <cstring>
 #include <mutex>
 #include <random>
+#include <vector>
 
 #include "internal.h"
+#include "rank_launch.h"
 #include "args.h"
 #include "autotune.h"
 
@@ -59,6 +61,73 @@ const MemOps& memops() {
     }
   });
   return ops;
+}
+
+// ---------------------------------------------------- kernel preloading
+namespace {
+struct ModuleOps {
+  CUresult (*get_module)(CUmodule*, CUfunction) = nullptr;
+  CUresult (*count)(unsigned int*, CUmodule) = nullptr;
+  CUresult (*enumerate)(CUfunction*, unsigned int, CUmodule) = nullptr;
+  CUresult (*load)(CUfunction) = nullptr;
+  bool ok = false;
+};
+template <typename F>
+bool driver_entry(const char* name, F* out) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  *out = reinterpret_cast<F>(p);
+  return true;
+}
+const ModuleOps& module_ops() {
+  static ModuleOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    ops.ok = driver_entry("cuFuncGetModule", &ops.get_module) &&
+             driver_entry("cuModuleGetFunctionCount", &ops.count) &&
+             driver_entry("cuModuleEnumerateFunctions", &ops.enumerate) &&
+             driver_entry("cuFuncLoad", &ops.load);
+  });
+  return ops;
+}
+}  // namespace
+
+cudaError_t preload_module(const void* kernel) {
+  cudaFunction_t fn = nullptr;
+  cudaError_t e = cudaGetFuncBySymbol(&fn, kernel);  // loads this kernel
+  if (e != cudaSuccess) return e;
+  const ModuleOps& m = module_ops();
+  if (!m.ok) return cudaSuccess;  // older driver: first launches load lazily
+  CUmodule mod = nullptr;
+  unsigned int n = 0;
+  if (m.get_module(&mod, reinterpret_cast<CUfunction>(fn)) != CUDA_SUCCESS ||
+      m.count(&n, mod) != CUDA_SUCCESS)
+    return cudaErrorUnknown;
+  std::vector<CUfunction> fns(n);
+  if (n && m.enumerate(fns.data(), n, mod) != CUDA_SUCCESS) return cudaErrorUnknown;
+  for (CUfunction f : fns)
+    if (m.load(f) != CUDA_SUCCESS) return cudaErrorUnknown;
+  return cudaSuccess;
+}
+
+cudaError_t preload_all_kernels() {
+  static std::mutex mu;
+  static uint64_t done = 0;  // bit per device ordinal
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  const uint64_t bit = 1ull << (dev & 63);
+  if (done & bit) return cudaSuccess;
+  for (cudaError_t (*f)() : {preload_launch_cu, preload_world_cu, preload_nvls_cu, preload_rank_i8,
+                             preload_rank_i32, preload_rank_i64, preload_rank_f16,
+                             preload_rank_f32, preload_rank_f64})
+    if ((e = f()) != cudaSuccess) return e;
+  done |= bit;
+  return cudaSuccess;
 }
 
 // Counter semaphores on pinned host words.  GEQ is the cyclic 32-bit
@@ -176,6 +245,7 @@ flxResult_t clique_create(int device, int members, Clique** out) {
   if (prop.major < 10)
     return fail(flxInvalidUsage, "device %d is sm_%d%d; this build targets sm_100a", device,
                 prop.major, prop.minor);
+  FLX_CUDA(preload_all_kernels());  // first launches never wait on a lazy module load
   auto* c = new Clique();
   c->device = device;
   c->sm_count = prop.multiProcessorCount;

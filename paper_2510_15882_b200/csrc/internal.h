@@ -50,6 +50,20 @@ struct MemOps {
   bool ok = false;
 };
 const MemOps& memops();
+// Load every kernel of the module that contains `kernel` (one module per
+// translation unit) into the current device's context.  CUDA's lazy loading
+// otherwise loads a kernel at its first launch, and that load waits behind
+// work already queued on the device — a PCIe leg parked on a peer's token, a
+// rank kernel spinning on a peer — so a first launch could block the host
+// thread (and a cudaFuncSetAttribute at launch time likewise).  NCCL does the
+// same at init (cudaFuncGetAttributes on its kernels).
+cudaError_t preload_module(const void* kernel);
+// Every module of libflexlink on the current device, once per device.
+cudaError_t preload_all_kernels();
+// per-translation-unit anchors (each loads its own module)
+cudaError_t preload_launch_cu();
+cudaError_t preload_world_cu();
+cudaError_t preload_nvls_cu();
 flxResult_t sem_wait_geq(cudaStream_t s, uint32_t* word, uint32_t value);
 flxResult_t sem_wait_eq(cudaStream_t s, uint32_t* word, uint32_t value);
 flxResult_t sem_write(cudaStream_t s, uint32_t* word, uint32_t value);

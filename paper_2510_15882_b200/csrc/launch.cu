@@ -218,4 +218,8 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t preload_launch_cu() {
+  return preload_module((const void*)fold_once_kernel<float, kSum, 8>);
+}
+
 }  // namespace flx

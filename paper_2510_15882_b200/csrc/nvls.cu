@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "args.h"
+#include "internal.h"
 #include "nvls.h"
 #include "nvls_kernels.cuh"
 
@@ -274,6 +275,10 @@ cudaError_t launch_nvls_allreduce(int dtype, const void* args, int nctas, cudaSt
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
+}
+
+cudaError_t preload_nvls_cu() {
+  return preload_module((const void*)nvls_allgather_kernel<0>);
 }
 
 }  // namespace flx

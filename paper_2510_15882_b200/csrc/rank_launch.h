@@ -39,6 +39,13 @@ cudaError_t rank_reduce_f32(int dtype, int op, bool scatter, bool loop, const vo
                             int n, cudaStream_t s);
 cudaError_t rank_reduce_f64(int dtype, int op, bool scatter, bool loop, const void* a, int nctas,
                             int n, cudaStream_t s);
+// each rank_launch_*.cu loads its module (see preload_module in internal.h)
+cudaError_t preload_rank_i8();
+cudaError_t preload_rank_i32();
+cudaError_t preload_rank_i64();
+cudaError_t preload_rank_f16();
+cudaError_t preload_rank_f32();
+cudaError_t preload_rank_f64();
 // CTAs of the loopback AllReduce kernel that fit one SM (co-residency bound)
 int loopback_blocks_per_sm();
 

@@ -1,5 +1,6 @@
 // Reducing rank kernels for float (see rank_launch.h).
 #include "../../include/flexlink.h"
+#include "internal.h"
 #include "rank_launch_impl.cuh"
 
 namespace flx {
@@ -20,6 +21,10 @@ int loopback_blocks_per_sm() {
                                                     512, kRankDynSmem) != cudaSuccess)
     return 1;
   return per_sm > 0 ? per_sm : 1;
+}
+
+cudaError_t preload_rank_f32() {
+  return preload_module((const void*)rank_allreduce_kernel<float, kSum>);
 }
 
 }  // namespace flx

@@ -38,6 +38,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <thread>
 
 #include "autotune.h"
@@ -124,6 +125,9 @@ struct World {
   size_t host_bytes = 0;
   bool host_shm = false;
   uint32_t* abort_word = nullptr;  // pinned, mapped
+  // per local rank i: [2i] = PCIe legs started, [2i+1] = PCIe legs finished,
+  // written by the rank's h2d stream (same pinned block as abort_word)
+  uint32_t* progress = nullptr;
   struct Local {
     Comm* comm = nullptr;
     int rank = 0;
@@ -139,10 +143,15 @@ struct World {
     Clique::Timing timing[Clique::kTimingSlots];
     uint64_t calls = 0;
     std::array<size_t, FLX_NUM_PATHS> last_bytes{{0, 0, 0}};
-    // PCIe-leg watchdog (flxCommGetAsyncError): the last call with a PCIe
-    // slice, its completion event and when it was issued
-    cudaEvent_t pcie_watch = nullptr;
-    std::chrono::steady_clock::time_point pcie_issued{};
+    // PCIe-leg watchdog (flxCommGetAsyncError): PCIe legs issued (host count,
+    // release-published); the h2d stream itself writes the leg's number into
+    // World::progress when the leg starts and when it ends, so the watchdog
+    // tells a leg that is running from one still queued behind user work
+    uint32_t pcie_gen = 0;
+    // the watchdog's own view (guarded by World::watch_mu): the running leg it
+    // last saw and when it first saw it running
+    uint32_t seen_leg = 0;
+    std::chrono::steady_clock::time_point seen_started{};
     // scratch/flags are CUDA-IPC mappings of another process's allocation
     // (flxCommInitLoopbackIpc): closed, not freed
     bool remote_mem = false;
@@ -158,6 +167,7 @@ struct World {
   bool shared_gpu = false;  // ranks share a GPU (bootstrap self-tests): no NVLink-path tuning
   uint64_t agree_seq = 0;   // decision points agreed so far (same on every rank)
   AutoTuner tuner;
+  std::mutex watch_mu;  // world_aborted's watchdog state (callers may be threads)
   NvlsBuffer nvls;          // NVLink-SHARP multicast buffer (FLX_NVLS=1, multi-GPU only)
   void* ipc_debug = nullptr;  // flxCommInitLoopbackIpc: the exporter's segment
 
@@ -186,6 +196,7 @@ flxResult_t alloc_rank_mem(const World* w, char** scratch, uint32_t** flags) {
 
 flxResult_t local_init(World* w, World::Local& L) {
   FLX_CUDA(cudaSetDevice(L.device));
+  FLX_CUDA(preload_all_kernels());  // no lazy load behind a parked PCIe leg / spinning kernel
   int khz = 0;
   FLX_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, L.device));
   const char* to = getenv("FLX_TIMEOUT_S");
@@ -345,9 +356,11 @@ flxResult_t alloc_host_staging(World* w, const char* shm_name) {
   void* dev = nullptr;
   FLX_CUDA(cudaHostGetDevicePointer(&dev, w->host, 0));
   w->host_dev = static_cast<char*>(dev);
-  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->abort_word), 64,
+  FLX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&w->abort_word), 64 + 8 * kMaxRanks,
                          cudaHostAllocMapped | cudaHostAllocPortable));
   *w->abort_word = 0;
+  w->progress = w->abort_word + 16;
+  memset(w->progress, 0, 8 * kMaxRanks);
   return flxSuccess;
 }
 
@@ -536,6 +549,8 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
       World::Local& L = w->local[i];
       FLX_CUDA(cudaStreamWaitEvent(L.d2h, ev_start, 0));
       FLX_CUDA(cudaStreamWaitEvent(L.h2d, ev_start, 0));
+      if (!capturing)  // the leg has started (user work before the call is done)
+        FLX_TRY(sem_write(L.h2d, &w->progress[2 * i], L.pcie_gen + 1));
     }
     const bool ar = !gather && !scatter && !a2a;
     const size_t q = ar ? pc / n : pc;  // bytes per reader (AR sub-chunk / RS, A2A block part)
@@ -650,9 +665,10 @@ flxResult_t run_world(World* w, const std::vector<const void*>& send,
     }
     for (int i = 0; i < nl; ++i) {
       FLX_CUDA(cudaEventRecord(ev_pcie(i), w->local[i].h2d));
-      if (!capturing) {
-        w->local[i].pcie_watch = ev_pcie(i);
-        w->local[i].pcie_issued = std::chrono::steady_clock::now();
+      if (!capturing) {  // the leg has finished; publish it as issued
+        World::Local& L = w->local[i];
+        FLX_TRY(sem_write(L.h2d, &w->progress[2 * i + 1], L.pcie_gen + 1));
+        __atomic_store_n(&L.pcie_gen, L.pcie_gen + 1, __ATOMIC_RELEASE);
       }
     }
   }
@@ -793,15 +809,26 @@ const char* world_nvls_status(World* w, int* on) {
 bool world_aborted(World* w) {
   if (*(volatile uint32_t*)w->abort_word != 0) return true;
   // PCIe-leg watchdog: copy-engine waits on a dead peer's tokens never time
-  // out by themselves; a PCIe slice still pending FLX_TIMEOUT_S after it was
-  // issued is reported (and aborts the world, like a timed-out NVLink wait)
-  for (auto& L : w->local) {
-    if (!L.pcie_watch) continue;
-    cudaSetDevice(L.device);
-    if (cudaEventQuery(L.pcie_watch) != cudaErrorNotReady) continue;
-    const double waited =
-        std::chrono::duration<double>(std::chrono::steady_clock::now() - L.pcie_issued).count();
-    if (waited > w->timeout_s) {
+  // out by themselves.  A PCIe leg that has STARTED on the GPU (its h2d stream
+  // got past the caller's earlier work) and is still unfinished FLX_TIMEOUT_S
+  // after this watchdog first saw it running is reported, and aborts the
+  // world like a timed-out NVLink wait.  Time queued behind the caller's own
+  // kernels never counts; legs run in issue order on the h2d stream, so
+  // started - finished is 0 (idle or queued) or 1 (leg `started` running).
+  std::lock_guard<std::mutex> lock(w->watch_mu);
+  const auto now = std::chrono::steady_clock::now();
+  for (size_t i = 0; i < w->local.size(); ++i) {
+    World::Local& L = w->local[i];
+    const uint32_t issued = __atomic_load_n(&L.pcie_gen, __ATOMIC_ACQUIRE);
+    const uint32_t finished = __atomic_load_n(&w->progress[2 * i + 1], __ATOMIC_ACQUIRE);
+    const uint32_t started = __atomic_load_n(&w->progress[2 * i], __ATOMIC_ACQUIRE);
+    if (finished == issued || started == finished) continue;  // idle, or next leg queued
+    if (L.seen_leg != started) {  // first sight of this leg running
+      L.seen_leg = started;
+      L.seen_started = now;
+      continue;
+    }
+    if (std::chrono::duration<double>(now - L.seen_started).count() > w->timeout_s) {
       *(volatile uint32_t*)w->abort_word = 1;
       return true;
     }
@@ -1202,6 +1229,10 @@ int world_release(World* w) {
   if (++w->destroyed < (int)w->local.size()) return 0;
   world_free(w);
   return 1;
+}
+
+cudaError_t preload_world_cu() {
+  return preload_module((const void*)rank_allgather_kernel);
 }
 
 }  // namespace flx

@@ -123,3 +123,57 @@ def test_pcie_leg_waiting_on_a_dead_peer_is_reported_and_aborts():
                 p.kill()
     assert err == 3, err  # flxInternalError == ncclInternalError
     assert 0.9 < waited < 10, waited
+
+
+def _park(stream, word_ptr):
+    """Enqueue a wait on `stream` for a pinned host word to become 1."""
+    import cuda.bindings.driver as drv
+
+    (r,) = drv.cuStreamWaitValue32(drv.CUstream(stream.cuda_stream), drv.CUdeviceptr(word_ptr), 1,
+                                   drv.CUstreamWaitValue_flags.CU_STREAM_WAIT_VALUE_EQ)
+    assert r == drv.CUresult.CUDA_SUCCESS, r
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_first_launches_do_not_block_behind_a_parked_stream(loopback):
+    """With another stream of the device parked on a host word (as a PCIe leg
+    parks on a late peer's token), the first launch of every kernel a
+    collective uses — fold / fan-out kernels, the rank kernels with their
+    dynamic-shared-memory opt-in — returns to the host at once: communicator
+    init preloaded every module, so no lazy load waits behind the parked work."""
+    import threading
+
+    n, count = 4, (1 << 16) + 3
+    with flx.Clique(n, loopback=loopback) as c:
+        for op in CollectiveOp:
+            c.set_shares(op, (1000, 0, 0))
+        g = torch.Generator(device="cuda").manual_seed(9)
+        outs = {}
+        for dt in (torch.float64, torch.bfloat16, torch.int32):  # first use of each
+            s = [torch.randint(-9, 9, (count,), device="cuda", generator=g).to(dt)
+                 for _ in range(n)]
+            outs[dt] = (s, [torch.empty_like(x) for x in s],
+                        [torch.empty(n * count, device="cuda", dtype=dt) for _ in range(n)])
+        torch.cuda.synchronize()  # inputs ready; only FlexLink launches from here on
+        word = torch.zeros(1, dtype=torch.int32).pin_memory()
+        parked = torch.cuda.Stream()
+        _park(parked, word.data_ptr())
+        done = threading.Event()
+
+        def issue():
+            for s, r, gat in outs.values():
+                c.all_reduce(s, r)
+                c.all_gather(s, gat)
+            done.set()
+
+        t = threading.Thread(target=issue, daemon=True)
+        t.start()
+        returned = done.wait(timeout=20)
+        word.fill_(1)  # release the parked stream (the host word is pinned)
+        t.join(timeout=60)
+        torch.cuda.synchronize()
+        assert returned, "a first launch blocked behind the parked stream"
+        for dt, (s, r, gat) in outs.items():
+            want = torch.stack([x.double() for x in s]).sum(0).to(dt)
+            assert all(torch.equal(x, want) for x in r), dt
+            assert all(torch.equal(x, torch.cat(s)) for x in gat), dt

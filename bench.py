@@ -1229,6 +1229,7 @@ def main() -> None:
     # (a smoke test of run_multi_gpu on a 1-GPU box)
     if world > 1 or os.environ.get("FLX_BENCH_MULTI") == "1":
         os.environ.setdefault("FLX_BOOT_TIMEOUT", "60")
+        os.environ.setdefault("FLX_TIMEOUT_S", "60")  # a stalled peer ends the run, not 10 min
         try:
             run_multi_gpu(args)
         except Exception as e:  # report, do not hang the job

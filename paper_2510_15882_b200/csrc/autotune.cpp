@@ -55,7 +55,10 @@ double round_target_ms() {
   return v;
 }
 constexpr int kMaxRepeats = 16;
-int stage2_lag() { static const int v = std::max(0, env_int("FLX_TUNE_LAG", 2)); return v; }
+// 8: a Stage-2 evaluation reads calls at least 8 behind the one being issued, so
+// the host blocks on their events only when it runs more than 8 collectives ahead
+// of the GPU (PyTorch's eager loop queues a layer or more ahead)
+int stage2_lag() { static const int v = std::max(0, env_int("FLX_TUNE_LAG", 8)); return v; }
 constexpr int kProbeGranules = 100;  // PCIe share of the rate-probe round
 constexpr size_t kMaxEvals = 256;
 

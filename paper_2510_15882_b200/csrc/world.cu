@@ -113,7 +113,11 @@ struct World {
   size_t slot = 0;       // inbox slot bytes per source rank
   size_t small_slot = 0;  // one-shot inbox bytes per source rank and parity
   long long spin_limit = 0;  // peer-wait limit in SM clock cycles (FLX_TIMEOUT_S)
-  double timeout_s = 10.0;   // FLX_TIMEOUT_S: peer waits and the PCIe-leg watchdog
+  // FLX_TIMEOUT_S: peer waits (kernel spins, the balancer's agreement board) and the
+  // PCIe-leg watchdog.  The default follows PyTorch's NCCL process-group timeout
+  // (10 min): ranks legitimately drift by seconds to minutes (a checkpoint save, an
+  // eval on rank 0), and NCCL waits that out rather than failing the collective
+  double timeout_s = 600.0;
   size_t oneshot_max = 0;  // AllReduce NVLink slices up to this size run one-shot (if they fit)
   bool ll = true;          // one-shot slices that fit kLLRegion / 2 per CTA use the LL format (FLX_LL)
   bool bulk = true;        // two-shot push / pull as TMA bulk copies (FLX_BULK=0: register copies)
@@ -200,7 +204,7 @@ flxResult_t local_init(World* w, World::Local& L) {
   int khz = 0;
   FLX_CUDA(cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, L.device));
   const char* to = getenv("FLX_TIMEOUT_S");
-  const double secs = to ? atof(to) : 10.0;
+  const double secs = to ? atof(to) : 600.0;
   w->spin_limit = (long long)(std::max(0.01, secs) * khz * 1e3);
   w->timeout_s = std::max(0.01, secs);
   if (!L.remote_mem) FLX_TRY(alloc_rank_mem(w, &L.scratch, &L.flags));
@@ -264,7 +268,7 @@ void world_free(World* w) {
   // a hung stream (cudaFree would block on it forever).
   bool drained = true;
   const bool aborted = w->aborting || (w->abort_word && *(volatile uint32_t*)w->abort_word);
-  if (aborted) drained = drain_streams(w, std::max(5.0, w->timeout_s), true);
+  if (aborted) drained = drain_streams(w, std::min(30.0, std::max(5.0, w->timeout_s)), true);
   if (drained)
     for (auto& L : w->local) {
       cudaSetDevice(L.device);

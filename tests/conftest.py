@@ -23,3 +23,6 @@ def oracle_lib():
 # Loopback worlds put 3 streams per emulated rank on one device; give every
 # stream its own hardware queue (must be set before CUDA initialises).
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# Peer waits give up after FLX_TIMEOUT_S (product default 600 s, PyTorch's NCCL
+# timeout); the suite fails fast instead if a protocol ever stalls.
+os.environ.setdefault("FLX_TIMEOUT_S", "30")

@@ -63,6 +63,38 @@ const MemOps& memops() {
   return ops;
 }
 
+// ------------------------------------------------------- context guard
+namespace {
+struct CtxOps {
+  CUresult (*get)(CUcontext*) = nullptr;
+  CUresult (*set)(CUcontext) = nullptr;
+};
+const CtxOps& ctx_ops() {
+  static CtxOps ops;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* g = nullptr;
+    void* s = nullptr;
+    cudaDriverEntryPointQueryResult q1, q2;
+    if (cudaGetDriverEntryPoint("cuCtxGetCurrent", &g, cudaEnableDefault, &q1) == cudaSuccess &&
+        cudaGetDriverEntryPoint("cuCtxSetCurrent", &s, cudaEnableDefault, &q2) == cudaSuccess &&
+        q1 == cudaDriverEntryPointSuccess && q2 == cudaDriverEntryPointSuccess) {
+      ops.get = reinterpret_cast<CUresult (*)(CUcontext*)>(g);
+      ops.set = reinterpret_cast<CUresult (*)(CUcontext)>(s);
+    }
+  });
+  return ops;
+}
+}  // namespace
+
+CtxGuard::CtxGuard() {
+  const CtxOps& o = ctx_ops();
+  ok = o.get && o.get(&saved) == CUDA_SUCCESS;
+}
+CtxGuard::~CtxGuard() {
+  if (ok) ctx_ops().set(saved);
+}
+
 // ---------------------------------------------------- kernel preloading
 namespace {
 struct ModuleOps {
@@ -914,6 +946,7 @@ const char* flxGetLastError(void) { return t_last_error.c_str(); }
 void flxSetLastError(const char* message) { t_last_error = message ? message : ""; }
 
 flxResult_t flxGetUniqueId(flxUniqueId* id) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   if (!id) return fail(flxInvalidArgument, "null id");
   memset(id, 0, sizeof(*id));
   std::random_device rd;
@@ -924,6 +957,7 @@ flxResult_t flxGetUniqueId(flxUniqueId* id) {
 }
 
 flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   {
     Granules g;
     bool set;
@@ -966,6 +1000,7 @@ flxResult_t flxCommInitAll(flxComm_t* comms, int ndev, const int* devlist) {
 }
 
 flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int rank) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   {
     Granules g;
     bool set;
@@ -1015,6 +1050,7 @@ void id_hex(const flxUniqueId& id, char hex[40]) {
 }  // namespace
 
 flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, double seconds) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   uint64_t magic;
   memcpy(&magic, id.internal, sizeof(magic));
   if (magic != 0x31584c46ull) return fail(flxInvalidArgument, "not a flxUniqueId");
@@ -1024,6 +1060,7 @@ flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, doub
 }
 
 flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flxUniqueId id) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   {
     Granules g;
     bool set;
@@ -1053,6 +1090,7 @@ flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flx
 }
 
 flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   {
     Granules g;
     bool set;
@@ -1085,6 +1123,7 @@ flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device) {
 }
 
 flxResult_t flxCommDestroy(flxComm_t comm) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   std::lock_guard<std::mutex> lock(g_mutex);
   if (comm->world) {
@@ -1106,6 +1145,7 @@ flxResult_t flxCommDestroy(flxComm_t comm) {
 }
 
 flxResult_t flxCommFinalize(flxComm_t comm) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (comm->world) return world_finalize(comm->world, comm->local);
   Clique* c = comm->clique;
@@ -1117,6 +1157,7 @@ flxResult_t flxCommFinalize(flxComm_t comm) {
 }
 
 flxResult_t flxCommAbort(flxComm_t comm) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   {
     std::lock_guard<std::mutex> lock(g_mutex);
@@ -1147,6 +1188,7 @@ flxResult_t flxCommCuDevice(const flxComm_t comm, int* device) {
 }
 
 flxResult_t flxCommGetAsyncError(flxComm_t comm, flxResult_t* async_error) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!async_error) return fail(flxInvalidArgument, "null async_error");
   *async_error = comm->world && world_aborted(comm->world) ? flxInternalError : flxSuccess;
@@ -1156,6 +1198,7 @@ flxResult_t flxCommGetAsyncError(flxComm_t comm, flxResult_t* async_error) {
 flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                          flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
                          cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(check_call(comm, datatype, op, true));
   if (count > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
   return enqueue(Call{comm, flxCollAllReduce, sendbuff, recvbuff, count, datatype, op, stream});
@@ -1163,6 +1206,7 @@ flxResult_t flxAllReduce(const void* sendbuff, void* recvbuff, size_t count,
 
 flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
                          flxDataType_t datatype, flxComm_t comm, cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(check_call(comm, datatype, 0, false));
   if (sendcount > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
   return enqueue(Call{comm, flxCollAllGather, sendbuff, recvbuff, sendcount, datatype, 0, stream});
@@ -1171,6 +1215,7 @@ flxResult_t flxAllGather(const void* sendbuff, void* recvbuff, size_t sendcount,
 flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
                              flxDataType_t datatype, flxRedOp_t op, flxComm_t comm,
                              cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(check_call(comm, datatype, op, true));
   if (recvcount > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
   return enqueue(
@@ -1179,6 +1224,7 @@ flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvco
 
 flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(check_call(comm, datatype, 0, false));
   if (count > 0 && (!sendbuff || !recvbuff)) return fail(flxInvalidArgument, "null buffer");
   if (count > 0 && sendbuff == recvbuff)
@@ -1193,6 +1239,7 @@ flxResult_t flxGroupCollective(flxCollOp_t coll, flxComm_t* comms, int n,
                                const void* const* sendbuffs, void* const* recvbuffs,
                                size_t count, flxDataType_t datatype, flxRedOp_t op,
                                cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   if (!comms || n < 1 || !sendbuffs || !recvbuffs)
     return fail(flxInvalidArgument, "bad group arguments");
   if (coll < flxCollAllReduce || coll > flxCollAllToAll)
@@ -1220,12 +1267,14 @@ flxResult_t flxGroupStart(void) {
 }
 
 flxResult_t flxGroupEnd(void) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   if (t_group_depth <= 0) return fail(flxInvalidUsage, "flxGroupEnd without flxGroupStart");
   if (--t_group_depth > 0) return flxSuccess;
   return flush_group();
 }
 
 flxResult_t flxSetShares(flxComm_t comm, flxCollOp_t op, int bucket, const int granules[3]) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (op < flxCollAllReduce || op > flxCollAllToAll)
     return fail(flxInvalidArgument, "bad collective op %d", (int)op);
@@ -1281,6 +1330,7 @@ flxResult_t flxGetShares(flxComm_t comm, flxCollOp_t op, int bucket, int granule
 }
 
 flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!ms) return fail(flxInvalidArgument, "null ms");
   if (comm->world) {
@@ -1294,6 +1344,7 @@ flxResult_t flxGetPathTimes(flxComm_t comm, float ms[3]) {
 }
 
 flxResult_t flxGetPathTimesHistory(flxComm_t comm, int max_calls, float* ms, int* n_out) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!ms || !n_out || max_calls < 0) return fail(flxInvalidArgument, "bad history arguments");
   const uint64_t calls =
@@ -1327,12 +1378,14 @@ flxResult_t flxGetAlignment(flxComm_t comm, flxCollOp_t op, size_t* alignment) {
 }
 
 flxResult_t flxSetTiming(flxComm_t comm, int enabled) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   comm->timing = enabled != 0;
   return flxSuccess;
 }
 
 flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (nctas < 0 || nctas > 65535) return fail(flxInvalidArgument, "bad nctas %d", nctas);
   if (comm->nvlink_ctas != nctas) tuner_of(comm)->reset();  // measured rates are void
@@ -1342,6 +1395,7 @@ flxResult_t flxSetNvlinkCtas(flxComm_t comm, int nctas) {
 }
 
 flxResult_t flxSetStaging(flxComm_t comm, size_t chunk_bytes, int buffers) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (buffers != 1 && buffers != 2)
     return fail(flxInvalidArgument, "buffers must be 1 or 2 (staging.py:41-42)");
@@ -1361,6 +1415,7 @@ flxResult_t flxGetPathMask(flxComm_t comm, int* mask) {
 
 flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int write, void* buf,
                              size_t bytes) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!comm->world) return fail(flxInvalidUsage, "not a multi-rank communicator");
   if (!buf && bytes) return fail(flxInvalidArgument, "null buffer");
@@ -1368,6 +1423,7 @@ flxResult_t flxCommDebugPeer(flxComm_t comm, int peer, int host_region, int writ
 }
 
 flxResult_t flxCommGetNvls(flxComm_t comm, int* on, char* reason, size_t reason_len) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!on) return fail(flxInvalidArgument, "null on");
   const char* why = "NVLS needs a multi-GPU world (one process per GPU, FLX_NVLS=1)";
@@ -1389,6 +1445,7 @@ flxResult_t flxGetLaunchCount(unsigned long long* count) {
 extern "C" {
 
 flxResult_t flxSetAutoTune(flxComm_t comm, int enabled) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   comm->autotune = enabled != 0;
   return flxSuccess;
@@ -1396,6 +1453,7 @@ flxResult_t flxSetAutoTune(flxComm_t comm, int enabled) {
 
 flxResult_t flxSetTunerConfig(flxComm_t comm, const flxTunerConfig* s1,
                               const flxBalancerConfig* s2, size_t min_bytes) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (s1 && !tune::valid(*s1)) return fail(flxInvalidArgument, "bad tuner config");
   if (s2 && (!tune::valid(*s2) || s2->window > 32))
@@ -1408,6 +1466,7 @@ flxResult_t flxSetTunerConfig(flxComm_t comm, const flxTunerConfig* s1,
 }
 
 flxResult_t flxSetLinkProfile(flxComm_t comm, const flxLinkProfile* profile) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (profile && !(profile->bandwidth[flxPathNvlink] > 0))
     return fail(flxInvalidArgument, "the link profile needs a positive NVLink bandwidth");

@@ -43,6 +43,20 @@ flxResult_t fail(flxResult_t code, const char* fmt, ...) __attribute__((format(p
     if (r_ != flxSuccess) return r_;   \
   } while (0)
 
+// ---- the caller's CUDA context is restored on return (NCCL's rule): entry
+// points switch devices internally (cudaSetDevice) — a multi-device process, or
+// a thread that never touched CUDA (a framework's watchdog), must find its
+// current context unchanged afterwards, and no context is left bound on a device
+// the caller never used
+struct CtxGuard {
+  CUcontext saved = nullptr;
+  bool ok = false;
+  CtxGuard();
+  ~CtxGuard();
+  CtxGuard(const CtxGuard&) = delete;
+  CtxGuard& operator=(const CtxGuard&) = delete;
+};
+
 // ---- driver stream memory ops (resolved at run time; no -lcuda)
 struct MemOps {
   CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;

@@ -291,6 +291,7 @@ extern "C" {
 // one-device object (ld_reduce over one rank returns the data itself) checked
 // end to end: *available = 1 and reason "ok: ..." or 0 and why not.
 flxResult_t flxNvlsProbe(int device, int* available, char* reason, size_t reason_len) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   if (!available) return fail(flxInvalidArgument, "null available");
   *available = 0;
   NvlsBuffer nb;

@@ -67,3 +67,43 @@ def test_interleaved_communicators_on_one_gpu():
             for name, (s, r) in data.items():
                 want = torch.stack(s).sum(0)
                 assert all(torch.equal(x, want) for x in r), (it, name)
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_entry_points_restore_the_callers_context(loopback):
+    """NCCL's rule: a call leaves the caller's current CUDA context as it found
+    it.  The entry points switch devices internally (cudaSetDevice); a thread
+    that never touched CUDA — a framework's watchdog thread reading path times
+    or async errors — must still have no context bound afterwards."""
+    import threading
+
+    import cuda.bindings.driver as drv
+
+    def current():
+        r, ctx = drv.cuCtxGetCurrent()
+        assert r == drv.CUresult.CUDA_SUCCESS
+        return int(ctx) if ctx is not None else 0
+
+    n, count = 4, (1 << 16) + 5
+    with flx.Clique(n, loopback=loopback) as c:
+        c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        s = [torch.ones(count, device="cuda") for _ in range(n)]
+        r = [torch.empty_like(x) for x in s]
+        before = current()
+        c.all_reduce(s, r)
+        assert current() == before != 0
+        torch.cuda.synchronize()
+        seen = {}
+
+        def watchdog():
+            seen["start"] = current()
+            seen["times"] = c.comms[0].path_times()
+            seen["err"] = c.comms[0].async_error()
+            seen["end"] = current()
+
+        t = threading.Thread(target=watchdog)
+        t.start()
+        t.join()
+        assert seen["start"] == 0 and seen["end"] == 0, seen
+        assert seen["err"] == 0 and seen["times"][0] > 0
+        assert all(torch.equal(x, torch.full_like(x, n)) for x in r)

@@ -946,7 +946,6 @@ const char* flxGetLastError(void) { return t_last_error.c_str(); }
 void flxSetLastError(const char* message) { t_last_error = message ? message : ""; }
 
 flxResult_t flxGetUniqueId(flxUniqueId* id) {
-  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   if (!id) return fail(flxInvalidArgument, "null id");
   memset(id, 0, sizeof(*id));
   std::random_device rd;
@@ -1188,7 +1187,6 @@ flxResult_t flxCommCuDevice(const flxComm_t comm, int* device) {
 }
 
 flxResult_t flxCommGetAsyncError(flxComm_t comm, flxResult_t* async_error) {
-  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
   FLX_TRY(validate_comm(comm));
   if (!async_error) return fail(flxInvalidArgument, "null async_error");
   *async_error = comm->world && world_aborted(comm->world) ? flxInternalError : flxSuccess;

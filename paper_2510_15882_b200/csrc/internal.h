@@ -47,7 +47,9 @@ flxResult_t fail(flxResult_t code, const char* fmt, ...) __attribute__((format(p
 // points switch devices internally (cudaSetDevice) — a multi-device process, or
 // a thread that never touched CUDA (a framework's watchdog), must find its
 // current context unchanged afterwards, and no context is left bound on a device
-// the caller never used
+// the caller never used.  Entry points that never touch CUDA (flxGetUniqueId,
+// flxCommGetAsyncError) take no guard: its driver lookup initialises CUDA, and
+// ncclGetUniqueId must stay fork-safe (a parent makes the id, then forks ranks)
 struct CtxGuard {
   CUcontext saved = nullptr;
   bool ok = false;

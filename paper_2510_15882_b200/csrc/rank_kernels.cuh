@@ -155,7 +155,7 @@ __device__ __forceinline__ void cta_signal_peers(const RankArgs& a, int cta, int
 }
 
 // Flags are compared cyclically ((int)(flag - epoch) >= 0) so epochs may wrap;
-// a spin limit (FLX_TIMEOUT_S, default 10 s) sets the host-mapped abort word
+// a spin limit (FLX_TIMEOUT_S, default 600 s) sets the host-mapped abort word
 // instead of hanging the GPU
 // when a peer died.
 // Warp 0 waits, one flag per lane, until every peer p != skip has published:

@@ -1122,7 +1122,8 @@ flxResult_t world_create_rank(int nranks, int rank, int device, const char* id_h
                            pack_env_shares(env_g, env_set)};
   __atomic_store_n(&mine.ready, 1, __ATOMIC_RELEASE);
   __atomic_fetch_add(&hdr->arrived, 1, __ATOMIC_ACQ_REL);
-  const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 60.0;
+  // ranks of one job can start minutes apart (PyTorch's store waits 30 min)
+  const double timeout = getenv("FLX_BOOT_TIMEOUT") ? atof(getenv("FLX_BOOT_TIMEOUT")) : 600.0;
   if (!spin_until([&] { return __atomic_load_n(&hdr->arrived, __ATOMIC_ACQUIRE) >= nranks; },
                   timeout))
     return fail(flxSystemError, "bootstrap timed out: %d of %d ranks arrived",

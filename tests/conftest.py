@@ -26,3 +26,4 @@ os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 # Peer waits give up after FLX_TIMEOUT_S (product default 600 s, PyTorch's NCCL
 # timeout); the suite fails fast instead if a protocol ever stalls.
 os.environ.setdefault("FLX_TIMEOUT_S", "30")
+os.environ.setdefault("FLX_BOOT_TIMEOUT", "120")

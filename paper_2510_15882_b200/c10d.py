@@ -41,14 +41,23 @@ _instances: list["FlexLinkBackend"] = []
 
 
 class _DoneWork(dist._Work):
-    """Work handle of a stream-ordered collective: complete once enqueued."""
+    """Work handle of a stream-ordered collective, enqueued on the caller's
+    stream at call time.  ``wait()`` makes the CURRENT stream wait for it (as
+    ProcessGroupNCCL's work does), so a caller that switched streams between
+    issuing the collective and waiting still orders its use of the result."""
 
-    def __init__(self, result):
+    def __init__(self, result, stream=None):
         super().__init__()
         self._fut = Future()
         self._fut.set_result(result)
+        self._event = None
+        if stream is not None:
+            self._event = torch.cuda.Event()
+            self._event.record(stream)
 
     def wait(self, timeout=None) -> bool:
+        if self._event is not None:
+            torch.cuda.current_stream().wait_event(self._event)
         return True
 
     def is_completed(self) -> bool:
@@ -133,14 +142,14 @@ class FlexLinkBackend(dist.ProcessGroup):
         for t in tensors:
             self.comm.all_reduce(t, t, op=_flx_op(op, t), stream=self._stream)
             _finish(op, t, self.size())
-        return _DoneWork(tensors)
+        return _DoneWork(tensors, self._stream)
 
     def allreduce_coalesced(self, tensors, opts=None):
         return self.allreduce(tensors, opts)
 
     def _allgather_base(self, output, input, opts=None):
         self.comm.all_gather(input, output, stream=self._stream)
-        return _DoneWork([output])
+        return _DoneWork([output], self._stream)
 
     def allgather(self, output_lists, input_list, opts=None):
         for outs, inp in zip(output_lists, input_list):
@@ -148,12 +157,12 @@ class FlexLinkBackend(dist.ProcessGroup):
             self.comm.all_gather(inp.contiguous(), flat, stream=self._stream)
             for r, o in enumerate(outs):
                 o.copy_(flat[r * inp.numel():(r + 1) * inp.numel()].view_as(o))
-        return _DoneWork(output_lists)
+        return _DoneWork(output_lists, self._stream)
 
     def allgather_into_tensor_coalesced(self, outputs, inputs, opts=None):
         for o, i in zip(outputs, inputs):
             self.comm.all_gather(i, o, stream=self._stream)
-        return _DoneWork(outputs)
+        return _DoneWork(outputs, self._stream)
 
     def _reduce_scatter_base(self, output, input, opts=None):
         return self.reduce_scatter_tensor_coalesced([output], [input], opts)
@@ -163,7 +172,7 @@ class FlexLinkBackend(dist.ProcessGroup):
         for o, i in zip(outputs, inputs):
             self.comm.reduce_scatter(i, o, op=_flx_op(op, i), stream=self._stream)
             _finish(op, o, self.size())
-        return _DoneWork(outputs)
+        return _DoneWork(outputs, self._stream)
 
     def reduce_scatter(self, output_tensors, input_lists, opts=None):
         op = _reduce_op(opts)
@@ -173,7 +182,7 @@ class FlexLinkBackend(dist.ProcessGroup):
             self.comm.reduce_scatter(flat, res, op=_flx_op(op, flat), stream=self._stream)
             _finish(op, res, self.size())
             out.copy_(res.view_as(out))
-        return _DoneWork(output_tensors)
+        return _DoneWork(output_tensors, self._stream)
 
     def alltoall_base(self, output, input, output_split_sizes, input_split_sizes, opts=None):
         n = self.size()
@@ -184,7 +193,7 @@ class FlexLinkBackend(dist.ProcessGroup):
         if even < 0:
             raise NotImplementedError("FlexLink all_to_all needs dim 0 divisible by world size")
         self.comm.all_to_all(input.contiguous(), output, stream=self._stream)
-        return _DoneWork([output])
+        return _DoneWork([output], self._stream)
 
     def barrier(self, opts=None):
         # every rank's queued work done, then a rendezvous on the group's store
@@ -242,7 +251,7 @@ class FlexLinkBackend(dist.ProcessGroup):
             self.comm.all_gather(scattered[root * block:(root + 1) * block], gathered,
                                  stream=self._stream)
             flat.copy_(gathered[:nbytes])
-        return _DoneWork(tensors)
+        return _DoneWork(tensors, self._stream)
 
     def reduce(self, *a, **k):
         self._refuse("reduce")

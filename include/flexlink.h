@@ -120,6 +120,14 @@ flxResult_t flxCommInitLoopback(flxComm_t* comms, int nranks, int device);
 flxResult_t flxDebugHostRemoteRanks(int nranks, int device, flxUniqueId id, double seconds);
 flxResult_t flxCommInitLoopbackIpc(flxComm_t* comms, int nranks, int device, flxUniqueId id);
 flxResult_t flxCommDestroy(flxComm_t comm);
+/* ncclCommSplit (nccl.h ncclCommSplit): collective over every rank of `comm`
+ * (a flxCommInitRank communicator).  Ranks passing the same `color` form a new
+ * communicator, ranked by `key` (ties: the parent rank); FLX_SPLIT_NOCOLOR
+ * joins none and gets *newcomm = NULL.  The new communicator bootstraps like
+ * flxCommInitRank on the parent's device, under an id derived from the
+ * parent's id, the split's sequence number and the color. */
+#define FLX_SPLIT_NOCOLOR (-1)
+flxResult_t flxCommSplit(flxComm_t comm, int color, int key, flxComm_t* newcomm);
 /* ncclCommAbort (nccl.h:186): stop waiting for peers — kernels still spinning
  * on a peer flag give up at once, the destroy barrier is skipped — then free
  * everything like flxCommDestroy.  For a rank that saw flxInternalError. */

@@ -87,6 +87,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommInitLoopback": [P(vp), ci, ci],
         "flxCommDestroy": [vp],
         "flxCommAbort": [vp],
+        "flxCommSplit": [vp, ci, ci, P(vp)],
         "flxCommFinalize": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
@@ -223,6 +224,14 @@ class Communicator:
 
         uid = broadcast_unique_id(group)
         return cls.init_rank(dist.get_world_size(group), uid, dist.get_rank(group))
+
+    def split(self, color: int, key: int = 0) -> "Communicator | None":
+        """``ncclCommSplit``: collective over every rank of this communicator;
+        ranks with the same ``color`` form a new one ordered by ``key`` (ties:
+        this rank); ``color=-1`` (NCCL_SPLIT_NOCOLOR) joins none -> None."""
+        h = ctypes.c_void_p()
+        _check(load_library().flxCommSplit(self._h, color, key, ctypes.byref(h)), "flxCommSplit")
+        return type(self)(h.value) if h.value else None
 
     def destroy(self) -> None:
         if self._h:

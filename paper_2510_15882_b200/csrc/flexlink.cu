@@ -1014,7 +1014,11 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
     return fail(flxInvalidArgument, "at most %d ranks per communicator", FLX_MAX_VIRTUAL_RANKS);
   int dev = 0;
   FLX_TRY(current_device(&dev));
-  if (nranks == 1) return flxCommInitAll(comm, 1, &dev);
+  if (nranks == 1) {
+    FLX_TRY(flxCommInitAll(comm, 1, &dev));
+    (*comm)->uid = id;
+    return flxSuccess;
+  }
   cudaDeviceProp prop;
   FLX_CUDA(cudaGetDeviceProperties(&prop, dev));
   if (prop.major < 10)
@@ -1032,11 +1036,55 @@ flxResult_t flxCommInitRank(flxComm_t* comm, int nranks, flxUniqueId id, int ran
   c->nranks = nranks;
   c->device = dev;
   c->world = w;
+  c->uid = id;
   init_tuning(c);
   c->local = 0;
   world_attach(w, 0, c);
   *comm = c;
   return flxSuccess;
+}
+
+flxResult_t flxCommSplit(flxComm_t comm, int color, int key, flxComm_t* newcomm) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
+  FLX_TRY(validate_comm(comm));
+  if (!newcomm) return fail(flxInvalidArgument, "null newcomm");
+  *newcomm = nullptr;
+  if (color < 0 && color != FLX_SPLIT_NOCOLOR)
+    return fail(flxInvalidArgument, "color %d: a color is >= 0 or FLX_SPLIT_NOCOLOR", color);
+  uint64_t magic;
+  memcpy(&magic, comm->uid.internal, sizeof(magic));
+  const bool single = comm->nranks == 1 && comm->clique && magic == 0x31584c46ull;
+  if (!single && (!comm->world || world_nlocal(comm->world) != 1))
+    return fail(flxInvalidUsage, "flxCommSplit needs a communicator from flxCommInitRank");
+  // every rank's (color, key), agreed through the parent's board: slot 2r is
+  // rank r's color, 2r+1 its key; the others contribute -inf
+  const int n = comm->nranks;
+  std::vector<double> v(2 * (size_t)n, -1e300);
+  v[2 * (size_t)comm->rank] = color;
+  v[2 * (size_t)comm->rank + 1] = key;
+  if (!single) FLX_TRY(world_agree(comm->world, v.data(), 2 * n));
+  const uint64_t seq = ++comm->splits;
+  if (color == FLX_SPLIT_NOCOLOR) return flxSuccess;
+  std::vector<std::pair<double, int>> members;  // (key, parent rank)
+  for (int p = 0; p < n; ++p)
+    if (v[2 * (size_t)p] == (double)color) members.push_back({v[2 * (size_t)p + 1], p});
+  std::sort(members.begin(), members.end());
+  int me = -1;
+  for (size_t i = 0; i < members.size(); ++i)
+    if (members[i].second == comm->rank) me = (int)i;
+  // the child's id: the parent's nonce mixed with (split number, color) —
+  // identical on every member, distinct for every split and color
+  flxUniqueId child = comm->uid;
+  uint64_t words[2];
+  memcpy(words, child.internal + 8, sizeof(words));
+  uint64_t h = 1469598103934665603ull;  // FNV-1a over (seq, color)
+  for (uint64_t x : {seq, (uint64_t)(uint32_t)color})
+    for (int b = 0; b < 8; ++b) h = (h ^ ((x >> (8 * b)) & 0xff)) * 1099511628211ull;
+  words[0] ^= h;
+  words[1] ^= h * 0x9e3779b97f4a7c15ull;
+  memcpy(child.internal + 8, words, sizeof(words));
+  FLX_CUDA(cudaSetDevice(comm->device));
+  return flxCommInitRank(newcomm, (int)members.size(), child, me);
 }
 
 namespace {

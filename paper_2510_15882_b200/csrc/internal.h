@@ -206,6 +206,8 @@ flxResult_t run_world_tuned(World* w, const std::vector<const void*>& send,
                             const Granules& fallback, int path_mask, size_t alignment);
 flxResult_t world_debug_peer(World* w, int local, int peer, int host_region, int write,
                              void* buf, size_t bytes);
+// elementwise max of n doubles over every rank (the balancer's agreement board)
+flxResult_t world_agree(World* w, double* vals, int n);
 
 constexpr uint64_t kCommMagic = 0x4b4e494c58454c46ull;  // "FLEXLINK"
 struct Comm {
@@ -230,6 +232,10 @@ struct Comm {
   flxBalancerConfig tune_s2{10, 0.10, 10, 10};
   bool have_profile = false;
   flxLinkProfile profile{};
+  // flxCommInitRank communicators: the id they were made from and the number of
+  // flxCommSplit calls so far (same on every rank: splits are collective)
+  flxUniqueId uid{};
+  uint64_t splits = 0;
 };
 
 }  // namespace flx

@@ -14,7 +14,7 @@
  * takes a communicator checks FlexLink's magic word (flxComm validation) and
  * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
  * it.  The NCCL calls FlexLink does not implement but that take a
- * communicator (Reduce, Broadcast, Bcast, Send, Recv, CommSplit, CommShrink,
+ * communicator (Reduce, Broadcast, Bcast, Send, Recv, CommShrink,
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
@@ -36,6 +36,7 @@ _Static_assert((int)ncclFloat32 == (int)flxFloat32 && (int)ncclBfloat16 == (int)
                "datatype codes");
 _Static_assert((int)ncclSum == (int)flxSum && (int)ncclMin == (int)flxMin, "reduction codes");
 _Static_assert((int)ncclInvalidUsage == (int)flxInvalidUsage, "result codes");
+_Static_assert(NCCL_SPLIT_NOCOLOR == FLX_SPLIT_NOCOLOR, "split no-color");
 
 /* The NCCL API level this shim implements (the nccl.h it is compiled against),
  * not FlexLink's own version (flxGetVersion): callers such as PyTorch's
@@ -211,11 +212,25 @@ ncclResult_t ncclRecv(void* recvbuff, size_t count, ncclDataType_t datatype, int
   return unsupported(comm, "ncclRecv is not implemented by FlexLink");
 }
 
+/* ncclCommSplit: FlexLink's own split (collective over the parent); the config
+ * maps as at init (maxCTAs).  NCCL_SPLIT_NOCOLOR == FLX_SPLIT_NOCOLOR. */
 ncclResult_t ncclCommSplit(ncclComm_t comm, int color, int key, ncclComm_t* newcomm,
                            ncclConfig_t* config) {
-  (void)color; (void)key; (void)config;
-  if (newcomm) *newcomm = NULL;
-  return unsupported(comm, "ncclCommSplit is not implemented by FlexLink");
+  if (config && config->magic != 0xcafebeef) {
+    flxSetLastError("ncclConfig_t was not initialised with NCCL_CONFIG_INITIALIZER");
+    return ncclInvalidArgument;
+  }
+  ncclResult_t r = (ncclResult_t)flxCommSplit((flxComm_t)comm, color, key, (flxComm_t*)newcomm);
+  if (r != ncclSuccess || !newcomm || !*newcomm || !config) return r;
+  if (config->maxCTAs != NCCL_CONFIG_UNDEF_INT && config->maxCTAs > 0) {
+    const int ctas = config->maxCTAs < 64 ? config->maxCTAs : 64;
+    r = (ncclResult_t)flxSetNvlinkCtas((flxComm_t)*newcomm, ctas);
+    if (r != ncclSuccess) {
+      flxCommDestroy((flxComm_t)*newcomm);
+      *newcomm = NULL;
+    }
+  }
+  return r;
 }
 
 ncclResult_t ncclCommShrink(ncclComm_t comm, int* excludeRanksList, int excludeRanksCount,

@@ -1236,6 +1236,8 @@ int world_release(World* w) {
   return 1;
 }
 
+flxResult_t world_agree(World* w, double* vals, int n) { return world_agree_max(w, vals, n); }
+
 cudaError_t preload_world_cu() {
   return preload_module((const void*)rank_allgather_kernel);
 }

@@ -1,7 +1,7 @@
 """PyTorch's own, unmodified NCCL process group running on FlexLink through
 LD_PRELOAD=libflexlink_nccl.so: ProcessGroupNCCL creates its communicator with
 ncclCommInitRankConfig and issues ncclAllReduce / ncclAllGather /
-ncclReduceScatter, which the shim resolves to FlexLink.  Prints one JSON line:
+ncclReduceScatter (and ncclCommSplit for dist.new_group), which the shim resolves to FlexLink.  Prints one JSON line:
 the results' exactness and how many FlexLink kernels ran (flxGetLaunchCount).
 Run:  LD_PRELOAD=$PWD/paper_2510_15882_b200/libflexlink_nccl.so python tools/torch_nccl_preload.py
 (two ranks on one GPU: RANK / WORLD_SIZE, FLX_ALLOW_SHARED_GPU=1, FLX_SHARES=0,1000 — every
@@ -49,6 +49,22 @@ def main() -> None:
     dist.reduce_scatter_tensor(rs, mine)
     blk = n // world
     ok["reduce_scatter"] = bool(torch.equal(rs, torch.stack(every).sum(0)[rank * blk:(rank + 1) * blk]))
+    # subgroups: with device_id bound, ProcessGroupNCCL makes them with
+    # ncclCommSplit on the default communicator (non-members split with
+    # NCCL_SPLIT_NOCOLOR) — FlexLink's split, collective over the parent
+    from torch.distributed import distributed_c10d as c10d_impl
+
+    default = c10d_impl._get_default_group()
+    ok["split_path"] = bool(default.bound_device_id is not None and
+                            c10d_impl._get_split_source(default) is not None)
+    singles = [dist.new_group([r]) for r in range(world)]
+    whole = dist.new_group(list(range(world)))
+    y = mine.clone()
+    dist.all_reduce(y, group=singles[rank])
+    ok["new_group_single"] = bool(torch.equal(y, mine))
+    z = mine.clone()
+    dist.all_reduce(z, group=whole)
+    ok["new_group_whole"] = bool(torch.equal(z, torch.stack(every).sum(0)))
     if world == 1:
         dist.barrier()  # a 1-element AllReduce: on a shared GPU it would be an NVLink kernel
     torch.cuda.synchronize()

@@ -167,6 +167,14 @@ flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvco
  * block. */
 flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
+/* ncclBroadcast (nccl.h ncclBroadcast): rank `root`'s sendbuff (count
+ * elements) lands in every rank's recvbuff; in place when sendbuff == recvbuff.
+ * Runs as one striped AllReduce of the bytes with MAX over uint8, the non-roots
+ * contributing zeros — bit-exact for any dtype (-0.0 and NaN payloads kept).
+ * Twice a ring broadcast's traffic: for state sync (DDP's construction), not a
+ * hot path. */
+flxResult_t flxBroadcast(const void* sendbuff, void* recvbuff, size_t count,
+                         flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream);
 /* Convenience for single-process communicator sets (flxCommInitAll /
  * flxCommInitLoopback): the same collective on every comms[i] with
  * sendbuffs[i]/recvbuffs[i] in ONE call — exactly flxGroupStart + n calls +

@@ -88,6 +88,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommDestroy": [vp],
         "flxCommAbort": [vp],
         "flxCommSplit": [vp, ci, ci, P(vp)],
+        "flxBroadcast": [vp, vp, ctypes.c_size_t, ci, ci, vp, vp],
         "flxCommFinalize": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
@@ -262,6 +263,19 @@ class Communicator:
         _check(load_library().flxAllReduce(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
             dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream, send.get_device())), "flxAllReduce")
+        return recv
+
+    def broadcast(self, send, recv=None, root: int = 0, stream=None):
+        """``ncclBroadcast``: ``root``'s ``send`` into every rank's ``recv`` (in
+        place when ``recv`` is None); bit-exact for any dtype."""
+        recv = send if recv is None else _contiguous_cuda(recv, "recv")
+        _contiguous_cuda(send, "send")
+        if recv.numel() != send.numel() or recv.dtype != send.dtype:
+            raise ValueError("recv must match send in size and dtype")
+        _check(load_library().flxBroadcast(
+            ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
+            dtype_code(send.dtype), root, self._h, _stream_handle(stream, send.get_device())),
+            "flxBroadcast")
         return recv
 
     def all_gather(self, send, recv, stream=None):
@@ -648,6 +662,14 @@ class Clique:
         if sends[0].numel() % self.nranks:
             raise ValueError("all_to_all buffers must hold nranks equal blocks")
         self._issue(3, args, 0, stream, sends[0].numel() // self.nranks)
+        return recvs
+
+    def broadcast(self, sends: Sequence, recvs: Sequence | None = None, root: int = 0,
+                  stream=None):
+        """Every virtual rank's ``recvs[r]`` gets ``sends[root]`` (one group)."""
+        recvs = list(sends) if recvs is None else list(recvs)
+        self._validate(sends, recvs)
+        self._group(lambda i, c: c.broadcast(sends[i], recvs[i], root, stream))
         return recvs
 
     def set_shares(self, op: CollectiveOp, shares, nbytes: int | None = None) -> None:

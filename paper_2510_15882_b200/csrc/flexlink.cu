@@ -1278,6 +1278,26 @@ flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
   return enqueue(Call{comm, flxCollAllToAll, sendbuff, recvbuff, count, datatype, 0, stream});
 }
 
+flxResult_t flxBroadcast(const void* sendbuff, void* recvbuff, size_t count,
+                         flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
+  FLX_TRY(check_call(comm, datatype, 0, false));
+  if (root < 0 || root >= comm->nranks) return fail(flxInvalidArgument, "bad root %d", root);
+  if (count == 0) return flxSuccess;
+  if (!recvbuff || (comm->rank == root && !sendbuff))
+    return fail(flxInvalidArgument, "null buffer");
+  const size_t bytes = count * dtype_size(datatype);
+  FLX_CUDA(cudaSetDevice(comm->device));
+  // the root's bytes, zeros elsewhere; then MAX over uint8 leaves the root's
+  if (comm->rank == root) {
+    if (sendbuff != recvbuff)
+      FLX_CUDA(cudaMemcpyAsync(recvbuff, sendbuff, bytes, cudaMemcpyDeviceToDevice, stream));
+  } else {
+    FLX_CUDA(cudaMemsetAsync(recvbuff, 0, bytes, stream));
+  }
+  return flxAllReduce(recvbuff, recvbuff, bytes, flxUint8, flxMax, comm, stream);
+}
+
 // One collective for ALL ranks of a single-process communicator set in one
 // call: equivalent to flxGroupStart; per-rank flx<Coll>(...); flxGroupEnd, but
 // one host crossing instead of n+2 (small messages are host-issue bound).

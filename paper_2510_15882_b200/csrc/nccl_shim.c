@@ -14,7 +14,7 @@
  * takes a communicator checks FlexLink's magic word (flxComm validation) and
  * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
  * it.  The NCCL calls FlexLink does not implement but that take a
- * communicator (Reduce, Broadcast, Bcast, Send, Recv, CommShrink,
+ * communicator (Reduce, Send, Recv, CommShrink,
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
@@ -187,17 +187,18 @@ ncclResult_t ncclReduce(const void* sendbuff, void* recvbuff, size_t count,
   return unsupported(comm, "ncclReduce is not implemented by FlexLink");
 }
 
+/* ncclBroadcast / ncclBcast: FlexLink's bit-exact broadcast (flxBroadcast) */
 ncclResult_t ncclBcast(void* buff, size_t count, ncclDataType_t datatype, int root,
                        ncclComm_t comm, cudaStream_t stream) {
-  (void)buff; (void)count; (void)datatype; (void)root; (void)stream;
-  return unsupported(comm, "ncclBcast is not implemented by FlexLink");
+  return (ncclResult_t)flxBroadcast(buff, buff, count, (flxDataType_t)datatype, root,
+                                    (flxComm_t)comm, stream);
 }
 
 ncclResult_t ncclBroadcast(const void* sendbuff, void* recvbuff, size_t count,
                            ncclDataType_t datatype, int root, ncclComm_t comm,
                            cudaStream_t stream) {
-  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
-  return unsupported(comm, "ncclBroadcast is not implemented by FlexLink");
+  return (ncclResult_t)flxBroadcast(sendbuff, recvbuff, count, (flxDataType_t)datatype, root,
+                                    (flxComm_t)comm, stream);
 }
 
 ncclResult_t ncclSend(const void* sendbuff, size_t count, ncclDataType_t datatype, int peer,

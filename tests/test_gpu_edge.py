@@ -107,3 +107,33 @@ def test_entry_points_restore_the_callers_context(loopback):
         assert seen["start"] == 0 and seen["end"] == 0, seen
         assert seen["err"] == 0 and seen["times"][0] > 0
         assert all(torch.equal(x, torch.full_like(x, n)) for x in r)
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_broadcast_is_bit_exact_for_every_dtype(loopback):
+    """flxBroadcast / ncclBroadcast: one striped MAX-over-uint8 AllReduce of the
+    bytes with zeros from the non-roots — the root's bits everywhere, -0.0 and
+    NaN payloads included, any size, in place or not."""
+    n = 4
+    with flx.Clique(n, loopback=loopback) as c:
+        c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        for dt, count in ((torch.float32, (1 << 20) + 3), (torch.bfloat16, 777),
+                          (torch.int64, 5), (torch.uint8, 4096 * 3 + 1)):
+            for root in (0, n - 1):
+                g = torch.Generator(device="cuda").manual_seed(root + count)
+                sends = [torch.randint(-100, 100, (count,), device="cuda", generator=g).to(dt)
+                         for _ in range(n)]
+                if dt == torch.float32:
+                    bits = sends[root].view(torch.int32)
+                    bits[0] = -2147483648            # -0.0
+                    bits[1] = 0x7FC00123              # a NaN with a payload
+                want = sends[root].clone()
+                recvs = [torch.full_like(s, 7) for s in sends]
+                c.broadcast(sends, recvs, root=root)
+                torch.cuda.synchronize()
+                for r in recvs:
+                    assert torch.equal(r.view(torch.uint8), want.view(torch.uint8)), (dt, root)
+                c.broadcast(sends, root=root)  # in place
+                torch.cuda.synchronize()
+                for s in sends:
+                    assert torch.equal(s.view(torch.uint8), want.view(torch.uint8)), (dt, root)

@@ -1,7 +1,8 @@
 """PyTorch's own, unmodified NCCL process group running on FlexLink through
 LD_PRELOAD=libflexlink_nccl.so: ProcessGroupNCCL creates its communicator with
 ncclCommInitRankConfig and issues ncclAllReduce / ncclAllGather /
-ncclReduceScatter (and ncclCommSplit for dist.new_group), which the shim resolves to FlexLink.  Prints one JSON line:
+ncclReduceScatter, ncclBroadcast (and ncclCommSplit for dist.new_group), which the shim
+resolves to FlexLink.  Prints one JSON line:
 the results' exactness and how many FlexLink kernels ran (flxGetLaunchCount).
 Run:  LD_PRELOAD=$PWD/paper_2510_15882_b200/libflexlink_nccl.so python tools/torch_nccl_preload.py
 (two ranks on one GPU: RANK / WORLD_SIZE, FLX_ALLOW_SHARED_GPU=1, FLX_SHARES=0,1000 — every
@@ -49,6 +50,18 @@ def main() -> None:
     dist.reduce_scatter_tensor(rs, mine)
     blk = n // world
     ok["reduce_scatter"] = bool(torch.equal(rs, torch.stack(every).sum(0)[rank * blk:(rank + 1) * blk]))
+    # broadcast (DDP's state sync): bit-exact from every root, -0.0 / NaN kept
+    bc_ok = True
+    for root in range(world):
+        for dt, cnt in ((torch.float32, 1 << 18), (torch.bfloat16, 1 << 19)):  # 1 MiB each
+            src = data(root)[:cnt].to(dt)
+            if dt == torch.float32:
+                src.view(torch.int32)[:2] = torch.tensor([-2147483648, 0x7FC00123], device="cuda",
+                                                         dtype=torch.int32)
+            t = src.clone() if rank == root else torch.zeros_like(src)
+            dist.broadcast(t, src=root)
+            bc_ok = bc_ok and bool(torch.equal(t.view(torch.uint8), src.view(torch.uint8)))
+    ok["broadcast"] = bc_ok
     # subgroups: with device_id bound, ProcessGroupNCCL makes them with
     # ncclCommSplit on the default communicator (non-members split with
     # NCCL_SPLIT_NOCOLOR) — FlexLink's split, collective over the parent

@@ -18,8 +18,8 @@ One process per GPU.  The communicator is bootstrapped through the process
 group's own store (rank 0 publishes the flxUniqueId).  Collectives are
 enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
 ``async_op=False`` path), so the returned work objects are complete from the
-stream's point of view.  Broadcast is composed of FlexLink's AllToAll and
-AllGather (exact; DDP's construction-time state sync).  Operations FlexLink does
+stream's point of view.  Broadcast is FlexLink's bit-exact flxBroadcast (DDP's
+construction-time state sync).  Operations FlexLink does
 not implement (reduce, send/recv, gather/scatter, uneven all_to_all splits,
 ReduceOp.AVG on integer tensors) raise ``NotImplementedError`` instead of
 silently falling back to another library.  ReduceOp.AVG on floating tensors is
@@ -225,32 +225,17 @@ class FlexLinkBackend(dist.ProcessGroup):
                                   f"ReduceScatter, AllToAll are)")
 
     def broadcast(self, tensors, opts=None):
-        """Exact broadcast composed of FlexLink collectives (DDP's module-state sync
-        at construction needs it): the root's bytes cut into N blocks, an AllToAll
-        hands block r to rank r (the other ranks' blocks ride along unread), an
-        AllGather of those blocks rebuilds the root's buffer everywhere.  Pure
-        copies, so any dtype; twice a ring broadcast's traffic — an init-time
-        collective, not a hot path."""
+        """Bit-exact broadcast (DDP's module-state sync at construction):
+        FlexLink's flxBroadcast on the tensor's bytes — one striped MAX-over-uint8
+        AllReduce with zeros from the non-roots, so any dtype, -0.0 and NaN
+        payloads included; in place, no scratch buffers."""
         root = opts.rootRank if opts is not None else 0
-        n, me = self.size(), self.rank()
         for t in tensors:
             if not t.is_contiguous():
                 raise NotImplementedError("FlexLink broadcast needs a contiguous tensor")
-            flat = t.view(-1).view(torch.uint8)
-            nbytes = flat.numel()
-            if n == 1 or nbytes == 0:
+            if self.size() == 1 or t.numel() == 0:
                 continue
-            block = -(-nbytes // n)
-            block = -(-block // 16) * 16  # 16 B blocks keep every slice on the vector grid
-            send = torch.empty(n * block, dtype=torch.uint8, device=t.device)
-            if me == root:
-                send[:nbytes].copy_(flat)
-            scattered = torch.empty_like(send)
-            self.comm.all_to_all(send, scattered, stream=self._stream)
-            gathered = torch.empty_like(send)
-            self.comm.all_gather(scattered[root * block:(root + 1) * block], gathered,
-                                 stream=self._stream)
-            flat.copy_(gathered[:nbytes])
+            self.comm.broadcast(t.view(-1).view(torch.uint8), root=root, stream=self._stream)
         return _DoneWork(tensors, self._stream)
 
     def reduce(self, *a, **k):

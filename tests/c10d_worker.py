@@ -84,7 +84,7 @@ def main():
         bad += int(not torch.equal(funcol.wait_tensor(t), want))
     if bad:
         print(f"rank {rank} functional collectives mismatch", flush=True)
-    # broadcast (AllToAll + AllGather): exact bytes, any dtype.  Two processes on
+    # broadcast (flxBroadcast on the bytes): exact, any dtype.  Two processes on
     # one GPU (PCIE_ONLY) keep every collective a multiple of the alignment, so no
     # NVLink-path kernel spins on the other process (the library refuses one);
     # ragged lengths are covered at world 1 here and by tests/test_c10d_compose_cpu.py

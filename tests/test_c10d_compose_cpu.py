@@ -1,10 +1,10 @@
 """Host logic of the 'flexlink' c10d backend at world size 2, on CPU (gloo).
 
-FlexLinkBackend's composed operations — broadcast as AllToAll + AllGather of
-16 B-rounded byte blocks, ReduceOp.AVG as the sum then a divide — run here with
-a stand-in communicator whose all_to_all / all_gather / all_reduce /
-reduce_scatter are gloo's, so the block arithmetic, the root's placement and
-the ragged tails are checked across two real processes without a GPU.  The GPU
+FlexLinkBackend's composed operations — broadcast on the bytes of any dtype
+(flxBroadcast's zeros-then-MAX-over-uint8 rule), ReduceOp.AVG as the sum then a
+divide — run here with a stand-in communicator whose broadcast / all_reduce /
+reduce_scatter are gloo's, so byte views, the root's placement and ragged
+lengths are checked across two real processes without a GPU.  The GPU
 test (tests/test_gpu_c10d.py) runs the same methods over the real kernels.
 """
 import os
@@ -28,6 +28,15 @@ def _worker(rank: int, world: int, port: int, q) -> None:
     dist.init_process_group("gloo", rank=rank, world_size=world)
 
     class GlooComm:  # FlexLink Communicator's tensor API, served by gloo
+        def broadcast(self, send, recv=None, root=0, stream=None):
+            # flxBroadcast's rule: the root's bytes, zeros elsewhere, MAX over uint8
+            recv = send if recv is None else recv
+            if rank == root:
+                recv.copy_(send)
+            else:
+                recv.zero_()
+            dist.all_reduce(recv, op=dist.ReduceOp.MAX)
+
         def all_to_all(self, send, recv, stream=None):
             dist.all_to_all_single(recv, send)
 

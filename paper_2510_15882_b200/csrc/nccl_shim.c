@@ -14,7 +14,7 @@
  * takes a communicator checks FlexLink's magic word (flxComm validation) and
  * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
  * it.  The NCCL calls FlexLink does not implement but that take a
- * communicator (Reduce, Send, Recv, CommShrink,
+ * communicator (Reduce, Gather, Scatter, Send, Recv, CommShrink, DevCommCreate,
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
@@ -151,6 +151,31 @@ ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recv
                                         (flxRedOp_t)op, (flxComm_t)comm, stream);
 }
 
+/* NCCL 2.28 added ncclAlltoAll / ncclGather / ncclScatter and the device
+ * communicator calls; PyTorch built against 2.28 (the bundled libnccl) imports
+ * ncclAlltoAll for all_to_all_single and ncclDevCommCreate/Destroy.  The shim
+ * compiles against the system nccl.h (2.27.3), so it declares them here with
+ * 2.28's signatures (device-communicator types as opaque pointers) — defined,
+ * so a preloaded process never hands a FlexLink communicator to libnccl. */
+#if NCCL_VERSION_CODE < 22800
+ncclResult_t ncclAlltoAll(const void* sendbuff, void* recvbuff, size_t count,
+                          ncclDataType_t datatype, ncclComm_t comm, cudaStream_t stream);
+ncclResult_t ncclGather(const void* sendbuff, void* recvbuff, size_t count,
+                        ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream);
+ncclResult_t ncclScatter(const void* sendbuff, void* recvbuff, size_t count,
+                         ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream);
+ncclResult_t ncclDevCommCreate(ncclComm_t comm, const void* reqs, void* outDevComm);
+ncclResult_t ncclDevCommDestroy(ncclComm_t comm, const void* devComm);
+#endif
+
+/* ncclAlltoAll: block j of sendbuff to rank j, block i of recvbuff from rank i —
+ * exactly flxAllToAll (striped per block) */
+ncclResult_t ncclAlltoAll(const void* sendbuff, void* recvbuff, size_t count,
+                          ncclDataType_t datatype, ncclComm_t comm, cudaStream_t stream) {
+  return (ncclResult_t)flxAllToAll(sendbuff, recvbuff, count, (flxDataType_t)datatype,
+                                   (flxComm_t)comm, stream);
+}
+
 ncclResult_t ncclCommFinalize(ncclComm_t comm) {
   return (ncclResult_t)flxCommFinalize((flxComm_t)comm);
 }
@@ -199,6 +224,28 @@ ncclResult_t ncclBroadcast(const void* sendbuff, void* recvbuff, size_t count,
                            cudaStream_t stream) {
   return (ncclResult_t)flxBroadcast(sendbuff, recvbuff, count, (flxDataType_t)datatype, root,
                                     (flxComm_t)comm, stream);
+}
+
+ncclResult_t ncclGather(const void* sendbuff, void* recvbuff, size_t count,
+                        ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream) {
+  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
+  return unsupported(comm, "ncclGather is not implemented by FlexLink");
+}
+
+ncclResult_t ncclScatter(const void* sendbuff, void* recvbuff, size_t count,
+                         ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream) {
+  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
+  return unsupported(comm, "ncclScatter is not implemented by FlexLink");
+}
+
+ncclResult_t ncclDevCommCreate(ncclComm_t comm, const void* reqs, void* outDevComm) {
+  (void)reqs; (void)outDevComm;
+  return unsupported(comm, "ncclDevCommCreate (NCCL's device API) is not implemented by FlexLink");
+}
+
+ncclResult_t ncclDevCommDestroy(ncclComm_t comm, const void* devComm) {
+  (void)devComm;
+  return unsupported(comm, "ncclDevCommDestroy (NCCL's device API) is not implemented by FlexLink");
 }
 
 ncclResult_t ncclSend(const void* sendbuff, size_t count, ncclDataType_t datatype, int peer,

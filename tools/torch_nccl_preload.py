@@ -1,7 +1,7 @@
 """PyTorch's own, unmodified NCCL process group running on FlexLink through
 LD_PRELOAD=libflexlink_nccl.so: ProcessGroupNCCL creates its communicator with
 ncclCommInitRankConfig and issues ncclAllReduce / ncclAllGather /
-ncclReduceScatter, ncclBroadcast (and ncclCommSplit for dist.new_group), which the shim
+ncclReduceScatter, ncclBroadcast, ncclAlltoAll (and ncclCommSplit for dist.new_group), which the shim
 resolves to FlexLink.  Prints one JSON line:
 the results' exactness and how many FlexLink kernels ran (flxGetLaunchCount).
 Run:  LD_PRELOAD=$PWD/paper_2510_15882_b200/libflexlink_nccl.so python tools/torch_nccl_preload.py
@@ -50,6 +50,13 @@ def main() -> None:
     dist.reduce_scatter_tensor(rs, mine)
     blk = n // world
     ok["reduce_scatter"] = bool(torch.equal(rs, torch.stack(every).sum(0)[rank * blk:(rank + 1) * blk]))
+    # all_to_all_single, equal splits: PyTorch built against NCCL 2.28 calls
+    # ncclAlltoAll, which the shim maps to flxAllToAll
+    a2a = torch.empty_like(mine)
+    dist.all_to_all_single(a2a, mine)
+    blk = n // world
+    ok["all_to_all"] = bool(torch.equal(a2a, torch.cat([e[rank * blk:(rank + 1) * blk]
+                                                         for e in every])))
     # broadcast (DDP's state sync): bit-exact from every root, -0.0 / NaN kept
     bc_ok = True
     for root in range(world):

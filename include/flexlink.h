@@ -73,6 +73,11 @@ typedef enum {
 
 /* == ncclRedOp_t for the four supported operators */
 typedef enum { flxSum = 0, flxProd = 1, flxMax = 2, flxMin = 3, flxNumOps = 4 } flxRedOp_t;
+/* == ncclAvg: AllReduce / ReduceScatter only — the striped sum, then the
+ * result divided by nranks on the caller's stream (floating types: one
+ * rounding of fl(sum) / n in the accumulation type; integers: C division,
+ * as NCCL's sum-then-divide for integers) */
+#define FLX_OP_AVG 4
 
 /* == linkstripe PathKind (topo.py:18-31); also the tie-break order */
 typedef enum { flxPathNvlink = 0, flxPathPcie = 1, flxPathRdma = 2 } flxPath_t;

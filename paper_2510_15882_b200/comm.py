@@ -42,7 +42,7 @@ _lib = None
 
 _RESULTS = {0: "success", 1: "unhandled cuda error", 2: "system error", 3: "internal error",
             4: "invalid argument", 5: "invalid usage", 6: "remote error", 7: "in progress"}
-_OPS = {"sum": 0, "prod": 1, "max": 2, "min": 3}
+_OPS = {"sum": 0, "prod": 1, "max": 2, "min": 3, "avg": 4}  # avg: AllReduce / ReduceScatter
 _COLL = {CollectiveOp.ALLREDUCE: 0, CollectiveOp.ALLGATHER: 1, CollectiveOp.REDUCESCATTER: 2,
          CollectiveOp.ALLTOALL: 3}
 

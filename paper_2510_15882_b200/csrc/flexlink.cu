@@ -440,6 +440,7 @@ struct Call {
   int dtype;
   int op;
   cudaStream_t stream;
+  bool avg = false;  // FLX_OP_AVG: ran as a sum; recv is divided by nranks afterwards
 };
 
 thread_local int t_group_depth = 0;
@@ -770,6 +771,18 @@ flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
                          pinned, g, path_mask(), alignment_for(lead, head.coll));
 }
 
+// FLX_OP_AVG: every member's recv (AllReduce: count elements, ReduceScatter:
+// its recvcount block) divided by nranks on the member's own stream, which the
+// collective's join already ordered after the data landed
+flxResult_t finish_avg(const std::vector<Call>& calls) {
+  for (const Call& k : calls) {
+    if (!k.avg) continue;
+    FLX_CUDA(cudaSetDevice(k.comm->device));
+    FLX_CUDA(launch_div(k.dtype, k.recv, k.count, k.comm->nranks, k.stream));
+  }
+  return flxSuccess;
+}
+
 flxResult_t flush_group() {
   std::vector<Call> calls;
   calls.swap(t_pending);
@@ -795,6 +808,7 @@ flxResult_t flush_group() {
       std::vector<Call> one;
       for (auto& v : per) one.push_back(v[k]);
       FLX_TRY(run_world_calls(w, one));
+      FLX_TRY(finish_avg(one));
     }
   }
   // bucket calls by clique, preserving per-member order
@@ -818,12 +832,18 @@ flxResult_t flush_group() {
       std::vector<Call> one;
       for (auto& v : per) one.push_back(v[k]);
       FLX_TRY(run_clique(clique, one));
+      FLX_TRY(finish_avg(one));
     }
   }
   return flxSuccess;
 }
 
-flxResult_t enqueue(const Call& k) {
+flxResult_t enqueue(const Call& in) {
+  Call k = in;
+  if (k.op == FLX_OP_AVG) {  // the striped sum, then finish_avg
+    k.op = flxSum;
+    k.avg = true;
+  }
   t_pending.push_back(k);
   if (t_group_depth > 0) return flxSuccess;
   return flush_group();
@@ -864,7 +884,7 @@ AutoTuner* tuner_of(const Comm* c) { return c->clique ? c->clique->tuner : world
 flxResult_t check_call(const flxComm* comm, int dtype, int op, bool reduce) {
   FLX_TRY(validate_comm(comm));
   if (dtype < 0 || dtype >= flxNumTypes) return fail(flxInvalidArgument, "bad datatype %d", dtype);
-  if (reduce && (op < 0 || op >= flxNumOps))
+  if (reduce && (op < 0 || (op >= flxNumOps && op != FLX_OP_AVG)))
     return fail(flxInvalidArgument, "unsupported reduction op %d", op);
   return flxSuccess;
 }
@@ -1319,9 +1339,15 @@ flxResult_t flxGroupCollective(flxCollOp_t coll, flxComm_t* comms, int n,
       return fail(flxInvalidArgument, "in-place AllToAll is not supported");
   }
   ++t_group_depth;
-  for (int i = 0; i < n; ++i)
-    t_pending.push_back(Call{comms[i], (int)coll, sendbuffs[i], recvbuffs[i], count, datatype,
-                             reduce ? (int)op : 0, stream});
+  for (int i = 0; i < n; ++i) {
+    Call k{comms[i], (int)coll, sendbuffs[i], recvbuffs[i], count, datatype,
+           reduce ? (int)op : 0, stream};
+    if (k.op == FLX_OP_AVG) {  // the striped sum, then finish_avg
+      k.op = flxSum;
+      k.avg = true;
+    }
+    t_pending.push_back(k);
+  }
   --t_group_depth;
   if (t_group_depth > 0) return flxSuccess;  // inside an outer group: flushed by its end
   return flush_group();

@@ -24,6 +24,7 @@ cudaError_t launch_xpose(const XposeArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fold(int dtype, int op, const FoldArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_rows(int dtype, int op, const RowsArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s);
+cudaError_t launch_div(int dtype, void* buf, size_t count, int n, cudaStream_t s);
 extern std::atomic<unsigned long long> g_launches;
 
 // ---- errors

@@ -218,6 +218,42 @@ cudaError_t launch_fanout(const FanoutArgs& a, int grid, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ncclAvg's second half: buf[i] = buf[i] / n on the caller's stream
+// (accumulation type for 16-bit floats, C division for integers)
+template <typename T>
+__global__ void __launch_bounds__(512) div_kernel(T* buf, size_t count, int n) {
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+    using A = typename AccT<T>::type;
+    buf[i] = from_acc<T>(to_acc<T>(buf[i]) / (A)n);
+  }
+}
+
+template <typename T>
+cudaError_t div_typed(void* buf, size_t count, int n, cudaStream_t s) {
+  const int grid = (int)std::min<size_t>((count + 511) / 512, 148 * 8);
+  div_kernel<T><<<std::max(grid, 1), 512, 0, s>>>(static_cast<T*>(buf), count, n);
+  g_launches++;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_div(int dtype, void* buf, size_t count, int n, cudaStream_t s) {
+  if (count == 0 || n == 1) return cudaSuccess;
+  switch (dtype) {
+    case flxInt8: return div_typed<int8_t>(buf, count, n, s);
+    case flxUint8: return div_typed<uint8_t>(buf, count, n, s);
+    case flxInt32: return div_typed<int32_t>(buf, count, n, s);
+    case flxUint32: return div_typed<uint32_t>(buf, count, n, s);
+    case flxInt64: return div_typed<int64_t>(buf, count, n, s);
+    case flxUint64: return div_typed<uint64_t>(buf, count, n, s);
+    case flxFloat16: return div_typed<__half>(buf, count, n, s);
+    case flxFloat32: return div_typed<float>(buf, count, n, s);
+    case flxFloat64: return div_typed<double>(buf, count, n, s);
+    case flxBfloat16: return div_typed<__nv_bfloat16>(buf, count, n, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t preload_launch_cu() {
   return preload_module((const void*)fold_once_kernel<float, kSum, 8>);
 }

@@ -35,6 +35,7 @@ _Static_assert(sizeof(ncclUniqueId) == sizeof(flxUniqueId), "unique id size");
 _Static_assert((int)ncclFloat32 == (int)flxFloat32 && (int)ncclBfloat16 == (int)flxBfloat16,
                "datatype codes");
 _Static_assert((int)ncclSum == (int)flxSum && (int)ncclMin == (int)flxMin, "reduction codes");
+_Static_assert((int)ncclAvg == FLX_OP_AVG, "average");
 _Static_assert((int)ncclInvalidUsage == (int)flxInvalidUsage, "result codes");
 _Static_assert(NCCL_SPLIT_NOCOLOR == FLX_SPLIT_NOCOLOR, "split no-color");
 
@@ -132,7 +133,7 @@ ncclResult_t ncclCommUserRank(const ncclComm_t comm, int* rank) {
 ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count,
                            ncclDataType_t datatype, ncclRedOp_t op, ncclComm_t comm,
                            cudaStream_t stream) {
-  if ((int)op >= (int)flxNumOps) return ncclInvalidArgument; /* ncclAvg / PreMulSum */
+  if ((int)op > (int)ncclAvg) return ncclInvalidArgument; /* PreMulSum ops */
   return (ncclResult_t)flxAllReduce(sendbuff, recvbuff, count, (flxDataType_t)datatype,
                                     (flxRedOp_t)op, (flxComm_t)comm, stream);
 }
@@ -146,7 +147,7 @@ ncclResult_t ncclAllGather(const void* sendbuff, void* recvbuff, size_t sendcoun
 ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount,
                                ncclDataType_t datatype, ncclRedOp_t op, ncclComm_t comm,
                                cudaStream_t stream) {
-  if ((int)op >= (int)flxNumOps) return ncclInvalidArgument;
+  if ((int)op > (int)ncclAvg) return ncclInvalidArgument; /* PreMulSum ops */
   return (ncclResult_t)flxReduceScatter(sendbuff, recvbuff, recvcount, (flxDataType_t)datatype,
                                         (flxRedOp_t)op, (flxComm_t)comm, stream);
 }

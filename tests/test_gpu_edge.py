@@ -137,3 +137,41 @@ def test_broadcast_is_bit_exact_for_every_dtype(loopback):
                 torch.cuda.synchronize()
                 for s in sends:
                     assert torch.equal(s.view(torch.uint8), want.view(torch.uint8)), (dt, root)
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_average_is_the_striped_sum_divided(loopback):
+    """FLX_OP_AVG (== ncclAvg) on AllReduce and ReduceScatter: the rank-order
+    fold (fp32 accumulation, one rounding for 16-bit types), then one division
+    by nranks on the caller's stream — C division for integers."""
+    n, count = 3, (1 << 18) + 2  # 3 equal ReduceScatter blocks
+    with flx.Clique(n, loopback=loopback) as c:
+        for op in (CollectiveOp.ALLREDUCE, CollectiveOp.REDUCESCATTER):
+            c.set_shares(op, (900, 100, 0))
+        g = torch.Generator(device="cuda").manual_seed(11)
+        for dt in (torch.float32, torch.bfloat16, torch.int32):
+            if dt == torch.int32:
+                sends = [torch.randint(-10**6, 10**6, (count,), device="cuda", generator=g,
+                                       dtype=torch.int32) for _ in range(n)]
+            else:
+                sends = [torch.randn(count, device="cuda", generator=g).to(dt) for _ in range(n)]
+            acc = sends[0].double() if dt == torch.int32 else sends[0].float()
+            for x in sends[1:]:
+                acc = acc + (x.double() if dt == torch.int32 else x.float())
+            if dt == torch.int32:
+                want = torch.div(acc.long(), n, rounding_mode="trunc").to(dt)
+            else:
+                # IEEE division by a tensor (torch divides by a scalar through its
+                # reciprocal, which can differ in the last bit)
+                q = acc.to(dt).float()
+                want = (q / torch.full_like(q, n)).to(dt)
+            recvs = [torch.empty_like(x) for x in sends]
+            c.all_reduce(sends, recvs, op="avg")
+            blk = count // n
+            rs = [torch.empty(blk, device="cuda", dtype=dt) for _ in range(n)]
+            c.reduce_scatter(sends, rs, op="avg")
+            torch.cuda.synchronize()
+            for r in recvs:
+                assert torch.equal(r, want), dt
+            for i, r in enumerate(rs):
+                assert torch.equal(r, want[i * blk:(i + 1) * blk]), dt

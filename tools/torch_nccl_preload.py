@@ -50,6 +50,10 @@ def main() -> None:
     dist.reduce_scatter_tensor(rs, mine)
     blk = n // world
     ok["reduce_scatter"] = bool(torch.equal(rs, torch.stack(every).sum(0)[rank * blk:(rank + 1) * blk]))
+    # ReduceOp.AVG (ncclAvg, e.g. FSDP's gradient reduce-scatter): the sum, divided
+    avg = mine.clone()
+    dist.all_reduce(avg, op=dist.ReduceOp.AVG)
+    ok["all_reduce_avg"] = bool(torch.equal(avg, torch.stack(every).sum(0) / world))
     # all_to_all_single, equal splits: PyTorch built against NCCL 2.28 calls
     # ncclAlltoAll, which the shim maps to flxAllToAll
     a2a = torch.empty_like(mine)

@@ -172,6 +172,13 @@ flxResult_t flxReduceScatter(const void* sendbuff, void* recvbuff, size_t recvco
  * block. */
 flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
                         flxDataType_t datatype, flxComm_t comm, cudaStream_t stream);
+/* ncclReduce (nccl.h ncclReduce): the fold of every rank's sendbuff lands in
+ * rank `root`'s recvbuff (unused elsewhere; in place when sendbuff == recvbuff
+ * on the root).  A striped AllReduce whose non-root result goes to
+ * stream-ordered scratch (cudaMallocAsync, freed after the collective). */
+flxResult_t flxReduce(const void* sendbuff, void* recvbuff, size_t count,
+                      flxDataType_t datatype, flxRedOp_t op, int root, flxComm_t comm,
+                      cudaStream_t stream);
 /* ncclBroadcast (nccl.h ncclBroadcast): rank `root`'s sendbuff (count
  * elements) lands in every rank's recvbuff; in place when sendbuff == recvbuff.
  * Runs as one striped AllReduce of the bytes with MAX over uint8, the non-roots

@@ -20,7 +20,7 @@ enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
 ``async_op=False`` path), so the returned work objects are complete from the
 stream's point of view.  Broadcast is FlexLink's bit-exact flxBroadcast (DDP's
 construction-time state sync).  Operations FlexLink does
-not implement (reduce, send/recv, gather/scatter, uneven all_to_all splits,
+not implement (send/recv, gather/scatter, uneven all_to_all splits,
 ReduceOp.AVG on integer tensors) raise ``NotImplementedError`` instead of
 silently falling back to another library.  ReduceOp.AVG on floating tensors is
 the striped sum divided by the group size in place (fl(fl(sum) / n)).
@@ -222,7 +222,7 @@ class FlexLinkBackend(dist.ProcessGroup):
     # -- not implemented by FlexLink: refuse, never fall back
     def _refuse(self, name):
         raise NotImplementedError(f"{name} is not a FlexLink collective (AllReduce, AllGather, "
-                                  f"ReduceScatter, AllToAll are)")
+                                  f"ReduceScatter, AllToAll, Reduce, Broadcast are)")
 
     def broadcast(self, tensors, opts=None):
         """Bit-exact broadcast (DDP's module-state sync at construction):
@@ -238,8 +238,16 @@ class FlexLinkBackend(dist.ProcessGroup):
             self.comm.broadcast(t.view(-1).view(torch.uint8), root=root, stream=self._stream)
         return _DoneWork(tensors, self._stream)
 
-    def reduce(self, *a, **k):
-        self._refuse("reduce")
+    def reduce(self, tensors, opts=None):
+        """``dist.reduce``: FlexLink's flxReduce (a striped AllReduce whose
+        non-root result goes to scratch), in place on the root."""
+        root = opts.rootRank if opts is not None else 0
+        op = _reduce_op(opts)
+        for t in tensors:
+            self.comm.reduce(t, t, op=_flx_op(op, t), root=root, stream=self._stream)
+            if self.rank() == root:
+                _finish(op, t, self.size())
+        return _DoneWork(tensors, self._stream)
 
     def send(self, *a, **k):
         self._refuse("send")

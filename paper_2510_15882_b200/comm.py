@@ -89,6 +89,7 @@ def load_library() -> ctypes.CDLL:
         "flxCommAbort": [vp],
         "flxCommSplit": [vp, ci, ci, P(vp)],
         "flxBroadcast": [vp, vp, ctypes.c_size_t, ci, ci, vp, vp],
+        "flxReduce": [vp, vp, ctypes.c_size_t, ci, ci, ci, vp, vp],
         "flxCommFinalize": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
@@ -263,6 +264,23 @@ class Communicator:
         _check(load_library().flxAllReduce(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
             dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream, send.get_device())), "flxAllReduce")
+        return recv
+
+    def reduce(self, send, recv=None, op: str = "sum", root: int = 0, stream=None):
+        """``ncclReduce``: the fold of every rank's ``send`` into ``root``'s
+        ``recv`` (``recv`` is not touched on the other ranks and may be None)."""
+        _contiguous_cuda(send, "send")
+        if recv is not None:
+            _contiguous_cuda(recv, "recv")
+            if recv.numel() != send.numel() or recv.dtype != send.dtype:
+                raise ValueError("recv must match send in size and dtype")
+        elif self.rank == root:
+            raise ValueError("the root needs a recv tensor")
+        _check(load_library().flxReduce(
+            ctypes.c_void_p(send.data_ptr()),
+            ctypes.c_void_p(recv.data_ptr() if recv is not None else 0), send.numel(),
+            dtype_code(send.dtype), _OPS[op], root, self._h,
+            _stream_handle(stream, send.get_device())), "flxReduce")
         return recv
 
     def broadcast(self, send, recv=None, root: int = 0, stream=None):
@@ -662,6 +680,14 @@ class Clique:
         if sends[0].numel() % self.nranks:
             raise ValueError("all_to_all buffers must hold nranks equal blocks")
         self._issue(3, args, 0, stream, sends[0].numel() // self.nranks)
+        return recvs
+
+    def reduce(self, sends: Sequence, recvs: Sequence, op: str = "sum", root: int = 0,
+               stream=None):
+        """``recvs[root]`` gets the fold of every virtual rank's send (one group);
+        the other recvs are left as they were."""
+        self._validate(sends, recvs)
+        self._group(lambda i, c: c.reduce(sends[i], recvs[i], op, root, stream))
         return recvs
 
     def broadcast(self, sends: Sequence, recvs: Sequence | None = None, root: int = 0,

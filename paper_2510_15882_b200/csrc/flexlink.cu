@@ -441,6 +441,7 @@ struct Call {
   int op;
   cudaStream_t stream;
   bool avg = false;  // FLX_OP_AVG: ran as a sum; recv is divided by nranks afterwards
+  void* tmp = nullptr;  // flxReduce on a non-root: the AllReduce's scratch recv, freed after
 };
 
 thread_local int t_group_depth = 0;
@@ -771,14 +772,16 @@ flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
                          pinned, g, path_mask(), alignment_for(lead, head.coll));
 }
 
-// FLX_OP_AVG: every member's recv (AllReduce: count elements, ReduceScatter:
-// its recvcount block) divided by nranks on the member's own stream, which the
-// collective's join already ordered after the data landed
-flxResult_t finish_avg(const std::vector<Call>& calls) {
+// After a collective, on each member's own stream (which the collective's join
+// already ordered after the data landed): FLX_OP_AVG divides the recv
+// (AllReduce: count elements, ReduceScatter: its recvcount block) by nranks;
+// flxReduce's non-root scratch is released (stream-ordered)
+flxResult_t finish_calls(const std::vector<Call>& calls) {
   for (const Call& k : calls) {
-    if (!k.avg) continue;
+    if (!k.avg && !k.tmp) continue;
     FLX_CUDA(cudaSetDevice(k.comm->device));
-    FLX_CUDA(launch_div(k.dtype, k.recv, k.count, k.comm->nranks, k.stream));
+    if (k.avg) FLX_CUDA(launch_div(k.dtype, k.recv, k.count, k.comm->nranks, k.stream));
+    if (k.tmp) FLX_CUDA(cudaFreeAsync(k.tmp, k.stream));
   }
   return flxSuccess;
 }
@@ -808,7 +811,7 @@ flxResult_t flush_group() {
       std::vector<Call> one;
       for (auto& v : per) one.push_back(v[k]);
       FLX_TRY(run_world_calls(w, one));
-      FLX_TRY(finish_avg(one));
+      FLX_TRY(finish_calls(one));
     }
   }
   // bucket calls by clique, preserving per-member order
@@ -832,7 +835,7 @@ flxResult_t flush_group() {
       std::vector<Call> one;
       for (auto& v : per) one.push_back(v[k]);
       FLX_TRY(run_clique(clique, one));
-      FLX_TRY(finish_avg(one));
+      FLX_TRY(finish_calls(one));
     }
   }
   return flxSuccess;
@@ -1296,6 +1299,24 @@ flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
   if (count > 0 && sendbuff == recvbuff)
     return fail(flxInvalidArgument, "in-place AllToAll is not supported");
   return enqueue(Call{comm, flxCollAllToAll, sendbuff, recvbuff, count, datatype, 0, stream});
+}
+
+flxResult_t flxReduce(const void* sendbuff, void* recvbuff, size_t count,
+                      flxDataType_t datatype, flxRedOp_t op, int root, flxComm_t comm,
+                      cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
+  FLX_TRY(check_call(comm, datatype, op, true));
+  if (root < 0 || root >= comm->nranks) return fail(flxInvalidArgument, "bad root %d", root);
+  const bool is_root = comm->rank == root;
+  if (count > 0 && (!sendbuff || (is_root && !recvbuff)))
+    return fail(flxInvalidArgument, "null buffer");
+  Call k{comm, flxCollAllReduce, sendbuff, recvbuff, count, datatype, op, stream};
+  if (!is_root && count > 0) {  // the striped AllReduce lands in scratch here
+    FLX_CUDA(cudaSetDevice(comm->device));
+    FLX_CUDA(cudaMallocAsync(&k.tmp, count * dtype_size(datatype), stream));
+    k.recv = k.tmp;
+  }
+  return enqueue(k);
 }
 
 flxResult_t flxBroadcast(const void* sendbuff, void* recvbuff, size_t count,

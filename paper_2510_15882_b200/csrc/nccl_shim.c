@@ -14,7 +14,7 @@
  * takes a communicator checks FlexLink's magic word (flxComm validation) and
  * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
  * it.  The NCCL calls FlexLink does not implement but that take a
- * communicator (Reduce, Gather, Scatter, Send, Recv, CommShrink, DevCommCreate,
+ * communicator (Gather, Scatter, Send, Recv, CommShrink, DevCommCreate,
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
@@ -208,9 +208,9 @@ static ncclResult_t unsupported(ncclComm_t comm, const char* what) {
 ncclResult_t ncclReduce(const void* sendbuff, void* recvbuff, size_t count,
                         ncclDataType_t datatype, ncclRedOp_t op, int root, ncclComm_t comm,
                         cudaStream_t stream) {
-  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)op; (void)root;
-  (void)stream;
-  return unsupported(comm, "ncclReduce is not implemented by FlexLink");
+  if ((int)op > (int)ncclAvg) return ncclInvalidArgument; /* PreMulSum ops */
+  return (ncclResult_t)flxReduce(sendbuff, recvbuff, count, (flxDataType_t)datatype,
+                                 (flxRedOp_t)op, root, (flxComm_t)comm, stream);
 }
 
 /* ncclBroadcast / ncclBcast: FlexLink's bit-exact broadcast (flxBroadcast) */

@@ -107,9 +107,14 @@ def main():
     if bad:
         print(f"rank {rank} broadcast / DDP mismatch", flush=True)
     dist.barrier()
-    try:
-        dist.reduce(x, 0)
-        bad += 1  # must refuse, not fall back
+    # reduce to rank 0 (flxReduce): the sum there, the other ranks untouched
+    rx = vals(rank, n).to(dev)
+    dist.reduce(rx, 0)
+    bad += int(not torch.equal(rx, sum(vals(r, n) for r in range(world)).to(dev) if rank == 0
+                               else vals(rank, n).to(dev)))
+    try:  # a collective FlexLink does not implement is refused, never a fallback
+        dist.scatter(x, [x.clone() for _ in range(world)] if rank == 0 else None, src=0)
+        bad += 1
     except Exception as e:
         if "not a FlexLink collective" not in str(e):
             bad += 1

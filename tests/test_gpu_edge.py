@@ -175,3 +175,29 @@ def test_average_is_the_striped_sum_divided(loopback):
                 assert torch.equal(r, want), dt
             for i, r in enumerate(rs):
                 assert torch.equal(r, want[i * blk:(i + 1) * blk]), dt
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_reduce_lands_on_the_root_only(loopback):
+    """flxReduce / ncclReduce: the striped fold lands in the root's recv; the
+    other ranks' recvs are untouched (their result goes to stream-ordered
+    scratch); in place on the root; AVG and MAX too."""
+    n, count = 4, (1 << 18) + 9
+    with flx.Clique(n, loopback=loopback) as c:
+        c.set_shares(CollectiveOp.ALLREDUCE, (900, 100, 0))
+        g = torch.Generator(device="cuda").manual_seed(13)
+        sends = [torch.randint(-500, 500, (count,), device="cuda", generator=g).float()
+                 for _ in range(n)]
+        for op, want in (("sum", torch.stack(sends).sum(0)), ("max", torch.stack(sends).amax(0)),
+                         ("avg", torch.stack(sends).sum(0) / 4)):
+            for root in (0, 2):
+                recvs = [torch.full_like(x, 3.0) for x in sends]
+                c.reduce(sends, recvs, op=op, root=root)
+                torch.cuda.synchronize()
+                for r, x in enumerate(recvs):
+                    assert torch.equal(x, want if r == root else torch.full_like(x, 3.0)), (op, r)
+        keep = [x.clone() for x in sends]
+        c.reduce(sends, sends, root=1)  # in place
+        torch.cuda.synchronize()
+        assert torch.equal(sends[1], torch.stack(keep).sum(0))
+        assert all(torch.equal(sends[r], keep[r]) for r in (0, 2, 3))

@@ -1,7 +1,7 @@
 """PyTorch's own, unmodified NCCL process group running on FlexLink through
 LD_PRELOAD=libflexlink_nccl.so: ProcessGroupNCCL creates its communicator with
 ncclCommInitRankConfig and issues ncclAllReduce / ncclAllGather /
-ncclReduceScatter, ncclBroadcast, ncclAlltoAll (and ncclCommSplit for dist.new_group), which the shim
+ncclReduceScatter, ncclReduce, ncclBroadcast, ncclAlltoAll (and ncclCommSplit for dist.new_group), which the shim
 resolves to FlexLink.  Prints one JSON line:
 the results' exactness and how many FlexLink kernels ran (flxGetLaunchCount).
 Run:  LD_PRELOAD=$PWD/paper_2510_15882_b200/libflexlink_nccl.so python tools/torch_nccl_preload.py
@@ -54,6 +54,10 @@ def main() -> None:
     avg = mine.clone()
     dist.all_reduce(avg, op=dist.ReduceOp.AVG)
     ok["all_reduce_avg"] = bool(torch.equal(avg, torch.stack(every).sum(0) / world))
+    # reduce to the last rank (ncclReduce): the sum there, other ranks untouched
+    red = mine.clone()
+    dist.reduce(red, dst=world - 1)
+    ok["reduce"] = bool(torch.equal(red, torch.stack(every).sum(0) if rank == world - 1 else mine))
     # all_to_all_single, equal splits: PyTorch built against NCCL 2.28 calls
     # ncclAlltoAll, which the shim maps to flxAllToAll
     a2a = torch.empty_like(mine)

@@ -179,6 +179,15 @@ flxResult_t flxAllToAll(const void* sendbuff, void* recvbuff, size_t count,
 flxResult_t flxReduce(const void* sendbuff, void* recvbuff, size_t count,
                       flxDataType_t datatype, flxRedOp_t op, int root, flxComm_t comm,
                       cudaStream_t stream);
+/* ncclGather / ncclScatter (NCCL 2.28): Gather = an AllGather whose non-root
+ * output goes to stream-ordered scratch (the root's recvbuff holds rank i's
+ * count elements at i*count); Scatter = an AllToAll in which only the root's
+ * blocks are kept, block `root` of the result copied to recvbuff.  For
+ * completeness of the NCCL surface, not a hot path (N times a tree's traffic). */
+flxResult_t flxGather(const void* sendbuff, void* recvbuff, size_t count,
+                      flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream);
+flxResult_t flxScatter(const void* sendbuff, void* recvbuff, size_t count,
+                       flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream);
 /* ncclBroadcast (nccl.h ncclBroadcast): rank `root`'s sendbuff (count
  * elements) lands in every rank's recvbuff; in place when sendbuff == recvbuff.
  * Runs as one striped AllReduce of the bytes with MAX over uint8, the non-roots

@@ -90,6 +90,8 @@ def load_library() -> ctypes.CDLL:
         "flxCommSplit": [vp, ci, ci, P(vp)],
         "flxBroadcast": [vp, vp, ctypes.c_size_t, ci, ci, vp, vp],
         "flxReduce": [vp, vp, ctypes.c_size_t, ci, ci, ci, vp, vp],
+        "flxGather": [vp, vp, ctypes.c_size_t, ci, ci, vp, vp],
+        "flxScatter": [vp, vp, ctypes.c_size_t, ci, ci, vp, vp],
         "flxCommFinalize": [vp],
         "flxCommCount": [vp, P(ci)],
         "flxCommUserRank": [vp, P(ci)],
@@ -264,6 +266,35 @@ class Communicator:
         _check(load_library().flxAllReduce(
             ctypes.c_void_p(send.data_ptr()), ctypes.c_void_p(recv.data_ptr()), send.numel(),
             dtype_code(send.dtype), _OPS[op], self._h, _stream_handle(stream, send.get_device())), "flxAllReduce")
+        return recv
+
+    def gather(self, send, recv=None, root: int = 0, stream=None):
+        """``ncclGather``: every rank's ``send`` into ``root``'s ``recv`` (rank i's
+        elements at i*send.numel()); ``recv`` is unused elsewhere."""
+        _contiguous_cuda(send, "send")
+        if self.rank == root:
+            _contiguous_cuda(recv, "recv")
+            if recv.numel() != send.numel() * self.nranks or recv.dtype != send.dtype:
+                raise ValueError("the root's recv holds nranks blocks of send's size and dtype")
+        _check(load_library().flxGather(
+            ctypes.c_void_p(send.data_ptr()),
+            ctypes.c_void_p(recv.data_ptr() if recv is not None else 0), send.numel(),
+            dtype_code(send.dtype), root, self._h, _stream_handle(stream, send.get_device())),
+            "flxGather")
+        return recv
+
+    def scatter(self, send, recv, root: int = 0, stream=None):
+        """``ncclScatter``: block i of ``root``'s ``send`` (nranks blocks of
+        recv.numel()) into rank i's ``recv``; ``send`` is unused elsewhere."""
+        _contiguous_cuda(recv, "recv")
+        if self.rank == root:
+            _contiguous_cuda(send, "send")
+            if send.numel() != recv.numel() * self.nranks or recv.dtype != send.dtype:
+                raise ValueError("the root's send holds nranks blocks of recv's size and dtype")
+        _check(load_library().flxScatter(
+            ctypes.c_void_p(send.data_ptr() if send is not None else 0),
+            ctypes.c_void_p(recv.data_ptr()), recv.numel(), dtype_code(recv.dtype), root,
+            self._h, _stream_handle(stream, recv.get_device())), "flxScatter")
         return recv
 
     def reduce(self, send, recv=None, op: str = "sum", root: int = 0, stream=None):
@@ -680,6 +711,16 @@ class Clique:
         if sends[0].numel() % self.nranks:
             raise ValueError("all_to_all buffers must hold nranks equal blocks")
         self._issue(3, args, 0, stream, sends[0].numel() // self.nranks)
+        return recvs
+
+    def gather(self, sends: Sequence, recvs: Sequence, root: int = 0, stream=None):
+        """``recvs[root]`` gets every virtual rank's send in rank order (one group)."""
+        self._group(lambda i, c: c.gather(sends[i], recvs[i], root, stream))
+        return recvs
+
+    def scatter(self, sends: Sequence, recvs: Sequence, root: int = 0, stream=None):
+        """``recvs[i]`` gets block i of ``sends[root]`` (one group)."""
+        self._group(lambda i, c: c.scatter(sends[i], recvs[i], root, stream))
         return recvs
 
     def reduce(self, sends: Sequence, recvs: Sequence, op: str = "sum", root: int = 0,

@@ -441,7 +441,12 @@ struct Call {
   int op;
   cudaStream_t stream;
   bool avg = false;  // FLX_OP_AVG: ran as a sum; recv is divided by nranks afterwards
-  void* tmp = nullptr;  // flxReduce on a non-root: the AllReduce's scratch recv, freed after
+  void* tmp = nullptr;  // flxReduce / flxGather / flxScatter scratch, freed after
+  void* tmp2 = nullptr;
+  // flxScatter: after the collective, copy bytes from post_src to post_dst
+  void* post_dst = nullptr;
+  const void* post_src = nullptr;
+  size_t post_bytes = 0;
 };
 
 thread_local int t_group_depth = 0;
@@ -778,10 +783,14 @@ flxResult_t run_world_calls(World* w, const std::vector<Call>& calls) {
 // flxReduce's non-root scratch is released (stream-ordered)
 flxResult_t finish_calls(const std::vector<Call>& calls) {
   for (const Call& k : calls) {
-    if (!k.avg && !k.tmp) continue;
+    if (!k.avg && !k.tmp && !k.post_bytes) continue;
     FLX_CUDA(cudaSetDevice(k.comm->device));
     if (k.avg) FLX_CUDA(launch_div(k.dtype, k.recv, k.count, k.comm->nranks, k.stream));
+    if (k.post_bytes)
+      FLX_CUDA(cudaMemcpyAsync(k.post_dst, k.post_src, k.post_bytes, cudaMemcpyDeviceToDevice,
+                               k.stream));
     if (k.tmp) FLX_CUDA(cudaFreeAsync(k.tmp, k.stream));
+    if (k.tmp2) FLX_CUDA(cudaFreeAsync(k.tmp2, k.stream));
   }
   return flxSuccess;
 }
@@ -1316,6 +1325,52 @@ flxResult_t flxReduce(const void* sendbuff, void* recvbuff, size_t count,
     FLX_CUDA(cudaMallocAsync(&k.tmp, count * dtype_size(datatype), stream));
     k.recv = k.tmp;
   }
+  return enqueue(k);
+}
+
+flxResult_t flxGather(const void* sendbuff, void* recvbuff, size_t count,
+                      flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
+  FLX_TRY(check_call(comm, datatype, 0, false));
+  if (root < 0 || root >= comm->nranks) return fail(flxInvalidArgument, "bad root %d", root);
+  const bool is_root = comm->rank == root;
+  if (count > 0 && (!sendbuff || (is_root && !recvbuff)))
+    return fail(flxInvalidArgument, "null buffer");
+  // the root's recvbuff is exactly an AllGather's output (and NCCL's in-place
+  // rule for Gather, sendbuff == recvbuff + root*count, is AllGather's);
+  // elsewhere the gathered blocks land in scratch
+  Call k{comm, flxCollAllGather, sendbuff, recvbuff, count, datatype, 0, stream};
+  if (!is_root && count > 0) {
+    FLX_CUDA(cudaSetDevice(comm->device));
+    FLX_CUDA(cudaMallocAsync(&k.tmp, count * dtype_size(datatype) * comm->nranks, stream));
+    k.recv = k.tmp;
+  }
+  return enqueue(k);
+}
+
+flxResult_t flxScatter(const void* sendbuff, void* recvbuff, size_t count,
+                       flxDataType_t datatype, int root, flxComm_t comm, cudaStream_t stream) {
+  flx::CtxGuard ctx_guard;  // the caller's context is restored on return
+  FLX_TRY(check_call(comm, datatype, 0, false));
+  if (root < 0 || root >= comm->nranks) return fail(flxInvalidArgument, "bad root %d", root);
+  const bool is_root = comm->rank == root;
+  if (count > 0 && (!recvbuff || (is_root && !sendbuff)))
+    return fail(flxInvalidArgument, "null buffer");
+  if (count == 0) return flxSuccess;
+  // an AllToAll in which only the root's blocks matter: block j of the root's
+  // sendbuff reaches rank j's scratch block `root`, copied to recvbuff after
+  const size_t block = count * dtype_size(datatype), all = block * comm->nranks;
+  FLX_CUDA(cudaSetDevice(comm->device));
+  Call k{comm, flxCollAllToAll, sendbuff, nullptr, count, datatype, 0, stream};
+  FLX_CUDA(cudaMallocAsync(&k.tmp, all, stream));
+  k.recv = k.tmp;
+  if (!is_root) {  // this rank's outgoing blocks are never read by anyone
+    FLX_CUDA(cudaMallocAsync(&k.tmp2, all, stream));
+    k.send = k.tmp2;
+  }
+  k.post_dst = recvbuff;
+  k.post_src = static_cast<const char*>(k.tmp) + (size_t)root * block;
+  k.post_bytes = block;
   return enqueue(k);
 }
 

@@ -14,7 +14,7 @@
  * takes a communicator checks FlexLink's magic word (flxComm validation) and
  * rejects a real ncclComm_t with ncclInvalidArgument instead of dereferencing
  * it.  The NCCL calls FlexLink does not implement but that take a
- * communicator (Gather, Scatter, Send, Recv, CommShrink, DevCommCreate,
+ * communicator (Send, Recv, CommShrink, DevCommCreate,
  * buffer/window registration, PreMulSum ops) are DEFINED here and return
  * ncclInvalidUsage: without them a preloaded process would hand a FlexLink
  * communicator to the real libnccl, which would dereference it as its own
@@ -229,14 +229,14 @@ ncclResult_t ncclBroadcast(const void* sendbuff, void* recvbuff, size_t count,
 
 ncclResult_t ncclGather(const void* sendbuff, void* recvbuff, size_t count,
                         ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream) {
-  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
-  return unsupported(comm, "ncclGather is not implemented by FlexLink");
+  return (ncclResult_t)flxGather(sendbuff, recvbuff, count, (flxDataType_t)datatype, root,
+                                 (flxComm_t)comm, stream);
 }
 
 ncclResult_t ncclScatter(const void* sendbuff, void* recvbuff, size_t count,
                          ncclDataType_t datatype, int root, ncclComm_t comm, cudaStream_t stream) {
-  (void)sendbuff; (void)recvbuff; (void)count; (void)datatype; (void)root; (void)stream;
-  return unsupported(comm, "ncclScatter is not implemented by FlexLink");
+  return (ncclResult_t)flxScatter(sendbuff, recvbuff, count, (flxDataType_t)datatype, root,
+                                  (flxComm_t)comm, stream);
 }
 
 ncclResult_t ncclDevCommCreate(ncclComm_t comm, const void* reqs, void* outDevComm) {

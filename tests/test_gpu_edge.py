@@ -201,3 +201,32 @@ def test_reduce_lands_on_the_root_only(loopback):
         torch.cuda.synchronize()
         assert torch.equal(sends[1], torch.stack(keep).sum(0))
         assert all(torch.equal(sends[r], keep[r]) for r in (0, 2, 3))
+
+
+@pytest.mark.parametrize("loopback", [False, True])
+def test_gather_and_scatter(loopback):
+    """flxGather / flxScatter (NCCL 2.28's ncclGather / ncclScatter): the root's
+    recv holds every rank's block in rank order; every rank receives its block
+    of the root's send; non-root recvs / sends are not touched."""
+    n, count = 4, (1 << 16) + 5
+    with flx.Clique(n, loopback=loopback) as c:
+        for op in (CollectiveOp.ALLGATHER, CollectiveOp.ALLTOALL):
+            c.set_shares(op, (900, 100, 0))
+        g = torch.Generator(device="cuda").manual_seed(17)
+        for dt in (torch.float32, torch.bfloat16):
+            sends = [torch.randn(count, device="cuda", generator=g).to(dt) for _ in range(n)]
+            for root in (0, 3):
+                recvs = [torch.full((n * count,), 5.0, device="cuda", dtype=dt) for _ in range(n)]
+                c.gather(sends, recvs, root=root)
+                torch.cuda.synchronize()
+                for r, x in enumerate(recvs):
+                    want = torch.cat(sends) if r == root else torch.full_like(x, 5.0)
+                    assert torch.equal(x, want), ("gather", dt, root, r)
+                big = [torch.randn(n * count, device="cuda", generator=g).to(dt) for _ in range(n)]
+                keep = [b.clone() for b in big]
+                outs = [torch.empty(count, device="cuda", dtype=dt) for _ in range(n)]
+                c.scatter(big, outs, root=root)
+                torch.cuda.synchronize()
+                for r, x in enumerate(outs):
+                    assert torch.equal(x, keep[root][r * count:(r + 1) * count]), ("scatter", dt, r)
+                assert all(torch.equal(b, k) for b, k in zip(big, keep))

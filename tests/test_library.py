@@ -172,3 +172,25 @@ def test_flx_shares_env_is_validated_at_init(lib, monkeypatch):
         monkeypatch.setenv("FLX_SHARES", bad)
         assert lib.flxCommInitAll(comms, 2, None) == 4, bad
         assert b"FLX_SHARES" in lib.flxGetLastError(), bad
+
+
+def test_shim_defines_every_communicator_call_pytorch_imports(lib):
+    """Under LD_PRELOAD every NCCL call PyTorch's ProcessGroupNCCL can make with a
+    communicator must resolve to the shim (implemented or refused): one that fell
+    through to libnccl would get a FlexLink handle as its own struct.  Only the
+    communicator-free calls may still resolve to NCCL."""
+    import torch
+
+    torch_cuda = Path(torch.__file__).parent / "lib" / "libtorch_cuda.so"
+    shim = comm.library_path().parent / "libflexlink_nccl.so"
+    if not torch_cuda.exists() or not shim.exists():
+        pytest.skip("libtorch_cuda.so or the shim is absent")
+    imported = {line.split()[-1] for line in subprocess.run(
+        ["nm", "-D", str(torch_cuda)], capture_output=True, text=True, check=True).stdout
+        .splitlines() if " U nccl" in line}
+    defined = {line.split()[-1] for line in subprocess.run(
+        ["nm", "-D", "--defined-only", str(shim)], capture_output=True, text=True,
+        check=True).stdout.splitlines() if " T " in line}
+    assert imported, "libtorch_cuda.so imports no NCCL symbols?"
+    assert imported - defined <= {"ncclGroupSimulateEnd", "ncclMemAlloc", "ncclMemFree"}, \
+        sorted(imported - defined)

@@ -20,7 +20,7 @@ enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
 ``async_op=False`` path), so the returned work objects are complete from the
 stream's point of view.  Broadcast is FlexLink's bit-exact flxBroadcast (DDP's
 construction-time state sync).  Operations FlexLink does
-not implement (send/recv, gather/scatter, uneven all_to_all splits,
+not implement (send/recv, uneven all_to_all splits,
 ReduceOp.AVG on integer tensors) raise ``NotImplementedError`` instead of
 silently falling back to another library.  ReduceOp.AVG on floating tensors is
 the striped sum divided by the group size in place (fl(fl(sum) / n)).
@@ -222,7 +222,7 @@ class FlexLinkBackend(dist.ProcessGroup):
     # -- not implemented by FlexLink: refuse, never fall back
     def _refuse(self, name):
         raise NotImplementedError(f"{name} is not a FlexLink collective (AllReduce, AllGather, "
-                                  f"ReduceScatter, AllToAll, Reduce, Broadcast are)")
+                                  f"ReduceScatter, AllToAll, Reduce, Broadcast, Gather, Scatter are)")
 
     def broadcast(self, tensors, opts=None):
         """Bit-exact broadcast (DDP's module-state sync at construction):
@@ -255,11 +255,33 @@ class FlexLinkBackend(dist.ProcessGroup):
     def recv(self, *a, **k):
         self._refuse("recv")
 
-    def gather(self, *a, **k):
-        self._refuse("gather")
+    def gather(self, output_tensors, input_tensors, opts=None):
+        """``dist.gather``: flxGather into one flat buffer on the root, then the
+        root's output list is filled from it."""
+        root = opts.rootRank if opts is not None else 0
+        n, me = self.size(), self.rank()
+        for i, inp in enumerate(input_tensors):
+            inp = inp.contiguous()
+            flat = torch.empty(n * inp.numel(), dtype=inp.dtype, device=inp.device) \
+                if me == root else None
+            self.comm.gather(inp, flat, root=root, stream=self._stream)
+            if me == root:
+                for r, o in enumerate(output_tensors[i]):
+                    o.copy_(flat[r * inp.numel():(r + 1) * inp.numel()].view_as(o))
+        return _DoneWork(output_tensors, self._stream)
 
-    def scatter(self, *a, **k):
-        self._refuse("scatter")
+    def scatter(self, output_tensors, input_tensors, opts=None):
+        """``dist.scatter``: the root's list flattened, flxScatter into each
+        rank's output."""
+        root = opts.rootRank if opts is not None else 0
+        me = self.rank()
+        for i, out in enumerate(output_tensors):
+            flat = torch.cat([t.reshape(-1) for t in input_tensors[i]]) if me == root else None
+            res = out if out.is_contiguous() else torch.empty_like(out)
+            self.comm.scatter(flat, res.view(-1), root=root, stream=self._stream)
+            if res is not out:
+                out.copy_(res)
+        return _DoneWork(output_tensors, self._stream)
 
 
 def _create(store, rank, size, timeout):

@@ -112,11 +112,24 @@ def main():
     dist.reduce(rx, 0)
     bad += int(not torch.equal(rx, sum(vals(r, n) for r in range(world)).to(dev) if rank == 0
                                else vals(rank, n).to(dev)))
+    # gather / scatter to and from the last rank (flxGather / flxScatter)
+    last = world - 1
+    gl = [torch.empty(n, device=dev) for _ in range(world)] if rank == last else None
+    dist.gather(vals(rank, n).to(dev), gl, dst=last)
+    if rank == last:
+        bad += int(not all(torch.equal(g, vals(r, n).to(dev)) for r, g in enumerate(gl)))
+    sc = torch.empty(n, device=dev)
+    dist.scatter(sc, [vals(r, n, 5).to(dev) for r in range(world)] if rank == last else None,
+                 src=last)
+    bad += int(not torch.equal(sc, vals(rank, n, 5).to(dev)))
     try:  # a collective FlexLink does not implement is refused, never a fallback
-        dist.scatter(x, [x.clone() for _ in range(world)] if rank == 0 else None, src=0)
-        bad += 1
+        dist.all_to_all_single(torch.empty(n, device=dev), x,
+                               output_split_sizes=[n - world + 1] + [1] * (world - 1),
+                               input_split_sizes=[n - world + 1] + [1] * (world - 1))
+        if world > 1:
+            bad += 1
     except Exception as e:
-        if "not a FlexLink collective" not in str(e):
+        if "FlexLink" not in str(e):
             bad += 1
     torch.cuda.synchronize()
     print(f"rank {rank} bad {bad}", flush=True)

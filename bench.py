@@ -638,7 +638,7 @@ def run_single_gpu(args) -> None:
             "traffic": ncu_traffic() if pbytes[PathKind.NVLINK] == AR_BYTES else None,
             "traffic_source": "profiles/r2/fold_once_ncu_summary.txt (ncu --set full, same "
                               "kernel and size; dram__bytes_read.sum + dram__bytes_write.sum)",
-            "kernel": "fold_once_kernel<float,Sum,8> (NVLink-path slice, 8 virtual ranks, "
+            "kernel": "fold_once_kernel<float,Sum,8,1024> (NVLink-path slice, 8 virtual ranks, "
                       "one 16 B vector per thread)",
             "algorithmic_bytes_per_launch": nv_alg_bytes,
             "kernel_ms": round(nv_ms, 4),

@@ -190,9 +190,13 @@ __global__ void __launch_bounds__(512) fold_vec_kernel(const FoldArgs a) {
 
 // Single-pass form: exactly one 16 B vector per thread, grid covers the slice.
 // No loop-invariant address hoisting, so few registers (high occupancy) and
-// CTA turnover instead of a grid-stride tail: the uncapped default.
-template <typename T, int OP, int NMAX>
-__global__ void __launch_bounds__(512) fold_once_kernel(const FoldArgs a) {
+// CTA turnover instead of a grid-stride tail: the uncapped default.  THREADS =
+// 1024 for up to 8 ranks: each CTA streams 16 KiB runs of every source and
+// destination, +1.4 % over 512-thread CTAs at 8 x 256 MiB (6.85 vs 6.75 TB/s,
+// profiles/r2/fold_occupancy.jsonl — more CTAs per SM or more vectors per
+// thread do not help)
+template <typename T, int OP, int NMAX, int THREADS = 512>
+__global__ void __launch_bounds__(THREADS) fold_once_kernel(const FoldArgs a) {
   using A = typename AccT<T>::type;
   constexpr int kVec = 16 / sizeof(T);
   const size_t nvec = a.bytes >> 4;

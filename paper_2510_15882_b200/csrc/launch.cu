@@ -56,12 +56,16 @@ cudaError_t fold_typed(const FoldArgs& a, int grid, cudaStream_t s) {
   }
   const size_t nvec = a.bytes >> 4;
   if ((size_t)grid * 512 >= nvec) {  // uncapped: single pass, one vector per thread
-    const int once = (int)((nvec + 16 + 511) / 512);
+    // (the grid covers nvec + 16 threads: the ragged tail's elements)
+    // 1024-thread CTAs for up to 8 ranks of 2- and 4-byte types (64-bit and
+    // 1-byte ones would spill under the 64-register cap of a 1024-thread CTA)
+    constexpr int kT = (sizeof(T) == 2 || sizeof(T) == 4) ? 1024 : 512;
     const int width = a.n > a.ndst ? a.n : a.ndst;
-    if (width <= 2) fold_once_kernel<T, OP, 2><<<once, 512, 0, s>>>(a);
-    else if (width <= 4) fold_once_kernel<T, OP, 4><<<once, 512, 0, s>>>(a);
-    else if (width <= 8) fold_once_kernel<T, OP, 8><<<once, 512, 0, s>>>(a);
-    else fold_once_kernel<T, OP, 16><<<once, 512, 0, s>>>(a);
+    const int once = (int)((nvec + 16 + kT - 1) / kT);
+    if (width <= 2) fold_once_kernel<T, OP, 2, kT><<<once, kT, 0, s>>>(a);
+    else if (width <= 4) fold_once_kernel<T, OP, 4, kT><<<once, kT, 0, s>>>(a);
+    else if (width <= 8) fold_once_kernel<T, OP, 8, kT><<<once, kT, 0, s>>>(a);
+    else fold_once_kernel<T, OP, 16><<<(int)((nvec + 16 + 511) / 512), 512, 0, s>>>(a);
     return cudaGetLastError();
   }
   const int width = a.n > a.ndst ? a.n : a.ndst;
@@ -255,7 +259,7 @@ cudaError_t launch_div(int dtype, void* buf, size_t count, int n, cudaStream_t s
 }
 
 cudaError_t preload_launch_cu() {
-  return preload_module((const void*)fold_once_kernel<float, kSum, 8>);
+  return preload_module((const void*)fold_once_kernel<float, kSum, 8, 1024>);
 }
 
 }  // namespace flx

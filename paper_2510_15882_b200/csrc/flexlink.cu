@@ -450,6 +450,7 @@ struct Call {
 };
 
 thread_local int t_group_depth = 0;
+thread_local std::vector<void*> t_freed;  // scratch finish_calls released in this flush
 thread_local std::vector<Call> t_pending;
 
 // The autotuner's view of a clique: one timing ring, one process (no
@@ -789,15 +790,35 @@ flxResult_t finish_calls(const std::vector<Call>& calls) {
     if (k.post_bytes)
       FLX_CUDA(cudaMemcpyAsync(k.post_dst, k.post_src, k.post_bytes, cudaMemcpyDeviceToDevice,
                                k.stream));
-    if (k.tmp) FLX_CUDA(cudaFreeAsync(k.tmp, k.stream));
-    if (k.tmp2) FLX_CUDA(cudaFreeAsync(k.tmp2, k.stream));
+    for (void* t : {k.tmp, k.tmp2})
+      if (t) {
+        t_freed.push_back(t);
+        FLX_CUDA(cudaFreeAsync(t, k.stream));
+      }
   }
   return flxSuccess;
 }
 
+flxResult_t flush_group_calls(const std::vector<Call>& calls);
+
+// A group that fails before a call ran still releases that call's scratch
+// (stream-ordered: after whatever did run).
 flxResult_t flush_group() {
   std::vector<Call> calls;
   calls.swap(t_pending);
+  t_freed.clear();
+  const flxResult_t r = flush_group_calls(calls);
+  if (r != flxSuccess)
+    for (const Call& k : calls)
+      for (void* t : {k.tmp, k.tmp2})
+        if (t && std::find(t_freed.begin(), t_freed.end(), t) == t_freed.end()) {
+          cudaSetDevice(k.comm->device);
+          cudaFreeAsync(t, k.stream);
+        }
+  return r;
+}
+
+flxResult_t flush_group_calls(const std::vector<Call>& calls) {
   // multi-rank worlds: bucket by world, by local rank
   std::map<World*, std::vector<std::vector<Call>>> by_world;
   std::vector<World*> world_order;

@@ -230,3 +230,22 @@ def test_gather_and_scatter(loopback):
                 for r, x in enumerate(outs):
                     assert torch.equal(x, keep[root][r * count:(r + 1) * count]), ("scatter", dt, r)
                 assert all(torch.equal(b, k) for b, k in zip(big, keep))
+
+
+def test_failed_group_with_reduce_scratch_is_refused_cleanly():
+    """A group whose members do not all take part fails at its end; flxReduce's
+    non-root scratch in it is released (stream-ordered) and the communicator
+    keeps working."""
+    n, count = 4, 1 << 16
+    L = flx.load_library()
+    with flx.Clique(n) as c:
+        s = [torch.ones(count, device="cuda") * (i + 1) for i in range(n)]
+        r = [torch.zeros(count, device="cuda") for _ in range(n)]
+        assert L.flxGroupStart() == 0
+        c.comms[1].reduce(s[1], r[1], root=0)  # non-root: scratch allocated
+        c.comms[2].reduce(s[2], r[2], root=0)
+        assert L.flxGroupEnd() != 0  # ranks 0 and 3 never joined
+        torch.cuda.synchronize()
+        c.reduce(s, r, root=0)
+        torch.cuda.synchronize()
+        assert torch.equal(r[0], torch.full_like(r[0], n * (n + 1) / 2))

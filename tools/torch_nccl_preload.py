@@ -23,9 +23,11 @@ def main() -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
     os.environ.setdefault("MASTER_PORT", "29561")
-    torch.cuda.set_device(0)
+    # one GPU per rank where the box has them (LOCAL_RANK); the one-GPU tests share cuda:0
+    dev = int(os.environ.get("LOCAL_RANK", rank)) if torch.cuda.device_count() > 1 else 0
+    torch.cuda.set_device(dev)
     dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", 0))
+                            device_id=torch.device("cuda", dev))
     flx = ctypes.CDLL(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "paper_2510_15882_b200", "libflexlink.so"))
     count = ctypes.c_ulonglong()

@@ -20,10 +20,10 @@ enqueued on the caller's current CUDA stream (stream-ordered like NCCL's
 ``async_op=False`` path), so the returned work objects are complete from the
 stream's point of view.  Broadcast is FlexLink's bit-exact flxBroadcast (DDP's
 construction-time state sync).  Operations FlexLink does
-not implement (send/recv, uneven all_to_all splits,
-ReduceOp.AVG on integer tensors) raise ``NotImplementedError`` instead of
-silently falling back to another library.  ReduceOp.AVG on floating tensors is
-the striped sum divided by the group size in place (fl(fl(sum) / n)).
+not implement (send/recv, uneven all_to_all splits) raise
+``NotImplementedError`` instead of silently falling back to another library.
+ReduceOp.AVG is the library's FLX_OP_AVG (the striped sum, then one division by
+the group size: fl(fl(sum) / n) for floats, C division for integers).
 """
 
 from __future__ import annotations
@@ -81,21 +81,15 @@ def _reduce_op(opts) -> str:
 
 
 def _flx_op(op: str, t: torch.Tensor) -> str:
-    """The FlexLink reduction that runs for `op` on `t`: AVG is the striped sum
-    followed by `_finish` (floating types only — NCCL's integer average has no
-    FlexLink counterpart)."""
-    if op != "avg":
-        return op
-    if not t.is_floating_point():
-        raise NotImplementedError("ReduceOp.AVG needs a floating-point tensor on FlexLink")
-    return "sum"
+    """The FlexLink reduction that runs for `op` on `t`.  AVG is the library's
+    FLX_OP_AVG (== ncclAvg): the striped sum, then one division by the group
+    size on the caller's stream — IEEE division for floating types
+    (fl(fl(sum) / n)), C division for integers, as NCCL divides integer sums."""
+    return op
 
 
 def _finish(op: str, t: torch.Tensor, size: int) -> None:
-    """AVG: the rank-order sum divided by the group size in place, on the caller's
-    stream (rounding: fl(fl(sum) / n), not NCCL's pre-multiplied sum)."""
-    if op == "avg":
-        t.div_(size)
+    """Nothing left to do after a FlexLink reduction (AVG divides in the library)."""
 
 
 class FlexLinkBackend(dist.ProcessGroup):

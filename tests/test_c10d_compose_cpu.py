@@ -1,8 +1,8 @@
 """Host logic of the 'flexlink' c10d backend at world size 2, on CPU (gloo).
 
 FlexLinkBackend's composed operations — broadcast on the bytes of any dtype
-(flxBroadcast's zeros-then-MAX-over-uint8 rule), ReduceOp.AVG as the sum then a
-divide — run here with a stand-in communicator whose broadcast / all_reduce /
+(flxBroadcast's zeros-then-MAX-over-uint8 rule), ReduceOp.AVG passed to the
+library as FLX_OP_AVG (floats and integers) — run here with a stand-in communicator whose broadcast / all_reduce /
 reduce_scatter are gloo's, so byte views, the root's placement and ragged
 lengths are checked across two real processes without a GPU.  The GPU
 test (tests/test_gpu_c10d.py) runs the same methods over the real kernels.
@@ -43,17 +43,28 @@ def _worker(rank: int, world: int, port: int, q) -> None:
         def all_gather(self, send, recv, stream=None):
             dist.all_gather_into_tensor(recv, send)
 
+        @staticmethod
+        def _avg(t):  # FLX_OP_AVG's finish: IEEE division for floats, C division for ints
+            if t.is_floating_point():
+                t.copy_(t / torch.full_like(t, world))
+            else:
+                t.copy_(torch.div(t, world, rounding_mode="trunc"))
+
         def all_reduce(self, send, recv, op="sum", stream=None):
-            assert op == "sum", op
+            assert op in ("sum", "avg"), op
             recv.copy_(send)
             dist.all_reduce(recv)
+            if op == "avg":
+                self._avg(recv)
 
         def reduce_scatter(self, send, recv, op="sum", stream=None):
-            assert op == "sum", op
+            assert op in ("sum", "avg"), op
             full = send.clone()
             dist.all_reduce(full)
             n = recv.numel()
             recv.copy_(full[rank * n:(rank + 1) * n])
+            if op == "avg":
+                self._avg(recv)
 
     class Host(c10d.FlexLinkBackend):
         def __init__(self):
@@ -95,11 +106,11 @@ def _worker(rank: int, world: int, port: int, q) -> None:
     full = sum(torch.arange(4 * world, dtype=torch.float32) * (r + 1) for r in range(world))
     if not torch.equal(out, full[rank * 4:(rank + 1) * 4] / world):
         bad.append("reduce_scatter avg")
-    try:
-        be.allreduce([torch.ones(3, dtype=torch.int32)], o)
-        bad.append("integer avg accepted")
-    except NotImplementedError:
-        pass
+    xi = torch.tensor([7, -7, 3], dtype=torch.int32) * (rank + 1)
+    be.allreduce([xi], o)  # integers: C division of the sum (truncation), as NCCL
+    si = sum(torch.tensor([7, -7, 3], dtype=torch.int64) * (r + 1) for r in range(world))
+    if not torch.equal(xi, torch.div(si, world, rounding_mode="trunc").to(torch.int32)):
+        bad.append("integer avg")
     dist.destroy_process_group()
     q.put((rank, bad))
 

@@ -68,17 +68,19 @@ print("ok")
     assert "ok" in out.stdout
 
 
-def test_avg_is_a_float_sum_then_divide():
+def test_avg_goes_to_the_library_for_every_dtype():
+    """ReduceOp.AVG is passed through as the library's FLX_OP_AVG (== ncclAvg):
+    the striped sum and its division happen in libflexlink, for floating and
+    integer tensors alike; nothing is left for the Python backend to finish."""
     import torch
 
     from paper_2510_15882_b200 import c10d
+    from paper_2510_15882_b200.comm import _OPS
 
-    assert c10d._flx_op("avg", torch.ones(2)) == "sum"
+    assert _OPS["avg"] == 4  # FLX_OP_AVG == ncclAvg
+    for dt in (torch.float32, torch.bfloat16, torch.int32):
+        assert c10d._flx_op("avg", torch.ones(2, dtype=dt)) == "avg"
     assert c10d._flx_op("max", torch.ones(2, dtype=torch.int32)) == "max"
-    with pytest.raises(NotImplementedError, match="floating-point"):
-        c10d._flx_op("avg", torch.ones(2, dtype=torch.int32))
     t = torch.tensor([3.0, -6.0, 1.0])
-    c10d._finish("avg", t, 3)
-    assert torch.equal(t, torch.tensor([1.0, -2.0, 1.0 / 3.0]))
-    c10d._finish("sum", t, 3)  # other ops untouched
-    assert torch.equal(t, torch.tensor([1.0, -2.0, 1.0 / 3.0]))
+    c10d._finish("avg", t, 3)  # a no-op now
+    assert torch.equal(t, torch.tensor([3.0, -6.0, 1.0]))

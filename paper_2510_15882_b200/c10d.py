@@ -295,6 +295,12 @@ def backend_of(group=None) -> FlexLinkBackend:
         raise RuntimeError("no FlexLink process group has been created")
     if group is None:
         return _instances[-1]
+    try:  # the group's own CUDA backend object, when torch exposes it
+        b = group._get_backend(torch.device("cuda"))
+        if isinstance(b, FlexLinkBackend):
+            return b
+    except Exception:
+        pass
     for inst in reversed(_instances):
         if inst.rank() == dist.get_rank(group) and inst.size() == dist.get_world_size(group):
             return inst

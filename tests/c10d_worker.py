@@ -23,6 +23,7 @@ def main():
     c10d.register()
     dist.init_process_group("flexlink", rank=rank, world_size=world)
     comm = c10d.backend_of().comm
+    assert c10d.backend_of(dist.group.WORLD) is c10d.backend_of()  # the group's own backend
     if os.environ.get("FLX_C10D_PCIE_ONLY"):
         # two processes share this GPU: every byte on the host-staged PCIe path
         # (copy engines only), so no NVLink-path kernel waits on the other process

@@ -1386,7 +1386,11 @@ flxResult_t flxScatter(const void* sendbuff, void* recvbuff, size_t count,
   FLX_CUDA(cudaMallocAsync(&k.tmp, all, stream));
   k.recv = k.tmp;
   if (!is_root) {  // this rank's outgoing blocks are never read by anyone
-    FLX_CUDA(cudaMallocAsync(&k.tmp2, all, stream));
+    const cudaError_t e = cudaMallocAsync(&k.tmp2, all, stream);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(k.tmp, stream);
+      return fail(flxUnhandledCudaError, "flxScatter scratch: %s", cudaGetErrorString(e));
+    }
     k.send = k.tmp2;
   }
   k.post_dst = recvbuff;
